@@ -1,0 +1,246 @@
+"""Pins for the CPU oracle (oracle/compose.c), run on the dev box with no GPU (-m "not gpu").
+
+Every check compares the oracle against something other than itself: printed paper arrays,
+hand-worked fixtures (tests/golden/, each citing its passage), the plain definition trim(P_N1),
+brute-force Eq. (1) path scores, Delannoy path counts, the trellis closed form, the identity
+special case and invariants.  See DESIGN.md "Oracle and pins".
+"""
+import collections
+
+import numpy as np
+import pytest
+
+import fstgen
+import golden_io
+import oracle
+import pins
+from fstgen import EPS
+
+
+# ----------------------------------------------------------------------------- generators
+def test_splitmix64_reference_vector():
+    # splitmix64(seed 0) reference outputs (Vigna's splitmix64.c, standard shift constants)
+    r = fstgen.SplitMix64(0)
+    assert [r.next() for _ in range(3)] == [0xE220A8397B1DCDAF, 0x6E789E6AA1B965F4, 0x06C45D188009454F]
+    r1, r2 = fstgen.SplitMix64(12345), fstgen.SplitMix64(12345)
+    blk = r2.block(100)
+    assert [r1.next() for _ in range(100)] == [int(x) for x in blk]
+    assert r1.next() == r2.next()
+
+
+def test_below_vec_matches_python():
+    r = fstgen.SplitMix64(7).block(1000)
+    for n in (1, 5, 20000, (1 << 31) - 1):
+        assert [int(x) for x in fstgen.below_vec(r, n)] == [(int(x) * n) >> 64 for x in r]
+
+
+def test_random_graph_shape():
+    g = fstgen.random_graph(256, 5, 10, 3)  # SPEC.md:386 [PAPER §4.1 parameters]
+    assert g.num_states == 256 and g.num_arcs == 1280
+    assert np.all(np.diff(g.row_ptr) == 5)
+    assert np.array_equal(g.ilabel, g.olabel) and g.ilabel.min() >= 0 and g.ilabel.max() < 10
+    assert g.is_start.sum() == 1 and g.is_start[0] and g.is_accept.sum() == 1 and g.is_accept[255]
+    g2 = fstgen.random_graph(256, 5, 10, 3)
+    assert g.to_text() == g2.to_text()
+
+
+def test_emissions_and_lexicon_shapes():
+    e = fstgen.emissions_graph(250, 1, tokens=69)  # SPEC.md:422 [PAPER §4.2: 251 nodes x 69 arcs]
+    assert e.num_states == 251 and e.num_arcs == 17250
+    # log-softmax rows sum to ~1 in probability
+    p = np.exp(e.weight.astype(np.float64).reshape(250, 69)).sum(axis=1)
+    assert np.allclose(p, 1.0, atol=1e-5)
+    words = fstgen.letter_lexicon(100, 5)
+    assert len({tuple(w) for w in words}) == 100 and all(w[-1] == 0 for w in words)
+    L = fstgen.lexicon_graph(words)
+    assert L.num_states == 1 + sum(len(w) for w in words) and L.num_arcs == sum(len(w) for w in words)
+    Lc = fstgen.closure(L)
+    assert Lc.num_states == L.num_states + 1 and Lc.num_arcs == L.num_arcs + 1 + 100
+    assert Lc.is_start.sum() == 1 and Lc.is_start[-1] and Lc.is_accept.sum() == 1 and Lc.is_accept[-1]
+
+
+def test_text_roundtrip():
+    A, _ = fstgen.config_c2(0, V=50)
+    B = fstgen.Fst.from_text(A.to_text())
+    for k in ("row_ptr", "ilabel", "olabel", "dst", "is_start", "is_accept"):
+        assert np.array_equal(getattr(A, k), getattr(B, k))
+    assert np.array_equal(A.weight.view(np.uint32), B.weight.view(np.uint32))
+    with pytest.raises(ValueError):
+        fstgen.Fst.from_text("nodes 2\narc 0 5 1 1 0.0\n")  # SPEC.md read_text example
+
+
+# ----------------------------------------------------------------------------- §3.2 Fig. 1 arrays
+def test_fig1_soa_in_adjacency():
+    g = golden_io.load("fig1_soa.txt")
+    A, ex = g["A"], g["expect"]
+    assert list(A.is_start) == ex["start"] and list(A.is_accept) == ex["accept"]
+    off, arcs = oracle.in_adjacency(A)
+    assert list(off) == ex["inArcOffset"] and list(arcs) == ex["inArcs"]
+    assert list(A.row_ptr) == ex["outArcOffset"]
+    span = arcs[off[2]:off[3]]
+    assert list(A.ilabel[span]) == ex["node2_in_ilabels"] and list(A.olabel[span]) == ex["node2_in_olabels"]
+
+
+# ----------------------------------------------------------------------------- hand fixtures
+@pytest.mark.parametrize("name", golden_io.ALL_COMPOSE_FIXTURES)
+def test_golden_fixture(name):
+    g = golden_io.load(name)
+    C = oracle.canonical(g["A"], g["B"])
+    pins.assert_canonical_equal(C, g["C"], name)
+    if "R" in g:
+        R = oracle.coaccessible(g["A"], g["B"])
+        VB = g["B"].num_states
+        assert sorted((int(k) // VB, int(k) % VB) for k in np.flatnonzero(R)) == g["R"]
+    assert pins.is_trim(C)
+
+
+def test_fig2_round_profile():
+    """frontier sizes 1,2,2 and 6,8,0 arc pairs explored per step."""
+    g = golden_io.load("f2_fig2.txt")
+    A, B = g["A"], g["B"]
+    C = oracle.compose(A, B)
+    lv = C["level"]
+    nlev = lv.max() + 1
+    frontier = [int((lv == k).sum()) for k in range(nlev)]
+    degA, degB = np.diff(A.row_ptr), np.diff(B.row_ptr)
+    explored = [int(sum(degA[C["pair_a"][s]] * degB[C["pair_b"][s]] for s in np.flatnonzero(lv == k)))
+                for k in range(nlev)]
+    assert frontier == g["levels"]["frontier"] and explored == g["levels"]["explored"]
+    # (0,1) is re-reached in step 2 (self-loop a0 x b3) but created only once
+    keys = list(zip(C["pair_a"], C["pair_b"]))
+    assert keys.count((0, 1)) == 1
+
+
+def test_signed_zero_and_tie_bits():
+    C = oracle.canonical(*[golden_io.load("f5b_tie.txt")[k] for k in "AB"])
+    assert C["weight"].view(np.uint32)[0] == np.float32(-1.25).view(np.uint32)
+    C = oracle.canonical(*[golden_io.load("f5a_signed_zero.txt")[k] for k in "AB"])
+    bits = sorted(int(b) for b in C["weight"].view(np.uint32))
+    assert bits == [0, 0, 0, 0x80000000, 0x80000000]
+
+
+# ----------------------------------------------------------------------------- plain definition
+def _check_plain(A, B, what):
+    C = oracle.canonical(A, B)
+    P = pins.plain_trim_product(A, B)
+    pins.assert_canonical_equal(C, P, what)
+    R = oracle.coaccessible(A, B)
+    assert np.array_equal(R, pins.plain_coaccessible(A, B)), what
+    assert pins.is_trim(C), what
+    return C
+
+
+@pytest.mark.parametrize("chunk", range(4))
+def test_c1_vs_plain_definition(chunk):
+    """configs[0]: 1000 seeds (250 per chunk) of trim(P_N1) vs Algorithm 1, incl. multi start/accept."""
+    nonempty = 0
+    for s in range(chunk * 250, (chunk + 1) * 250):
+        A, B = fstgen.config_c1(s)
+        C = _check_plain(A, B, f"c1 seed {s}")
+        nonempty += C["num_states"] > 0
+    assert nonempty > 50
+
+
+@pytest.mark.parametrize("seed", range(60))
+def test_eps_dags_vs_plain_definition(seed):
+    A = fstgen.random_dag(8, 3, 4, 0.25, 3 * seed + 1)
+    B = fstgen.random_dag(8, 3, 4, 0.25, 3 * seed + 2)
+    _check_plain(A, B, f"eps dag {seed}")
+
+
+def test_eps_cyclic_vs_plain_definition():
+    for s in range(40):
+        A = fstgen.random_graph(12, 3, 4, 500 + s, acceptor=False, eps_prob=0.3, weights="dyadic64")
+        B = fstgen.random_graph(12, 3, 4, 900 + s, acceptor=False, eps_prob=0.3, weights="dyadic64")
+        _check_plain(A, B, f"eps cyclic {s}")
+
+
+# ----------------------------------------------------------------------------- Eq. (1) brute force
+L_MAX = 6
+
+
+def _bounded_table(table, L):
+    return {k: v for k, v in table.items() if len(k[0]) <= L}
+
+
+@pytest.mark.parametrize("seed", range(0, 200, 5))
+def test_eq1_bruteforce_eps_free(seed):
+    """configs[0] (eps-free, cyclic): per (x,z) with |x| <= L the multiset of composed path scores
+    equals {s_a + s_b} over matched path pairs (no duplicates); logsumexp equal (Eq. (1))."""
+    A, B = fstgen.config_c1(seed)
+    C = oracle.compose(A, B)
+    exp = _bounded_table(pins.eq1_bruteforce(A, B, max_len=L_MAX), L_MAX)
+    got = _bounded_table(pins.composed_path_table(C, max_len=L_MAX), L_MAX)
+    assert set(got) == set(exp)
+    for k in exp:
+        assert got[k] == exp[k], k
+    lg, le = pins.logsumexp_table(got), pins.logsumexp_table(exp)
+    for k in le:
+        assert abs(lg[k] - le[k]) <= 1e-12 * max(1.0, abs(le[k]))
+
+
+@pytest.mark.parametrize("seed", range(100))
+def test_eq1_delannoy_eps_dags(seed):
+    """eps DAGs: each matched path pair yields prod_i D(k_i, m_i) composed paths of score s_a + s_b;
+    the max (Viterbi) score and the (x,z) support equal brute force exactly."""
+    eps = 0.2 if seed % 2 else 0.3
+    A = fstgen.random_dag(7, 3, 3, eps, 7919 * seed + 11)
+    B = fstgen.random_dag(7, 3, 3, eps, 7919 * seed + 13)
+    C = oracle.compose(A, B)
+    exp = pins.eq1_bruteforce(A, B)
+    got = pins.composed_path_table(C)
+    assert set(got) == set(exp)
+    for k in exp:
+        assert got[k] == exp[k], k
+        assert max(got[k]) == max(exp[k])
+
+
+def test_delannoy_inflation_is_exercised():
+    hit = 0
+    for seed in range(60):
+        A = fstgen.random_dag(7, 3, 3, 0.3, 7919 * seed + 11)
+        B = fstgen.random_dag(7, 3, 3, 0.3, 7919 * seed + 13)
+        exp = pins.eq1_bruteforce(A, B)
+        hit += any(c > 1 for cnt in exp.values() for c in cnt.values())
+    assert hit > 0
+    assert pins.delannoy(1, 1) == 3 and pins.delannoy(2, 2) == 13 and pins.delannoy(0, 5) == 1
+
+
+# ----------------------------------------------------------------------------- special cases
+@pytest.mark.parametrize("seed", range(3))
+def test_identity_special_case(seed):
+    A = fstgen.random_graph(1000, 4, 8, 77 + seed, acceptor=False, eps_prob=0.1)
+    Id = fstgen.identity_fst(range(8))
+    pins.assert_canonical_equal(oracle.canonical(A, Id), pins.identity_expected(A), "A o Id")
+
+
+def test_acceptor_intersection():
+    """Acceptor o acceptor = automaton intersection (textbook product + trim); labels are l:l."""
+    done = 0
+    for V, D in ((60, 4), (80, 5), (50, 6)):
+        A, B = fstgen.config_c4(V=V, D=D)
+        C = _check_plain(A, B, f"acceptor {V}/{D}")
+        assert np.array_equal(C["ilabel"], C["olabel"])
+        done += C["num_arcs"] > 0
+    assert done >= 2
+
+
+def test_trellis_lexicon():
+    """A = emissions (T=20), B = closure(lexicon of 100 words): closed-form trellis."""
+    words = fstgen.letter_lexicon(100, 99)
+    B = fstgen.closure(fstgen.lexicon_graph(words))
+    A = fstgen.emissions_graph(20, 98)
+    C = oracle.canonical(A, B)
+    pins.assert_canonical_equal(C, pins.trellis_compose(A, B), "trellis")
+    assert C["num_states"] > 1000 and pins.is_trim(C)
+
+
+def test_size_bounds_and_R_superset():
+    A, B = fstgen.config_c2(0, V=300)
+    C = oracle.canonical(A, B)
+    R = oracle.coaccessible(A, B)
+    keys = C["pair_a"].astype(np.int64) * B.num_states + C["pair_b"]
+    assert np.all(R[keys] == 1) and R.sum() >= C["num_states"]
+    assert C["num_states"] <= A.num_states * B.num_states
+    assert C["row_ptr"][-1] == C["num_arcs"] and np.all(np.diff(C["row_ptr"]) >= 0)
+    assert pins.is_trim(C)
