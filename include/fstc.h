@@ -1,0 +1,167 @@
+/*
+ * fstc.h -- C ABI of the B200-native eager WFST composition library (libfstc.so).
+ *
+ * The library implements the data-parallel hot path of arXiv 2110.02848 ("parallel composition
+ * of WFSTs on GPUs"): eager, trimmed composition C = A o B in the log semiring with epsilon
+ * transitions.  The calls follow the paper's statement of the problem -- "Input: Transducers A and
+ * B ... Return: The composed graph C" (Algorithm 1) -- over the
+ * structure-of-arrays transducer of §3.2 (start/accept flags, per-arc label /
+ * weight / node arrays, per-node arc offsets).
+ *
+ * Semantics:
+ *   * epsilon = FST_EPS (-1).  Labels are int32 >= -1.  Only A.olabel and B.ilabel are matched.
+ *   * Moves from a pair (u_a,u_b) -- reading N1:
+ *       M1  e_a in out(u_a), e_b in out(u_b), olabel(e_a) == ilabel(e_b) (eps == eps included)
+ *           -> (dst e_a, dst e_b), label ilabel(e_a):olabel(e_b), weight fl32(w_a + w_b)
+ *       M2  e_a with olabel eps, B stays -> (dst e_a, u_b), label ilabel(e_a):eps, weight w_a (bits)
+ *       M3  e_b with ilabel eps, A stays -> (u_a, dst e_b), label eps:olabel(e_b), weight w_b (bits)
+ *   * Output = trim(product): exactly the pairs reachable from a start pair (S_A x S_B) AND
+ *     co-accessible to an accept pair (F_A x F_B), with every move between them.
+ *   * Output numbering: states in ascending pair key  a * V_B + b ; arcs of a state in a fixed
+ *     deterministic enumeration order.  Repeated calls give bit-identical outputs.
+ *
+ * Threading / streams: every call takes a CUDA stream (cudaStream_t passed as void*; NULL = the
+ * legacy default stream).  fst_create and fst_compose* are BLOCKING: they return when their
+ * results are complete (composition sizes are data dependent).  Handles are immutable after
+ * creation and may be shared by concurrent calls on different streams.
+ *
+ * Errors: every fst_status != FST_OK leaves the outputs untouched (or NULL) and sets a
+ * thread-local message readable with fst_last_error().  There is no CPU fallback: if no CUDA
+ * device is usable the calls fail with FST_E_CUDA.
+ */
+#ifndef FSTC_H_
+#define FSTC_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FST_EPS (-1) /* epsilon label (reading 1) */
+
+typedef struct fst* fst_handle; /* opaque; owns its device memory */
+
+typedef enum {
+  FST_OK = 0,
+  FST_E_INVALID_ARG = 1,   /* NULL pointer, negative size, n < 0, ... */
+  FST_E_INVALID_GRAPH = 2, /* fst_create validation failed (see fst_desc) */
+  FST_E_OOM = 3,           /* device allocation failed */
+  FST_E_CAPACITY = 4,      /* pair space / output beyond what the library can address */
+  FST_E_CUDA = 5,          /* CUDA runtime error (message in fst_last_error) */
+  FST_E_NCCL = 6,          /* reserved for the sharded multi-GPU mode */
+  FST_E_INTERNAL = 7       /* internal consistency check failed (a bug) */
+} fst_status;
+
+typedef enum { FST_MEM_DEVICE = 0, FST_MEM_HOST = 1 } fst_memory;
+
+/* Input transducer, CSR grouped by source state ("five arrays each with E
+ * entries" + "outArcOffset").  Arcs of state v are [row_ptr[v], row_ptr[v+1]); their order inside a
+ * row is arbitrary (the library builds its own label-sorted views).  All arrays are BORROWED for
+ * the duration of fst_create only and live in device memory (memory = FST_MEM_DEVICE) or in host
+ * memory (FST_MEM_HOST; pinned memory gives the fastest upload).  Validated, else
+ * FST_E_INVALID_GRAPH: row_ptr[0] == 0, non-decreasing, row_ptr[V] == E; 0 <= dst < V;
+ * labels >= -1; weights finite (no NaN / +-inf); flags in {0,1}.  V < 2^31, E < 2^31. */
+typedef struct {
+  int32_t num_states;       /* V >= 0 */
+  int64_t num_arcs;         /* E >= 0 */
+  const int64_t* row_ptr;   /* [V+1] */
+  const int32_t* ilabel;    /* [E] input label  */
+  const int32_t* olabel;    /* [E] output label */
+  const int32_t* dst;       /* [E] destination state ("output node") */
+  const float* weight;      /* [E] log-semiring weight */
+  const uint8_t* is_start;  /* [V] start flags */
+  const uint8_t* is_accept; /* [V] accept flags */
+  int32_t memory;           /* fst_memory: where the arrays above live */
+} fst_desc;
+
+/* Read-only view of a handle's arrays (DEVICE pointers owned by the handle, valid until fst_free).
+ * Composed graphs also carry pair_a/pair_b: the (a,b) pair of every state (SPEC "pairKeys");
+ * they are NULL for handles made by fst_create. */
+typedef struct {
+  int32_t num_states;
+  int64_t num_arcs;
+  const int64_t* row_ptr; /* [V+1] */
+  const int32_t* ilabel;  /* [E] */
+  const int32_t* olabel;  /* [E] */
+  const int32_t* dst;     /* [E] */
+  const float* weight;    /* [E] */
+  const uint8_t* is_start;
+  const uint8_t* is_accept;
+  const int32_t* pair_a; /* [V] or NULL */
+  const int32_t* pair_b; /* [V] or NULL */
+} fst_view;
+
+/* Per-composition statistics (filled by fst_compose*; timings only when profiling is on). */
+typedef struct {
+  int32_t levels_stage1;  /* BFS levels of the backward co-accessibility stage (Alg. 1 line 3) */
+  int32_t levels_stage2;  /* BFS levels of the forward stage (Alg. 1 lines 12-31) */
+  int64_t num_coaccessible; /* |R| over the pair space (profiling only; else -1) */
+  int64_t pair_space;     /* V_A * V_B summed over the call */
+  float ms_stage1;        /* CUDA-event time of the backward BFS (profiling only) */
+  float ms_stage2;        /* forward BFS */
+  float ms_number;        /* popcount directory + scans + output allocation */
+  float ms_emit;          /* emit kernel (writes the composed CSR) */
+  float ms_total;         /* whole call */
+  int64_t launches;       /* kernels launched by the call */
+  int64_t emit_launches;  /* of which emit kernels */
+  int64_t expand_launches;/* of which BFS level kernels */
+} fst_compose_stats;
+
+/* Upload + validate + build label-sorted adjacency views.  On success *out is a
+ * new handle.  Synchronises `stream`. */
+fst_status fst_create(const fst_desc* desc, void* stream, fst_handle* out);
+
+/* C = trim(A o B) (Algorithm 1 semantics, two-stage frontier BFS on the GPU).  *c receives a new
+ * handle (possibly with 0 states: an empty result is FST_OK).  a and b may be the same handle. */
+fst_status fst_compose(fst_handle a, fst_handle b, void* stream, fst_handle* c);
+
+/* n independent compositions c[i] = a[i] o b[i] advanced together in one level loop over
+ * concatenated pair spaces.  All-or-nothing: on error every c[i] is NULL. */
+fst_status fst_compose_batch(int32_t n, const fst_handle* a, const fst_handle* b, void* stream,
+                             fst_handle* c);
+
+/* Releases a handle and its device memory.  NULL-safe. */
+void fst_free(fst_handle h);
+
+/* Fills *v with the handle's sizes and device pointers. */
+fst_status fst_info(fst_handle h, fst_view* v);
+
+/* Copies a handle's arrays into caller-provided HOST buffers sized from fst_info (any pointer may
+ * be NULL to skip that array; pair_a/pair_b only for composed handles).  Synchronous. */
+fst_status fst_copy_to_host(fst_handle h, void* stream, int64_t* row_ptr, int32_t* ilabel,
+                            int32_t* olabel, int32_t* dst, float* weight, uint8_t* is_start,
+                            uint8_t* is_accept, int32_t* pair_a, int32_t* pair_b);
+
+/* Statistics of the composition that produced handle c (composed handles only). */
+fst_status fst_get_stats(fst_handle c, fst_compose_stats* s);
+
+/* Debug accessor for the §3.2 adjacency arrays (Fig. 1 golden test): role 0 = in-arcs grouped by
+ * destination (inArcOffset / inArcs), role 1 = out-arcs grouped by source.
+ * Within a node, arcs are sorted by the label the view matches on (olabel for in-view... see
+ * DESIGN.md) and then by arc index.  offsets [V+1], arc_ids [E], HOST buffers. */
+fst_status fst_adjacency(fst_handle h, int32_t role, int32_t match_on_olabel, int64_t* offsets,
+                         int64_t* arc_ids);
+
+/* Frontier size of every BFS level of the call that produced composed handle c (stage 1 = backward
+ * co-accessibility BFS, stage 2 = forward BFS; the Fig. 2 round profile).  Writes
+ * min(cap, levels) entries to the HOST array `sizes` and returns the number of levels (or -1). */
+int32_t fst_level_sizes(fst_handle c, int32_t stage, int64_t* sizes, int32_t cap);
+
+/* Profiling: when on, fst_compose* records CUDA events per phase (fst_compose_stats) and
+ * computes |R|.  Off by default. */
+void fst_set_profiling(int32_t on);
+
+/* Total kernels launched by this process through the library (monotone counter). */
+int64_t fst_launch_count(void);
+
+/* Thread-local message for the last non-OK status of this thread ("" if none). */
+const char* fst_last_error(void);
+
+/* Library version string. */
+const char* fst_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FSTC_H_ */

@@ -1,0 +1,10 @@
+"""B200-native eager WFST composition (arXiv 2110.02848) -- Python binding of libfstc.so.
+
+The compute path is the CUDA library (``csrc/`` -> ``libfstc.so``, C ABI in ``include/fstc.h``);
+this package only marshals arguments.  It never imports ``oracle/``.
+"""
+from .fstc import (FST_EPS, Fst, FstError, compose, fst_compose, fst_compose_batch, fst_create,
+                   fst_launch_count, fst_set_profiling, fst_version, load_library)
+
+__all__ = ["FST_EPS", "Fst", "FstError", "compose", "fst_compose", "fst_compose_batch", "fst_create",
+           "fst_launch_count", "fst_set_profiling", "fst_version", "load_library"]

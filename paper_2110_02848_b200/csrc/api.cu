@@ -1,0 +1,185 @@
+// api.cu -- the extern "C" boundary of libfstc (include/fstc.h): argument checks, error plumbing,
+// handle lifetime, host copies, statistics.  All compute is in create.cu / compose.cu kernels.
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <atomic>
+#include <vector>
+
+#include "fstc_handle.h"
+#include "fstc_internal.cuh"
+
+namespace fstc {
+
+static thread_local char g_err[512] = "";
+static std::atomic<int64_t> g_launches{0};
+static std::atomic<int> g_profiling{0};
+
+void set_error(fst_status st, const char* fmt, ...) {
+  (void)st;
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+void count_launch(int64_t n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+bool profiling_enabled() { return g_profiling.load(std::memory_order_relaxed) != 0; }
+
+int sm_count() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+std::vector<int64_t>& level_sizes_slot(fst* h, int stage) { return h->level_sizes[stage == 1 ? 0 : 1]; }
+
+fst_status compose_impl(int32_t n, const fst_handle* a, const fst_handle* b, cudaStream_t s, fst_handle* c);
+
+fst_status device_ready() {
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess || n == 0) {
+    cudaGetLastError();
+    set_error(FST_E_CUDA, "no usable CUDA device (%s); libfstc has no CPU fallback", cudaGetErrorString(e));
+    return FST_E_CUDA;
+  }
+  static bool pool_done = false;
+  if (!pool_done) {  // keep freed stream-ordered memory in the pool (repeat compositions reuse it)
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t thr = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    pool_done = true;
+  }
+  return FST_OK;
+}
+
+}  // namespace fstc
+
+using namespace fstc;
+
+extern "C" {
+
+fst_status fst_compose(fst_handle a, fst_handle b, void* stream, fst_handle* c) {
+  if (!a || !b || !c) {
+    set_error(FST_E_INVALID_ARG, "fst_compose: NULL argument");
+    return FST_E_INVALID_ARG;
+  }
+  fst_status st = device_ready();
+  if (st) return st;
+  return compose_impl(1, &a, &b, (cudaStream_t)stream, c);
+}
+
+fst_status fst_compose_batch(int32_t n, const fst_handle* a, const fst_handle* b, void* stream, fst_handle* c) {
+  if (n < 0 || (n > 0 && (!a || !b || !c))) {
+    set_error(FST_E_INVALID_ARG, "fst_compose_batch: bad arguments (n=%d)", n);
+    return FST_E_INVALID_ARG;
+  }
+  if (n == 0) return FST_OK;
+  fst_status st = device_ready();
+  if (st) return st;
+  return compose_impl(n, a, b, (cudaStream_t)stream, c);
+}
+
+void fst_free(fst_handle h) { delete h; }
+
+fst_status fst_info(fst_handle h, fst_view* v) {
+  if (!h || !v) {
+    set_error(FST_E_INVALID_ARG, "fst_info: NULL argument");
+    return FST_E_INVALID_ARG;
+  }
+  v->num_states = h->V;
+  v->num_arcs = h->E;
+  v->row_ptr = h->row_ptr;
+  v->ilabel = h->ilabel;
+  v->olabel = h->olabel;
+  v->dst = h->dst;
+  v->weight = h->weight;
+  v->is_start = h->is_start;
+  v->is_accept = h->is_accept;
+  v->pair_a = h->composed ? h->pair_a : nullptr;
+  v->pair_b = h->composed ? h->pair_b : nullptr;
+  return FST_OK;
+}
+
+fst_status fst_copy_to_host(fst_handle h, void* stream, int64_t* row_ptr, int32_t* ilabel, int32_t* olabel,
+                            int32_t* dst, float* weight, uint8_t* is_start, uint8_t* is_accept, int32_t* pair_a,
+                            int32_t* pair_b) {
+  if (!h) {
+    set_error(FST_E_INVALID_ARG, "fst_copy_to_host: NULL handle");
+    return FST_E_INVALID_ARG;
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t V = h->V, E = h->E;
+#define CPY(dst_, src_, bytes_) \
+  if ((dst_) && (bytes_) > 0) FSTC_CUDA_TRY(cudaMemcpyAsync(dst_, src_, bytes_, cudaMemcpyDeviceToHost, s));
+  CPY(row_ptr, h->row_ptr, 8 * (V + 1));
+  CPY(ilabel, h->ilabel, 4 * E);
+  CPY(olabel, h->olabel, 4 * E);
+  CPY(dst, h->dst, 4 * E);
+  CPY(weight, h->weight, 4 * E);
+  CPY(is_start, h->is_start, V);
+  CPY(is_accept, h->is_accept, V);
+  if (h->composed) {
+    CPY(pair_a, h->pair_a, 4 * V);
+    CPY(pair_b, h->pair_b, 4 * V);
+  }
+#undef CPY
+  FSTC_CUDA_TRY(cudaStreamSynchronize(s));
+  return FST_OK;
+}
+
+fst_status fst_get_stats(fst_handle c, fst_compose_stats* s) {
+  if (!c || !s || !c->composed) {
+    set_error(FST_E_INVALID_ARG, "fst_get_stats: need a composed handle");
+    return FST_E_INVALID_ARG;
+  }
+  *s = c->stats;
+  return FST_OK;
+}
+
+int32_t fst_level_sizes(fst_handle c, int32_t stage, int64_t* sizes, int32_t cap) {
+  if (!c || !c->composed || (stage != 1 && stage != 2)) return -1;
+  const std::vector<int64_t>& v = level_sizes_slot(c, stage);
+  for (int32_t i = 0; i < cap && i < (int32_t)v.size(); ++i) sizes[i] = v[i];
+  return (int32_t)v.size();
+}
+
+fst_status fst_adjacency(fst_handle h, int32_t role, int32_t match_on_olabel, int64_t* offsets, int64_t* arc_ids) {
+  if (!h || !offsets || (h->E > 0 && !arc_ids) || (role != 0 && role != 1)) {
+    set_error(FST_E_INVALID_ARG, "fst_adjacency: bad arguments");
+    return FST_E_INVALID_ARG;
+  }
+  if (!h->has_views) {
+    set_error(FST_E_INVALID_ARG, "fst_adjacency: handle has no views (composed handles build them on use)");
+    return FST_E_INVALID_ARG;
+  }
+  int k = role == 0 ? (match_on_olabel ? kInByOlabel : kInByIlabel) : (match_on_olabel ? kOutByOlabel : kOutByIlabel);
+  std::vector<int32_t> off(h->V + 1), arc(h->E);
+  FSTC_CUDA_TRY(cudaMemcpy(off.data(), h->views[k].off, 4 * (h->V + 1), cudaMemcpyDeviceToHost));
+  if (h->E) FSTC_CUDA_TRY(cudaMemcpy(arc.data(), h->views[k].arc, 4 * h->E, cudaMemcpyDeviceToHost));
+  for (int64_t i = 0; i <= h->V; ++i) offsets[i] = off[i];
+  for (int64_t i = 0; i < h->E; ++i) arc_ids[i] = arc[i];
+  return FST_OK;
+}
+
+void fst_set_profiling(int32_t on) { g_profiling.store(on ? 1 : 0); }
+
+int64_t fst_launch_count(void) { return g_launches.load(); }
+
+const char* fst_last_error(void) { return g_err; }
+
+const char* fst_version(void) { return "fstc 0.1 (sm_100a)"; }
+
+}  // extern "C"

@@ -1,0 +1,129 @@
+// fstc_internal.cuh -- internal data structures of libfstc (B200 / sm_100a).
+//
+// Layout in HBM:
+//   * Input FST handle: the CSR as given plus four label-sorted adjacency VIEWS (SoA, int32):
+//       out-by-olabel (A role, forward), in-by-olabel (A role, backward),
+//       out-by-ilabel (B role, forward), in-by-ilabel (B role, backward).
+//     Each view: off[V+1], key[E] (the matched label, ascending within a node, eps = -1 first so
+//     eps arcs are a prefix), other[E] (dst for out-views, src for in-views), carry[E] (the label
+//     that is copied to the output: ilabel for the A role, olabel for the B role), w[E], arc[E].
+//   * Pair space of a composition: V_A rows of ceil(V_B/32) 32-bit words; bit (a,b) lives in word
+//     W + a*wpr + b/32, bit b%32.  Rows are split into BLOCKS of 32 words (1024 pairs), the unit of
+//     frontier scheduling and of state / arc numbering.  Batches concatenate pair spaces
+//     (W, K = word / block bases per composition).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/fstc.h"
+
+namespace fstc {
+
+constexpr int kWordsPerBlock = 32;    // 32 words x 32 bits = 1024 pairs per block
+constexpr int kPairsPerBlock = 1024;
+
+struct ViewDev {
+  const int32_t* off;    // [V+1]
+  const int32_t* key;    // [E] matched label, sorted within node
+  const int32_t* other;  // [E] other-end node
+  const int32_t* carry;  // [E] label carried to the output
+  const float* w;        // [E] weight
+};
+
+// One composition inside a (possibly batched) call.
+struct CompDev {
+  ViewDev Af, Ab, Bf, Bb;  // forward (out) / backward (in) views of A (by olabel) and B (by ilabel)
+  const uint8_t* startA;
+  const uint8_t* startB;
+  const uint8_t* accA;
+  const uint8_t* accB;
+  const int32_t* startListA;
+  const int32_t* startListB;
+  const int32_t* accListA;
+  const int32_t* accListB;
+  int32_t nStartA, nStartB, nAccA, nAccB;
+  int32_t VA, VB;
+  int32_t wpr, bpr;  // words per row, blocks per row
+  int64_t W;         // first word of this composition's pair space
+  int64_t K;         // first block
+  // outputs (filled before the emit kernel)
+  int64_t* row_ptr;
+  int32_t* ilabel;
+  int32_t* olabel;
+  int32_t* dst;
+  float* weight;
+  uint8_t* is_start;
+  uint8_t* is_accept;
+  int32_t* pair_a;
+  int32_t* pair_b;
+};
+
+// Per-level control block (ring of 3).
+struct LevelCtrl {
+  unsigned long long count;    // number of active blocks in the list of this level
+  unsigned long long nnew;     // states discovered (claimed) into this level's frontier
+  unsigned long long pad[2];
+};
+
+// Workspace of one compose call (device pointers).
+struct Work {
+  uint32_t* R;        // co-accessible bitmap
+  uint32_t* V;        // visited (accessible & co-accessible) bitmap
+  uint32_t* F[2];     // frontier bitmaps (double buffered, self-cleaning)
+  uint8_t* flag[2];   // per-block "has frontier bits" flags (self-cleaning)
+  int32_t* list[2];   // active block lists
+  LevelCtrl* ctrl;    // [3]
+  unsigned long long* kept;  // [nblocks] arcs of C leaving each block's states (stage-2 count)
+  int32_t* vcount;    // [nblocks] states of C per block
+  uint16_t* wpre;     // [nwords] exclusive popcount prefix of V inside the block
+  int64_t* idbase;    // [nblocks+1] exclusive scan of vcount
+  int64_t* arcbase;   // [nblocks+1] exclusive scan of kept
+  unsigned long long* nnew_hist;  // [kMaxLevelStats] per-level discoveries (stats)
+  int32_t* err;       // [1] internal consistency flag
+  int64_t nwords, nblocks;
+  int32_t ncomp;
+  const CompDev* comps;  // [ncomp] device copy
+};
+
+constexpr int kMaxLevelStats = 1 << 16;
+
+__device__ __forceinline__ int find_comp(const CompDev* __restrict__ comps, int ncomp, int64_t blk) {
+  // largest i with comps[i].K <= blk
+  int lo = 0, hi = ncomp - 1;
+  while (lo < hi) {
+    int mid = (lo + hi + 1) >> 1;
+    if (comps[mid].K <= blk) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+
+}  // namespace fstc
+
+// ---------------------------------------------------------------------------------------------
+// host-side helpers shared by the translation units
+namespace fstc {
+void set_error(fst_status st, const char* fmt, ...);
+void count_launch(int64_t n = 1);
+int sm_count();
+}  // namespace fstc
+
+#define FSTC_CUDA_TRY(expr)                                                                   \
+  do {                                                                                        \
+    cudaError_t _e = (expr);                                                                  \
+    if (_e != cudaSuccess) {                                                                  \
+      fstc::set_error(FST_E_CUDA, "%s failed: %s (%s:%d)", #expr, cudaGetErrorString(_e),     \
+                      __FILE__, __LINE__);                                                    \
+      return _e == cudaErrorMemoryAllocation ? FST_E_OOM : FST_E_CUDA;                        \
+    }                                                                                         \
+  } while (0)
+
+#define FSTC_LAUNCH_CHECK()                                                                   \
+  do {                                                                                        \
+    fstc::count_launch();                                                                     \
+    cudaError_t _e = cudaGetLastError();                                                      \
+    if (_e != cudaSuccess) {                                                                  \
+      fstc::set_error(FST_E_CUDA, "kernel launch failed: %s (%s:%d)", cudaGetErrorString(_e), \
+                      __FILE__, __LINE__);                                                    \
+      return FST_E_CUDA;                                                                      \
+    }                                                                                         \
+  } while (0)

@@ -1,0 +1,255 @@
+"""Thin ctypes binding of libfstc (include/fstc.h) -- argument marshalling only.
+
+Every step of composition runs in the CUDA kernels of libfstc.so; this module only converts
+numpy arrays / torch tensors into the C descriptors and back.  There is no CPU fallback: if the
+library is missing or no CUDA device is usable, every call raises ``FstError``.
+
+Names mirror the C ABI: fst_create, fst_compose, fst_compose_batch, fst_free, fst_info,
+fst_copy_to_host, fst_get_stats, fst_level_sizes, fst_adjacency.  ``Fst`` is a small owning
+wrapper around a handle.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+from typing import Dict, List, Optional, Sequence
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libfstc.so")
+
+FST_EPS = -1
+FST_MEM_DEVICE, FST_MEM_HOST = 0, 1
+STATUS = {0: "FST_OK", 1: "FST_E_INVALID_ARG", 2: "FST_E_INVALID_GRAPH", 3: "FST_E_OOM", 4: "FST_E_CAPACITY",
+          5: "FST_E_CUDA", 6: "FST_E_NCCL", 7: "FST_E_INTERNAL"}
+
+EXPORTED = ["fst_create", "fst_compose", "fst_compose_batch", "fst_free", "fst_info", "fst_copy_to_host",
+            "fst_get_stats", "fst_level_sizes", "fst_adjacency", "fst_set_profiling", "fst_launch_count",
+            "fst_last_error", "fst_version"]
+
+
+class FstError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+class fst_desc(C.Structure):
+    _fields_ = [("num_states", C.c_int32), ("num_arcs", C.c_int64), ("row_ptr", C.c_void_p),
+                ("ilabel", C.c_void_p), ("olabel", C.c_void_p), ("dst", C.c_void_p), ("weight", C.c_void_p),
+                ("is_start", C.c_void_p), ("is_accept", C.c_void_p), ("memory", C.c_int32)]
+
+
+class fst_view(C.Structure):
+    _fields_ = [("num_states", C.c_int32), ("num_arcs", C.c_int64), ("row_ptr", C.c_void_p),
+                ("ilabel", C.c_void_p), ("olabel", C.c_void_p), ("dst", C.c_void_p), ("weight", C.c_void_p),
+                ("is_start", C.c_void_p), ("is_accept", C.c_void_p), ("pair_a", C.c_void_p),
+                ("pair_b", C.c_void_p)]
+
+
+class fst_compose_stats(C.Structure):
+    _fields_ = [("levels_stage1", C.c_int32), ("levels_stage2", C.c_int32), ("num_coaccessible", C.c_int64),
+                ("pair_space", C.c_int64), ("ms_stage1", C.c_float), ("ms_stage2", C.c_float),
+                ("ms_number", C.c_float), ("ms_emit", C.c_float), ("ms_total", C.c_float),
+                ("launches", C.c_int64), ("emit_launches", C.c_int64), ("expand_launches", C.c_int64)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+_lib = None
+_lock = threading.Lock()
+
+
+def load_library(path: str = LIB_PATH) -> C.CDLL:
+    """Loads libfstc.so (built by ``__graft_entry__.build()``); raises if absent."""
+    global _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(path):
+            raise FstError(5, f"{path} not built -- run `python -c 'import __graft_entry__ as g; g.build()'`")
+        lib = C.CDLL(path)
+        vp = C.c_void_p
+        lib.fst_create.argtypes = [C.POINTER(fst_desc), vp, C.POINTER(vp)]
+        lib.fst_compose.argtypes = [vp, vp, vp, C.POINTER(vp)]
+        lib.fst_compose_batch.argtypes = [C.c_int32, C.POINTER(vp), C.POINTER(vp), vp, C.POINTER(vp)]
+        lib.fst_free.argtypes = [vp]
+        lib.fst_free.restype = None
+        lib.fst_info.argtypes = [vp, C.POINTER(fst_view)]
+        lib.fst_copy_to_host.argtypes = [vp, vp] + [vp] * 9
+        lib.fst_get_stats.argtypes = [vp, C.POINTER(fst_compose_stats)]
+        lib.fst_level_sizes.argtypes = [vp, C.c_int32, vp, C.c_int32]
+        lib.fst_level_sizes.restype = C.c_int32
+        lib.fst_adjacency.argtypes = [vp, C.c_int32, C.c_int32, vp, vp]
+        lib.fst_set_profiling.argtypes = [C.c_int32]
+        lib.fst_set_profiling.restype = None
+        lib.fst_launch_count.restype = C.c_int64
+        lib.fst_last_error.restype = C.c_char_p
+        lib.fst_version.restype = C.c_char_p
+        for name in ("fst_create", "fst_compose", "fst_compose_batch", "fst_info", "fst_copy_to_host",
+                     "fst_get_stats", "fst_adjacency"):
+            getattr(lib, name).restype = C.c_int
+        _lib = lib
+        return lib
+
+
+def _check(st: int):
+    if st != 0:
+        raise FstError(st, load_library().fst_last_error().decode())
+
+
+def _stream_ptr(stream) -> Optional[int]:
+    if stream is None:
+        try:
+            import torch
+            if torch.cuda.is_available():
+                return torch.cuda.current_stream().cuda_stream
+        except Exception:  # pragma: no cover
+            pass
+        return None
+    if isinstance(stream, int):
+        return stream
+    return stream.cuda_stream  # torch.cuda.Stream
+
+
+# ------------------------------------------------------------------------------------------ ABI
+def fst_create(fst_like, stream=None) -> "Fst":
+    """fst_like: an object with num_states, row_ptr, ilabel, olabel, dst, weight, is_start,
+    is_accept as numpy arrays (host upload) or torch CUDA tensors (device)."""
+    lib = load_library()
+    arrays = [fst_like.row_ptr, fst_like.ilabel, fst_like.olabel, fst_like.dst, fst_like.weight,
+              fst_like.is_start, fst_like.is_accept]
+    dtypes = [np.int64, np.int32, np.int32, np.int32, np.float32, np.uint8, np.uint8]
+    keep = []
+    if all(hasattr(a, "data_ptr") for a in arrays):  # torch tensors
+        import torch
+        ptrs = []
+        for a, dt in zip(arrays, dtypes):
+            assert a.is_cuda and a.is_contiguous() and a.element_size() == np.dtype(dt).itemsize
+            ptrs.append(a.data_ptr() if a.numel() else None)
+        mem = FST_MEM_DEVICE
+        E = int(arrays[1].numel())
+    else:
+        ptrs = []
+        for a, dt in zip(arrays, dtypes):
+            a = np.ascontiguousarray(a, dtype=dt)
+            keep.append(a)
+            ptrs.append(a.ctypes.data if a.size else None)
+        mem = FST_MEM_HOST
+        E = int(keep[1].size)
+    d = fst_desc(int(fst_like.num_states), E, *ptrs, mem)
+    h = C.c_void_p()
+    _check(lib.fst_create(C.byref(d), _stream_ptr(stream), C.byref(h)))
+    return Fst(h)
+
+
+def fst_compose(a: "Fst", b: "Fst", stream=None) -> "Fst":
+    lib = load_library()
+    h = C.c_void_p()
+    _check(lib.fst_compose(a.handle, b.handle, _stream_ptr(stream), C.byref(h)))
+    return Fst(h)
+
+
+def fst_compose_batch(a: Sequence["Fst"], b: Sequence["Fst"], stream=None) -> List["Fst"]:
+    lib = load_library()
+    n = len(a)
+    assert len(b) == n
+    A = (C.c_void_p * n)(*[x.handle for x in a])
+    B = (C.c_void_p * n)(*[x.handle for x in b])
+    out = (C.c_void_p * n)()
+    _check(lib.fst_compose_batch(n, A, B, _stream_ptr(stream), out))
+    return [Fst(C.c_void_p(out[i])) for i in range(n)]
+
+
+def fst_set_profiling(on: bool):
+    load_library().fst_set_profiling(1 if on else 0)
+
+
+def fst_launch_count() -> int:
+    return int(load_library().fst_launch_count())
+
+
+def fst_version() -> str:
+    return load_library().fst_version().decode()
+
+
+class Fst:
+    """Owning wrapper of an fst_handle (freed on garbage collection or ``free()``)."""
+
+    def __init__(self, handle: C.c_void_p):
+        self.handle = handle
+
+    def free(self):
+        if self.handle and self.handle.value:
+            load_library().fst_free(self.handle)
+        self.handle = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+    def info(self) -> fst_view:
+        v = fst_view()
+        _check(load_library().fst_info(self.handle, C.byref(v)))
+        return v
+
+    @property
+    def num_states(self) -> int:
+        return int(self.info().num_states)
+
+    @property
+    def num_arcs(self) -> int:
+        return int(self.info().num_arcs)
+
+    def to_host(self, stream=None) -> Dict[str, np.ndarray]:
+        """fst_copy_to_host into fresh numpy arrays (pair_a/pair_b for composed graphs)."""
+        v = self.info()
+        V, E = int(v.num_states), int(v.num_arcs)
+        out = {"num_states": V, "num_arcs": E,
+               "row_ptr": np.zeros(V + 1, np.int64), "ilabel": np.zeros(E, np.int32),
+               "olabel": np.zeros(E, np.int32), "dst": np.zeros(E, np.int32), "weight": np.zeros(E, np.float32),
+               "is_start": np.zeros(V, np.uint8), "is_accept": np.zeros(V, np.uint8)}
+        composed = bool(v.pair_a)
+        if composed:
+            out["pair_a"] = np.zeros(V, np.int32)
+            out["pair_b"] = np.zeros(V, np.int32)
+        ptr = lambda k: out[k].ctypes.data if k in out and out[k].size else None
+        _check(load_library().fst_copy_to_host(self.handle, _stream_ptr(stream), ptr("row_ptr"), ptr("ilabel"),
+                                               ptr("olabel"), ptr("dst"), ptr("weight"), ptr("is_start"),
+                                               ptr("is_accept"), ptr("pair_a"), ptr("pair_b")))
+        return out
+
+    def stats(self) -> dict:
+        s = fst_compose_stats()
+        _check(load_library().fst_get_stats(self.handle, C.byref(s)))
+        return s.as_dict()
+
+    def level_sizes(self, stage: int) -> List[int]:
+        lib = load_library()
+        n = lib.fst_level_sizes(self.handle, stage, None, 0)
+        if n < 0:
+            raise FstError(1, "not a composed handle")
+        buf = np.zeros(max(n, 1), np.int64)
+        lib.fst_level_sizes(self.handle, stage, buf.ctypes.data, n)
+        return [int(x) for x in buf[:n]]
+
+    def adjacency(self, role: int, match_on_olabel: bool):
+        v = self.info()
+        off = np.zeros(int(v.num_states) + 1, np.int64)
+        arcs = np.zeros(max(1, int(v.num_arcs)), np.int64)
+        _check(load_library().fst_adjacency(self.handle, role, 1 if match_on_olabel else 0, off.ctypes.data,
+                                            arcs.ctypes.data))
+        return off, arcs[: int(v.num_arcs)]
+
+
+def compose(A, B, stream=None) -> Dict[str, np.ndarray]:
+    """Convenience: host arrays in, composed graph (numpy, GPU numbering) out."""
+    a = fst_create(A, stream)
+    b = fst_create(B, stream)
+    c = fst_compose(a, b, stream)
+    return c.to_host(stream)
