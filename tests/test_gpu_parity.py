@@ -102,10 +102,13 @@ def test_c1_all_seeds(fst):
 
 @pytest.mark.parametrize("seed", range(10))
 def test_c2_eps_1k(fst, seed):
-    """configs[1]: 1k-state transducers with eps (p=0.1 per tape), 20 symbols, degree 4."""
+    """configs[1]: 1k-state transducers with eps (p=0.1 per tape), 20 symbols, degree 4.  About half
+    of the seeds give an empty composition (the single accept pair is not reachable backwards);
+    those are the "no start pair in R" edge case and must also match."""
     A, B = fstgen.config_c2(seed)
     got = check(fst, A, B, f"c2 seed {seed}")
-    assert got["num_arcs"] > 0
+    if seed in (0, 3, 8, 9):
+        assert got["num_arcs"] > 250000
 
 
 def test_c3_lexicon_emissions(fst):
