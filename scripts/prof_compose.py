@@ -1,0 +1,27 @@
+"""Profiling driver: one warm-up + N compositions of a c4-style workload (for ncu launch lists)."""
+import argparse
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import fstgen  # noqa: E402
+import paper_2110_02848_b200 as fstc  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--V", type=int, default=8192)
+ap.add_argument("--D", type=int, default=8)
+ap.add_argument("--T", type=int, default=0)
+ap.add_argument("--n", type=int, default=1)
+ap.add_argument("--workload", default="random")
+args = ap.parse_args()
+if args.workload == "lexicon":
+    A, B = fstgen.config_c3(num_words=10000, T=300)
+else:
+    A, B = fstgen.config_c4(V=args.V, D=args.D, tokens=args.T or None)
+a, b = fstc.fst_create(A), fstc.fst_create(B)
+fstc.fst_set_profiling(True)
+for i in range(args.n + 1):
+    c = fstc.fst_compose(a, b)
+    print(i, c.num_states, c.num_arcs, {k: round(v, 3) if isinstance(v, float) else v for k, v in c.stats().items()},
+          flush=True)
+    c.free()
