@@ -100,12 +100,14 @@ typedef struct {
   int64_t pair_space;     /* V_A * V_B summed over the call */
   float ms_stage1;        /* CUDA-event time of the backward BFS (profiling only) */
   float ms_stage2;        /* forward BFS */
-  float ms_number;        /* popcount directory + scans + output allocation */
+  float ms_number;        /* popcount directory + scans (+ |R| when profiling) */
+  float ms_alloc;         /* output allocation */
   float ms_emit;          /* emit kernel (writes the composed CSR) */
   float ms_total;         /* whole call */
   int64_t launches;       /* kernels launched by the call */
   int64_t emit_launches;  /* of which emit kernels */
   int64_t expand_launches;/* of which BFS level kernels */
+  int64_t staged_tasks;   /* chunk tasks of the BFS levels that used shared-memory staging */
 } fst_compose_stats;
 
 /* Upload + validate + build label-sorted adjacency views.  On success *out is a

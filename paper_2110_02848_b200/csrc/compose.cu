@@ -14,10 +14,14 @@
 //   emit     re-enumerate the moves of every state of C, write each arc at a scan-derived slot
 //            (pass 2; deterministic slots replace the paper's atomic cursors).
 //
-// Work decomposition (B200-first, not the paper's thread-per-arc-pair): a CTA owns one 1024-pair
-// block (row u_a, 1024 consecutive u_b).  It compacts the block's frontier bits, then walks the
-// B-side arcs of those states with one thread per arc ("item"), finding the matching A arcs of
-// row u_a by binary search in the label-sorted A view.  Moves M1/M2/M3 of N1.
+// Work decomposition (B200-first, not the paper's thread-per-arc-pair): one CTA task is a CHUNK =
+// a run of 1024-pair blocks of one pair-space row u_a.  All moves out of row u_a land in the few
+// destination rows {dst(e_a)} U {u_a}; the CTA stages the A row (label mask table) and those
+// destination rows' bitmaps / rank tables in shared memory, then streams the B-side "items" (one
+// sentinel + the out-arcs of every state, contiguous in B's view) of the chunk.  Candidates are
+// tested and claimed in shared memory and merged into the global bitmaps one 32-bit word at a
+// time.  Sparse chunks and rows whose staging does not fit fall back to compacted per-state work
+// with global test-and-set.
 #include <stdio.h>
 #include <string.h>
 
@@ -36,196 +40,646 @@ bool profiling_enabled();
 
 namespace {
 
-constexpr int kThreads = 256;
-constexpr int kStatesPerThread = kPairsPerBlock / kThreads;  // 4
+constexpr int kThreads = 512;
+constexpr int kWarps = kThreads / 32;
+constexpr int kAMax = 64;           // A-row arcs staged in shared memory
+constexpr int kSlotMax = 32;        // destination rows staged in shared memory
+constexpr int kChunkMaxBlocks = 32; // blocks per chunk (<= 1024 words)
+constexpr int kDynSmem = 88 * 1024; // staging area (destination rows)
+constexpr int kSimpleMoves = 4;    // warps whose items have <= this many moves skip the expansion
+constexpr int kHeavy = 64;         // states with more B arcs are walked cooperatively by the CTA
+constexpr int kWCap = 160;         // per-warp output window of the fast emit (arcs)
 
 struct Ctx {
-  // device pointers of the workspace (passed by value to every kernel)
   uint32_t* R;
   uint32_t* V;
   uint32_t* F0;
   uint32_t* F1;
-  uint32_t* flag0;
+  uint32_t* flag0;  // per chunk
   uint32_t* flag1;
-  int32_t* list0;
+  int32_t* list0;   // active chunk lists
   int32_t* list1;
   LevelCtrl* ctrl;
-  unsigned long long* kept;
-  int32_t* vcount;
-  uint16_t* wpre;
-  int64_t* idbase;
-  int64_t* arcbase;
-  unsigned long long* hist;  // per-level discovered states
-  unsigned long long* misc;  // [0] nonempty levels, [1] |R|, [2] emit consistency errors
+  unsigned long long* kept;  // per block
+  int32_t* vcount;           // per block
+  uint16_t* wpre;            // per word
+  int64_t* idbase;           // per block (+1)
+  int64_t* arcbase;          // per block (+1)
+  unsigned long long* hist;  // per-level frontier sizes
+  unsigned long long* misc;  // [0] nonempty levels, [1] |R|, [2] emit consistency errors, [3] staged tasks
   const CompDev* comps;
-  const int64_t* seedbase;  // [ncomp+1] prefix of seed-pair counts
+  const int64_t* seedbase;
   int32_t ncomp;
-  int64_t nwords, nblocks;
+  int64_t nwords, nblocks, nchunks;
 };
 
-struct BlockInfo {
+struct Chunk {
   int comp;
   int32_t ua;
-  int32_t ub0;
-  int32_t nwords;
-  int64_t word0;
+  int32_t b0, b1;   // blocks [b0, b1) of the row
+  int64_t rowW;     // global word index of (ua, 0)
 };
 
-__device__ __forceinline__ BlockInfo decode_block(const Ctx& cx, int64_t blk) {
-  BlockInfo bi;
-  bi.comp = cx.ncomp == 1 ? 0 : find_comp(cx.comps, cx.ncomp, blk);
-  const CompDev& C = cx.comps[bi.comp];
-  int64_t local = blk - C.K;
-  bi.ua = (int32_t)(local / C.bpr);
-  int32_t j = (int32_t)(local - (int64_t)bi.ua * C.bpr);
-  bi.ub0 = j * kPairsPerBlock;
-  bi.nwords = min(kWordsPerBlock, C.wpr - j * kWordsPerBlock);
-  bi.word0 = C.W + (int64_t)bi.ua * C.wpr + (int64_t)j * kWordsPerBlock;
-  return bi;
+__device__ __forceinline__ int find_comp_q(const CompDev* __restrict__ comps, int ncomp, int64_t q) {
+  int lo = 0, hi = ncomp - 1;
+  while (lo < hi) {
+    int mid = (lo + hi + 1) >> 1;
+    if (comps[mid].Q <= q) lo = mid; else hi = mid - 1;
+  }
+  return lo;
 }
 
-__device__ __forceinline__ int32_t lower_bound_key(const int32_t* __restrict__ key, int32_t lo, int32_t hi,
-                                                   int32_t x) {
+__device__ __forceinline__ Chunk decode_chunk(const Ctx& cx, int64_t q) {
+  Chunk ch;
+  ch.comp = cx.ncomp == 1 ? 0 : find_comp_q(cx.comps, cx.ncomp, q);
+  const CompDev& C = cx.comps[ch.comp];
+  int64_t local = q - C.Q;
+  ch.ua = (int32_t)(local / C.cpr);
+  int32_t j = (int32_t)(local - (int64_t)ch.ua * C.cpr);
+  ch.b0 = j * C.CB;
+  ch.b1 = min(ch.b0 + C.CB, C.bpr);
+  ch.rowW = C.W + (int64_t)ch.ua * C.wpr;
+  return ch;
+}
+
+__device__ __forceinline__ int64_t chunk_of(const CompDev& C, int32_t row, int32_t col) {
+  return C.Q + (int64_t)row * C.cpr + ((col >> 10) / C.CB);
+}
+
+__device__ __forceinline__ int32_t lower_bound_g(const int32_t* __restrict__ key, int32_t lo, int32_t hi, int32_t x) {
   while (lo < hi) {
     int32_t mid = (lo + hi) >> 1;
     if (__ldg(&key[mid]) < x) lo = mid + 1; else hi = mid;
   }
   return lo;
 }
-
-// Frontier mark of a newly claimed pair: F_next bit, block flag, block list append.
-__device__ __forceinline__ void push_frontier(const CompDev& C, int32_t va, int32_t vb, int64_t w, uint32_t bit,
-                                              uint32_t* __restrict__ Fn, uint32_t* __restrict__ flagn,
-                                              int32_t* __restrict__ listn, LevelCtrl* ctrln) {
-  atomicOr(&Fn[w], bit);
-  int64_t blk = C.K + (int64_t)va * C.bpr + (vb >> 10);
-  if (*((volatile uint32_t*)&flagn[blk]) == 0 && atomicExch(&flagn[blk], 1u) == 0) {
-    unsigned long long pos = atomicAdd(&ctrln->count, 1ull);
-    listn[pos] = (int32_t)blk;
-  }
-}
-
-// Visit a candidate pair: stage-2 filter (R), test-then-set claim on the visited bitmap.
-template <bool kFilter>
-__device__ __forceinline__ void visit(const CompDev& C, int32_t va, int32_t vb, uint32_t* __restrict__ vis,
-                                      const uint32_t* __restrict__ R, uint32_t* __restrict__ Fn,
-                                      uint32_t* __restrict__ flagn, int32_t* __restrict__ listn, LevelCtrl* ctrln,
-                                      unsigned& kept, unsigned& nnew) {
-  const int64_t w = C.W + (int64_t)va * C.wpr + (vb >> 5);
-  const uint32_t bit = 1u << (vb & 31);
-  if (kFilter) {
-    if (!(__ldg(&R[w]) & bit)) return;
-    ++kept;
-  }
-  if (*((volatile uint32_t*)&vis[w]) & bit) return;  // test before the atomic (bits only get set)
-  uint32_t old = atomicOr(&vis[w], bit);
-  if (old & bit) return;
-  ++nnew;
-  push_frontier(C, va, vb, w, bit, Fn, flagn, listn, ctrln);
-}
-
-// Shared per-block staging of the CTA: compacted states of one 1024-pair block and their item
-// offsets.  Item 0 of a state is its "M2 item" (only in the emit pass, or when A's row has eps
-// outputs); the following items are the B-side arcs of the state in view order.
-struct BlockSmem {
-  uint32_t words[kWordsPerBlock];
-  int32_t wpre[kWordsPerBlock + 1];
-  int32_t state[kPairsPerBlock];      // u_b of the i-th set bit
-  int32_t scan[kPairsPerBlock + 1];   // item offsets
-  int32_t a0, a1, aeps;               // A row [a0,a1), eps prefix [a0,aeps)
-  unsigned long long red[kThreads / 32 + 1];
-  int32_t red32[kThreads / 32 + 1];
-};
-
-// Compact the set bits of s.words into s.state (ascending u_b).
-__device__ __forceinline__ void compact_bits(BlockSmem& s, int32_t ub0) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int i = warp; i < kWordsPerBlock; i += kThreads / 32) {
-    uint32_t w = s.words[i];
-    if ((w >> lane) & 1u) {
-      int pos = s.wpre[i] + __popc(w & ((1u << lane) - 1u));
-      s.state[pos] = ub0 + i * 32 + lane;
-    }
-  }
-}
-
-// Load the block's words of `bits` (optionally clearing them), prefix popcounts into s.
-__device__ __forceinline__ void load_words(BlockSmem& s, uint32_t* bits, const BlockInfo& bi, bool clear) {
-  if (threadIdx.x < 32) {
-    const int lane = threadIdx.x;
-    uint32_t w = 0;
-    if (lane < bi.nwords) {
-      w = bits[bi.word0 + lane];
-      if (clear && w) bits[bi.word0 + lane] = 0u;
-    }
-    s.words[lane] = w;
-    int pc = __popc(w);
-    int inc = warp_incl_scan(pc);
-    s.wpre[lane] = inc - pc;
-    if (lane == 31) s.wpre[32] = inc;
-  }
-}
-
-// Item offsets of the nst compacted states: items(state) = extra + deg_B(state).  Returns total.
-__device__ __forceinline__ int32_t scan_items(BlockSmem& s, int nst, const int32_t* __restrict__ Boff, int extra) {
-  int32_t c[kStatesPerThread];
-  int32_t sum = 0;
-#pragma unroll
-  for (int k = 0; k < kStatesPerThread; ++k) {
-    int i = threadIdx.x * kStatesPerThread + k;
-    c[k] = 0;
-    if (i < nst) {
-      int32_t ub = s.state[i];
-      c[k] = extra + __ldg(&Boff[ub + 1]) - __ldg(&Boff[ub]);
-    }
-    sum += c[k];
-  }
-  int32_t tot;
-  int32_t ex = block_excl_scan(sum, s.red32, &tot);
-#pragma unroll
-  for (int k = 0; k < kStatesPerThread; ++k) {
-    int i = threadIdx.x * kStatesPerThread + k;
-    if (i < nst) s.scan[i] = ex;
-    ex += c[k];
-  }
-  if (threadIdx.x == 0) s.scan[nst] = tot;
-  __syncthreads();
-  return tot;
-}
-
-__device__ __forceinline__ int item_state(const BlockSmem& s, int nst, int32_t item) {
-  // last state i with scan[i] <= item
-  int lo = 0, hi = nst - 1;
+__device__ __forceinline__ int32_t lower_bound_s(const int32_t* key, int32_t lo, int32_t hi, int32_t x) {
   while (lo < hi) {
-    int mid = (lo + hi + 1) >> 1;
-    if (s.scan[mid] <= item) lo = mid; else hi = mid - 1;
+    int32_t mid = (lo + hi) >> 1;
+    if (key[mid] < x) lo = mid + 1; else hi = mid;
   }
   return lo;
 }
 
-// Enumerate the moves of one item; f(va, vb, kind, ea, eb) with kind 1 = M1, 2 = M2, 3 = M3.
-// ea / eb are view positions.  Order: M2 item -> A eps prefix; B item -> M1 matches then M3.
-template <typename Fn>
-__device__ __forceinline__ void for_item_moves(const ViewDev& Av, const ViewDev& Bv, const BlockSmem& s,
-                                               int32_t ua, int32_t ub, int32_t k, int extra, Fn&& f) {
-  if (k < extra) {  // M2 item
-    for (int32_t ea = s.a0; ea < s.aeps; ++ea) f(__ldg(&Av.other[ea]), ub, 2, ea, -1);
-    return;
+// Mark a newly claimed pair in the next frontier: bits, chunk flag and list append.
+__device__ __forceinline__ void push_bits(const CompDev& C, int32_t row, int32_t col, int64_t gw, uint32_t bits,
+                                          uint32_t* __restrict__ Fn, uint32_t* __restrict__ flagn,
+                                          int32_t* __restrict__ listn, LevelCtrl* ctrln) {
+  atomicOr(&Fn[gw], bits);
+  const int64_t q = chunk_of(C, row, col);
+  if (*((volatile uint32_t*)&flagn[q]) == 0 && atomicExch(&flagn[q], 1u) == 0) {
+    unsigned long long pos = atomicAdd(&ctrln->count, 1ull);
+    listn[pos] = (int32_t)q;
   }
-  const int32_t eb = __ldg(&Bv.off[ub]) + (k - extra);
-  const int32_t lab = __ldg(&Bv.key[eb]);
-  const int32_t ob = __ldg(&Bv.other[eb]);
-  int32_t ea = lower_bound_key(Av.key, s.a0, s.a1, lab);
-  for (; ea < s.a1 && __ldg(&Av.key[ea]) == lab; ++ea) f(__ldg(&Av.other[ea]), ob, 1, ea, eb);
-  if (lab == FST_EPS) f(ua, ob, 3, -1, eb);
 }
 
-__device__ __forceinline__ void load_arow(BlockSmem& s, const ViewDev& Av, int32_t ua) {
+// ------------------------------------------------------------------------------ shared state
+struct TaskSmem {
+  uint32_t fw[kChunkMaxBlocks * 32];  // source bits of the chunk (frontier or V)
+  int32_t a_key[kAMax];
+  int32_t a_other[kAMax];
+  int32_t a_slot[kAMax];
+  int32_t a_carry[kAMax];
+  float a_w[kAMax];
+  unsigned long long labmask[64];     // labmask[l+1] = A-row positions with olabel l (l < 63)
+  int32_t slot_row[kSlotMax];
+  int32_t a0, a1, deg, aeps, m, arow_smem, dst_staged, small;
+  int32_t state[kPairsPerBlock];      // compacted source states of a sparse block (ascending u_b)
+  int32_t scan[kPairsPerBlock + 1];   // their item offsets
+  int32_t bwpre[33];
+  int32_t wtot[kWarps + 1];
+  int32_t red32[kWarps + 1];
+  unsigned long long keptb;
+  // label-major path: A-row label groups and their B segment ranges
+  int32_t G;                              // groups (0 = label-major path unavailable for this row)
+  int32_t g_label[kAMax + 1];
+  unsigned long long g_mask[kAMax + 1];   // A-row positions with the group's olabel
+  int32_t g_s0[kAMax + 1], g_s1[kAMax + 1];
+  int32_t g_lo[kAMax + 1];                // per block: first segment of the group in the block
+  int32_t g_pre[kAMax + 2];               // per block: item prefix over groups
+  int32_t cur[kPairsPerBlock + 1];        // emit: per-state arc cursor / count
+  int32_t nheavy;
+  unsigned long long keptc[kChunkMaxBlocks];  // per-block kept counts of the chunk (stage 2)
+};
+
+// Label groups of the staged A row, matched against B's label-major index (thread 0).
+__device__ void build_groups(TaskSmem& s, const ViewDev& Bv) {
+  if (threadIdx.x != 0) return;
+  s.G = 0;
+  if (!s.arow_smem) return;
+  const int nlab = Bv.nlab;
+  const bool b_has_eps = nlab > 0 && __ldg(&Bv.lab_val[0]) == FST_EPS;
+  int G = 0;
+  int k = 0;
+  if (b_has_eps && !(s.deg > 0 && s.a_key[0] == FST_EPS)) {  // eps group for M3 even without A eps arcs
+    s.g_label[G] = FST_EPS;
+    s.g_mask[G] = 0ull;
+    ++G;
+  }
+  while (k < s.deg) {
+    const int32_t lab = s.a_key[k];
+    unsigned long long m = 0ull;
+    while (k < s.deg && s.a_key[k] == lab) m |= 1ull << k++;
+    s.g_label[G] = lab;
+    s.g_mask[G] = m;
+    ++G;
+  }
+  int out = 0;
+  for (int g = 0; g < G; ++g) {  // keep groups whose label occurs in B
+    const int32_t lab = s.g_label[g];
+    int lo = 0, hi = nlab;
+    while (lo < hi) {
+      int mid = (lo + hi) >> 1;
+      if (__ldg(&Bv.lab_val[mid]) < lab) lo = mid + 1; else hi = mid;
+    }
+    if (lo < nlab && __ldg(&Bv.lab_val[lo]) == lab) {
+      s.g_label[out] = lab;
+      s.g_mask[out] = s.g_mask[g];
+      s.g_s0[out] = __ldg(&Bv.lab_seg[lo]);
+      s.g_s1[out] = __ldg(&Bv.lab_seg[lo + 1]);
+      ++out;
+    }
+  }
+  s.G = out > 0 ? out : -1;  // -1: label-major possible but nothing matches
+}
+
+// Segment ranges of every group for states [ub0, ub1); returns the total item count.
+__device__ __forceinline__ int block_groups(TaskSmem& s, const ViewDev& Bv, int32_t ub0, int32_t ub1) {
+  if ((int)threadIdx.x < s.G) {
+    const int g = threadIdx.x;
+    int lo = s.g_s0[g], hi = s.g_s1[g];
+    while (lo < hi) {
+      int mid = (lo + hi) >> 1;
+      if (__ldg(&Bv.seg_node[mid]) < ub0) lo = mid + 1; else hi = mid;
+    }
+    int lo2 = lo, hi2 = s.g_s1[g];
+    while (lo2 < hi2) {
+      int mid = (lo2 + hi2) >> 1;
+      if (__ldg(&Bv.seg_node[mid]) < ub1) lo2 = mid + 1; else hi2 = mid;
+    }
+    s.g_lo[g] = lo;
+    s.g_pre[g + 1] = lo2 - lo;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    s.g_pre[0] = 0;
+    for (int g = 0; g < s.G; ++g) s.g_pre[g + 1] += s.g_pre[g];
+  }
+  __syncthreads();
+  return s.G > 0 ? s.g_pre[s.G] : 0;
+}
+
+__device__ __forceinline__ int item_group(const TaskSmem& s, int i) {
+  int g = 0;
+  while (g + 1 < s.G && s.g_pre[g + 1] <= i) ++g;
+  return g;
+}
+
+// Stage the A row u_a of view Av: arcs (label-sorted), label masks, destination-row slots.
+// dst_words = shared words needed per destination row; staging succeeds iff m * dst_words fits.
+__device__ void stage_arow(TaskSmem& s, const CompDev& C, const ViewDev& Av, int32_t ua, int dst_words) {
   if (threadIdx.x == 0) {
     s.a0 = __ldg(&Av.off[ua]);
     s.a1 = __ldg(&Av.off[ua + 1]);
-    s.aeps = lower_bound_key(Av.key, s.a0, s.a1, 0);
+    s.deg = s.a1 - s.a0;
+    s.arow_smem = s.deg <= kAMax;
+    s.small = s.arow_smem && C.smallA;
+    s.aeps = 0;
   }
+  __syncthreads();
+  if (s.arow_smem) {
+    for (int k = threadIdx.x; k < s.deg; k += kThreads) {
+      s.a_key[k] = __ldg(&Av.key[s.a0 + k]);
+      s.a_other[k] = __ldg(&Av.other[s.a0 + k]);
+      s.a_carry[k] = __ldg(&Av.carry[s.a0 + k]);
+      s.a_w[k] = __ldg(&Av.w[s.a0 + k]);
+    }
+    if (threadIdx.x < 64) s.labmask[threadIdx.x] = 0ull;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (s.arow_smem) {
+      int aeps = 0;
+      while (aeps < s.deg && s.a_key[aeps] < 0) ++aeps;
+      s.aeps = aeps;
+      if (s.small)
+        for (int k = 0; k < s.deg; ++k) s.labmask[s.a_key[k] + 1] |= 1ull << k;
+      // destination-row slots: slot 0 = u_a (M3 moves), then distinct dst rows
+      int m = 1;
+      s.slot_row[0] = ua;
+      bool ok = true;
+      for (int k = 0; k < s.deg; ++k) {
+        int r = s.a_other[k], j = 0;
+        while (j < m && s.slot_row[j] != r) ++j;
+        if (j == m) {
+          if (m == kSlotMax) { ok = false; break; }
+          s.slot_row[m++] = r;
+        }
+        s.a_slot[k] = j;
+      }
+      s.m = m;
+      s.dst_staged = ok && (int64_t)m * dst_words <= kDynSmem / 4;
+      if (!ok) s.small = 0;  // slots incomplete: the fast paths need a slot for every A arc
+    } else {
+      s.aeps = lower_bound_g(Av.key, s.a0, s.a1, 0) - s.a0;
+      s.m = 0;
+      s.dst_staged = 0;
+    }
+  }
+  __syncthreads();
+}
+
+// One B-side item (a state's sentinel, or one of its B arcs) and its matching A arcs.
+struct Item {
+  unsigned long long mask;  // s.small: A-row positions of the matches
+  int32_t lo;               // otherwise: first matching A-row position
+  int32_t n;                // moves of the item (M2 | M1 [+ M3])
+  int32_t col;              // B-side destination: other end of the arc, u_b for the sentinel
+  int32_t it, ub;           // item index, source state
+  int32_t kind;             // 1 = arc (M1, then M3 if eps), 2 = sentinel (M2)
+  int32_t m3;
+};
+
+__device__ __forceinline__ Item make_item(const TaskSmem& s, const ViewDev& Av, int32_t it, int32_t ub, int2 kd,
+                                          bool valid) {
+  Item x;
+  x.mask = 0ull;
+  x.lo = 0;
+  x.n = 0;
+  x.col = kd.y;
+  x.it = it;
+  x.ub = ub;
+  x.kind = 1;
+  x.m3 = 0;
+  if (!valid) return x;
+  if (kd.x == kSentinel) {  // M2: A arcs with olabel eps, B stays
+    x.kind = 2;
+    x.col = ub;
+    if (s.small) {
+      x.mask = s.labmask[0];
+      x.n = __popcll(x.mask);
+    } else {
+      x.n = s.aeps;
+    }
+    return x;
+  }
+  const int32_t lab = kd.x;
+  if (s.small) {
+    x.mask = (lab + 1 < 64) ? s.labmask[lab + 1] : 0ull;
+    x.n = __popcll(x.mask);
+  } else if (s.arow_smem) {
+    x.lo = lower_bound_s(s.a_key, 0, s.deg, lab);
+    x.n = lower_bound_s(s.a_key, x.lo, s.deg, lab + 1) - x.lo;
+  } else {
+    const int32_t lo = lower_bound_g(Av.key, s.a0, s.a1, lab);
+    x.lo = lo - s.a0;
+    x.n = lower_bound_g(Av.key, lo, s.a1, lab + 1) - lo;
+  }
+  x.m3 = lab == FST_EPS;
+  x.n += x.m3;
+  return x;
+}
+
+// A candidate move: destination (row, col) (slot = staged destination-row index or -1), kind
+// 1 = M1, 2 = M2, 3 = M3, k = A-row position (-1 for M3), eb = B view position (-1 for M2).
+struct Cand {
+  int32_t slot, row, col, kind, k, eb;
+};
+
+__device__ __forceinline__ int kth_bit(unsigned long long m, int k) {
+  for (int i = 0; i < k; ++i) m &= m - 1;
+  return __ffsll((long long)m) - 1;
+}
+
+// The k-th move (0 <= k < x.n) of item x: M1/M2 matches in A-row order, then M3.
+__device__ __forceinline__ Cand item_move(const TaskSmem& s, const ViewDev& Av, int32_t ua, const Item& x, int k) {
+  Cand cd;
+  cd.col = x.col;
+  cd.eb = x.kind == 1 ? x.it - x.ub - 1 : -1;
+  if (k < x.n - x.m3) {
+    const int a = s.small ? kth_bit(x.mask, k) : x.lo + k;
+    cd.kind = x.kind;
+    cd.k = a;
+    if (s.arow_smem) {
+      cd.slot = s.a_slot[a];
+      cd.row = s.a_other[a];
+    } else {
+      cd.slot = -1;
+      cd.row = __ldg(&Av.other[s.a0 + a]);
+    }
+  } else {
+    cd.kind = 3;
+    cd.k = -1;
+    cd.slot = 0;
+    cd.row = ua;
+  }
+  return cd;
+}
+
+// Warp-cooperative expansion of the 32 lanes' items into rounds of (up to) 32 candidates, in item
+// order then match order.  f(active, cand, round) is called by ALL lanes every round (so it may use
+// warp ballots).  This keeps the candidate work convergent whatever the per-item match counts.
+template <typename F>
+__device__ __forceinline__ void warp_expand(const TaskSmem& s, const ViewDev& Av, int32_t ua, const Item& x, F&& f) {
+  const int lane = threadIdx.x & 31;
+  const int incl = warp_incl_scan(x.n);
+  const int start = incl - x.n;
+  const int total = __shfl_sync(0xffffffffu, incl, 31);
+  for (int r = 0; r < total; r += 32) {
+    const int c = r + lane;
+    int j = 0;
+#pragma unroll
+    for (int step = 16; step > 0; step >>= 1) {
+      const int sj = __shfl_sync(0xffffffffu, start, j + step);
+      if (sj <= c) j += step;
+    }
+    const int rank = c - __shfl_sync(0xffffffffu, start, j);
+    const unsigned mlo = __shfl_sync(0xffffffffu, (unsigned)x.mask, j);
+    const unsigned mhi = __shfl_sync(0xffffffffu, (unsigned)(x.mask >> 32), j);
+    const int lo = __shfl_sync(0xffffffffu, x.lo, j);
+    const int n = __shfl_sync(0xffffffffu, x.n, j);
+    const int m3 = __shfl_sync(0xffffffffu, x.m3, j);
+    const int col = __shfl_sync(0xffffffffu, x.col, j);
+    const int kind = __shfl_sync(0xffffffffu, x.kind, j);
+    const int it = __shfl_sync(0xffffffffu, x.it, j);
+    const int ub = __shfl_sync(0xffffffffu, x.ub, j);
+    const bool act = c < total;
+    Cand cd;
+    cd.col = col;
+    cd.eb = kind == 1 ? it - ub - 1 : -1;
+    if (act && rank < n - m3) {
+      const int k = s.small ? kth_bit(((unsigned long long)mhi << 32) | mlo, rank) : lo + rank;
+      cd.kind = kind == 2 ? 2 : 1;
+      cd.k = k;
+      if (s.arow_smem) {
+        cd.slot = s.a_slot[k];
+        cd.row = s.a_other[k];
+      } else {
+        cd.slot = -1;
+        cd.row = __ldg(&Av.other[s.a0 + k]);
+      }
+    } else {
+      cd.kind = 3;
+      cd.k = -1;
+      cd.slot = 0;
+      cd.row = ua;
+    }
+    f(act, cd, r);
+  }
+}
+
+// Source bits of the chunk -> s.fw (optionally consuming them).  Returns the popcount (all threads).
+__device__ __forceinline__ int load_chunk_bits(TaskSmem& s, uint32_t* bits, const CompDev& C, const Chunk& ch,
+                                               bool consume) {
+  const int w0 = ch.b0 * 32, w1 = min(ch.b1 * 32, C.wpr);
+  int cnt = 0;
+  for (int w = w0 + threadIdx.x; w < w1; w += kThreads) {
+    uint32_t x = bits[ch.rowW + w];
+    if (consume && x) bits[ch.rowW + w] = 0u;
+    s.fw[w - w0] = x;
+    cnt += __popc(x);
+  }
+  cnt = warp_sum(cnt);
+  if ((threadIdx.x & 31) == 0) s.red32[threadIdx.x >> 5] = cnt;
+  __syncthreads();
+  int tot = 0;
+  for (int i = 0; i < kWarps; ++i) tot += s.red32[i];
+  __syncthreads();
+  return tot;
+}
+
+// Number of source bits of block `blk` in s.fw (all threads; one barrier).
+__device__ __forceinline__ int block_popc(TaskSmem& s, const CompDev& C, const Chunk& ch, int32_t blk) {
+  const int lw0 = (blk - ch.b0) * 32;
+  const int nw = min(32, C.wpr - blk * 32);
+  if (threadIdx.x < 32) {
+    const int pc = threadIdx.x < nw ? __popc(s.fw[lw0 + threadIdx.x]) : 0;
+    const int t = warp_sum(pc);
+    if (threadIdx.x == 0) s.red32[kWarps] = t;
+  }
+  __syncthreads();
+  const int t = s.red32[kWarps];
+  __syncthreads();
+  return t;
+}
+
+__device__ __forceinline__ bool src_bit(const TaskSmem& s, int lw0, int32_t ub0, int32_t ub) {
+  return (s.fw[lw0 + ((ub - ub0) >> 5)] >> (ub & 31)) & 1u;
+}
+
+// Walk the items of block `blk` whose source state bit is set in s.fw.  Dense blocks stream the
+// contiguous item range of B's view; sparse blocks compact their states first.  g(valid, it, ub, kd)
+// is called by every thread in every round (uniform trip count; g may __syncthreads).
+template <typename G>
+__device__ __forceinline__ void for_block_items(TaskSmem& s, const ViewDev& Bv, const CompDev& C, const Chunk& ch,
+                                                int32_t blk, G&& g) {
+  const int lw0 = (blk - ch.b0) * 32;
+  const int nw = min(32, C.wpr - blk * 32);
+  const int32_t ub0 = blk * kPairsPerBlock;
+  const int32_t ub1 = min(ub0 + kPairsPerBlock, C.VB);
+  if (threadIdx.x < 32) {
+    uint32_t w = threadIdx.x < nw ? s.fw[lw0 + threadIdx.x] : 0u;
+    int pc = __popc(w);
+    int inc = warp_incl_scan(pc);
+    s.bwpre[threadIdx.x] = inc - pc;
+    if (threadIdx.x == 31) s.bwpre[32] = inc;
+  }
+  __syncthreads();
+  const int nst = s.bwpre[32];
+  if (nst == 0) return;
+  if (nst * 4 >= (ub1 - ub0)) {  // dense: stream every item of the block (next round prefetched)
+    const int32_t i0 = __ldg(&Bv.off[ub0]) + ub0;
+    const int32_t i1 = __ldg(&Bv.off[ub1]) + ub1;
+    int32_t it = i0 + threadIdx.x;
+    int2 kd = make_int2(0, 0);
+    int32_t ub = ub0;
+    if (it < i1) {
+      kd = __ldg(&Bv.ikd[it]);
+      ub = __ldg(&Bv.isrc[it]);
+    }
+    for (int32_t base = i0; base < i1; base += kThreads) {
+      const int32_t nit = it + kThreads;
+      int2 nkd = make_int2(0, 0);
+      int32_t nub = ub0;
+      if (nit < i1) {
+        nkd = __ldg(&Bv.ikd[nit]);
+        nub = __ldg(&Bv.isrc[nit]);
+      }
+      const bool valid = it < i1 && ((s.fw[lw0 + ((ub - ub0) >> 5)] >> (ub & 31)) & 1u);
+      g(valid, it, ub, kd);
+      it = nit;
+      kd = nkd;
+      ub = nub;
+    }
+  } else {  // sparse: compact the states, scan their item counts (1 sentinel + deg_B)
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int i = warp; i < nw; i += kWarps) {
+      uint32_t w = s.fw[lw0 + i];
+      if ((w >> lane) & 1u) s.state[s.bwpre[i] + __popc(w & ((1u << lane) - 1u))] = ub0 + i * 32 + lane;
+    }
+    __syncthreads();
+    int32_t c0 = 0, c1 = 0;
+    const int i0s = threadIdx.x * 2;
+    if (i0s < nst) { int32_t ub = s.state[i0s]; c0 = 1 + __ldg(&Bv.off[ub + 1]) - __ldg(&Bv.off[ub]); }
+    if (i0s + 1 < nst) { int32_t ub = s.state[i0s + 1]; c1 = 1 + __ldg(&Bv.off[ub + 1]) - __ldg(&Bv.off[ub]); }
+    int32_t tot;
+    int32_t ex = block_excl_scan(c0 + c1, s.red32, &tot);
+    if (i0s < nst) s.scan[i0s] = ex;
+    if (i0s + 1 < nst) s.scan[i0s + 1] = ex + c0;
+    if (threadIdx.x == 0) s.scan[nst] = tot;
+    __syncthreads();
+    for (int32_t base = 0; base < tot; base += kThreads) {
+      const int32_t li = base + threadIdx.x;
+      const bool valid = li < tot;
+      int2 kd = make_int2(0, 0);
+      int32_t ub = ub0, it = 0;
+      if (valid) {
+        int lo = 0, hi = nst - 1;
+        while (lo < hi) {
+          int mid = (lo + hi + 1) >> 1;
+          if (s.scan[mid] <= li) lo = mid; else hi = mid - 1;
+        }
+        ub = s.state[lo];
+        it = __ldg(&Bv.off[ub]) + ub + (li - s.scan[lo]);
+        kd = __ldg(&Bv.ikd[it]);
+      }
+      g(valid, it, ub, kd);
+    }
+  }
+  __syncthreads();
+}
+
+// ------------------------------------------------------------------------------ fast paths
+// Lean per-state walkers for the common case: A row staged with label masks (olabels < 63, <= 64
+// arcs) and the destination rows staged in shared memory.  One thread walks one state's B arcs
+// (packed (label, other) items); states with more than kHeavy arcs are walked by the whole CTA.
+
+// f(slot, col, kind, a, eb) for every move of state ub (M2, then per B arc: M1 matches, M3).
+template <typename F>
+__device__ __forceinline__ void fast_arc(const TaskSmem& s, int2 x, int32_t eb, F&& f) {
+  unsigned long long m = (unsigned)(x.x + 1) < 64u ? s.labmask[x.x + 1] : 0ull;
+  while (m) {
+    const int a = __ffsll((long long)m) - 1;
+    m &= m - 1;
+    f(s.a_slot[a], x.y, 1, a, eb);
+  }
+  if (x.x == FST_EPS) f(0, x.y, 3, -1, eb);
+}
+
+template <typename F>
+__device__ __forceinline__ void fast_state(const TaskSmem& s, const int2* __restrict__ ikd, int32_t ub, int32_t e,
+                                           int32_t e1, F&& f) {
+  for (int a = 0; a < s.aeps; ++a) f(s.a_slot[a], ub, 2, a, -1);
+  // items e .. e1-1 are the arcs (view positions e - ub - 1)
+  for (; e + 2 <= e1; e += 2) {
+    const int2 x0 = __ldg(&ikd[e]), x1 = __ldg(&ikd[e + 1]);
+    fast_arc(s, x0, e - ub - 1, f);
+    fast_arc(s, x1, e - ub, f);
+  }
+  if (e < e1) fast_arc(s, __ldg(&ikd[e]), e - ub - 1, f);
+}
+
+// BFS block: claims into the staged NEW bits.  Returns false (nothing done) never; heavy states are
+// walked cooperatively after the per-thread pass.
+template <bool kStage2>
+__device__ __forceinline__ void bfs_block_fast(TaskSmem& s, const ViewDev& Bv, int32_t ub0, int32_t ub1, int lw0,
+                                               int wpr, const uint32_t* Rs, const uint32_t* VS, uint32_t* NW,
+                                               unsigned& kept) {
+  const int2* __restrict__ ikd = Bv.ikd;
+  const int32_t* __restrict__ off = Bv.off;
+  auto cand = [&](int slot, int32_t col, int, int, int32_t) {
+    const int idx = slot * wpr + (col >> 5);
+    const uint32_t bit = 1u << (col & 31);
+    if (kStage2) {
+      if (!(Rs[idx] & bit)) return;
+      ++kept;
+    }
+    if ((VS[idx] | NW[idx]) & bit) return;
+    atomicOr(&NW[idx], bit);
+  };
+  if (threadIdx.x == 0) s.nheavy = 0;
+  __syncthreads();
+  for (int i = threadIdx.x; i < ub1 - ub0; i += kThreads) {
+    if (!((s.fw[lw0 + (i >> 5)] >> (i & 31)) & 1u)) continue;
+    const int32_t ub = ub0 + i;
+    const int32_t e = __ldg(&off[ub]) + ub + 1, e1 = __ldg(&off[ub + 1]) + ub + 1;
+    if (e1 - e > kHeavy) {
+      for (int a = 0; a < s.aeps; ++a) cand(s.a_slot[a], ub, 2, a, -1);
+      s.state[atomicAdd(&s.nheavy, 1)] = ub;
+      continue;
+    }
+    fast_state(s, ikd, ub, e, e1, cand);
+  }
+  __syncthreads();
+  for (int h = 0; h < s.nheavy; ++h) {
+    const int32_t ub = s.state[h];
+    const int32_t e0 = __ldg(&off[ub]) + ub + 1, e1 = __ldg(&off[ub + 1]) + ub + 1;
+    for (int32_t e = e0 + threadIdx.x; e < e1; e += kThreads) fast_arc(s, __ldg(&ikd[e]), e - ub - 1, cand);
+  }
+  __syncthreads();
+}
+
+
+// Whole-chunk BFS walk (fast path): one thread per source state of the chunk, no per-block barriers.
+// kStaged: candidates claimed in the staged NEW bits; else test-and-set on the global bitmaps.
+// Per-block kept counts (stage 2) are accumulated warp-aggregated in s.keptc[].
+template <bool kStage2, bool kStaged, typename Glob>
+__device__ __forceinline__ void bfs_chunk_fast(TaskSmem& s, const ViewDev& Bv, int32_t cub0, int32_t cub1, int wpr,
+                                               const uint32_t* Rs, const uint32_t* VS, uint32_t* NW, Glob&& glob) {
+  const int2* __restrict__ ikd = Bv.ikd;
+  const int32_t* __restrict__ off = Bv.off;
+  unsigned kept = 0;
+  auto cand = [&](int slot, int32_t col, int, int, int32_t) {
+    if (kStaged) {
+      const int idx = slot * wpr + (col >> 5);
+      const uint32_t bit = 1u << (col & 31);
+      if (kStage2) {
+        if (!(Rs[idx] & bit)) return;
+        ++kept;
+      }
+      if ((VS[idx] | NW[idx]) & bit) return;
+      atomicOr(&NW[idx], bit);
+    } else {
+      kept += glob(slot, col);
+    }
+  };
+  if (threadIdx.x == 0) s.nheavy = 0;
+  if (threadIdx.x < kChunkMaxBlocks) s.keptc[threadIdx.x] = 0ull;
+  __syncthreads();
+  const int n = cub1 - cub0;
+  for (int i0 = 0; i0 < n; i0 += kThreads) {  // uniform trip count: warps stay inside one block
+    const int i = i0 + threadIdx.x;
+    kept = 0;
+    if (i < n && ((s.fw[i >> 5] >> (i & 31)) & 1u)) {
+      const int32_t ub = cub0 + i;
+      const int32_t e = __ldg(&off[ub]) + ub + 1, e1 = __ldg(&off[ub + 1]) + ub + 1;
+      if (e1 - e > kHeavy) {
+        for (int a = 0; a < s.aeps; ++a) cand(s.a_slot[a], ub, 2, a, -1);
+        const int h = atomicAdd(&s.nheavy, 1);
+        if (h < kPairsPerBlock) s.state[h] = ub;
+        else fast_state(s, ikd, ub, e, e1, cand);  // list full: walk it here
+      } else {
+        fast_state(s, ikd, ub, e, e1, cand);
+      }
+    }
+    if (kStage2) {
+      const unsigned long long k = warp_sum((unsigned long long)kept);
+      if ((threadIdx.x & 31) == 0 && k) atomicAdd(&s.keptc[(i0 + (threadIdx.x & ~31)) >> 10], k);
+    }
+  }
+  __syncthreads();
+  const int nh = min(s.nheavy, kPairsPerBlock);
+  for (int h = 0; h < nh; ++h) {
+    const int32_t ub = s.state[h];
+    const int32_t e0 = __ldg(&off[ub]) + ub + 1, e1 = __ldg(&off[ub + 1]) + ub + 1;
+    kept = 0;
+    for (int32_t e = e0 + threadIdx.x; e < e1; e += kThreads) fast_arc(s, __ldg(&ikd[e]), e - ub - 1, cand);
+    if (kStage2) {
+      const unsigned long long k = warp_sum((unsigned long long)kept);
+      if ((threadIdx.x & 31) == 0 && k) atomicAdd(&s.keptc[(ub - cub0) >> 10], k);
+    }
+  }
+  __syncthreads();
 }
 
 // ------------------------------------------------------------------------------ seeds
@@ -233,32 +687,36 @@ template <bool kStage2>
 __global__ void k_seed(Ctx cx) {
   const int64_t total = cx.seedbase[cx.ncomp];
   uint32_t* vis = kStage2 ? cx.V : cx.R;
-  unsigned kept = 0, nnew = 0;
+  unsigned nnew = 0;
   for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < total; g += (int64_t)gridDim.x * blockDim.x) {
-    int c = 0;
-    {
-      int lo = 0, hi = cx.ncomp - 1;
-      while (lo < hi) {
-        int mid = (lo + hi + 1) >> 1;
-        if (cx.seedbase[mid] <= g) lo = mid; else hi = mid - 1;
-      }
-      c = lo;
+    int lo = 0, hi = cx.ncomp - 1;
+    while (lo < hi) {
+      int mid = (lo + hi + 1) >> 1;
+      if (cx.seedbase[mid] <= g) lo = mid; else hi = mid - 1;
     }
-    const CompDev& C = cx.comps[c];
-    int64_t i = g - cx.seedbase[c];
+    const CompDev& C = cx.comps[lo];
+    int64_t i = g - cx.seedbase[lo];
     int32_t nb = kStage2 ? C.nStartB : C.nAccB;
     int32_t va = kStage2 ? C.startListA[i / nb] : C.accListA[i / nb];
     int32_t vb = kStage2 ? C.startListB[i % nb] : C.accListB[i % nb];
-    visit<kStage2>(C, va, vb, vis, cx.R, cx.F0, cx.flag0, cx.list0, &cx.ctrl[0], kept, nnew);
+    const int64_t gw = C.W + (int64_t)va * C.wpr + (vb >> 5);
+    const uint32_t bit = 1u << (vb & 31);
+    if (kStage2 && !(cx.R[gw] & bit)) continue;
+    if (atomicOr(&vis[gw], bit) & bit) continue;
+    ++nnew;
+    push_bits(C, va, vb, gw, bit, cx.F0, cx.flag0, cx.list0, &cx.ctrl[0]);
   }
   nnew = warp_sum(nnew);
   if ((threadIdx.x & 31) == 0 && nnew) atomicAdd(&cx.ctrl[0].nnew, (unsigned long long)nnew);
 }
 
 // ------------------------------------------------------------------------------ one BFS level
-template <bool kForward>
-__global__ void __launch_bounds__(kThreads) k_expand(Ctx cx, int level) {
-  __shared__ BlockSmem s;
+// kStage2 = false: backward BFS over in-views, visited set R.
+// kStage2 = true : forward BFS over out-views, filter R, visited set V, per-block kept counts.
+template <bool kStage2>
+__global__ void __launch_bounds__(kThreads, 2) k_level(Ctx cx, int level) {
+  __shared__ TaskSmem s;
+  extern __shared__ uint32_t dyn[];
   const int p = level & 1;
   LevelCtrl* ctrl_cur = &cx.ctrl[level % 3];
   LevelCtrl* ctrl_nxt = &cx.ctrl[(level + 1) % 3];
@@ -268,7 +726,7 @@ __global__ void __launch_bounds__(kThreads) k_expand(Ctx cx, int level) {
   uint32_t* flagn = p ? cx.flag0 : cx.flag1;
   const int32_t* listc = p ? cx.list1 : cx.list0;
   int32_t* listn = p ? cx.list0 : cx.list1;
-  uint32_t* vis = kForward ? cx.V : cx.R;
+  uint32_t* vis = kStage2 ? cx.V : cx.R;
   const unsigned long long nlist = *((volatile unsigned long long*)&ctrl_cur->count);
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     LevelCtrl* z = &cx.ctrl[(level + 2) % 3];
@@ -281,41 +739,156 @@ __global__ void __launch_bounds__(kThreads) k_expand(Ctx cx, int level) {
   }
   unsigned nnew = 0;
   for (unsigned long long e = blockIdx.x; e < nlist; e += gridDim.x) {
-    const int64_t blk = listc[e];
-    const BlockInfo bi = decode_block(cx, blk);
-    const CompDev& C = cx.comps[bi.comp];
-    const ViewDev& Av = kForward ? C.Af : C.Ab;
-    const ViewDev& Bv = kForward ? C.Bf : C.Bb;
-    load_words(s, Fc, bi, true);
-    load_arow(s, Av, bi.ua);
-    if (threadIdx.x == 0) flagc[blk] = 0u;
-    __syncthreads();
-    const int nst = s.wpre[32];
-    const int extra = s.aeps > s.a0 ? 1 : 0;
-    compact_bits(s, bi.ub0);
-    __syncthreads();
-    const int32_t total = scan_items(s, nst, Bv.off, extra);
+    const int64_t q = listc[e];
+    const Chunk ch = decode_chunk(cx, q);
+    const CompDev& C = cx.comps[ch.comp];
+    const ViewDev& Av = kStage2 ? C.Af : C.Ab;
+    const ViewDev& Bv = kStage2 ? C.Bf : C.Bb;
+    if (threadIdx.x == 0) flagc[q] = 0u;
+    const int nst = load_chunk_bits(s, Fc, C, ch, true);
+    if (nst == 0) continue;
+    const int wpr = C.wpr;
+    const int per_word = kStage2 ? 3 : 2;  // R, V-snapshot, NEW  |  R-snapshot, NEW
+    stage_arow(s, C, Av, ch.ua, per_word * wpr);
+    // stage destination rows only when the chunk has enough work to amortise the staging traffic
+    const bool staged = s.dst_staged && (int64_t)nst * 16 >= (int64_t)s.m * wpr;
+    uint32_t* Rs = dyn;
+    uint32_t* VS = kStage2 ? dyn + s.m * wpr : dyn;
+    uint32_t* NW = VS + s.m * wpr;
+    if (staged) {
+      const int m = s.m;
+      for (int i = threadIdx.x; i < m * wpr; i += kThreads) {
+        const int r = i / wpr, w = i - r * wpr;
+        const int64_t gw = C.W + (int64_t)s.slot_row[r] * wpr + w;
+        if (kStage2) {
+          Rs[i] = __ldg(&cx.R[gw]);
+          VS[i] = cx.V[gw];
+        } else {
+          VS[i] = cx.R[gw];
+        }
+        NW[i] = 0u;
+      }
+      __syncthreads();
+    }
     unsigned kept = 0;
-    for (int32_t base = 0; base < total; base += kThreads) {
-      const int32_t it = base + threadIdx.x;
-      if (it < total) {
-        const int st = item_state(s, nst, it);
-        const int32_t ub = s.state[st];
-        for_item_moves(Av, Bv, s, bi.ua, ub, it - s.scan[st], extra,
-                       [&](int32_t va, int32_t vb, int, int32_t, int32_t) {
-                         visit<kForward>(C, va, vb, vis, cx.R, Fn, flagn, listn, ctrl_nxt, kept, nnew);
-                       });
+    auto sink = [&](bool act, const Cand& c, int) {
+      if (!act) return;
+      const uint32_t bit = 1u << (c.col & 31);
+      if (staged) {
+        const int i = c.slot * wpr + (c.col >> 5);
+        if (kStage2) {
+          if (!(Rs[i] & bit)) return;
+          ++kept;
+        }
+        if ((VS[i] | NW[i]) & bit) return;
+        atomicOr(&NW[i], bit);
+      } else {
+        const int64_t gw = C.W + (int64_t)c.row * wpr + (c.col >> 5);
+        if (kStage2) {
+          if (!(__ldg(&cx.R[gw]) & bit)) return;
+          ++kept;
+        }
+        if (vis[gw] & bit) return;  // test before the atomic (bits only get set)
+        if (atomicOr(&vis[gw], bit) & bit) return;
+        ++nnew;
+        push_bits(C, c.row, c.col, gw, bit, Fn, flagn, listn, ctrl_nxt);
+      }
+    };
+    if (s.small) {  // fast path: whole chunk in one barrier-free pass
+      const int32_t cub0 = ch.b0 * kPairsPerBlock, cub1 = min(ch.b1 * kPairsPerBlock, C.VB);
+      if (staged) {
+        bfs_chunk_fast<kStage2, true>(s, Bv, cub0, cub1, wpr, Rs, VS, NW, [](int, int32_t) { return 0u; });
+      } else {
+        bfs_chunk_fast<kStage2, false>(s, Bv, cub0, cub1, wpr, Rs, VS, NW, [&](int slot, int32_t col) -> unsigned {
+          const int32_t row = s.slot_row[slot];
+          const int64_t gw = C.W + (int64_t)row * wpr + (col >> 5);
+          const uint32_t bit = 1u << (col & 31);
+          unsigned k = 0;
+          if (kStage2) {
+            if (!(__ldg(&cx.R[gw]) & bit)) return 0u;
+            k = 1;
+          }
+          if (vis[gw] & bit) return k;
+          if (atomicOr(&vis[gw], bit) & bit) return k;
+          ++nnew;
+          push_bits(C, row, col, gw, bit, Fn, flagn, listn, ctrl_nxt);
+          return k;
+        });
+      }
+      if (kStage2 && (int)threadIdx.x < ch.b1 - ch.b0 && s.keptc[threadIdx.x])
+        cx.kept[C.K + (int64_t)ch.ua * C.bpr + ch.b0 + threadIdx.x] += s.keptc[threadIdx.x];
+    }
+    build_groups(s, Bv);
+    __syncthreads();
+    for (int32_t blk = s.small ? ch.b1 : ch.b0; blk < ch.b1; ++blk) {
+      kept = 0;
+      const int32_t ub0 = blk * kPairsPerBlock, ub1 = min(ub0 + kPairsPerBlock, C.VB);
+      const int lw0 = (blk - ch.b0) * 32;
+      const int nb = block_popc(s, C, ch, blk);
+      if (nb == 0) continue;
+      if (s.G != 0 && nb * 4 >= ub1 - ub0) {
+        // dense block, label-major: only B arcs whose label occurs in the A row
+        const int total = block_groups(s, Bv, ub0, ub1);
+        if (s.aeps > 0) {  // M2 moves of every source state
+          for (int32_t ub = ub0 + threadIdx.x; ub < ub1; ub += kThreads)
+            if (src_bit(s, lw0, ub0, ub))
+              for (int a = 0; a < s.aeps; ++a) sink(true, Cand{s.a_slot[a], s.a_other[a], ub, 2, a, -1}, 0);
+        }
+        for (int i = threadIdx.x; i < total; i += kThreads) {
+          const int g = item_group(s, i);
+          const int32_t sid = s.g_lo[g] + (i - s.g_pre[g]);
+          const int32_t ub = __ldg(&Bv.seg_node[sid]);
+          if (!src_bit(s, lw0, ub0, ub)) continue;
+          const int32_t e0 = __ldg(&Bv.seg_beg[sid]), e1 = __ldg(&Bv.seg_beg[sid + 1]);
+          const unsigned long long gm = s.g_mask[g];
+          const bool eps = s.g_label[g] == FST_EPS;
+          for (int32_t j = e0; j < e1; ++j) {
+            const int32_t ob = __ldg(&Bv.lm_other[j]);
+            for (unsigned long long m = gm; m; m &= m - 1) {
+              const int a = __ffsll((long long)m) - 1;
+              sink(true, Cand{s.a_slot[a], s.a_other[a], ob, 1, a, -1}, 0);
+            }
+            if (eps) sink(true, Cand{0, ch.ua, ob, 3, -1, -1}, 0);
+          }
+        }
+        __syncthreads();
+      } else
+      for_block_items(s, Bv, C, ch, blk, [&](bool valid, int32_t it, int32_t ub, int2 kd) {
+        const Item x = make_item(s, Av, it, ub, kd, valid);
+        const int maxn = __reduce_max_sync(0xffffffffu, (unsigned)x.n);
+        if (maxn <= kSimpleMoves) {  // few moves per item: every lane walks its own
+          for (int k = 0; k < maxn; ++k)
+            if (k < x.n) sink(true, item_move(s, Av, ch.ua, x, k), 0);
+        } else {
+          warp_expand(s, Av, ch.ua, x, sink);
+        }
+      });
+      if (kStage2) {  // pass-1 arc count of this block
+        if (threadIdx.x == 0) s.keptb = 0ull;
+        __syncthreads();
+        unsigned long long k = warp_sum((unsigned long long)kept);
+        if ((threadIdx.x & 31) == 0 && k) atomicAdd(&s.keptb, k);
+        __syncthreads();
+        if (threadIdx.x == 0 && s.keptb) cx.kept[C.K + (int64_t)ch.ua * C.bpr + blk] += s.keptb;
+        __syncthreads();
       }
     }
-    if (kForward) {  // pass-1 arc count of this block
-      unsigned long long k = warp_sum((unsigned long long)kept);
-      if ((threadIdx.x & 31) == 0) s.red[threadIdx.x >> 5] = k;
+    if (staged) {  // merge the claimed bits into the global visited / frontier bitmaps
       __syncthreads();
-      if (threadIdx.x == 0) {
-        unsigned long long t = 0;
-        for (int w = 0; w < kThreads / 32; ++w) t += s.red[w];
-        cx.kept[blk] += t;
+      const int m = s.m;
+      for (int i = threadIdx.x; i < m * wpr; i += kThreads) {
+        const uint32_t nb = NW[i];
+        if (!nb) continue;
+        const int r = i / wpr, w = i - r * wpr;
+        const int32_t row = s.slot_row[r];
+        const int64_t gw = C.W + (int64_t)row * wpr + w;
+        const uint32_t win = nb & ~atomicOr(&vis[gw], nb);
+        if (win) {
+          nnew += __popc(win);
+          push_bits(C, row, w * 32, gw, win, Fn, flagn, listn, ctrl_nxt);
+        }
       }
+      if (threadIdx.x == 0) atomicAdd(&cx.misc[3], 1ull);
     }
     __syncthreads();
   }
@@ -329,11 +902,17 @@ __global__ void k_block_counts(Ctx cx) {
   const int lane = threadIdx.x & 31;
   const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
   for (int64_t blk = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); blk < cx.nblocks; blk += warps) {
-    const BlockInfo bi = decode_block(cx, blk);
-    uint32_t w = lane < bi.nwords ? cx.V[bi.word0 + lane] : 0u;
+    int c = cx.ncomp == 1 ? 0 : find_comp(cx.comps, cx.ncomp, blk);
+    const CompDev& C = cx.comps[c];
+    const int64_t local = blk - C.K;
+    const int32_t ua = (int32_t)(local / C.bpr);
+    const int32_t j = (int32_t)(local - (int64_t)ua * C.bpr);
+    const int nw = min(32, C.wpr - j * 32);
+    const int64_t w0 = C.W + (int64_t)ua * C.wpr + (int64_t)j * 32;
+    uint32_t w = lane < nw ? cx.V[w0 + lane] : 0u;
     int pc = __popc(w);
     int inc = warp_incl_scan(pc);
-    if (lane < bi.nwords) cx.wpre[bi.word0 + lane] = (uint16_t)(inc - pc);
+    if (lane < nw) cx.wpre[w0 + lane] = (uint16_t)(inc - pc);
     if (lane == 31) cx.vcount[blk] = inc;
   }
 }
@@ -366,106 +945,400 @@ __global__ void k_finish_rowptr(Ctx cx, const int64_t* __restrict__ tot) {
 
 // ------------------------------------------------------------------------------ emit
 // Writes the composed CSR: per state (pair_a, pair_b, flags, row_ptr), per arc (dst id, labels,
-// weight).  Arc slots = block arc base + CTA running prefix (deterministic; no cursor atomics).
-__global__ void __launch_bounds__(kThreads) k_emit(Ctx cx, const int64_t* __restrict__ tot) {
-  __shared__ BlockSmem s;
-  for (int64_t blk = blockIdx.x; blk < cx.nblocks; blk += gridDim.x) {
-    if (cx.vcount[blk] == 0) continue;
-    const BlockInfo bi = decode_block(cx, blk);
-    const CompDev& C = cx.comps[bi.comp];
+// weight).  Per round of kThreads items: phase 1 counts each warp's kept moves, a CTA prefix over
+// the warp totals gives every warp its slot base, phase 2 re-expands and writes the kept moves at
+// consecutive slots (warp ballots; coalesced streaming stores).  Slots = block arc base + running
+// prefix in (state, item, match) order: deterministic, no cursor atomics.
+__global__ void __launch_bounds__(kThreads, 2) k_emit(Ctx cx, const int64_t* __restrict__ tot) {
+  __shared__ TaskSmem s;
+  extern __shared__ uint32_t dyn[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int64_t q = blockIdx.x; q < cx.nchunks; q += gridDim.x) {
+    const Chunk ch = decode_chunk(cx, q);
+    const CompDev& C = cx.comps[ch.comp];
+    const int64_t kb0 = C.K + (int64_t)ch.ua * C.bpr;  // global block index of (ua, block 0)
+    if (cx.idbase[kb0 + ch.b1] == cx.idbase[kb0 + ch.b0]) continue;  // no states in the chunk
     const ViewDev& Av = C.Af;
     const ViewDev& Bv = C.Bf;
-    const int64_t id_comp = tot[2 * bi.comp];
-    const int64_t arc_comp = tot[2 * bi.comp + 1];
-    load_words(s, cx.V, bi, false);
-    load_arow(s, Av, bi.ua);
-    __syncthreads();
-    const int nst = s.wpre[32];
-    compact_bits(s, bi.ub0);
-    __syncthreads();
-    const int32_t total = scan_items(s, nst, Bv.off, 1);
-    const int64_t id0 = cx.idbase[blk] - id_comp;
-    int64_t run = cx.arcbase[blk] - arc_comp;  // running arc slot of this CTA
-    const int64_t run0 = run;
-    const int32_t ua = bi.ua;
-    auto kept_of = [&](int32_t va, int32_t vb) -> bool {
-      const int64_t w = C.W + (int64_t)va * C.wpr + (vb >> 5);
-      return (__ldg(&cx.V[w]) >> (vb & 31)) & 1u;
-    };
-    for (int32_t base = 0; base < total; base += kThreads) {
-      const int32_t it = base + threadIdx.x;
-      int st = 0;
-      int32_t ub = 0, k = 0;
-      unsigned cnt = 0;
-      if (it < total) {
-        st = item_state(s, nst, it);
-        ub = s.state[st];
-        k = it - s.scan[st];
-        for_item_moves(Av, Bv, s, ua, ub, k, 1, [&](int32_t va, int32_t vb, int, int32_t, int32_t) {
-          cnt += kept_of(va, vb);
-        });
+    const int64_t id_comp = tot[2 * ch.comp];
+    const int64_t arc_comp = tot[2 * ch.comp + 1];
+    const int wpr = C.wpr;
+    load_chunk_bits(s, cx.V, C, ch, false);
+    stage_arow(s, C, Av, ch.ua, 2 * wpr);
+    const bool staged = s.dst_staged;
+    uint32_t* Vs = dyn;                           // V words of the staged rows
+    int32_t* RB = (int32_t*)(dyn + s.m * wpr);    // rank base of every staged word
+    if (staged) {
+      for (int i = threadIdx.x; i < s.m * wpr; i += kThreads) {
+        const int r = i / wpr, w = i - r * wpr;
+        const int32_t row = s.slot_row[r];
+        const int64_t gw = C.W + (int64_t)row * wpr + w;
+        Vs[i] = __ldg(&cx.V[gw]);
+        const int64_t blk = C.K + (int64_t)row * C.bpr + (w >> 5);
+        RB[i] = (int32_t)(__ldg(&cx.idbase[blk]) - id_comp + __ldg(&cx.wpre[gw]));
       }
-      unsigned long long tot_chunk;
-      unsigned long long ex = block_excl_scan((unsigned long long)cnt, s.red, &tot_chunk);
-      if (it < total) {
-        int64_t pos = run + (int64_t)ex;
-        if (k == 0) {  // the state's first item: per-state outputs
-          const int64_t id = id0 + st;
-          C.row_ptr[id] = pos;
-          C.pair_a[id] = ua;
-          C.pair_b[id] = ub;
-          C.is_start[id] = (uint8_t)(__ldg(&C.startA[ua]) & __ldg(&C.startB[ub]));
-          C.is_accept[id] = (uint8_t)(__ldg(&C.accA[ua]) & __ldg(&C.accB[ub]));
-        }
-        for_item_moves(Av, Bv, s, ua, ub, k, 1, [&](int32_t va, int32_t vb, int kind, int32_t ea, int32_t eb) {
-          const int64_t w = C.W + (int64_t)va * C.wpr + (vb >> 5);
-          const uint32_t word = __ldg(&cx.V[w]);
-          if (!((word >> (vb & 31)) & 1u)) return;
-          const int64_t vblk = C.K + (int64_t)va * C.bpr + (vb >> 10);
-          const int64_t did = __ldg(&cx.idbase[vblk]) - id_comp + __ldg(&cx.wpre[w]) +
-                              __popc(word & ((1u << (vb & 31)) - 1u));
-          int32_t il, ol;
-          float wt;
-          if (kind == 1) {
-            il = __ldg(&Av.carry[ea]);
-            ol = __ldg(&Bv.carry[eb]);
-            wt = __fadd_rn(__ldg(&Av.w[ea]), __ldg(&Bv.w[eb]));  // one IEEE binary32 add, RN-even
-          } else if (kind == 2) {
-            il = __ldg(&Av.carry[ea]);
-            ol = FST_EPS;
-            wt = __ldg(&Av.w[ea]);  // bit copy
-          } else {
-            il = FST_EPS;
-            ol = __ldg(&Bv.carry[eb]);
-            wt = __ldg(&Bv.w[eb]);
-          }
-          C.dst[pos] = (int32_t)did;
-          C.ilabel[pos] = il;
-          C.olabel[pos] = ol;
-          C.weight[pos] = wt;
-          ++pos;
-        });
-      }
-      run += (int64_t)tot_chunk;
+      __syncthreads();
     }
-    if (threadIdx.x == 0 && (unsigned long long)(run - run0) != cx.kept[blk]) atomicAdd(&cx.misc[2], 1ull);
+    // state id of pair (row, col) inside its composition; present = the pair is a state of C
+    auto rank_of = [&](int slot, int32_t row, int32_t col, bool& present) -> int32_t {
+      const uint32_t bit = 1u << (col & 31);
+      const uint32_t lowmask = bit - 1u;
+      if (staged) {
+        const int i = slot * wpr + (col >> 5);
+        const uint32_t w = Vs[i];
+        present = w & bit;
+        return RB[i] + __popc(w & lowmask);
+      }
+      const int64_t gw = C.W + (int64_t)row * wpr + (col >> 5);
+      const uint32_t w = __ldg(&cx.V[gw]);
+      present = w & bit;
+      if (!present) return 0;
+      const int64_t blk = C.K + (int64_t)row * C.bpr + (col >> 10);
+      return (int32_t)(__ldg(&cx.idbase[blk]) - id_comp + __ldg(&cx.wpre[gw]) + __popc(w & lowmask));
+    };
+    const int32_t ua = ch.ua;
+    const uint8_t stA = __ldg(&C.startA[ua]), acA = __ldg(&C.accA[ua]);
+    auto emit_arc = [&](const Cand& c, int64_t pos) {
+      bool pr;
+      const int32_t did = rank_of(c.slot, c.row, c.col, pr);
+      int32_t il, ol;
+      float wt;
+      if (c.kind == 1) {
+        const int2 b = __ldg(&Bv.cw[c.eb]);
+        il = __ldg(&Av.carry[s.a0 + c.k]);
+        ol = b.x;
+        wt = __fadd_rn(__ldg(&Av.w[s.a0 + c.k]), __int_as_float(b.y));  // one binary32 add, RN-even
+      } else if (c.kind == 2) {
+        il = __ldg(&Av.carry[s.a0 + c.k]);
+        ol = FST_EPS;
+        wt = __ldg(&Av.w[s.a0 + c.k]);  // bit copy
+      } else {
+        const int2 b = __ldg(&Bv.cw[c.eb]);
+        il = FST_EPS;
+        ol = b.x;
+        wt = __int_as_float(b.y);  // bit copy
+      }
+      __stcs(&C.dst[pos], did);
+      __stcs(&C.ilabel[pos], il);
+      __stcs(&C.olabel[pos], ol);
+      __stcs(&C.weight[pos], wt);
+    };
+    build_groups(s, Bv);
+    __syncthreads();
+    for (int32_t blk = ch.b0; blk < ch.b1; ++blk) {
+      const int64_t gblk = kb0 + blk;
+      if (cx.vcount[gblk] == 0) continue;
+      int64_t run = cx.arcbase[gblk] - arc_comp;
+      const int64_t run0 = run;
+      const int32_t ub0 = blk * kPairsPerBlock, ub1 = min(ub0 + kPairsPerBlock, C.VB);
+      const int lw0 = (blk - ch.b0) * 32;
+      bool fastE = staged && s.small && (2 * s.m * wpr + kWarps * kWCap * 4) * 4 <= kDynSmem;
+      if (fastE) {  // the per-thread walk is only used when no state of the block is heavy
+        int hv = 0;
+        for (int i = threadIdx.x; i < ub1 - ub0; i += kThreads)
+          if (src_bit(s, lw0, ub0, ub0 + i) && __ldg(&Bv.off[ub0 + i + 1]) - __ldg(&Bv.off[ub0 + i]) > kHeavy) hv = 1;
+        fastE = !__syncthreads_or(hv);
+      }
+      if (fastE) {
+        const int2* __restrict__ ikd = Bv.ikd;
+        const int32_t* __restrict__ boff = Bv.off;
+        const int2* __restrict__ bcw = Bv.cw;
+        const int nub = ub1 - ub0;
+        auto present = [&](int slot, int32_t col) -> bool {
+          return (Vs[slot * wpr + (col >> 5)] >> (col & 31)) & 1u;
+        };
+        // count: states 2t, 2t+1 of thread t
+        int c2[2] = {0, 0};
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          const int i = 2 * threadIdx.x + j;
+          if (i < nub && src_bit(s, lw0, ub0, ub0 + i)) {
+            const int32_t ub = ub0 + i;
+            int c = 0;
+            fast_state(s, ikd, ub, __ldg(&boff[ub]) + ub + 1, __ldg(&boff[ub + 1]) + ub + 1,
+                       [&](int slot, int32_t col, int, int, int32_t) { c += present(slot, col); });
+            c2[j] = c;
+          }
+        }
+        int btot;
+        const int ex = block_excl_scan(c2[0] + c2[1], s.red32, &btot);
+        s.cur[2 * threadIdx.x] = ex;
+        s.cur[2 * threadIdx.x + 1] = ex + c2[0];
+        if (threadIdx.x == 0) {
+          s.cur[kPairsPerBlock] = btot;
+          if ((unsigned long long)btot != cx.kept[gblk]) atomicAdd(&cx.misc[2], 1ull);
+        }
+        __syncthreads();
+        // write: warp w owns states [64w, 64w+64) in two rounds of 32; its arcs are contiguous and are
+        // staged per window of kWCap slots in shared memory, then stored coalesced
+        uint32_t* wb = dyn + 2 * s.m * wpr + warp * kWCap * 4;
+        int32_t* bd = (int32_t*)wb;
+        int32_t* bi = (int32_t*)(wb + kWCap);
+        int32_t* bo = (int32_t*)(wb + 2 * kWCap);
+        float* bw = (float*)(wb + 3 * kWCap);
+        for (int r = 0; r < 2; ++r) {
+          const int first = warp * 64 + r * 32;
+          const int i = first + lane;
+          const int32_t ub = ub0 + i;
+          const bool has = i < nub && src_bit(s, lw0, ub0, ub);
+          const int q0 = s.cur[first], q1 = s.cur[first + 32];
+          const int my0 = s.cur[i], my1 = s.cur[i + 1];
+          if (has) {  // per-state outputs
+            bool pr;
+            const int32_t id = rank_of(0, ua, ub, pr);
+            __stcs((long long*)&C.row_ptr[id], (long long)(run + my0));
+            __stcs(&C.pair_a[id], ua);
+            __stcs(&C.pair_b[id], ub);
+            C.is_start[id] = (uint8_t)(stA & __ldg(&C.startB[ub]));
+            C.is_accept[id] = (uint8_t)(acA & __ldg(&C.accB[ub]));
+          }
+          for (int win = q0; win < q1; win += kWCap) {
+            if (has && my1 > win && my0 < win + kWCap) {
+              int p = my0;
+              fast_state(s, ikd, ub, __ldg(&boff[ub]) + ub + 1, __ldg(&boff[ub + 1]) + ub + 1,
+                         [&](int slot, int32_t col, int kind, int a, int32_t eb) {
+                           bool pr;
+                           const int32_t did = rank_of(slot, 0, col, pr);
+                           if (!pr) return;
+                           const int t = p - win;
+                           ++p;
+                           if (t < 0 || t >= kWCap) return;
+                           int32_t il, ol;
+                           float wt;
+                           if (kind == 1) {
+                             const int2 b = __ldg(&bcw[eb]);
+                             il = s.a_carry[a];
+                             ol = b.x;
+                             wt = __fadd_rn(s.a_w[a], __int_as_float(b.y));  // one binary32 add, RN-even
+                           } else if (kind == 2) {
+                             il = s.a_carry[a];
+                             ol = FST_EPS;
+                             wt = s.a_w[a];  // bit copy
+                           } else {
+                             const int2 b = __ldg(&bcw[eb]);
+                             il = FST_EPS;
+                             ol = b.x;
+                             wt = __int_as_float(b.y);  // bit copy
+                           }
+                           bd[t] = did;
+                           bi[t] = il;
+                           bo[t] = ol;
+                           bw[t] = wt;
+                         });
+            }
+            __syncwarp();
+            const int n = min(kWCap, q1 - win);
+            for (int t = lane; t < n; t += 32) {
+              const int64_t pos = run + win + t;
+              __stcs(&C.dst[pos], bd[t]);
+              __stcs(&C.ilabel[pos], bi[t]);
+              __stcs(&C.olabel[pos], bo[t]);
+              __stcs(&C.weight[pos], bw[t]);
+            }
+            __syncwarp();
+          }
+        }
+        run += btot;
+        __syncthreads();
+      } else if (s.G != 0 && cx.vcount[gblk] * 4 >= ub1 - ub0) {
+        // dense block, label-major.  count: per-state kept moves (M2 first, then the groups)
+        const int total = block_groups(s, Bv, ub0, ub1);
+        for (int i = threadIdx.x; i < kPairsPerBlock; i += kThreads) {
+          const int32_t ub = ub0 + i;
+          int c = 0;
+          if (ub < ub1 && src_bit(s, lw0, ub0, ub)) {
+            for (int a = 0; a < s.aeps; ++a) {
+              bool pr;
+              rank_of(s.a_slot[a], s.a_other[a], ub, pr);
+              c += pr;
+            }
+          }
+          s.cur[i] = c;
+        }
+        __syncthreads();
+        for (int i = threadIdx.x; i < total; i += kThreads) {
+          const int g = item_group(s, i);
+          const int32_t sid = s.g_lo[g] + (i - s.g_pre[g]);
+          const int32_t ub = __ldg(&Bv.seg_node[sid]);
+          if (!src_bit(s, lw0, ub0, ub)) continue;
+          const int32_t e0 = __ldg(&Bv.seg_beg[sid]), e1 = __ldg(&Bv.seg_beg[sid + 1]);
+          const unsigned long long gm = s.g_mask[g];
+          const bool eps = s.g_label[g] == FST_EPS;
+          int c = 0;
+          for (int32_t j = e0; j < e1; ++j) {
+            const int32_t ob = __ldg(&Bv.lm_other[j]);
+            for (unsigned long long m = gm; m; m &= m - 1) {
+              const int a = __ffsll((long long)m) - 1;
+              bool pr;
+              rank_of(s.a_slot[a], s.a_other[a], ob, pr);
+              c += pr;
+            }
+            if (eps) {
+              bool pr;
+              rank_of(0, ua, ob, pr);
+              c += pr;
+            }
+          }
+          if (c) atomicAdd(&s.cur[ub - ub0], c);
+        }
+        __syncthreads();
+        // exclusive scan of the per-state counts -> state start offsets
+        const int i0 = 2 * threadIdx.x;
+        const int c0 = s.cur[i0], c1 = s.cur[i0 + 1];
+        int btot;
+        const int ex = block_excl_scan(c0 + c1, s.red32, &btot);
+        if (threadIdx.x == 0 && (unsigned long long)btot != cx.kept[gblk]) atomicAdd(&cx.misc[2], 1ull);
+        // per-state outputs and M2 arcs; cursors
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          const int i = i0 + j;
+          const int32_t ub = ub0 + i;
+          int64_t pos = run + ex + (j ? c0 : 0);
+          if (ub < ub1 && src_bit(s, lw0, ub0, ub)) {
+            bool pr;
+            const int32_t id = rank_of(0, ua, ub, pr);
+            __stcs((long long*)&C.row_ptr[id], (long long)pos);
+            __stcs(&C.pair_a[id], ua);
+            __stcs(&C.pair_b[id], ub);
+            C.is_start[id] = (uint8_t)(stA & __ldg(&C.startB[ub]));
+            C.is_accept[id] = (uint8_t)(acA & __ldg(&C.accB[ub]));
+            for (int a = 0; a < s.aeps; ++a) {
+              const Cand c{s.a_slot[a], s.a_other[a], ub, 2, a, -1};
+              bool p2;
+              rank_of(c.slot, c.row, c.col, p2);
+              if (p2) emit_arc(c, pos++);
+            }
+          }
+          s.cur[i] = (int32_t)(pos - run);
+        }
+        __syncthreads();
+        // groups in label order; a state has at most one segment per group, so its cursor is
+        // owned by one thread per group pass
+        for (int g = 0; g < s.G; ++g) {
+          const int n = s.g_pre[g + 1] - s.g_pre[g];
+          const unsigned long long gm = s.g_mask[g];
+          const bool eps = s.g_label[g] == FST_EPS;
+          for (int i = threadIdx.x; i < n; i += kThreads) {
+            const int32_t sid = s.g_lo[g] + i;
+            const int32_t ub = __ldg(&Bv.seg_node[sid]);
+            if (!src_bit(s, lw0, ub0, ub)) continue;
+            const int32_t e0 = __ldg(&Bv.seg_beg[sid]), e1 = __ldg(&Bv.seg_beg[sid + 1]);
+            int64_t pos = run + s.cur[ub - ub0];
+            for (int32_t j = e0; j < e1; ++j) {
+              const int32_t ob = __ldg(&Bv.lm_other[j]);
+              const int32_t eb = __ldg(&Bv.lm_pos[j]);
+              for (unsigned long long m = gm; m; m &= m - 1) {
+                const int a = __ffsll((long long)m) - 1;
+                const Cand c{s.a_slot[a], s.a_other[a], ob, 1, a, eb};
+                bool pr;
+                rank_of(c.slot, c.row, c.col, pr);
+                if (pr) emit_arc(c, pos++);
+              }
+              if (eps) {
+                const Cand c{0, ua, ob, 3, -1, eb};
+                bool pr;
+                rank_of(0, ua, ob, pr);
+                if (pr) emit_arc(c, pos++);
+              }
+            }
+            s.cur[ub - ub0] = (int32_t)(pos - run);
+          }
+          __syncthreads();
+        }
+        run += btot;
+      } else
+      for_block_items(s, Bv, C, ch, blk, [&](bool valid, int32_t it, int32_t ub, int2 kd) {
+        const Item x = make_item(s, Av, it, ub, kd, valid);
+        const int maxn = __reduce_max_sync(0xffffffffu, (unsigned)x.n);
+        const bool simple = maxn <= kSimpleMoves;
+        // phase 1: kept moves of this lane (simple) / of this warp (expanded)
+        unsigned lk = 0, keptbits = 0;
+        if (simple) {
+          for (int k = 0; k < maxn; ++k) {
+            if (k < x.n) {
+              const Cand c = item_move(s, Av, ua, x, k);
+              bool pr;
+              rank_of(c.slot, c.row, c.col, pr);
+              if (pr) {
+                keptbits |= 1u << k;
+                ++lk;
+              }
+            }
+          }
+        } else {
+          warp_expand(s, Av, ua, x, [&](bool act, const Cand& c, int) {
+            bool pr = false;
+            if (act) rank_of(c.slot, c.row, c.col, pr);
+            if (lane == 0) lk += __popc(__ballot_sync(0xffffffffu, pr));
+            else __ballot_sync(0xffffffffu, pr);
+          });
+        }
+        const unsigned linc = warp_incl_scan(lk);  // simple: lane prefix; expanded: lane 0 holds the total
+        const unsigned wk = simple ? __shfl_sync(0xffffffffu, linc, 31) : __shfl_sync(0xffffffffu, lk, 0);
+        if (lane == 0) s.wtot[warp] = (int32_t)wk;
+        __syncthreads();
+        int64_t wbase, rtot;
+        {
+          const int32_t t = lane < kWarps ? s.wtot[lane] : 0;
+          const int32_t inc = warp_incl_scan(t);
+          wbase = run + __shfl_sync(0xffffffffu, inc - t, warp);
+          rtot = __shfl_sync(0xffffffffu, inc, kWarps - 1);
+        }
+        // phase 2: write
+        const bool sent = valid && x.kind == 2;
+        int64_t spos = -1;
+        if (simple) {
+          int64_t pos = wbase + (linc - lk);
+          spos = pos;
+          for (int k = 0; k < maxn; ++k)
+            if ((keptbits >> k) & 1u) emit_arc(item_move(s, Av, ua, x, k), pos++);
+        } else {
+          const int start = warp_incl_scan(x.n) - x.n;
+          unsigned before = 0;
+          warp_expand(s, Av, ua, x, [&](bool act, const Cand& c, int r) {
+            bool pr = false;
+            if (act) rank_of(c.slot, c.row, c.col, pr);
+            const unsigned bal = __ballot_sync(0xffffffffu, pr);
+            if (sent && start >= r && start < r + 32) spos = wbase + before + __popc(bal & ((1u << (start - r)) - 1u));
+            if (pr) emit_arc(c, wbase + before + __popc(bal & ((1u << lane) - 1u)));
+            before += __popc(bal);
+          });
+          if (sent && spos < 0) spos = wbase + before;
+        }
+        if (sent) {  // per-state outputs of a state of C
+          bool pr;
+          const int32_t id = rank_of(0, ua, ub, pr);
+          __stcs((long long*)&C.row_ptr[id], (long long)spos);
+          __stcs(&C.pair_a[id], ua);
+          __stcs(&C.pair_b[id], ub);
+          C.is_start[id] = (uint8_t)(stA & __ldg(&C.startB[ub]));
+          C.is_accept[id] = (uint8_t)(acA & __ldg(&C.accB[ub]));
+        }
+        run += rtot;
+        __syncthreads();
+      });
+      if (threadIdx.x == 0 && (unsigned long long)(run - run0) != cx.kept[gblk]) atomicAdd(&cx.misc[2], 1ull);
+      __syncthreads();
+    }
     __syncthreads();
   }
 }
 
 inline unsigned nblk(int64_t n, int t) { return (unsigned)std::max<int64_t>(1, (n + t - 1) / t); }
 
-int g_grid_expand = 0, g_grid_emit = 0;
+int g_grid = 0;
 
-void init_grids() {
-  if (g_grid_expand) return;
-  int sms = sm_count();
+fst_status init_kernels() {
+  if (g_grid) return FST_OK;
+  FSTC_CUDA_TRY(cudaFuncSetAttribute(k_level<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kDynSmem));
+  FSTC_CUDA_TRY(cudaFuncSetAttribute(k_level<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kDynSmem));
+  FSTC_CUDA_TRY(cudaFuncSetAttribute(k_emit, cudaFuncAttributeMaxDynamicSharedMemorySize, kDynSmem));
   int occ = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_expand<true>, kThreads, 0);
-  g_grid_expand = sms * std::max(occ, 1);
-  occ = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_emit, kThreads, 0);
-  g_grid_emit = sms * std::max(occ, 1);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_level<true>, kThreads, kDynSmem);
+  int occ2 = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, k_emit, kThreads, kDynSmem);
+  g_grid = sm_count() * std::max(1, std::min(occ, occ2));
+  return FST_OK;
 }
 
 struct EventTimer {
@@ -491,17 +1364,17 @@ struct EventTimer {
   }
 };
 
-// Runs one BFS stage (level loop); returns the number of non-empty levels.
-template <bool kForward>
-fst_status run_stage(const Ctx& cx, cudaStream_t s, unsigned long long* h_pinned, int64_t* expand_launches,
+// Runs one BFS stage (level loop); fills the per-level frontier sizes.
+template <bool kStage2>
+fst_status run_stage(const Ctx& cx, cudaStream_t s, unsigned long long* h_pinned, int64_t* level_launches,
                      std::vector<int64_t>* sizes) {
   int level = 0;
   int batch = 1;
   for (;;) {
     for (int k = 0; k < batch; ++k, ++level) {
-      k_expand<kForward><<<g_grid_expand, kThreads, 0, s>>>(cx, level);
+      k_level<kStage2><<<g_grid, kThreads, kDynSmem, s>>>(cx, level);
       FSTC_LAUNCH_CHECK();
-      ++*expand_launches;
+      ++*level_launches;
     }
     FSTC_CUDA_TRY(cudaMemcpyAsync(h_pinned, &cx.ctrl[level % 3].count, sizeof(unsigned long long),
                                   cudaMemcpyDeviceToHost, s));
@@ -509,37 +1382,32 @@ fst_status run_stage(const Ctx& cx, cudaStream_t s, unsigned long long* h_pinned
     if (*h_pinned == 0) break;
     batch = std::min(batch * 2, 8);  // speculative level batches: empty levels are no-op launches
   }
-  unsigned long long nl = 0;
   FSTC_CUDA_TRY(cudaMemcpyAsync(h_pinned, cx.misc, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
   FSTC_CUDA_TRY(cudaStreamSynchronize(s));
-  nl = *h_pinned;
-  if (sizes) {
-    int n = (int)std::min<unsigned long long>(nl, kMaxLevelStats);
-    std::vector<unsigned long long> tmp(n);
-    if (n) {
-      FSTC_CUDA_TRY(cudaMemcpyAsync(tmp.data(), cx.hist, sizeof(unsigned long long) * n, cudaMemcpyDeviceToHost, s));
-      FSTC_CUDA_TRY(cudaStreamSynchronize(s));
-    }
-    sizes->assign(tmp.begin(), tmp.end());
+  const unsigned long long nl = *h_pinned;
+  const int n = (int)std::min<unsigned long long>(nl, kMaxLevelStats);
+  std::vector<unsigned long long> tmp(n);
+  if (n) {
+    FSTC_CUDA_TRY(cudaMemcpyAsync(tmp.data(), cx.hist, sizeof(unsigned long long) * n, cudaMemcpyDeviceToHost, s));
+    FSTC_CUDA_TRY(cudaStreamSynchronize(s));
   }
+  sizes->assign(tmp.begin(), tmp.end());
   return FST_OK;
+}
+
+unsigned long long* pinned_scratch() {
+  static thread_local unsigned long long* p = nullptr;
+  if (!p && cudaMallocHost(&p, 64 * sizeof(unsigned long long)) != cudaSuccess) p = nullptr;
+  return p;
 }
 
 }  // namespace
 
-// Pinned host scratch (one per thread).
-static unsigned long long* pinned_scratch() {
-  static thread_local unsigned long long* p = nullptr;
-  if (!p) {
-    if (cudaMallocHost(&p, 64 * sizeof(unsigned long long)) != cudaSuccess) p = nullptr;
-  }
-  return p;
-}
-
 std::vector<int64_t>& level_sizes_slot(fst* h, int stage);
 
 fst_status compose_impl(int32_t n, const fst_handle* a, const fst_handle* b, cudaStream_t s, fst_handle* c) {
-  EventTimer t_total(profiling_enabled(), s);
+  const bool prof = profiling_enabled();
+  EventTimer t_total(prof, s);
   for (int i = 0; i < n; ++i) c[i] = nullptr;
   for (int i = 0; i < n; ++i) {
     if (!a[i] || !b[i]) {
@@ -551,18 +1419,22 @@ fst_status compose_impl(int32_t n, const fst_handle* a, const fst_handle* b, cud
     st = ensure_views(b[i], s);
     if (st) return st;
   }
-  init_grids();
+  fst_status st = init_kernels();
+  if (st) return st;
   const int64_t launches0 = fst_launch_count();
   // ---- layout of the concatenated pair space
+  int64_t total_rows = 0;
+  for (int i = 0; i < n; ++i) total_rows += a[i]->V;
+  const int64_t target_tasks = 8ll * g_grid;
   std::vector<CompDev> comps(n);
   std::vector<int64_t> seed1(n + 1, 0), seed2(n + 1, 0);
-  int64_t W = 0, K = 0, pairs = 0;
+  int64_t W = 0, K = 0, Q = 0, pairs = 0;
   for (int i = 0; i < n; ++i) {
     const fst* A = a[i];
     const fst* B = b[i];
     CompDev& C = comps[i];
     memset(&C, 0, sizeof(C));
-    auto vd = [](const View& v) { return ViewDev{v.off, v.key, v.other, v.carry, v.w}; };
+    auto vd = [](const View& v) { return ViewDev{v.off, v.key, v.other, v.carry, v.w, v.cw, v.ikd, v.isrc, v.lm_other, v.lm_pos, v.seg_node, v.seg_beg, v.lab_val, v.lab_seg, v.nlab}; };
     C.Af = vd(A->views[kOutByOlabel]);
     C.Ab = vd(A->views[kInByOlabel]);
     C.Bf = vd(B->views[kOutByIlabel]);
@@ -575,16 +1447,25 @@ fst_status compose_impl(int32_t n, const fst_handle* a, const fst_handle* b, cud
     C.VB = B->V;
     C.wpr = (B->V + 31) / 32;
     C.bpr = (C.wpr + kWordsPerBlock - 1) / kWordsPerBlock;
+    // chunks: enough CTA tasks to fill the GPU, at most kChunkMaxBlocks blocks each
+    int64_t want = total_rows > 0 ? (target_tasks + total_rows - 1) / total_rows : 1;
+    int32_t cpr = (int32_t)std::max<int64_t>(1, std::min<int64_t>(want, C.bpr));
+    cpr = std::max<int32_t>(cpr, (C.bpr + kChunkMaxBlocks - 1) / kChunkMaxBlocks);
+    C.CB = std::max<int32_t>(1, (C.bpr + cpr - 1) / cpr);
+    C.cpr = std::max<int32_t>(1, (C.bpr + C.CB - 1) / C.CB);
+    C.smallA = A->max_olabel < 63;
     C.W = W;
     C.K = K;
+    C.Q = Q;
     W += (int64_t)C.VA * C.wpr;
     K += (int64_t)C.VA * C.bpr;
+    Q += (int64_t)C.VA * C.cpr;
     pairs += (int64_t)C.VA * C.VB;
     seed1[i + 1] = seed1[i] + (int64_t)C.nAccA * C.nAccB;
     seed2[i + 1] = seed2[i] + (int64_t)C.nStartA * C.nStartB;
   }
-  const int64_t nwords = W, nblocks = K;
-  if (nblocks >= INT32_MAX) {
+  const int64_t nwords = W, nblocks = K, nchunks = Q;
+  if (nblocks >= INT32_MAX || nchunks >= INT32_MAX) {
     set_error(FST_E_CAPACITY, "pair space too large (%lld blocks)", (long long)nblocks);
     return FST_E_CAPACITY;
   }
@@ -592,8 +1473,8 @@ fst_status compose_impl(int32_t n, const fst_handle* a, const fst_handle* b, cud
   size_t off = 0;
   auto take = [&](size_t bytes) { size_t o = off; off += (bytes + 255) & ~size_t(255); return o; };
   const size_t oR = take(4 * nwords), oV = take(4 * nwords), oF0 = take(4 * nwords), oF1 = take(4 * nwords);
-  const size_t ofl0 = take(4 * nblocks), ofl1 = take(4 * nblocks);
-  const size_t ol0 = take(4 * nblocks), ol1 = take(4 * nblocks);
+  const size_t ofl0 = take(4 * nchunks), ofl1 = take(4 * nchunks);
+  const size_t ol0 = take(4 * nchunks), ol1 = take(4 * nchunks);
   const size_t octrl = take(sizeof(LevelCtrl) * 3);
   const size_t okept = take(8 * nblocks), ovc = take(4 * nblocks), owpre = take(2 * nwords);
   const size_t oid = take(8 * (nblocks + 1)), oarc = take(8 * (nblocks + 1));
@@ -602,7 +1483,7 @@ fst_status compose_impl(int32_t n, const fst_handle* a, const fst_handle* b, cud
   const size_t ocomps = take(sizeof(CompDev) * n), oseed1 = take(8 * (n + 1)), oseed2 = take(8 * (n + 1));
   const size_t otot = take(8 * 2 * (n + 1));
   BufferPtr wb;
-  fst_status st = alloc_buffer(off, s, &wb);
+  st = alloc_buffer(off, s, &wb);
   if (st) {
     if (st == FST_E_OOM) set_error(FST_E_CAPACITY, "pair space workspace (%zu bytes) does not fit", off);
     return st == FST_E_OOM ? FST_E_CAPACITY : st;
@@ -630,6 +1511,8 @@ fst_status compose_impl(int32_t n, const fst_handle* a, const fst_handle* b, cud
   cx.ncomp = n;
   cx.nwords = nwords;
   cx.nblocks = nblocks;
+  cx.nchunks = nchunks;
+  cx.seedbase = nullptr;
   int64_t* d_seed1 = (int64_t*)(base + oseed1);
   int64_t* d_seed2 = (int64_t*)(base + oseed2);
   int64_t* d_tot = (int64_t*)(base + otot);
@@ -639,7 +1522,6 @@ fst_status compose_impl(int32_t n, const fst_handle* a, const fst_handle* b, cud
     set_error(FST_E_CUDA, "cudaMallocHost failed");
     return FST_E_CUDA;
   }
-
   // zero: R, V, F0, F1, flags (contiguous), ctrl, kept, misc
   FSTC_CUDA_TRY(cudaMemsetAsync(base + oR, 0, ol0 - oR, s));
   FSTC_CUDA_TRY(cudaMemsetAsync(base + octrl, 0, sizeof(LevelCtrl) * 3, s));
@@ -652,9 +1534,8 @@ fst_status compose_impl(int32_t n, const fst_handle* a, const fst_handle* b, cud
   fst_compose_stats stats{};
   stats.pair_space = pairs;
   stats.num_coaccessible = -1;
-  int64_t expand_launches = 0;
+  int64_t level_launches = 0;
   std::vector<int64_t> sizes1, sizes2;
-  const bool prof = profiling_enabled();
 
   // ---- stage 1: co-accessible set R (backward BFS from accept pairs)
   {
@@ -663,7 +1544,7 @@ fst_status compose_impl(int32_t n, const fst_handle* a, const fst_handle* b, cud
     if (seed1[n] > 0) {
       k_seed<false><<<nblk(seed1[n], 256), 256, 0, s>>>(cx);
       FSTC_LAUNCH_CHECK();
-      st = run_stage<false>(cx, s, hp, &expand_launches, &sizes1);
+      st = run_stage<false>(cx, s, hp, &level_launches, &sizes1);
       if (st) return st;
     }
     stats.levels_stage1 = (int32_t)sizes1.size();
@@ -678,7 +1559,7 @@ fst_status compose_impl(int32_t n, const fst_handle* a, const fst_handle* b, cud
     if (seed2[n] > 0 && seed1[n] > 0) {
       k_seed<true><<<nblk(seed2[n], 256), 256, 0, s>>>(cx);
       FSTC_LAUNCH_CHECK();
-      st = run_stage<true>(cx, s, hp, &expand_launches, &sizes2);
+      st = run_stage<true>(cx, s, hp, &level_launches, &sizes2);
       if (st) return st;
     }
     stats.levels_stage2 = (int32_t)sizes2.size();
@@ -686,6 +1567,13 @@ fst_status compose_impl(int32_t n, const fst_handle* a, const fst_handle* b, cud
   }
   // ---- numbering: per-block state counts, word prefixes, scans, per-composition totals
   std::vector<int64_t> tot(2 * (n + 1));
+  std::vector<fst*> outs(n, nullptr);
+  auto cleanup = [&]() {
+    for (auto*& h : outs) {
+      delete h;
+      h = nullptr;
+    }
+  };
   {
     EventTimer t(prof, s);
     k_block_counts<<<nblk(nblocks * 32, 256), 256, 0, s>>>(cx);
@@ -701,14 +1589,14 @@ fst_status compose_impl(int32_t n, const fst_handle* a, const fst_handle* b, cud
       FSTC_LAUNCH_CHECK();
     }
     FSTC_CUDA_TRY(cudaMemcpyAsync(tot.data(), d_tot, 8 * 2 * (n + 1), cudaMemcpyDeviceToHost, s));
-    if (prof) FSTC_CUDA_TRY(cudaMemcpyAsync(hp + 1, cx.misc + 1, 8, cudaMemcpyDeviceToHost, s));
+    FSTC_CUDA_TRY(cudaMemcpyAsync(hp + 1, cx.misc + 1, 8, cudaMemcpyDeviceToHost, s));
     FSTC_CUDA_TRY(cudaStreamSynchronize(s));
     if (prof) stats.num_coaccessible = (int64_t)hp[1];
-    // ---- output allocation (one buffer per composition)
-    std::vector<fst*> outs(n, nullptr);
-    auto cleanup = [&]() {
-      for (auto* h : outs) delete h;
-    };
+    stats.ms_number = t.stop();
+  }
+  // ---- output allocation (one buffer per composition)
+  {
+    EventTimer t(prof, s);
     for (int i = 0; i < n; ++i) {
       const int64_t nv = tot[2 * i + 2] - tot[2 * i], ne = tot[2 * i + 3] - tot[2 * i + 1];
       if (nv >= INT32_MAX) {
@@ -755,39 +1643,40 @@ fst_status compose_impl(int32_t n, const fst_handle* a, const fst_handle* b, cud
       C.pair_b = h->pair_b;
     }
     FSTC_CUDA_TRY(cudaMemcpyAsync(d_comps, comps.data(), sizeof(CompDev) * n, cudaMemcpyHostToDevice, s));
-    stats.ms_number = t.stop();
-    // ---- emit
-    {
-      EventTimer te(prof, s);
-      k_emit<<<g_grid_emit, kThreads, 0, s>>>(cx, d_tot);
-      FSTC_LAUNCH_CHECK();
-      k_finish_rowptr<<<nblk(n, 128), 128, 0, s>>>(cx, d_tot);
-      FSTC_LAUNCH_CHECK();
-      FSTC_CUDA_TRY(cudaMemcpyAsync(hp + 2, cx.misc + 2, 8, cudaMemcpyDeviceToHost, s));
-      cudaError_t e = cudaStreamSynchronize(s);
-      if (e != cudaSuccess) {
-        cleanup();
-        set_error(FST_E_CUDA, "compose: %s", cudaGetErrorString(e));
-        return FST_E_CUDA;
-      }
-      stats.ms_emit = te.stop();
-      if (hp[2] != 0) {
-        cleanup();
-        set_error(FST_E_INTERNAL, "emit/count mismatch in %llu blocks", hp[2]);
-        return FST_E_INTERNAL;
-      }
+    stats.ms_alloc = t.stop();
+  }
+  // ---- emit
+  {
+    EventTimer te(prof, s);
+    k_emit<<<g_grid, kThreads, kDynSmem, s>>>(cx, d_tot);
+    FSTC_LAUNCH_CHECK();
+    stats.ms_emit = te.stop();
+    k_finish_rowptr<<<nblk(n, 128), 128, 0, s>>>(cx, d_tot);
+    FSTC_LAUNCH_CHECK();
+    FSTC_CUDA_TRY(cudaMemcpyAsync(hp + 2, cx.misc + 2, 16, cudaMemcpyDeviceToHost, s));
+    cudaError_t e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) {
+      cleanup();
+      set_error(FST_E_CUDA, "compose: %s", cudaGetErrorString(e));
+      return FST_E_CUDA;
     }
-    wb.reset();
-    stats.ms_total = t_total.stop();
-    stats.launches = fst_launch_count() - launches0;
-    stats.expand_launches = expand_launches;
-    stats.emit_launches = 1;
-    for (int i = 0; i < n; ++i) {
-      outs[i]->stats = stats;
-      level_sizes_slot(outs[i], 1) = sizes1;
-      level_sizes_slot(outs[i], 2) = sizes2;
-      c[i] = outs[i];
+    if (hp[2] != 0) {
+      cleanup();
+      set_error(FST_E_INTERNAL, "emit/count mismatch in %llu blocks", hp[2]);
+      return FST_E_INTERNAL;
     }
+    stats.staged_tasks = (int64_t)hp[3];
+  }
+  wb.reset();
+  stats.ms_total = t_total.stop();
+  stats.launches = fst_launch_count() - launches0;
+  stats.expand_launches = level_launches;
+  stats.emit_launches = 1;
+  for (int i = 0; i < n; ++i) {
+    outs[i]->stats = stats;
+    level_sizes_slot(outs[i], 1) = sizes1;
+    level_sizes_slot(outs[i], 2) = sizes2;
+    c[i] = outs[i];
   }
   return FST_OK;
 }

@@ -155,15 +155,18 @@ __global__ void k_gather_view(int64_t E, const int32_t* __restrict__ perm, const
                               const int32_t* __restrict__ other_src, const int32_t* __restrict__ carry_src,
                               const float* __restrict__ w_src, int32_t* __restrict__ key,
                               int32_t* __restrict__ other, int32_t* __restrict__ carry, float* __restrict__ w,
-                              int32_t* __restrict__ arc) {
+                              int32_t* __restrict__ arc, int2* __restrict__ cw) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= E) return;
   int32_t e = perm[i];
-  key[i] = key_src[e];
-  other[i] = other_src[e];
-  carry[i] = carry_src[e];
-  w[i] = w_src[e];
+  const int32_t k = key_src[e], o = other_src[e], c = carry_src[e];
+  const float x = w_src[e];
+  key[i] = k;
+  other[i] = o;
+  carry[i] = c;
+  w[i] = x;
   arc[i] = e;
+  cw[i] = make_int2(c, __float_as_int(x));
 }
 
 // off[v] = first sorted position whose node >= v  (node = key >> LB)
@@ -174,6 +177,69 @@ __global__ void k_view_offsets(int32_t V, int64_t E, const unsigned long long* _
   int64_t prev = i > 0 ? (int64_t)(keys[i - 1] >> LB) : -1;
   int64_t cur = i < E ? (int64_t)(keys[i] >> LB) : (int64_t)V;
   for (int64_t v = prev + 1; v <= cur; ++v) off[v] = (int32_t)i;
+}
+
+// items of a view: node v owns [off[v]+v, off[v+1]+v+1): sentinel, then its arcs in view order
+__global__ void k_view_items(int32_t V, int64_t E, const int32_t* __restrict__ off, const int32_t* __restrict__ key,
+                             const int32_t* __restrict__ other, const unsigned long long* __restrict__ keys, int LB,
+                             int2* __restrict__ ikd, int32_t* __restrict__ isrc) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < E) {
+    const int32_t v = (int32_t)(keys[i] >> LB);
+    ikd[i + v + 1] = make_int2(key[i], other[i]);
+    isrc[i + v + 1] = v;
+  }
+  if (i < V) {
+    ikd[off[i] + i] = make_int2(kSentinel, (int32_t)i);
+    isrc[off[i] + i] = (int32_t)i;
+  }
+}
+
+// label-major keys: ((label+1) << NB) | node, payload = view position
+__global__ void k_lm_keys(int64_t E, const unsigned long long* __restrict__ vkeys, int LB, int NB,
+                          const int32_t* __restrict__ key, unsigned long long* __restrict__ out,
+                          int32_t* __restrict__ vals) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= E) return;
+  const unsigned long long node = vkeys[i] >> LB;
+  out[i] = ((unsigned long long)(uint32_t)(key[i] + 1) << NB) | node;
+  vals[i] = (int32_t)i;
+}
+
+__global__ void k_lm_flags(int64_t E, const unsigned long long* __restrict__ keys, const int32_t* __restrict__ vals,
+                           int NB, const int32_t* __restrict__ other, int32_t* __restrict__ lm_other,
+                           int32_t* __restrict__ lm_pos, int32_t* __restrict__ segf, int32_t* __restrict__ labf) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= E) return;
+  const int32_t p = vals[i];
+  lm_pos[i] = p;
+  lm_other[i] = other[p];
+  const unsigned long long k = keys[i];
+  segf[i] = (i == 0 || k != keys[i - 1]) ? 1 : 0;
+  labf[i] = (i == 0 || (k >> NB) != (keys[i - 1] >> NB)) ? 1 : 0;
+}
+
+__global__ void k_lm_scatter(int64_t E, const unsigned long long* __restrict__ keys, int NB,
+                             const int32_t* __restrict__ segf, const int32_t* __restrict__ labf,
+                             const int64_t* __restrict__ segi, const int64_t* __restrict__ labi,
+                             int32_t* __restrict__ seg_node, int32_t* __restrict__ seg_beg,
+                             int32_t* __restrict__ lab_val, int32_t* __restrict__ lab_seg) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i > E) return;
+  if (i == E) {
+    seg_beg[segi[E]] = (int32_t)E;
+    lab_seg[labi[E]] = (int32_t)segi[E];
+    return;
+  }
+  const unsigned long long k = keys[i];
+  if (segf[i]) {
+    seg_node[segi[i]] = (int32_t)(k & ((1ull << NB) - 1));
+    seg_beg[segi[i]] = (int32_t)i;
+  }
+  if (labf[i]) {
+    lab_val[labi[i]] = (int32_t)(k >> NB) - 1;
+    lab_seg[labi[i]] = (int32_t)segi[i];
+  }
 }
 
 // start / accept lists in ascending state order (single CTA, block scan)
@@ -211,24 +277,6 @@ int bits_for(int64_t x) {  // bits to represent values in [0, x]
 
 }  // namespace
 
-fst_status alloc_buffer(size_t bytes, cudaStream_t s, BufferPtr* out) {
-  auto b = std::make_shared<DeviceBuffer>();
-  bytes = (bytes + 255) & ~size_t(255);
-  if (bytes == 0) bytes = 256;
-  cudaError_t e = cudaMallocAsync(&b->ptr, bytes, s);
-  if (e != cudaSuccess) {
-    b->ptr = nullptr;
-    cudaGetLastError();
-    set_error(e == cudaErrorMemoryAllocation ? FST_E_OOM : FST_E_CUDA, "cudaMallocAsync(%zu) failed: %s",
-              bytes, cudaGetErrorString(e));
-    return e == cudaErrorMemoryAllocation ? FST_E_OOM : FST_E_CUDA;
-  }
-  b->bytes = bytes;
-  b->stream = s;
-  *out = std::move(b);
-  return FST_OK;
-}
-
 // Simple bump allocator over one buffer.
 struct Carve {
   char* p;
@@ -255,7 +303,9 @@ fst_status build_views(fst* h, cudaStream_t s, int32_t max_il, int32_t max_ol) {
   }
   size_t vbytes = 0;
   for (int k = 0; k < 4; ++k)
-    vbytes += carve_bytes<int32_t>(V + 1) + 4 * carve_bytes<int32_t>(E) + carve_bytes<float>(E);
+    vbytes += carve_bytes<int32_t>(V + 1) + 4 * carve_bytes<int32_t>(E) + carve_bytes<float>(E) +
+              carve_bytes<int2>(E) + carve_bytes<int2>(E + V) + carve_bytes<int32_t>(E + V) +
+              4 * carve_bytes<int32_t>(E) + 2 * carve_bytes<int32_t>(E + 1);
   vbytes += 2 * carve_bytes<int32_t>(V);
   BufferPtr vb;
   fst_status st = alloc_buffer(vbytes, s, &vb);
@@ -270,6 +320,15 @@ fst_status build_views(fst* h, cudaStream_t s, int32_t max_il, int32_t max_ol) {
     w.carry = cv.take<int32_t>(E);
     w.arc = cv.take<int32_t>(E);
     w.w = cv.take<float>(E);
+    w.cw = cv.take<int2>(E);
+    w.ikd = cv.take<int2>(E + V);
+    w.isrc = cv.take<int32_t>(E + V);
+    w.lm_other = cv.take<int32_t>(E);
+    w.lm_pos = cv.take<int32_t>(E);
+    w.seg_node = cv.take<int32_t>(E);
+    w.seg_beg = cv.take<int32_t>(E + 1);
+    w.lab_val = cv.take<int32_t>(E);
+    w.lab_seg = cv.take<int32_t>(E + 1);
   }
   h->start_list = cv.take<int32_t>(V);
   h->accept_list = cv.take<int32_t>(V);
@@ -279,7 +338,8 @@ fst_status build_views(fst* h, cudaStream_t s, int32_t max_il, int32_t max_ol) {
   size_t tbytes = carve_bytes<int32_t>(E) + 2 * carve_bytes<unsigned long long>(E) +
                   2 * carve_bytes<int32_t>(E) + carve_bytes<int32_t>(16 * ntiles) +
                   carve_bytes<int64_t>(16 * ntiles + 1) + carve_bytes<int64_t>(scan_tmp_elems(16 * ntiles)) +
-                  carve_bytes<int32_t>(4);
+                  carve_bytes<int32_t>(8) + 2 * carve_bytes<int32_t>(E) + 2 * carve_bytes<int64_t>(E + 1) +
+                  carve_bytes<int64_t>(scan_tmp_elems(E)) + carve_bytes<unsigned long long>(E);
   BufferPtr tb;
   st = alloc_buffer(tbytes, s, &tb);
   if (st) return st;
@@ -292,7 +352,15 @@ fst_status build_views(fst* h, cudaStream_t s, int32_t max_il, int32_t max_ol) {
   int32_t* hist = ct.take<int32_t>(16 * ntiles);
   int64_t* hoff = ct.take<int64_t>(16 * ntiles + 1);
   int64_t* stmp = ct.take<int64_t>(scan_tmp_elems(16 * ntiles));
-  int32_t* counts = ct.take<int32_t>(4);
+  int32_t* counts = ct.take<int32_t>(8);
+  int32_t* segf = ct.take<int32_t>(E);
+  int32_t* labf = ct.take<int32_t>(E);
+  int64_t* segi = ct.take<int64_t>(E + 1);
+  int64_t* labi = ct.take<int64_t>(E + 1);
+  int64_t* etmp = ct.take<int64_t>(scan_tmp_elems(E));
+  unsigned long long* vkeys = ct.take<unsigned long long>(E);
+  int64_t lm_counts[2][2] = {{0, 0}, {0, 0}};
+  FSTC_CUDA_TRY(cudaMemsetAsync(counts, 0, 8 * sizeof(int32_t), s));
 
   if (E > 0) {
     k_arc_src<<<nblk(E, 256), 256, 0, s>>>(V, E, h->row_ptr, src);
@@ -327,25 +395,69 @@ fst_status build_views(fst* h, cudaStream_t s, int32_t max_il, int32_t max_ol) {
         std::swap(va, vbv);
       }
       k_gather_view<<<nblk(E, 256), 256, 0, s>>>(E, va, label, other, carry, h->weight, w.key, w.other, w.carry,
-                                                 w.w, w.arc);
+                                                 w.w, w.arc, w.cw);
       FSTC_LAUNCH_CHECK();
       k_view_offsets<<<nblk(E + 1, 256), 256, 0, s>>>(V, E, ka, LB, w.off);
       FSTC_LAUNCH_CHECK();
+      k_view_items<<<nblk(std::max<int64_t>(E, V), 256), 256, 0, s>>>(V, E, w.off, w.key, w.other, ka, LB, w.ikd,
+                                                                        w.isrc);
+      FSTC_LAUNCH_CHECK();
+      if (!by_ol) {  // B role: label-major segment index
+        FSTC_CUDA_TRY(cudaMemcpyAsync(vkeys, ka, sizeof(unsigned long long) * E, cudaMemcpyDeviceToDevice, s));
+        k_lm_keys<<<nblk(E, 256), 256, 0, s>>>(E, vkeys, LB, NB, w.key, k0, v0);
+        FSTC_LAUNCH_CHECK();
+        unsigned long long* la = k0;
+        unsigned long long* lb = k1;
+        int32_t* pa = v0;
+        int32_t* pb = v1;
+        for (int shift = 0; shift < bits; shift += 4) {
+          k_radix_hist<<<(unsigned)ntiles, kSortThreads, 0, s>>>(la, E, shift, hist, (int)ntiles);
+          FSTC_LAUNCH_CHECK();
+          st = exclusive_scan_i32(hist, 16 * ntiles, hoff, stmp, s);
+          if (st) return st;
+          k_radix_scatter<<<(unsigned)ntiles, kSortThreads, 0, s>>>(la, pa, E, shift, hoff, (int)ntiles, lb, pb);
+          FSTC_LAUNCH_CHECK();
+          std::swap(la, lb);
+          std::swap(pa, pb);
+        }
+        k_lm_flags<<<nblk(E, 256), 256, 0, s>>>(E, la, pa, NB, w.other, w.lm_other, w.lm_pos, segf, labf);
+        FSTC_LAUNCH_CHECK();
+        st = exclusive_scan_i32(segf, E, segi, etmp, s);
+        if (st) return st;
+        st = exclusive_scan_i32(labf, E, labi, etmp, s);
+        if (st) return st;
+        k_lm_scatter<<<nblk(E + 1, 256), 256, 0, s>>>(E, la, NB, segf, labf, segi, labi, w.seg_node, w.seg_beg,
+                                                       w.lab_val, w.lab_seg);
+        FSTC_LAUNCH_CHECK();
+        const int slot = k == kOutByIlabel ? 0 : 1;
+        FSTC_CUDA_TRY(cudaMemcpyAsync(&lm_counts[slot][0], segi + E, 8, cudaMemcpyDeviceToHost, s));
+        FSTC_CUDA_TRY(cudaMemcpyAsync(&lm_counts[slot][1], labi + E, 8, cudaMemcpyDeviceToHost, s));
+      }
     } else {
       FSTC_CUDA_TRY(cudaMemsetAsync(w.off, 0, sizeof(int32_t) * (V + 1), s));
+      if (V > 0) {
+        k_view_items<<<nblk(V, 256), 256, 0, s>>>(V, 0, w.off, w.key, w.other, nullptr, LB, w.ikd, w.isrc);
+        FSTC_LAUNCH_CHECK();
+      }
     }
+
   }
   if (V > 0) {
     k_flag_lists<<<1, 1024, 0, s>>>(V, h->is_start, h->is_accept, h->start_list, h->accept_list, counts);
     FSTC_LAUNCH_CHECK();
-    int32_t hc[2];
+  }
+  {
+    int32_t hc[8];
     FSTC_CUDA_TRY(cudaMemcpyAsync(hc, counts, sizeof(hc), cudaMemcpyDeviceToHost, s));
     FSTC_CUDA_TRY(cudaStreamSynchronize(s));
-    h->n_start = hc[0];
-    h->n_accept = hc[1];
-  } else {
-    h->n_start = h->n_accept = 0;
-    FSTC_CUDA_TRY(cudaStreamSynchronize(s));
+    h->n_start = V > 0 ? hc[0] : 0;
+    h->n_accept = V > 0 ? hc[1] : 0;
+    h->max_ilabel = max_il;
+    h->max_olabel = max_ol;
+    h->views[kOutByIlabel].nseg = (int32_t)lm_counts[0][0];
+    h->views[kOutByIlabel].nlab = (int32_t)lm_counts[0][1];
+    h->views[kInByIlabel].nseg = (int32_t)lm_counts[1][0];
+    h->views[kInByIlabel].nlab = (int32_t)lm_counts[1][1];
   }
   tb.reset();  // stream-ordered free after the work above
   h->has_views = true;

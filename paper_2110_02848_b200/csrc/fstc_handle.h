@@ -10,13 +10,16 @@
 
 namespace fstc {
 
-// Stream-ordered device allocation released with cudaFreeAsync on the owning stream.
+void release_buffer(void* ptr, size_t bytes, cudaStream_t s);  // memory.cu
+
+// Stream-ordered device allocation, released on the owning stream (large buffers go back to the
+// library's buffer cache, see memory.cu).
 struct DeviceBuffer {
   void* ptr = nullptr;
   size_t bytes = 0;
   cudaStream_t stream = nullptr;
   ~DeviceBuffer() {
-    if (ptr) cudaFreeAsync(ptr, stream);
+    if (ptr) release_buffer(ptr, bytes, stream);
   }
 };
 using BufferPtr = std::shared_ptr<DeviceBuffer>;
@@ -33,6 +36,18 @@ struct View {
   int32_t* carry = nullptr;  // [E]
   float* w = nullptr;        // [E]
   int32_t* arc = nullptr;    // [E] original arc index
+  int2* cw = nullptr;        // [E] packed (carry, weight bits): the per-arc data of the emit
+  int2* ikd = nullptr;       // [E+V] items: per node a sentinel (kSentinel, node) then (key, other) of its arcs
+  int32_t* isrc = nullptr;   // [E+V] item -> node
+  // label-major segment index (B-role views): arcs ordered by (label, node, view position); a
+  // segment is a run of equal (label, node)
+  int32_t* lm_other = nullptr;  // [E] other-end node
+  int32_t* lm_pos = nullptr;    // [E] view position
+  int32_t* seg_node = nullptr;  // [E] node of segment s
+  int32_t* seg_beg = nullptr;   // [E+1] first label-major index of segment s
+  int32_t* lab_val = nullptr;   // [E] distinct labels, ascending
+  int32_t* lab_seg = nullptr;   // [E+1] first segment of each distinct label
+  int32_t nseg = 0, nlab = 0;
 };
 
 }  // namespace fstc
@@ -58,6 +73,7 @@ struct fst {
   int32_t* start_list = nullptr;
   int32_t* accept_list = nullptr;
   int32_t n_start = 0, n_accept = 0;
+  int32_t max_ilabel = -1, max_olabel = -1;
   fst_compose_stats stats{};
   std::vector<int64_t> level_sizes[2];  // frontier size per BFS level, stage 1 / stage 2
   std::vector<fstc::BufferPtr> buffers;  // owned (or shared with a batch) device memory

@@ -28,7 +28,21 @@ struct ViewDev {
   const int32_t* other;  // [E] other-end node
   const int32_t* carry;  // [E] label carried to the output
   const float* w;        // [E] weight
+  const int2* cw;         // [E] packed (carry, weight bits)
+  const int2* ikd;        // [E+V] items: node v owns items [off[v]+v, off[v+1]+v+1): a sentinel
+                          //       (kSentinel, v) then (key, other) of its arcs in view order
+  const int32_t* isrc;    // [E+V] item -> node
+  // label-major segment index (B role): see View in fstc_handle.h
+  const int32_t* lm_other;
+  const int32_t* lm_pos;
+  const int32_t* seg_node;
+  const int32_t* seg_beg;
+  const int32_t* lab_val;
+  const int32_t* lab_seg;
+  int32_t nlab;
 };
+
+constexpr int32_t kSentinel = INT32_MIN;
 
 // One composition inside a (possibly batched) call.
 struct CompDev {
@@ -44,8 +58,11 @@ struct CompDev {
   int32_t nStartA, nStartB, nAccA, nAccB;
   int32_t VA, VB;
   int32_t wpr, bpr;  // words per row, blocks per row
+  int32_t cpr, CB;   // chunks per row, blocks per chunk (a chunk is one CTA task)
+  int32_t smallA;    // A's olabels < 63: label-mask matching of an A row is possible
   int64_t W;         // first word of this composition's pair space
   int64_t K;         // first block
+  int64_t Q;         // first chunk
   // outputs (filled before the emit kernel)
   int64_t* row_ptr;
   int32_t* ilabel;
@@ -60,29 +77,9 @@ struct CompDev {
 
 // Per-level control block (ring of 3).
 struct LevelCtrl {
-  unsigned long long count;    // number of active blocks in the list of this level
+  unsigned long long count;    // number of active chunks in the list of this level
   unsigned long long nnew;     // states discovered (claimed) into this level's frontier
   unsigned long long pad[2];
-};
-
-// Workspace of one compose call (device pointers).
-struct Work {
-  uint32_t* R;        // co-accessible bitmap
-  uint32_t* V;        // visited (accessible & co-accessible) bitmap
-  uint32_t* F[2];     // frontier bitmaps (double buffered, self-cleaning)
-  uint8_t* flag[2];   // per-block "has frontier bits" flags (self-cleaning)
-  int32_t* list[2];   // active block lists
-  LevelCtrl* ctrl;    // [3]
-  unsigned long long* kept;  // [nblocks] arcs of C leaving each block's states (stage-2 count)
-  int32_t* vcount;    // [nblocks] states of C per block
-  uint16_t* wpre;     // [nwords] exclusive popcount prefix of V inside the block
-  int64_t* idbase;    // [nblocks+1] exclusive scan of vcount
-  int64_t* arcbase;   // [nblocks+1] exclusive scan of kept
-  unsigned long long* nnew_hist;  // [kMaxLevelStats] per-level discoveries (stats)
-  int32_t* err;       // [1] internal consistency flag
-  int64_t nwords, nblocks;
-  int32_t ncomp;
-  const CompDev* comps;  // [ncomp] device copy
 };
 
 constexpr int kMaxLevelStats = 1 << 16;

@@ -52,8 +52,9 @@ class fst_view(C.Structure):
 class fst_compose_stats(C.Structure):
     _fields_ = [("levels_stage1", C.c_int32), ("levels_stage2", C.c_int32), ("num_coaccessible", C.c_int64),
                 ("pair_space", C.c_int64), ("ms_stage1", C.c_float), ("ms_stage2", C.c_float),
-                ("ms_number", C.c_float), ("ms_emit", C.c_float), ("ms_total", C.c_float),
-                ("launches", C.c_int64), ("emit_launches", C.c_int64), ("expand_launches", C.c_int64)]
+                ("ms_number", C.c_float), ("ms_alloc", C.c_float), ("ms_emit", C.c_float),
+                ("ms_total", C.c_float), ("launches", C.c_int64), ("emit_launches", C.c_int64),
+                ("expand_launches", C.c_int64), ("staged_tasks", C.c_int64)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
