@@ -142,6 +142,8 @@ struct TaskSmem {
   int32_t a_carry[kAMax];
   float a_w[kAMax];
   unsigned long long labmask[64];     // labmask[l+1] = A-row positions with olabel l (l < 63)
+  uint32_t labmask32[64];             // the same for rows of <= 32 arcs
+  int32_t mask32;
   int32_t slot_row[kSlotMax];
   int32_t a0, a1, deg, aeps, m, arow_smem, dst_staged, small;
   int32_t state[kPairsPerBlock];      // compacted source states of a sparse block (ascending u_b)
@@ -264,6 +266,8 @@ __device__ void stage_arow(TaskSmem& s, const CompDev& C, const ViewDev& Av, int
       s.aeps = aeps;
       if (s.small)
         for (int k = 0; k < s.deg; ++k) s.labmask[s.a_key[k] + 1] |= 1ull << k;
+      s.mask32 = s.deg <= 32;
+      for (int l = 0; l < 64; ++l) s.labmask32[l] = (uint32_t)s.labmask[l];
       // destination-row slots: slot 0 = u_a (M3 moves), then distinct dst rows
       int m = 1;
       s.slot_row[0] = ua;
@@ -555,77 +559,61 @@ __device__ __forceinline__ void for_block_items(TaskSmem& s, const ViewDev& Bv, 
 // (packed (label, other) items); states with more than kHeavy arcs are walked by the whole CTA.
 
 // f(slot, col, kind, a, eb) for every move of state ub (M2, then per B arc: M1 matches, M3).
-template <typename F>
+template <bool kM32, typename F>
 __device__ __forceinline__ void fast_arc(const TaskSmem& s, int2 x, int32_t eb, F&& f) {
-  unsigned long long m = (unsigned)(x.x + 1) < 64u ? s.labmask[x.x + 1] : 0ull;
-  while (m) {
-    const int a = __ffsll((long long)m) - 1;
-    m &= m - 1;
-    f(s.a_slot[a], x.y, 1, a, eb);
+  if (kM32) {
+    uint32_t m = (unsigned)(x.x + 1) < 64u ? s.labmask32[x.x + 1] : 0u;
+    while (m) {
+      const int a = __ffs(m) - 1;
+      m &= m - 1;
+      f(s.a_slot[a], x.y, 1, a, eb);
+    }
+  } else {
+    unsigned long long m = (unsigned)(x.x + 1) < 64u ? s.labmask[x.x + 1] : 0ull;
+    while (m) {
+      const int a = __ffsll((long long)m) - 1;
+      m &= m - 1;
+      f(s.a_slot[a], x.y, 1, a, eb);
+    }
   }
   if (x.x == FST_EPS) f(0, x.y, 3, -1, eb);
 }
 
-template <typename F>
+template <bool kM32, typename F>
 __device__ __forceinline__ void fast_state(const TaskSmem& s, const int2* __restrict__ ikd, int32_t ub, int32_t e,
                                            int32_t e1, F&& f) {
   for (int a = 0; a < s.aeps; ++a) f(s.a_slot[a], ub, 2, a, -1);
   // items e .. e1-1 are the arcs (view positions e - ub - 1)
   for (; e + 2 <= e1; e += 2) {
     const int2 x0 = __ldg(&ikd[e]), x1 = __ldg(&ikd[e + 1]);
-    fast_arc(s, x0, e - ub - 1, f);
-    fast_arc(s, x1, e - ub, f);
+    fast_arc<kM32>(s, x0, e - ub - 1, f);
+    fast_arc<kM32>(s, x1, e - ub, f);
   }
-  if (e < e1) fast_arc(s, __ldg(&ikd[e]), e - ub - 1, f);
+  if (e < e1) fast_arc<kM32>(s, __ldg(&ikd[e]), e - ub - 1, f);
 }
 
-// BFS block: claims into the staged NEW bits.  Returns false (nothing done) never; heavy states are
-// walked cooperatively after the per-thread pass.
-template <bool kStage2>
-__device__ __forceinline__ void bfs_block_fast(TaskSmem& s, const ViewDev& Bv, int32_t ub0, int32_t ub1, int lw0,
-                                               int wpr, const uint32_t* Rs, const uint32_t* VS, uint32_t* NW,
-                                               unsigned& kept) {
-  const int2* __restrict__ ikd = Bv.ikd;
-  const int32_t* __restrict__ off = Bv.off;
-  auto cand = [&](int slot, int32_t col, int, int, int32_t) {
-    const int idx = slot * wpr + (col >> 5);
-    const uint32_t bit = 1u << (col & 31);
-    if (kStage2) {
-      if (!(Rs[idx] & bit)) return;
-      ++kept;
-    }
-    if ((VS[idx] | NW[idx]) & bit) return;
-    atomicOr(&NW[idx], bit);
-  };
-  if (threadIdx.x == 0) s.nheavy = 0;
+// Compact the set bits of s.fw[w0, w1) (at most 1024 of them) into s.state; word w0 holds states
+// ub_w0 ..  Returns the count (all threads).
+__device__ __forceinline__ int compact_words(TaskSmem& s, int w0, int w1, int32_t ub_w0) {
+  const int wa = w0 + 2 * threadIdx.x;
+  const uint32_t x0 = wa < w1 ? s.fw[wa] : 0u, x1 = wa + 1 < w1 ? s.fw[wa + 1] : 0u;
+  int tot;
+  const int ex = block_excl_scan(__popc(x0) + __popc(x1), s.red32, &tot);
+  int pos = ex;
+  for (uint32_t m = x0; m; m &= m - 1) s.state[pos++] = ub_w0 + 64 * threadIdx.x + __ffs(m) - 1;
+  for (uint32_t m = x1; m; m &= m - 1) s.state[pos++] = ub_w0 + 64 * threadIdx.x + 32 + __ffs(m) - 1;
   __syncthreads();
-  for (int i = threadIdx.x; i < ub1 - ub0; i += kThreads) {
-    if (!((s.fw[lw0 + (i >> 5)] >> (i & 31)) & 1u)) continue;
-    const int32_t ub = ub0 + i;
-    const int32_t e = __ldg(&off[ub]) + ub + 1, e1 = __ldg(&off[ub + 1]) + ub + 1;
-    if (e1 - e > kHeavy) {
-      for (int a = 0; a < s.aeps; ++a) cand(s.a_slot[a], ub, 2, a, -1);
-      s.state[atomicAdd(&s.nheavy, 1)] = ub;
-      continue;
-    }
-    fast_state(s, ikd, ub, e, e1, cand);
-  }
-  __syncthreads();
-  for (int h = 0; h < s.nheavy; ++h) {
-    const int32_t ub = s.state[h];
-    const int32_t e0 = __ldg(&off[ub]) + ub + 1, e1 = __ldg(&off[ub + 1]) + ub + 1;
-    for (int32_t e = e0 + threadIdx.x; e < e1; e += kThreads) fast_arc(s, __ldg(&ikd[e]), e - ub - 1, cand);
-  }
-  __syncthreads();
+  return tot;
 }
 
 
 // Whole-chunk BFS walk (fast path): one thread per source state of the chunk, no per-block barriers.
 // kStaged: candidates claimed in the staged NEW bits; else test-and-set on the global bitmaps.
 // Per-block kept counts (stage 2) are accumulated warp-aggregated in s.keptc[].
-template <bool kStage2, bool kStaged, typename Glob>
-__device__ __forceinline__ void bfs_chunk_fast(TaskSmem& s, const ViewDev& Bv, int32_t cub0, int32_t cub1, int wpr,
-                                               const uint32_t* Rs, const uint32_t* VS, uint32_t* NW, Glob&& glob) {
+template <bool kStage2, bool kStaged, bool kM32, typename Glob>
+__device__ __forceinline__ void bfs_chunk_fast(TaskSmem& s, const ViewDev& Bv, int32_t cub0, int32_t cub1, int nst,
+                                               int wpr, const uint32_t* Rs, const uint32_t* VS, uint32_t* NW,
+                                               Glob&& glob) {
   const int2* __restrict__ ikd = Bv.ikd;
   const int32_t* __restrict__ off = Bv.off;
   unsigned kept = 0;
@@ -645,35 +633,79 @@ __device__ __forceinline__ void bfs_chunk_fast(TaskSmem& s, const ViewDev& Bv, i
   };
   if (threadIdx.x == 0) s.nheavy = 0;
   if (threadIdx.x < kChunkMaxBlocks) s.keptc[threadIdx.x] = 0ull;
-  __syncthreads();
-  const int n = cub1 - cub0;
-  for (int i0 = 0; i0 < n; i0 += kThreads) {  // uniform trip count: warps stay inside one block
-    const int i = i0 + threadIdx.x;
-    kept = 0;
-    if (i < n && ((s.fw[i >> 5] >> (i & 31)) & 1u)) {
-      const int32_t ub = cub0 + i;
-      const int32_t e = __ldg(&off[ub]) + ub + 1, e1 = __ldg(&off[ub + 1]) + ub + 1;
-      if (e1 - e > kHeavy) {
-        for (int a = 0; a < s.aeps; ++a) cand(s.a_slot[a], ub, 2, a, -1);
-        const int h = atomicAdd(&s.nheavy, 1);
-        if (h < kPairsPerBlock) s.state[h] = ub;
-        else fast_state(s, ikd, ub, e, e1, cand);  // list full: walk it here
-      } else {
-        fast_state(s, ikd, ub, e, e1, cand);
+  // walk a compacted list of source states: each warp takes 32 consecutive states and spreads their
+  // arcs over its lanes in rounds of 32 (uniform, coalesced); heavy states are deferred to the CTA
+  const int lane = threadIdx.x & 31;
+  auto walk = [&](int n) {
+    for (int base = (threadIdx.x & ~31); base < n; base += kThreads) {
+      const int k = base + lane;
+      int32_t ub = 0, e = 0, deg = 0;
+      if (k < n) {
+        ub = s.state[k];
+        e = __ldg(&off[ub]) + ub + 1;
+        deg = __ldg(&off[ub + 1]) + ub + 1 - e;
+        kept = 0;
+        for (int a = 0; a < s.aeps; ++a) cand(s.a_slot[a], ub, 2, a, -1);  // M2 moves of the state
+        if (kStage2 && kept) atomicAdd(&s.keptc[(ub - cub0) >> 10], (unsigned long long)kept);
+        if (deg > kHeavy) {
+          const int h = atomicAdd(&s.nheavy, 1);
+          if (h < kPairsPerBlock) {
+            s.cur[h] = ub;
+            deg = 0;
+          }
+        }
+      }
+      const int incl = warp_incl_scan(deg);
+      const int start = incl - deg;
+      const int total = __shfl_sync(0xffffffffu, incl, 31);
+      kept = 0;
+      // kept moves are attributed to the 1024-pair block of the arc's source state
+      int kb = (__shfl_sync(0xffffffffu, ub, 0) - cub0) >> 10;
+      for (int r = 0; r < total; r += 32) {
+        const int c = r + lane;
+        int j = 0;
+#pragma unroll
+        for (int step = 16; step > 0; step >>= 1)
+          if (__shfl_sync(0xffffffffu, start, j + step) <= c) j += step;
+        const int32_t ej = __shfl_sync(0xffffffffu, e, j) + (c - __shfl_sync(0xffffffffu, start, j));
+        const int32_t uj = __shfl_sync(0xffffffffu, ub, j);
+        if (c < total) {
+          if (kStage2 && ((uj - cub0) >> 10) != kb) {
+            if (kept) atomicAdd(&s.keptc[kb], (unsigned long long)kept);
+            kept = 0;
+            kb = (uj - cub0) >> 10;
+          }
+          fast_arc<kM32>(s, __ldg(&ikd[ej]), ej - uj - 1, cand);
+        }
+      }
+      if (kStage2) {
+        if (__all_sync(0xffffffffu, kb == __shfl_sync(0xffffffffu, kb, 0))) {
+          const unsigned long long t = warp_sum((unsigned long long)kept);
+          if (lane == 0 && t) atomicAdd(&s.keptc[kb], t);
+        } else if (kept) {
+          atomicAdd(&s.keptc[kb], (unsigned long long)kept);
+        }
       }
     }
-    if (kStage2) {
-      const unsigned long long k = warp_sum((unsigned long long)kept);
-      if ((threadIdx.x & 31) == 0 && k) atomicAdd(&s.keptc[(i0 + (threadIdx.x & ~31)) >> 10], k);
+  };
+  const int nw = (cub1 - cub0 + 31) >> 5;
+  if (nst <= kPairsPerBlock) {  // sparse chunk: one compaction for all of it
+    const int n = compact_words(s, 0, nw, cub0);
+    walk(n);
+    __syncthreads();
+  } else {
+    for (int w0 = 0; w0 < nw; w0 += 32) {
+      const int n = compact_words(s, w0, min(w0 + 32, nw), cub0 + 32 * w0);
+      walk(n);
+      __syncthreads();
     }
   }
-  __syncthreads();
   const int nh = min(s.nheavy, kPairsPerBlock);
   for (int h = 0; h < nh; ++h) {
-    const int32_t ub = s.state[h];
+    const int32_t ub = s.cur[h];
     const int32_t e0 = __ldg(&off[ub]) + ub + 1, e1 = __ldg(&off[ub + 1]) + ub + 1;
     kept = 0;
-    for (int32_t e = e0 + threadIdx.x; e < e1; e += kThreads) fast_arc(s, __ldg(&ikd[e]), e - ub - 1, cand);
+    for (int32_t e = e0 + threadIdx.x; e < e1; e += kThreads) fast_arc<kM32>(s, __ldg(&ikd[e]), e - ub - 1, cand);
     if (kStage2) {
       const unsigned long long k = warp_sum((unsigned long long)kept);
       if ((threadIdx.x & 31) == 0 && k) atomicAdd(&s.keptc[(ub - cub0) >> 10], k);
@@ -794,26 +826,29 @@ __global__ void __launch_bounds__(kThreads, 2) k_level(Ctx cx, int level) {
         push_bits(C, c.row, c.col, gw, bit, Fn, flagn, listn, ctrl_nxt);
       }
     };
-    if (s.small) {  // fast path: whole chunk in one barrier-free pass
+    if (s.small) {  // fast path: compacted source states, one thread per state
       const int32_t cub0 = ch.b0 * kPairsPerBlock, cub1 = min(ch.b1 * kPairsPerBlock, C.VB);
+      auto glob = [&](int slot, int32_t col) -> unsigned {
+        const int32_t row = s.slot_row[slot];
+        const int64_t gw = C.W + (int64_t)row * wpr + (col >> 5);
+        const uint32_t bit = 1u << (col & 31);
+        unsigned k = 0;
+        if (kStage2) {
+          if (!(__ldg(&cx.R[gw]) & bit)) return 0u;
+          k = 1;
+        }
+        if (vis[gw] & bit) return k;
+        if (atomicOr(&vis[gw], bit) & bit) return k;
+        ++nnew;
+        push_bits(C, row, col, gw, bit, Fn, flagn, listn, ctrl_nxt);
+        return k;
+      };
       if (staged) {
-        bfs_chunk_fast<kStage2, true>(s, Bv, cub0, cub1, wpr, Rs, VS, NW, [](int, int32_t) { return 0u; });
+        if (s.mask32) bfs_chunk_fast<kStage2, true, true>(s, Bv, cub0, cub1, nst, wpr, Rs, VS, NW, glob);
+        else bfs_chunk_fast<kStage2, true, false>(s, Bv, cub0, cub1, nst, wpr, Rs, VS, NW, glob);
       } else {
-        bfs_chunk_fast<kStage2, false>(s, Bv, cub0, cub1, wpr, Rs, VS, NW, [&](int slot, int32_t col) -> unsigned {
-          const int32_t row = s.slot_row[slot];
-          const int64_t gw = C.W + (int64_t)row * wpr + (col >> 5);
-          const uint32_t bit = 1u << (col & 31);
-          unsigned k = 0;
-          if (kStage2) {
-            if (!(__ldg(&cx.R[gw]) & bit)) return 0u;
-            k = 1;
-          }
-          if (vis[gw] & bit) return k;
-          if (atomicOr(&vis[gw], bit) & bit) return k;
-          ++nnew;
-          push_bits(C, row, col, gw, bit, Fn, flagn, listn, ctrl_nxt);
-          return k;
-        });
+        if (s.mask32) bfs_chunk_fast<kStage2, false, true>(s, Bv, cub0, cub1, nst, wpr, Rs, VS, NW, glob);
+        else bfs_chunk_fast<kStage2, false, false>(s, Bv, cub0, cub1, nst, wpr, Rs, VS, NW, glob);
       }
       if (kStage2 && (int)threadIdx.x < ch.b1 - ch.b0 && s.keptc[threadIdx.x])
         cx.kept[C.K + (int64_t)ch.ua * C.bpr + ch.b0 + threadIdx.x] += s.keptc[threadIdx.x];
@@ -1055,8 +1090,8 @@ __global__ void __launch_bounds__(kThreads, 2) k_emit(Ctx cx, const int64_t* __r
           if (i < nub && src_bit(s, lw0, ub0, ub0 + i)) {
             const int32_t ub = ub0 + i;
             int c = 0;
-            fast_state(s, ikd, ub, __ldg(&boff[ub]) + ub + 1, __ldg(&boff[ub + 1]) + ub + 1,
-                       [&](int slot, int32_t col, int, int, int32_t) { c += present(slot, col); });
+            fast_state<false>(s, ikd, ub, __ldg(&boff[ub]) + ub + 1, __ldg(&boff[ub + 1]) + ub + 1,
+                              [&](int slot, int32_t col, int, int, int32_t) { c += present(slot, col); });
             c2[j] = c;
           }
         }
@@ -1095,7 +1130,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_emit(Ctx cx, const int64_t* __r
           for (int win = q0; win < q1; win += kWCap) {
             if (has && my1 > win && my0 < win + kWCap) {
               int p = my0;
-              fast_state(s, ikd, ub, __ldg(&boff[ub]) + ub + 1, __ldg(&boff[ub + 1]) + ub + 1,
+              fast_state<false>(s, ikd, ub, __ldg(&boff[ub]) + ub + 1, __ldg(&boff[ub + 1]) + ub + 1,
                          [&](int slot, int32_t col, int kind, int a, int32_t eb) {
                            bool pr;
                            const int32_t did = rank_of(slot, 0, col, pr);

@@ -24,4 +24,7 @@ for i in range(args.n + 1):
     c = fstc.fst_compose(a, b)
     print(i, c.num_states, c.num_arcs, {k: round(v, 3) if isinstance(v, float) else v for k, v in c.stats().items()},
           flush=True)
+    if i == args.n:
+        print("stage1 levels", c.level_sizes(1))
+        print("stage2 levels", c.level_sizes(2))
     c.free()
