@@ -592,6 +592,132 @@ __device__ __forceinline__ void fast_state(const TaskSmem& s, const int2* __rest
   if (e < e1) fast_arc<kM32>(s, __ldg(&ikd[e]), e - ub - 1, f);
 }
 
+// Same walk over the 16-byte items (label, other, carry, weight bits): g(slot, col, kind, a, carry, wbits)
+template <bool kM32, typename G>
+__device__ __forceinline__ void fast_state4(const TaskSmem& s, const int4* __restrict__ ikcw, int32_t ub, int32_t e,
+                                            int32_t e1, G&& g) {
+  for (int a = 0; a < s.aeps; ++a) g(s.a_slot[a], ub, 2, a, 0, 0);
+  auto one = [&](const int4 x) {
+    if (kM32) {
+      uint32_t m = (unsigned)(x.x + 1) < 64u ? s.labmask32[x.x + 1] : 0u;
+      while (m) {
+        const int a = __ffs(m) - 1;
+        m &= m - 1;
+        g(s.a_slot[a], x.y, 1, a, x.z, x.w);
+      }
+    } else {
+      unsigned long long m = (unsigned)(x.x + 1) < 64u ? s.labmask[x.x + 1] : 0ull;
+      while (m) {
+        const int a = __ffsll((long long)m) - 1;
+        m &= m - 1;
+        g(s.a_slot[a], x.y, 1, a, x.z, x.w);
+      }
+    }
+    if (x.x == FST_EPS) g(0, x.y, 3, -1, x.z, x.w);
+  };
+  for (; e + 2 <= e1; e += 2) {
+    const int4 x0 = __ldg(&ikcw[e]), x1 = __ldg(&ikcw[e + 1]);
+    one(x0);
+    one(x1);
+  }
+  if (e < e1) one(__ldg(&ikcw[e]));
+}
+
+// Fast emit of one dense block (staged rows, label masks, no heavy state): per-thread state walks,
+// block scan of per-state counts, then per-warp windows of kWCap slots staged in shared memory and
+// stored coalesced.  Returns the block's arc count.
+template <bool kM32, typename Rank, typename StateOut>
+__device__ __forceinline__ int emit_block_fast(TaskSmem& s, const ViewDev& Bv, const CompDev& C, int32_t ub0,
+                                               int32_t ub1, int lw0, int wpr, const uint32_t* Vs, uint32_t* wb,
+                                               int64_t run, Rank&& rank_of, StateOut&& state_out) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int2* __restrict__ ikd = Bv.ikd;
+  const int4* __restrict__ ikcw = Bv.ikcw;
+  const int32_t* __restrict__ boff = Bv.off;
+  const int nub = ub1 - ub0;
+  auto present = [&](int slot, int32_t col) -> bool { return (Vs[slot * wpr + (col >> 5)] >> (col & 31)) & 1u; };
+  // count: states 2t, 2t+1 of thread t
+  int c2[2] = {0, 0};
+#pragma unroll
+  for (int j = 0; j < 2; ++j) {
+    const int i = 2 * threadIdx.x + j;
+    if (i < nub && ((s.fw[lw0 + (i >> 5)] >> (i & 31)) & 1u)) {
+      const int32_t ub = ub0 + i;
+      int c = 0;
+      fast_state<kM32>(s, ikd, ub, __ldg(&boff[ub]) + ub + 1, __ldg(&boff[ub + 1]) + ub + 1,
+                       [&](int slot, int32_t col, int, int, int32_t) { c += present(slot, col); });
+      c2[j] = c;
+    }
+  }
+  int btot;
+  const int ex = block_excl_scan(c2[0] + c2[1], s.red32, &btot);
+  s.cur[2 * threadIdx.x] = ex;
+  s.cur[2 * threadIdx.x + 1] = ex + c2[0];
+  if (threadIdx.x == 0) s.cur[kPairsPerBlock] = btot;
+  __syncthreads();
+  int32_t* bd = (int32_t*)wb;
+  int32_t* bi = (int32_t*)(wb + kWCap);
+  int32_t* bo = (int32_t*)(wb + 2 * kWCap);
+  float* bw = (float*)(wb + 3 * kWCap);
+  for (int r = 0; r < 2; ++r) {
+    const int first = warp * 64 + r * 32;
+    const int i = first + lane;
+    const int32_t ub = ub0 + i;
+    const bool has = i < nub && ((s.fw[lw0 + (i >> 5)] >> (i & 31)) & 1u);
+    const int q0 = s.cur[first], q1 = s.cur[first + 32];
+    const int my0 = s.cur[i], my1 = s.cur[i + 1];
+    if (has) state_out(ub, run + my0);
+    for (int win = q0; win < q1; win += kWCap) {
+      if (has && my1 > win && my0 < win + kWCap) {
+        int p = my0;
+        fast_state4<kM32>(s, ikcw, ub, __ldg(&boff[ub]) + ub + 1, __ldg(&boff[ub + 1]) + ub + 1,
+                          [&](int slot, int32_t col, int kind, int a, int32_t carry, int32_t wbits) {
+                            bool pr;
+                            const int32_t did = rank_of(slot, col, pr);
+                            if (!pr) return;
+                            const int t = p - win;
+                            ++p;
+                            if ((unsigned)t >= (unsigned)kWCap) return;
+                            int32_t il, ol;
+                            float wt;
+                            if (kind == 1) {
+                              il = s.a_carry[a];
+                              ol = carry;
+                              wt = __fadd_rn(s.a_w[a], __int_as_float(wbits));  // one binary32 add, RN-even
+                            } else if (kind == 2) {
+                              il = s.a_carry[a];
+                              ol = FST_EPS;
+                              wt = s.a_w[a];  // bit copy
+                            } else {
+                              il = FST_EPS;
+                              ol = carry;
+                              wt = __int_as_float(wbits);  // bit copy
+                            }
+                            bd[t] = did;
+                            bi[t] = il;
+                            bo[t] = ol;
+                            bw[t] = wt;
+                          });
+      }
+      __syncwarp();
+      const int n = min(kWCap, q1 - win);
+      int32_t* __restrict__ od = C.dst;
+      int32_t* __restrict__ oi = C.ilabel;
+      int32_t* __restrict__ oo = C.olabel;
+      float* __restrict__ ow = C.weight;
+      for (int t = lane; t < n; t += 32) {
+        const int64_t pos = run + win + t;
+        __stcs(&od[pos], bd[t]);
+        __stcs(&oi[pos], bi[t]);
+        __stcs(&oo[pos], bo[t]);
+        __stcs(&ow[pos], bw[t]);
+      }
+      __syncwarp();
+    }
+  }
+  return btot;
+}
+
 // Compact the set bits of s.fw[w0, w1) (at most 1024 of them) into s.state; word w0 holds states
 // ub_w0 ..  Returns the count (all threads).
 __device__ __forceinline__ int compact_words(TaskSmem& s, int w0, int w1, int32_t ub_w0) {
@@ -1075,104 +1201,20 @@ __global__ void __launch_bounds__(kThreads, 2) k_emit(Ctx cx, const int64_t* __r
         fastE = !__syncthreads_or(hv);
       }
       if (fastE) {
-        const int2* __restrict__ ikd = Bv.ikd;
-        const int32_t* __restrict__ boff = Bv.off;
-        const int2* __restrict__ bcw = Bv.cw;
-        const int nub = ub1 - ub0;
-        auto present = [&](int slot, int32_t col) -> bool {
-          return (Vs[slot * wpr + (col >> 5)] >> (col & 31)) & 1u;
-        };
-        // count: states 2t, 2t+1 of thread t
-        int c2[2] = {0, 0};
-#pragma unroll
-        for (int j = 0; j < 2; ++j) {
-          const int i = 2 * threadIdx.x + j;
-          if (i < nub && src_bit(s, lw0, ub0, ub0 + i)) {
-            const int32_t ub = ub0 + i;
-            int c = 0;
-            fast_state<false>(s, ikd, ub, __ldg(&boff[ub]) + ub + 1, __ldg(&boff[ub + 1]) + ub + 1,
-                              [&](int slot, int32_t col, int, int, int32_t) { c += present(slot, col); });
-            c2[j] = c;
-          }
-        }
-        int btot;
-        const int ex = block_excl_scan(c2[0] + c2[1], s.red32, &btot);
-        s.cur[2 * threadIdx.x] = ex;
-        s.cur[2 * threadIdx.x + 1] = ex + c2[0];
-        if (threadIdx.x == 0) {
-          s.cur[kPairsPerBlock] = btot;
-          if ((unsigned long long)btot != cx.kept[gblk]) atomicAdd(&cx.misc[2], 1ull);
-        }
-        __syncthreads();
-        // write: warp w owns states [64w, 64w+64) in two rounds of 32; its arcs are contiguous and are
-        // staged per window of kWCap slots in shared memory, then stored coalesced
         uint32_t* wb = dyn + 2 * s.m * wpr + warp * kWCap * 4;
-        int32_t* bd = (int32_t*)wb;
-        int32_t* bi = (int32_t*)(wb + kWCap);
-        int32_t* bo = (int32_t*)(wb + 2 * kWCap);
-        float* bw = (float*)(wb + 3 * kWCap);
-        for (int r = 0; r < 2; ++r) {
-          const int first = warp * 64 + r * 32;
-          const int i = first + lane;
-          const int32_t ub = ub0 + i;
-          const bool has = i < nub && src_bit(s, lw0, ub0, ub);
-          const int q0 = s.cur[first], q1 = s.cur[first + 32];
-          const int my0 = s.cur[i], my1 = s.cur[i + 1];
-          if (has) {  // per-state outputs
-            bool pr;
-            const int32_t id = rank_of(0, ua, ub, pr);
-            __stcs((long long*)&C.row_ptr[id], (long long)(run + my0));
-            __stcs(&C.pair_a[id], ua);
-            __stcs(&C.pair_b[id], ub);
-            C.is_start[id] = (uint8_t)(stA & __ldg(&C.startB[ub]));
-            C.is_accept[id] = (uint8_t)(acA & __ldg(&C.accB[ub]));
-          }
-          for (int win = q0; win < q1; win += kWCap) {
-            if (has && my1 > win && my0 < win + kWCap) {
-              int p = my0;
-              fast_state<false>(s, ikd, ub, __ldg(&boff[ub]) + ub + 1, __ldg(&boff[ub + 1]) + ub + 1,
-                         [&](int slot, int32_t col, int kind, int a, int32_t eb) {
-                           bool pr;
-                           const int32_t did = rank_of(slot, 0, col, pr);
-                           if (!pr) return;
-                           const int t = p - win;
-                           ++p;
-                           if (t < 0 || t >= kWCap) return;
-                           int32_t il, ol;
-                           float wt;
-                           if (kind == 1) {
-                             const int2 b = __ldg(&bcw[eb]);
-                             il = s.a_carry[a];
-                             ol = b.x;
-                             wt = __fadd_rn(s.a_w[a], __int_as_float(b.y));  // one binary32 add, RN-even
-                           } else if (kind == 2) {
-                             il = s.a_carry[a];
-                             ol = FST_EPS;
-                             wt = s.a_w[a];  // bit copy
-                           } else {
-                             const int2 b = __ldg(&bcw[eb]);
-                             il = FST_EPS;
-                             ol = b.x;
-                             wt = __int_as_float(b.y);  // bit copy
-                           }
-                           bd[t] = did;
-                           bi[t] = il;
-                           bo[t] = ol;
-                           bw[t] = wt;
-                         });
-            }
-            __syncwarp();
-            const int n = min(kWCap, q1 - win);
-            for (int t = lane; t < n; t += 32) {
-              const int64_t pos = run + win + t;
-              __stcs(&C.dst[pos], bd[t]);
-              __stcs(&C.ilabel[pos], bi[t]);
-              __stcs(&C.olabel[pos], bo[t]);
-              __stcs(&C.weight[pos], bw[t]);
-            }
-            __syncwarp();
-          }
-        }
+        auto rk = [&](int slot, int32_t col, bool& pr) -> int32_t { return rank_of(slot, 0, col, pr); };
+        auto so = [&](int32_t ub, int64_t at) {
+          bool pr;
+          const int32_t id = rank_of(0, ua, ub, pr);
+          __stcs((long long*)&C.row_ptr[id], (long long)at);
+          __stcs(&C.pair_a[id], ua);
+          __stcs(&C.pair_b[id], ub);
+          C.is_start[id] = (uint8_t)(stA & __ldg(&C.startB[ub]));
+          C.is_accept[id] = (uint8_t)(acA & __ldg(&C.accB[ub]));
+        };
+        const int btot = s.mask32 ? emit_block_fast<true>(s, Bv, C, ub0, ub1, lw0, wpr, Vs, wb, run, rk, so)
+                                  : emit_block_fast<false>(s, Bv, C, ub0, ub1, lw0, wpr, Vs, wb, run, rk, so);
+        if (threadIdx.x == 0 && (unsigned long long)btot != cx.kept[gblk]) atomicAdd(&cx.misc[2], 1ull);
         run += btot;
         __syncthreads();
       } else if (s.G != 0 && cx.vcount[gblk] * 4 >= ub1 - ub0) {
@@ -1469,7 +1511,7 @@ fst_status compose_impl(int32_t n, const fst_handle* a, const fst_handle* b, cud
     const fst* B = b[i];
     CompDev& C = comps[i];
     memset(&C, 0, sizeof(C));
-    auto vd = [](const View& v) { return ViewDev{v.off, v.key, v.other, v.carry, v.w, v.cw, v.ikd, v.isrc, v.lm_other, v.lm_pos, v.seg_node, v.seg_beg, v.lab_val, v.lab_seg, v.nlab}; };
+    auto vd = [](const View& v) { return ViewDev{v.off, v.key, v.other, v.carry, v.w, v.cw, v.ikd, v.isrc, v.ikcw, v.lm_other, v.lm_pos, v.seg_node, v.seg_beg, v.lab_val, v.lab_seg, v.nlab}; };
     C.Af = vd(A->views[kOutByOlabel]);
     C.Ab = vd(A->views[kInByOlabel]);
     C.Bf = vd(B->views[kOutByIlabel]);

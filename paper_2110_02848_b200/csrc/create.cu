@@ -182,15 +182,19 @@ __global__ void k_view_offsets(int32_t V, int64_t E, const unsigned long long* _
 // items of a view: node v owns [off[v]+v, off[v+1]+v+1): sentinel, then its arcs in view order
 __global__ void k_view_items(int32_t V, int64_t E, const int32_t* __restrict__ off, const int32_t* __restrict__ key,
                              const int32_t* __restrict__ other, const unsigned long long* __restrict__ keys, int LB,
-                             int2* __restrict__ ikd, int32_t* __restrict__ isrc) {
+                             const int2* __restrict__ cw, int2* __restrict__ ikd, int32_t* __restrict__ isrc,
+                             int4* __restrict__ ikcw) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < E) {
     const int32_t v = (int32_t)(keys[i] >> LB);
+    const int2 c = cw[i];
     ikd[i + v + 1] = make_int2(key[i], other[i]);
+    ikcw[i + v + 1] = make_int4(key[i], other[i], c.x, c.y);
     isrc[i + v + 1] = v;
   }
   if (i < V) {
     ikd[off[i] + i] = make_int2(kSentinel, (int32_t)i);
+    ikcw[off[i] + i] = make_int4(kSentinel, (int32_t)i, 0, 0);
     isrc[off[i] + i] = (int32_t)i;
   }
 }
@@ -304,7 +308,7 @@ fst_status build_views(fst* h, cudaStream_t s, int32_t max_il, int32_t max_ol) {
   size_t vbytes = 0;
   for (int k = 0; k < 4; ++k)
     vbytes += carve_bytes<int32_t>(V + 1) + 4 * carve_bytes<int32_t>(E) + carve_bytes<float>(E) +
-              carve_bytes<int2>(E) + carve_bytes<int2>(E + V) + carve_bytes<int32_t>(E + V) +
+              carve_bytes<int2>(E) + carve_bytes<int2>(E + V) + carve_bytes<int32_t>(E + V) + carve_bytes<int4>(E + V) +
               4 * carve_bytes<int32_t>(E) + 2 * carve_bytes<int32_t>(E + 1);
   vbytes += 2 * carve_bytes<int32_t>(V);
   BufferPtr vb;
@@ -323,6 +327,7 @@ fst_status build_views(fst* h, cudaStream_t s, int32_t max_il, int32_t max_ol) {
     w.cw = cv.take<int2>(E);
     w.ikd = cv.take<int2>(E + V);
     w.isrc = cv.take<int32_t>(E + V);
+    w.ikcw = cv.take<int4>(E + V);
     w.lm_other = cv.take<int32_t>(E);
     w.lm_pos = cv.take<int32_t>(E);
     w.seg_node = cv.take<int32_t>(E);
@@ -399,8 +404,8 @@ fst_status build_views(fst* h, cudaStream_t s, int32_t max_il, int32_t max_ol) {
       FSTC_LAUNCH_CHECK();
       k_view_offsets<<<nblk(E + 1, 256), 256, 0, s>>>(V, E, ka, LB, w.off);
       FSTC_LAUNCH_CHECK();
-      k_view_items<<<nblk(std::max<int64_t>(E, V), 256), 256, 0, s>>>(V, E, w.off, w.key, w.other, ka, LB, w.ikd,
-                                                                        w.isrc);
+      k_view_items<<<nblk(std::max<int64_t>(E, V), 256), 256, 0, s>>>(V, E, w.off, w.key, w.other, ka, LB, w.cw,
+                                                                        w.ikd, w.isrc, w.ikcw);
       FSTC_LAUNCH_CHECK();
       if (!by_ol) {  // B role: label-major segment index
         FSTC_CUDA_TRY(cudaMemcpyAsync(vkeys, ka, sizeof(unsigned long long) * E, cudaMemcpyDeviceToDevice, s));
@@ -436,7 +441,8 @@ fst_status build_views(fst* h, cudaStream_t s, int32_t max_il, int32_t max_ol) {
     } else {
       FSTC_CUDA_TRY(cudaMemsetAsync(w.off, 0, sizeof(int32_t) * (V + 1), s));
       if (V > 0) {
-        k_view_items<<<nblk(V, 256), 256, 0, s>>>(V, 0, w.off, w.key, w.other, nullptr, LB, w.ikd, w.isrc);
+        k_view_items<<<nblk(V, 256), 256, 0, s>>>(V, 0, w.off, w.key, w.other, nullptr, LB, w.cw, w.ikd, w.isrc,
+                                                  w.ikcw);
         FSTC_LAUNCH_CHECK();
       }
     }

@@ -39,6 +39,7 @@ struct View {
   int2* cw = nullptr;        // [E] packed (carry, weight bits): the per-arc data of the emit
   int2* ikd = nullptr;       // [E+V] items: per node a sentinel (kSentinel, node) then (key, other) of its arcs
   int32_t* isrc = nullptr;   // [E+V] item -> node
+  int4* ikcw = nullptr;      // [E+V] items with (key, other, carry, weight bits); sentinel = (kSentinel, node, 0, 0)
   // label-major segment index (B-role views): arcs ordered by (label, node, view position); a
   // segment is a run of equal (label, node)
   int32_t* lm_other = nullptr;  // [E] other-end node

@@ -32,6 +32,7 @@ struct ViewDev {
   const int2* ikd;        // [E+V] items: node v owns items [off[v]+v, off[v+1]+v+1): a sentinel
                           //       (kSentinel, v) then (key, other) of its arcs in view order
   const int32_t* isrc;    // [E+V] item -> node
+  const int4* ikcw;       // [E+V] items with (key, other, carry, weight bits)
   // label-major segment index (B role): see View in fstc_handle.h
   const int32_t* lm_other;
   const int32_t* lm_pos;
