@@ -36,8 +36,11 @@ WORKLOADS = {
     "c4": ("configs[3] large random composition: acceptors V=20000, D=8, 16 tokens", 20000, 8, 16),
     "c4-d4": ("configs[3] large random composition: acceptors V=20000, D=4, 8 tokens", 20000, 4, 8),
     "c4-paper": ("paper point PAPER.md:316-325: acceptors V=8192, D=5, 10 tokens", 8192, 5, 10),
+    "c5": ("configs[4] batched lexicon x emissions: closure(10k-word letter lexicon) composed with "
+           "32 emissions graphs per GPU (T_i = 100 + rand(401), 28 tokens), fst_compose_batch", 0, 0, 28),
 }
 REF_SAMPLE_V = {"c4": 1024, "c4-d4": 2048, "c4-paper": 1024}  # oracle sample sizes (~2-8 s per step)
+UTTS_PER_GPU = 32
 L2_FLUSH_BYTES = 512 << 20
 
 
@@ -47,6 +50,17 @@ def peaks():
         d = json.load(open(p))
         return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
     return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def c5_shard(rank: int, world: int):
+    """LPT shard (by frames T_i) of the 32*world-utterance batch for this rank; closure(lexicon)."""
+    from paper_2110_02848_b200 import parallel
+    n = UTTS_PER_GPU * world
+    Ts = [100 + fstgen.SplitMix64(10000 + i).below(401) for i in range(n)]
+    mine = parallel.shard_for_rank(Ts, rank, world)
+    B = fstgen.closure(fstgen.lexicon_graph(fstgen.letter_lexicon(10000, 4321)))
+    As = [fstgen.emissions_graph(Ts[i], 10000 + i) for i in mine]
+    return As, B, mine
 
 
 def make_inputs(workload: str, rank: int):
@@ -120,10 +134,7 @@ def run_reference(args):
         return 0
     import oracle
     oracle.build()
-    V = REF_SAMPLE_V[args.workload]
-    _, _, D, T = WORKLOADS[args.workload]
-    A = fstgen.random_graph(V, D, T, 1000 + V + D)
-    B = fstgen.random_graph(V, D, T, 2000 + V + D)
+    A, B, sample = reference_sample(args.workload)
     for _ in range(args.warmup):
         oracle.compose(A, B)
     times, arcs = [], 0
@@ -139,24 +150,33 @@ def run_reference(args):
         "impl": "reference", "metric": "composed arcs/sec", "value": value, "unit": "arcs/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": WORKLOADS[args.workload][0], "sample": f"oracle on V={V} (same generator, D={D}, "
-                   f"{T} tokens): {arcs} composed arcs per step", "parallelism": "single host thread"},
+        "config": {"workload": WORKLOADS[args.workload][0], "sample": f"{sample}: {arcs} composed arcs per step",
+                   "parallelism": "single host thread"},
         "cpu_baseline": {"value": value, "unit": "arcs/s", "cores": cores, "kind": "oracle",
-                         "sample": f"Algorithm 1 C oracle, V={V} D={D} T={T}, {arcs} arcs/step, single-threaded"},
+                         "sample": f"Algorithm 1 C oracle on {sample}, {arcs} arcs/step, single-threaded"},
         "e2e": {"value": value, "unit": "arcs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
     return 0
 
 
-# ------------------------------------------------------------------------------------ our arm
-def cpu_baseline(workload: str, budget_s: float = 12.0):
-    import oracle
-    oracle.build()
+def reference_sample(workload: str):
+    """Bounded sample of the workload for the CPU oracle (about 2-10 s per composition)."""
+    if workload == "c5":
+        As, B, _ = c5_shard(0, 1)
+        return As[0], B, f"utterance 0 of the c5 batch (T={As[0].num_states - 1}) o closure(10k-word lexicon)"
     V = REF_SAMPLE_V[workload]
     _, _, D, T = WORKLOADS[workload]
     A = fstgen.random_graph(V, D, T, 1000 + V + D)
     B = fstgen.random_graph(V, D, T, 2000 + V + D)
+    return A, B, f"random acceptors V={V} D={D} {T} tokens (same generator as the workload, scaled down)"
+
+
+# ------------------------------------------------------------------------------------ our arm
+def cpu_baseline(workload: str, budget_s: float = 12.0):
+    import oracle
+    oracle.build()
+    A, B, sample = reference_sample(workload)
     t_end = time.perf_counter() + budget_s
     n, tot, arcs = 0, 0.0, 0
     while n < 2 or time.perf_counter() < t_end:
@@ -168,12 +188,13 @@ def cpu_baseline(workload: str, budget_s: float = 12.0):
         if n >= 20:
             break
     return {"value": arcs * n / tot, "unit": "arcs/s", "cores": 1, "kind": "oracle",
-            "sample": f"{n} runs of the Algorithm 1 C oracle on V={V} D={D} {T} tokens (same generator as the "
-                      f"workload, scaled down), {arcs} composed arcs each, single host thread"}
+            "sample": f"{n} runs of the Algorithm 1 C oracle on {sample}, {arcs} composed arcs each, "
+                      f"single host thread"}
 
 
 def run_ours(args):
     import torch
+    from paper_2110_02848_b200 import parallel
     rank, local_rank, world = dist_env()
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
@@ -190,13 +211,25 @@ def run_ours(args):
         pg.barrier()
     fstc.load_library()
     stream = torch.cuda.Stream(device=dev)
-    A, B = make_inputs(args.workload, rank)
-    P = A.num_states * B.num_states
+    if args.workload == "c5":
+        As, B, mine = c5_shard(rank, world)
+        parallelism = (f"{world} rank(s); the {UTTS_PER_GPU * world}-utterance batch LPT-sharded by frames "
+                       f"(this rank: {len(As)} utterances, one fst_compose_batch call)")
+    else:
+        A, B = make_inputs(args.workload, rank)
+        As = [A]
+        parallelism = f"{world} independent replica(s), one composition per GPU (seeds offset by rank)"
+    P = sum(A.num_states * B.num_states for A in As)
     with torch.cuda.stream(stream):
-        a = fstc.fst_create(A, stream)
-        b_ = fstc.fst_create(B, stream)
+        ha = [fstc.fst_create(A, stream) for A in As]
+        hb = fstc.fst_create(B, stream)
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.int32, device=dev)
     fstc.fst_set_profiling(True)
+
+    def compose_all():
+        if len(ha) == 1:
+            return [fstc.fst_compose(ha[0], hb, stream)]
+        return fstc.fst_compose_batch(ha, [hb] * len(ha), stream)
 
     def step():
         with torch.cuda.stream(stream):
@@ -204,13 +237,14 @@ def run_ours(args):
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-            c = fstc.fst_compose(a, b_, stream)
+            cs = compose_all()
             e1.record(stream)
         e1.synchronize()
         ms = e0.elapsed_time(e1)
-        st = c.stats()
-        info = (c.num_states, c.num_arcs)
-        c.free()
+        st = cs[0].stats()
+        info = (sum(c.num_states for c in cs), sum(c.num_arcs for c in cs))
+        for c in cs:
+            c.free()
         return ms, st, info
 
     for _ in range(args.warmup):
@@ -233,16 +267,7 @@ def run_ours(args):
     clocks = sampler.stop()
     tot_ms = sum(times)
     V_C, E_C = info
-    # max over ranks of the device time; sum of arcs
-    if pg:
-        t = torch.tensor([tot_ms], dtype=torch.float64, device=dev)
-        pg.all_reduce(t, op=pg.ReduceOp.MAX)
-        max_ms = float(t.item())
-        e = torch.tensor([float(E_C)], dtype=torch.float64, device=dev)
-        pg.all_reduce(e, op=pg.ReduceOp.SUM)
-        arcs_all = float(e.item())
-    else:
-        max_ms, arcs_all = tot_ms, float(E_C)
+    max_ms, arcs_all = parallel.reduce_timing(tot_ms, float(E_C), pg, dev)
     value = arcs_all * args.steps / (max_ms / 1e3)
 
     # ---------------- roofline of the dominant kernel (emit) and of the whole step
@@ -274,18 +299,19 @@ def run_ours(args):
     # ---------------- e2e through the C ABI with host buffers (pinned), copies inside the timed region
     e2e = None
     if not args.no_e2e:
-        e2e = run_e2e(args, fstc, A, B, stream, dev, pg, rank)
+        e2e = run_e2e(args, fstc, As, B, stream, dev, pg)
 
     line = {
         "metric": "composed arcs/sec", "value": value, "unit": "arcs/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": max_ms / args.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": WORKLOADS[args.workload][0], "V_A": A.num_states, "V_B": B.num_states,
-                   "E_A": A.num_arcs, "E_B": B.num_arcs, "pair_space": P, "V_C": V_C, "E_C": E_C,
+        "config": {"workload": WORKLOADS[args.workload][0], "compositions_per_gpu": len(As),
+                   "V_A": sum(A.num_states for A in As), "V_B": B.num_states,
+                   "E_A": sum(A.num_arcs for A in As), "E_B": B.num_arcs, "pair_space": P, "V_C": V_C, "E_C": E_C,
                    "coaccessible": R, "levels": [stats[-1]["levels_stage1"], stats[-1]["levels_stage2"]],
-                   "parallelism": f"{world} independent replica(s), one composition per GPU (seeds offset by rank)",
-                   "l2": "flushed before every step (512 MiB write), outside the timed events; working set "
-                         "(bitmaps 200 MB + 24 GB output) exceeds L2"},
+                   "parallelism": parallelism,
+                   "l2": "flushed before every step (512 MiB write), outside the timed events; the working set "
+                         "(pair-space bitmaps + composed graph) exceeds L2"},
         "phases_ms": {"stage1_backward_bfs": s1, "stage2_forward_bfs": s2, "numbering": num, "emit": emit_ms},
         "roofline": roof,
         "step_roofline": step_roof,
@@ -304,75 +330,70 @@ def run_ours(args):
     return 0
 
 
-def run_e2e(args, fstc, A, B, stream, dev, pg, rank):
-    """Host pinned inputs -> fst_create x2 -> fst_compose -> fst_copy_to_host (whole graph) per step."""
+def run_e2e(args, fstc, As, B, stream, dev, pg):
+    """Pinned host inputs -> fst_create (FST_MEM_HOST) for every input -> fst_compose[_batch] ->
+    fst_copy_to_host of every composed graph into pinned host memory, per step."""
     import torch
-
-    def pinned(x):
-        t = torch.from_numpy(np.ascontiguousarray(x)).pin_memory()
-        return t
+    from paper_2110_02848_b200 import parallel
+    keys = ("row_ptr", "ilabel", "olabel", "dst", "weight", "is_start", "is_accept")
 
     class H:
         pass
 
-    hosts = []
-    for g in (A, B):
+    def host(g):
         h = H()
         h.num_states = g.num_states
-        for k in ("row_ptr", "ilabel", "olabel", "dst", "weight", "is_start", "is_accept"):
-            setattr(h, k, pinned(getattr(g, k)))
-        hosts.append(h)
-    h2d = sum(getattr(h, k).numel() * getattr(h, k).element_size() for h in hosts
-              for k in ("row_ptr", "ilabel", "olabel", "dst", "weight", "is_start", "is_accept"))
+        for k in keys:  # pinned tensors, viewed as numpy for the binding (host memory)
+            setattr(h, k, torch.from_numpy(np.ascontiguousarray(getattr(g, k))).pin_memory().numpy())
+        return h
 
-    def as_np(h):  # the binding takes numpy for host memory; pinned tensors viewed as numpy keep the pinning
-        o = H()
-        o.num_states = h.num_states
-        for k in ("row_ptr", "ilabel", "olabel", "dst", "weight", "is_start", "is_accept"):
-            setattr(o, k, getattr(h, k).numpy())
-        return o
+    hAs = [host(A) for A in As]
+    hB = host(B)
+    h2d = sum(getattr(h, k).nbytes for h in hAs + [hB] for k in keys)
 
-    hA, hB = as_np(hosts[0]), as_np(hosts[1])
-    # output buffers (pinned), sized from a first run
-    c = fstc.fst_compose(fstc.fst_create(hA, stream), fstc.fst_create(hB, stream), stream)
-    V, E = c.num_states, c.num_arcs
-    c.free()
-    out = {k: torch.empty(n, dtype=dt).pin_memory() for k, n, dt in (
-        ("row_ptr", V + 1, torch.int64), ("ilabel", E, torch.int32), ("olabel", E, torch.int32),
-        ("dst", E, torch.int32), ("weight", E, torch.float32), ("is_start", V, torch.uint8),
-        ("is_accept", V, torch.uint8), ("pair_a", V, torch.int32), ("pair_b", V, torch.int32))}
-    d2h = sum(t.numel() * t.element_size() for t in out.values())
+    def compose(a_list, b):
+        if len(a_list) == 1:
+            return [fstc.fst_compose(a_list[0], b, stream)]
+        return fstc.fst_compose_batch(a_list, [b] * len(a_list), stream)
+
+    cs = compose([fstc.fst_create(h, stream) for h in hAs], fstc.fst_create(hB, stream))
+    sizes = [(c.num_states, c.num_arcs) for c in cs]
+    for c in cs:
+        c.free()
+    outs = []
+    for V, E in sizes:
+        outs.append({k: torch.empty(n, dtype=dt).pin_memory() for k, n, dt in (
+            ("row_ptr", V + 1, torch.int64), ("ilabel", E, torch.int32), ("olabel", E, torch.int32),
+            ("dst", E, torch.int32), ("weight", E, torch.float32), ("is_start", V, torch.uint8),
+            ("is_accept", V, torch.uint8), ("pair_a", V, torch.int32), ("pair_b", V, torch.int32))})
+    d2h = sum(t.numel() * t.element_size() for o in outs for t in o.values())
     lib = fstc.load_library()
-    ptr = {k: t.data_ptr() for k, t in out.items()}
+    order = ("row_ptr", "ilabel", "olabel", "dst", "weight", "is_start", "is_accept", "pair_a", "pair_b")
     nsteps = max(1, min(args.steps, args.e2e_steps))
     if pg:
         pg.barrier()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     for _ in range(nsteps):
-        a = fstc.fst_create(hA, stream)
+        a_list = [fstc.fst_create(h, stream) for h in hAs]
         b = fstc.fst_create(hB, stream)
-        c = fstc.fst_compose(a, b, stream)
-        st = lib.fst_copy_to_host(c.handle, stream.cuda_stream, ptr["row_ptr"], ptr["ilabel"], ptr["olabel"],
-                                  ptr["dst"], ptr["weight"], ptr["is_start"], ptr["is_accept"], ptr["pair_a"],
-                                  ptr["pair_b"])
-        assert st == 0
-        c.free(); a.free(); b.free()
+        cs = compose(a_list, b)
+        for c, o in zip(cs, outs):
+            st = lib.fst_copy_to_host(c.handle, stream.cuda_stream, *[o[k].data_ptr() if o[k].numel() else None
+                                                                       for k in order])
+            assert st == 0
+            c.free()
+        for a in a_list:
+            a.free()
+        b.free()
     torch.cuda.synchronize()
     dt = time.perf_counter() - t0
-    if pg:
-        t = torch.tensor([dt], dtype=torch.float64, device=dev)
-        pg.all_reduce(t, op=pg.ReduceOp.MAX)
-        dt = float(t.item())
-        e = torch.tensor([float(E)], dtype=torch.float64, device=dev)
-        pg.all_reduce(e, op=pg.ReduceOp.SUM)
-        E_all = float(e.item())
-    else:
-        E_all = float(E)
+    E_tot = sum(E for _, E in sizes)
+    dt, E_all = parallel.reduce_timing(dt, float(E_tot), pg, dev)
     return {"value": E_all * nsteps / dt, "unit": "arcs/s", "h2d_bytes_per_step": int(h2d),
             "d2h_bytes_per_step": int(d2h), "steps": nsteps,
-            "path": "pinned host arrays -> fst_create(FST_MEM_HOST) x2 -> fst_compose -> fst_copy_to_host "
-                    "(whole composed graph into pinned host memory)"}
+            "path": "pinned host arrays -> fst_create(FST_MEM_HOST) -> fst_compose(_batch) -> fst_copy_to_host "
+                    "(whole composed graphs into pinned host memory)"}
 
 
 def main():
@@ -381,7 +402,7 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="c4", choices=sorted(WORKLOADS))
+    ap.add_argument("--workload", default=os.environ.get("FSTC_BENCH_WORKLOAD", "c4"), choices=sorted(WORKLOADS))
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")

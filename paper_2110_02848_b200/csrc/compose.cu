@@ -636,29 +636,70 @@ __device__ __forceinline__ int emit_block_fast(TaskSmem& s, const ViewDev& Bv, c
   const int32_t* __restrict__ boff = Bv.off;
   const int nub = ub1 - ub0;
   auto present = [&](int slot, int32_t col) -> bool { return (Vs[slot * wpr + (col >> 5)] >> (col & 31)) & 1u; };
-  // count: states 2t, 2t+1 of thread t
-  int c2[2] = {0, 0};
+  // count: states 2t, 2t+1 of thread t; heavy states (> kHeavy arcs) are counted by the whole CTA
+  if (threadIdx.x == 0) s.nheavy = 0;
+  __syncthreads();
 #pragma unroll
   for (int j = 0; j < 2; ++j) {
     const int i = 2 * threadIdx.x + j;
+    int c = 0;
     if (i < nub && ((s.fw[lw0 + (i >> 5)] >> (i & 31)) & 1u)) {
       const int32_t ub = ub0 + i;
-      int c = 0;
-      fast_state<kM32>(s, ikd, ub, __ldg(&boff[ub]) + ub + 1, __ldg(&boff[ub + 1]) + ub + 1,
-                       [&](int slot, int32_t col, int, int, int32_t) { c += present(slot, col); });
-      c2[j] = c;
+      const int32_t e = __ldg(&boff[ub]) + ub + 1, e1 = __ldg(&boff[ub + 1]) + ub + 1;
+      if (e1 - e > kHeavy) {
+        s.state[atomicAdd(&s.nheavy, 1)] = i;
+      } else {
+        fast_state<kM32>(s, ikd, ub, e, e1, [&](int slot, int32_t col, int, int, int32_t) { c += present(slot, col); });
+      }
     }
+    s.cur[i] = c;
   }
+  __syncthreads();
+  const int nheavy = s.nheavy;
+  for (int h = 0; h < nheavy; ++h) {
+    const int i = s.state[h];
+    const int32_t ub = ub0 + i;
+    const int32_t e0 = __ldg(&boff[ub]) + ub + 1, e1 = __ldg(&boff[ub + 1]) + ub + 1;
+    int c = 0;
+    if (threadIdx.x == 0)
+      for (int a = 0; a < s.aeps; ++a) c += present(s.a_slot[a], ub);
+    for (int32_t e = e0 + threadIdx.x; e < e1; e += kThreads)
+      fast_arc<kM32>(s, __ldg(&ikd[e]), e - ub - 1, [&](int slot, int32_t col, int, int, int32_t) { c += present(slot, col); });
+    c = warp_sum(c);
+    if (lane == 0 && c) atomicAdd(&s.cur[i], c);
+    __syncthreads();
+  }
+  const int c0 = s.cur[2 * threadIdx.x], c1 = s.cur[2 * threadIdx.x + 1];
+  __syncthreads();
   int btot;
-  const int ex = block_excl_scan(c2[0] + c2[1], s.red32, &btot);
+  const int ex = block_excl_scan(c0 + c1, s.red32, &btot);
   s.cur[2 * threadIdx.x] = ex;
-  s.cur[2 * threadIdx.x + 1] = ex + c2[0];
+  s.cur[2 * threadIdx.x + 1] = ex + c0;
   if (threadIdx.x == 0) s.cur[kPairsPerBlock] = btot;
   __syncthreads();
   int32_t* bd = (int32_t*)wb;
   int32_t* bi = (int32_t*)(wb + kWCap);
   int32_t* bo = (int32_t*)(wb + 2 * kWCap);
   float* bw = (float*)(wb + 3 * kWCap);
+  int32_t* __restrict__ od = C.dst;
+  int32_t* __restrict__ oi = C.ilabel;
+  int32_t* __restrict__ oo = C.olabel;
+  float* __restrict__ ow = C.weight;
+  auto fill = [&](int kind, int a, int32_t carry, int32_t wbits, int32_t& il, int32_t& ol, float& wt) {
+    if (kind == 1) {
+      il = s.a_carry[a];
+      ol = carry;
+      wt = __fadd_rn(s.a_w[a], __int_as_float(wbits));  // one binary32 add, RN-even
+    } else if (kind == 2) {
+      il = s.a_carry[a];
+      ol = FST_EPS;
+      wt = s.a_w[a];  // bit copy
+    } else {
+      il = FST_EPS;
+      ol = carry;
+      wt = __int_as_float(wbits);  // bit copy
+    }
+  };
   for (int r = 0; r < 2; ++r) {
     const int first = warp * 64 + r * 32;
     const int i = first + lane;
@@ -667,45 +708,32 @@ __device__ __forceinline__ int emit_block_fast(TaskSmem& s, const ViewDev& Bv, c
     const int q0 = s.cur[first], q1 = s.cur[first + 32];
     const int my0 = s.cur[i], my1 = s.cur[i + 1];
     if (has) state_out(ub, run + my0);
+    const int32_t e = has ? __ldg(&boff[ub]) + ub + 1 : 0, e1 = has ? __ldg(&boff[ub + 1]) + ub + 1 : 0;
+    const bool walk = has && e1 - e <= kHeavy;  // heavy states are written by the whole CTA below
     for (int win = q0; win < q1; win += kWCap) {
-      if (has && my1 > win && my0 < win + kWCap) {
+      const bool mine = walk && my1 > win && my0 < win + kWCap;
+      if (!__any_sync(0xffffffffu, mine)) continue;  // window entirely inside a heavy state's range
+      if (mine) {
         int p = my0;
-        fast_state4<kM32>(s, ikcw, ub, __ldg(&boff[ub]) + ub + 1, __ldg(&boff[ub + 1]) + ub + 1,
-                          [&](int slot, int32_t col, int kind, int a, int32_t carry, int32_t wbits) {
-                            bool pr;
-                            const int32_t did = rank_of(slot, col, pr);
-                            if (!pr) return;
-                            const int t = p - win;
-                            ++p;
-                            if ((unsigned)t >= (unsigned)kWCap) return;
-                            int32_t il, ol;
-                            float wt;
-                            if (kind == 1) {
-                              il = s.a_carry[a];
-                              ol = carry;
-                              wt = __fadd_rn(s.a_w[a], __int_as_float(wbits));  // one binary32 add, RN-even
-                            } else if (kind == 2) {
-                              il = s.a_carry[a];
-                              ol = FST_EPS;
-                              wt = s.a_w[a];  // bit copy
-                            } else {
-                              il = FST_EPS;
-                              ol = carry;
-                              wt = __int_as_float(wbits);  // bit copy
-                            }
-                            bd[t] = did;
-                            bi[t] = il;
-                            bo[t] = ol;
-                            bw[t] = wt;
-                          });
+        fast_state4<kM32>(s, ikcw, ub, e, e1, [&](int slot, int32_t col, int kind, int a, int32_t carry, int32_t wbits) {
+          bool pr;
+          const int32_t did = rank_of(slot, col, pr);
+          if (!pr) return;
+          const int t = p - win;
+          ++p;
+          if ((unsigned)t >= (unsigned)kWCap) return;
+          int32_t il, ol;
+          float wt;
+          fill(kind, a, carry, wbits, il, ol, wt);
+          bd[t] = did;
+          bi[t] = il;
+          bo[t] = ol;
+          bw[t] = wt;
+        });
       }
       __syncwarp();
       const int n = min(kWCap, q1 - win);
-      int32_t* __restrict__ od = C.dst;
-      int32_t* __restrict__ oi = C.ilabel;
-      int32_t* __restrict__ oo = C.olabel;
-      float* __restrict__ ow = C.weight;
-      for (int t = lane; t < n; t += 32) {
+      for (int t = lane; t < n; t += 32) {  // slots of heavy states get overwritten below
         const int64_t pos = run + win + t;
         __stcs(&od[pos], bd[t]);
         __stcs(&oi[pos], bi[t]);
@@ -713,6 +741,50 @@ __device__ __forceinline__ int emit_block_fast(TaskSmem& s, const ViewDev& Bv, c
         __stcs(&ow[pos], bw[t]);
       }
       __syncwarp();
+    }
+  }
+  __syncthreads();
+  for (int h = 0; h < nheavy; ++h) {  // heavy states: M2 (thread 0), then rounds of kThreads arcs
+    const int i = s.state[h];
+    const int32_t ub = ub0 + i;
+    const int32_t e0 = __ldg(&boff[ub]) + ub + 1, e1 = __ldg(&boff[ub + 1]) + ub + 1;
+    int64_t p0 = run + s.cur[i];
+    auto put = [&](int slot, int32_t col, int kind, int a, int32_t carry, int32_t wbits, int64_t pos) {
+      bool pr;
+      const int32_t did = rank_of(slot, col, pr);
+      int32_t il, ol;
+      float wt;
+      fill(kind, a, carry, wbits, il, ol, wt);
+      __stcs(&od[pos], did);
+      __stcs(&oi[pos], il);
+      __stcs(&oo[pos], ol);
+      __stcs(&ow[pos], wt);
+    };
+    int m2 = 0;
+    for (int a = 0; a < s.aeps; ++a) m2 += present(s.a_slot[a], ub);
+    if (threadIdx.x == 0) {
+      int64_t q = p0;
+      for (int a = 0; a < s.aeps; ++a)
+        if (present(s.a_slot[a], ub)) put(s.a_slot[a], ub, 2, a, 0, 0, q++);
+    }
+    p0 += m2;
+    for (int32_t eb = e0; eb < e1; eb += kThreads) {
+      const int32_t e = eb + threadIdx.x;
+      int4 x = make_int4(0, 0, 0, 0);
+      int c = 0;
+      if (e < e1) {
+        x = __ldg(&ikcw[e]);
+        fast_arc<kM32>(s, make_int2(x.x, x.y), 0, [&](int slot, int32_t col, int, int, int32_t) { c += present(slot, col); });
+      }
+      int tchunk;
+      const int exh = block_excl_scan(c, s.red32, &tchunk);
+      if (c) {
+        int64_t q = p0 + exh;
+        fast_arc<kM32>(s, make_int2(x.x, x.y), 0, [&](int slot, int32_t col, int kind, int a, int32_t) {
+          if (present(slot, col)) put(slot, col, kind, a, x.z, x.w, q++);
+        });
+      }
+      p0 += tchunk;
     }
   }
   return btot;
@@ -1193,13 +1265,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_emit(Ctx cx, const int64_t* __r
       const int64_t run0 = run;
       const int32_t ub0 = blk * kPairsPerBlock, ub1 = min(ub0 + kPairsPerBlock, C.VB);
       const int lw0 = (blk - ch.b0) * 32;
-      bool fastE = staged && s.small && (2 * s.m * wpr + kWarps * kWCap * 4) * 4 <= kDynSmem;
-      if (fastE) {  // the per-thread walk is only used when no state of the block is heavy
-        int hv = 0;
-        for (int i = threadIdx.x; i < ub1 - ub0; i += kThreads)
-          if (src_bit(s, lw0, ub0, ub0 + i) && __ldg(&Bv.off[ub0 + i + 1]) - __ldg(&Bv.off[ub0 + i]) > kHeavy) hv = 1;
-        fastE = !__syncthreads_or(hv);
-      }
+      const bool fastE = staged && s.small && (2 * s.m * wpr + kWarps * kWCap * 4) * 4 <= kDynSmem;
       if (fastE) {
         uint32_t* wb = dyn + 2 * s.m * wpr + warp * kWCap * 4;
         auto rk = [&](int slot, int32_t col, bool& pr) -> int32_t { return rank_of(slot, 0, col, pr); };

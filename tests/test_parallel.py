@@ -1,0 +1,65 @@
+"""Multi-process host logic on CPU (gloo, world size 2): LPT sharding of independent compositions and
+the max/sum timing reduction used by bench.py.  No GPU needed."""
+import os
+import socket
+
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2110_02848_b200 import parallel
+
+
+def test_lpt_partition_complete_disjoint_balanced():
+    costs = [100 + (7919 * i) % 401 for i in range(256)]  # c5-like frame counts in [100, 500]
+    for world in (1, 2, 4, 8):
+        parts = parallel.lpt_partition(costs, world)
+        flat = sorted(i for p in parts for i in p)
+        assert flat == list(range(256))
+        assert parallel.imbalance(costs, world) < 1.05
+    assert parallel.lpt_partition([5, 1, 1, 1, 1, 1], 2) == [[0], [1, 2, 3, 4, 5]]
+    with pytest.raises(ValueError):
+        parallel.lpt_partition([1], 0)
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    costs = [100 + (7919 * i) % 401 for i in range(64)]
+    mine = parallel.shard_for_rank(costs, rank, world)
+    # every rank must see the same partition
+    allp = [None] * world
+    dist.all_gather_object(allp, mine)
+    ms, units = parallel.reduce_timing(10.0 * (rank + 1), float(len(mine)), dist)
+    q.put((rank, allp, ms, units))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_gloo_world2_sharding_and_reduction():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(2)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    res.sort()
+    allp0, allp1 = res[0][1], res[1][1]
+    assert allp0 == allp1
+    assert sorted(allp0[0] + allp0[1]) == list(range(64)) and not set(allp0[0]) & set(allp0[1])
+    for _, _, ms, units in res:
+        assert ms == 20.0 and units == 64.0
