@@ -831,24 +831,51 @@ __device__ __forceinline__ void bfs_chunk_fast(TaskSmem& s, const ViewDev& Bv, i
   };
   if (threadIdx.x == 0) s.nheavy = 0;
   if (threadIdx.x < kChunkMaxBlocks) s.keptc[threadIdx.x] = 0ull;
-  // walk a compacted list of source states: each warp takes 32 consecutive states and spreads their
-  // arcs over its lanes in rounds of 32 (uniform, coalesced); heavy states are deferred to the CTA
-  const int lane = threadIdx.x & 31;
-  auto walk = [&](int n) {
-    for (int base = (threadIdx.x & ~31); base < n; base += kThreads) {
-      const int k = base + lane;
+  __syncthreads();
+  // Each warp owns 32-word (1024-pair) segments of the chunk: it selects the segment's frontier states
+  // 32 at a time (warp scan over the words' popcounts + in-word select, no shared memory, no CTA
+  // barrier) and spreads the 32 states' B arcs over its lanes in rounds of 32 (uniform, coalesced
+  // packed-item loads).  States with more than kHeavy arcs are deferred to the whole CTA.
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nw = (cub1 - cub0 + 31) >> 5;
+  for (int seg = warp; seg * 32 < nw; seg += kWarps) {
+    const int wi = seg * 32 + lane;
+    const uint32_t word = wi < nw ? s.fw[wi] : 0u;
+    const int pc = __popc(word);
+    const int winc = warp_incl_scan(pc);
+    const int wex = winc - pc;
+    const int stot = __shfl_sync(0xffffffffu, winc, 31);
+    unsigned long long segkept = 0;
+    for (int b0 = 0; b0 < stot; b0 += 32) {
+      const int k = b0 + lane;
+      int j = 0;
+#pragma unroll
+      for (int step = 16; step > 0; step >>= 1)
+        if (__shfl_sync(0xffffffffu, wex, j + step) <= k) j += step;
+      uint32_t wj = __shfl_sync(0xffffffffu, word, j);
+      int r = k - __shfl_sync(0xffffffffu, wex, j);
       int32_t ub = 0, e = 0, deg = 0;
-      if (k < n) {
-        ub = s.state[k];
+      if (k < stot) {
+        int pos = 0;  // r-th set bit of wj (binary search on popcounts)
+#pragma unroll
+        for (int h = 16; h > 0; h >>= 1) {
+          const int c = __popc(wj & ((1u << h) - 1u));
+          if (r >= c) {
+            r -= c;
+            pos += h;
+            wj >>= h;
+          }
+        }
+        ub = cub0 + (seg * 32 + j) * 32 + pos;
         e = __ldg(&off[ub]) + ub + 1;
         deg = __ldg(&off[ub + 1]) + ub + 1 - e;
         kept = 0;
         for (int a = 0; a < s.aeps; ++a) cand(s.a_slot[a], ub, 2, a, -1);  // M2 moves of the state
-        if (kStage2 && kept) atomicAdd(&s.keptc[(ub - cub0) >> 10], (unsigned long long)kept);
+        segkept += kept;
         if (deg > kHeavy) {
-          const int h = atomicAdd(&s.nheavy, 1);
-          if (h < kPairsPerBlock) {
-            s.cur[h] = ub;
+          const int hh = atomicAdd(&s.nheavy, 1);
+          if (hh < kPairsPerBlock) {
+            s.cur[hh] = ub;
             deg = 0;
           }
         }
@@ -857,47 +884,24 @@ __device__ __forceinline__ void bfs_chunk_fast(TaskSmem& s, const ViewDev& Bv, i
       const int start = incl - deg;
       const int total = __shfl_sync(0xffffffffu, incl, 31);
       kept = 0;
-      // kept moves are attributed to the 1024-pair block of the arc's source state
-      int kb = (__shfl_sync(0xffffffffu, ub, 0) - cub0) >> 10;
-      for (int r = 0; r < total; r += 32) {
-        const int c = r + lane;
-        int j = 0;
+      for (int rr = 0; rr < total; rr += 32) {
+        const int c = rr + lane;
+        int jj = 0;
 #pragma unroll
         for (int step = 16; step > 0; step >>= 1)
-          if (__shfl_sync(0xffffffffu, start, j + step) <= c) j += step;
-        const int32_t ej = __shfl_sync(0xffffffffu, e, j) + (c - __shfl_sync(0xffffffffu, start, j));
-        const int32_t uj = __shfl_sync(0xffffffffu, ub, j);
-        if (c < total) {
-          if (kStage2 && ((uj - cub0) >> 10) != kb) {
-            if (kept) atomicAdd(&s.keptc[kb], (unsigned long long)kept);
-            kept = 0;
-            kb = (uj - cub0) >> 10;
-          }
-          fast_arc<kM32>(s, __ldg(&ikd[ej]), ej - uj - 1, cand);
-        }
+          if (__shfl_sync(0xffffffffu, start, jj + step) <= c) jj += step;
+        const int32_t ej = __shfl_sync(0xffffffffu, e, jj) + (c - __shfl_sync(0xffffffffu, start, jj));
+        const int32_t uj = __shfl_sync(0xffffffffu, ub, jj);
+        if (c < total) fast_arc<kM32>(s, __ldg(&ikd[ej]), ej - uj - 1, cand);
       }
-      if (kStage2) {
-        if (__all_sync(0xffffffffu, kb == __shfl_sync(0xffffffffu, kb, 0))) {
-          const unsigned long long t = warp_sum((unsigned long long)kept);
-          if (lane == 0 && t) atomicAdd(&s.keptc[kb], t);
-        } else if (kept) {
-          atomicAdd(&s.keptc[kb], (unsigned long long)kept);
-        }
-      }
+      segkept += kept;
     }
-  };
-  const int nw = (cub1 - cub0 + 31) >> 5;
-  if (nst <= kPairsPerBlock) {  // sparse chunk: one compaction for all of it
-    const int n = compact_words(s, 0, nw, cub0);
-    walk(n);
-    __syncthreads();
-  } else {
-    for (int w0 = 0; w0 < nw; w0 += 32) {
-      const int n = compact_words(s, w0, min(w0 + 32, nw), cub0 + 32 * w0);
-      walk(n);
-      __syncthreads();
+    if (kStage2) {  // the segment is exactly one 1024-pair block
+      const unsigned long long t = warp_sum(segkept);
+      if (lane == 0 && t) atomicAdd(&s.keptc[seg], t);
     }
   }
+  __syncthreads();
   const int nh = min(s.nheavy, kPairsPerBlock);
   for (int h = 0; h < nh; ++h) {
     const int32_t ub = s.cur[h];
@@ -1051,8 +1055,10 @@ __global__ void __launch_bounds__(kThreads, 2) k_level(Ctx cx, int level) {
       if (kStage2 && (int)threadIdx.x < ch.b1 - ch.b0 && s.keptc[threadIdx.x])
         cx.kept[C.K + (int64_t)ch.ua * C.bpr + ch.b0 + threadIdx.x] += s.keptc[threadIdx.x];
     }
-    build_groups(s, Bv);
-    __syncthreads();
+    if (!s.small) {
+      build_groups(s, Bv);
+      __syncthreads();
+    }
     for (int32_t blk = s.small ? ch.b1 : ch.b0; blk < ch.b1; ++blk) {
       kept = 0;
       const int32_t ub0 = blk * kPairsPerBlock, ub1 = min(ub0 + kPairsPerBlock, C.VB);
