@@ -161,6 +161,7 @@ struct TaskSmem {
   int32_t g_pre[kAMax + 2];               // per block: item prefix over groups
   int32_t cur[kPairsPerBlock + 1];        // emit: per-state arc cursor / count
   int32_t nheavy;
+  int32_t segnext;
   unsigned long long keptc[kChunkMaxBlocks];  // per-block kept counts of the chunk (stage 2)
 };
 
@@ -829,18 +830,26 @@ __device__ __forceinline__ void bfs_chunk_fast(TaskSmem& s, const ViewDev& Bv, i
       kept += glob(slot, col);
     }
   };
-  if (threadIdx.x == 0) s.nheavy = 0;
+  if (threadIdx.x == 0) {
+    s.nheavy = 0;
+    s.segnext = 0;
+  }
   if (threadIdx.x < kChunkMaxBlocks) s.keptc[threadIdx.x] = 0ull;
   __syncthreads();
   // Each warp owns 32-word (1024-pair) segments of the chunk: it selects the segment's frontier states
   // 32 at a time (warp scan over the words' popcounts + in-word select, no shared memory, no CTA
   // barrier) and spreads the 32 states' B arcs over its lanes in rounds of 32 (uniform, coalesced
   // packed-item loads).  States with more than kHeavy arcs are deferred to the whole CTA.
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
   const int nw = (cub1 - cub0 + 31) >> 5;
-  for (int seg = warp; seg * 32 < nw; seg += kWarps) {
-    const int wi = seg * 32 + lane;
-    const uint32_t word = wi < nw ? s.fw[wi] : 0u;
+  constexpr int kSegWords = 8;  // 256-pair segments, handed out dynamically (load balance)
+  for (;;) {
+    int seg = 0;
+    if (lane == 0) seg = atomicAdd(&s.segnext, 1);
+    seg = __shfl_sync(0xffffffffu, seg, 0);
+    if (seg * kSegWords >= nw) break;
+    const int wi = seg * kSegWords + lane;
+    const uint32_t word = (lane < kSegWords && wi < nw) ? s.fw[wi] : 0u;
     const int pc = __popc(word);
     const int winc = warp_incl_scan(pc);
     const int wex = winc - pc;
@@ -866,7 +875,7 @@ __device__ __forceinline__ void bfs_chunk_fast(TaskSmem& s, const ViewDev& Bv, i
             wj >>= h;
           }
         }
-        ub = cub0 + (seg * 32 + j) * 32 + pos;
+        ub = cub0 + (seg * kSegWords + j) * 32 + pos;
         e = __ldg(&off[ub]) + ub + 1;
         deg = __ldg(&off[ub + 1]) + ub + 1 - e;
         kept = 0;
@@ -896,9 +905,9 @@ __device__ __forceinline__ void bfs_chunk_fast(TaskSmem& s, const ViewDev& Bv, i
       }
       segkept += kept;
     }
-    if (kStage2) {  // the segment is exactly one 1024-pair block
+    if (kStage2) {  // the segment lies inside one 1024-pair block
       const unsigned long long t = warp_sum(segkept);
-      if (lane == 0 && t) atomicAdd(&s.keptc[seg], t);
+      if (lane == 0 && t) atomicAdd(&s.keptc[seg / (32 / kSegWords)], t);
     }
   }
   __syncthreads();
@@ -1262,8 +1271,11 @@ __global__ void __launch_bounds__(kThreads, 2) k_emit(Ctx cx, const int64_t* __r
       __stcs(&C.olabel[pos], ol);
       __stcs(&C.weight[pos], wt);
     };
-    build_groups(s, Bv);
-    __syncthreads();
+    const bool fastE = staged && s.small && (2 * s.m * wpr + kWarps * kWCap * 4) * 4 <= kDynSmem;
+    if (!fastE) {
+      build_groups(s, Bv);
+      __syncthreads();
+    }
     for (int32_t blk = ch.b0; blk < ch.b1; ++blk) {
       const int64_t gblk = kb0 + blk;
       if (cx.vcount[gblk] == 0) continue;
@@ -1271,7 +1283,6 @@ __global__ void __launch_bounds__(kThreads, 2) k_emit(Ctx cx, const int64_t* __r
       const int64_t run0 = run;
       const int32_t ub0 = blk * kPairsPerBlock, ub1 = min(ub0 + kPairsPerBlock, C.VB);
       const int lw0 = (blk - ch.b0) * 32;
-      const bool fastE = staged && s.small && (2 * s.m * wpr + kWarps * kWCap * 4) * 4 <= kDynSmem;
       if (fastE) {
         uint32_t* wb = dyn + 2 * s.m * wpr + warp * kWCap * 4;
         auto rk = [&](int slot, int32_t col, bool& pr) -> int32_t { return rank_of(slot, 0, col, pr); };
