@@ -67,6 +67,7 @@ struct Ctx {
   int64_t* arcbase;          // per block (+1)
   unsigned long long* hist;  // per-level frontier sizes
   unsigned long long* misc;  // [0] nonempty levels, [1] |R|, [2] emit consistency errors, [3] staged tasks
+  uint8_t* cnt8;             // per pair: out-degree in C recorded by the stage-2 fast path (255 = recount)
   const CompDev* comps;
   const int64_t* seedbase;
   int32_t ncomp;
@@ -630,7 +631,8 @@ __device__ __forceinline__ void fast_state4(const TaskSmem& s, const int4* __res
 template <bool kM32, typename Rank, typename StateOut>
 __device__ __forceinline__ int emit_block_fast(TaskSmem& s, const ViewDev& Bv, const CompDev& C, int32_t ub0,
                                                int32_t ub1, int lw0, int wpr, const uint32_t* Vs, uint32_t* wb,
-                                               int64_t run, Rank&& rank_of, StateOut&& state_out) {
+                                               const uint8_t* __restrict__ cnt8row, int64_t run, Rank&& rank_of,
+                                               StateOut&& state_out) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int2* __restrict__ ikd = Bv.ikd;
   const int4* __restrict__ ikcw = Bv.ikcw;
@@ -650,7 +652,10 @@ __device__ __forceinline__ int emit_block_fast(TaskSmem& s, const ViewDev& Bv, c
       if (e1 - e > kHeavy) {
         s.state[atomicAdd(&s.nheavy, 1)] = i;
       } else {
-        fast_state<kM32>(s, ikd, ub, e, e1, [&](int slot, int32_t col, int, int, int32_t) { c += present(slot, col); });
+        c = cnt8row[ub];  // out-degree in C recorded by the stage-2 fast path (never 255 for <= kHeavy arcs
+        if (c == 255)     // unless the count saturated: then count here)
+          fast_state<kM32>(s, ikd, ub, e, e1, [&](int slot, int32_t col, int, int, int32_t) { c += present(slot, col); }),
+              c -= 255;
       }
     }
     s.cur[i] = c;
@@ -812,7 +817,7 @@ __device__ __forceinline__ int compact_words(TaskSmem& s, int w0, int w1, int32_
 template <bool kStage2, bool kStaged, bool kM32, typename Glob>
 __device__ __forceinline__ void bfs_chunk_fast(TaskSmem& s, const ViewDev& Bv, int32_t cub0, int32_t cub1, int nst,
                                                int wpr, const uint32_t* Rs, const uint32_t* VS, uint32_t* NW,
-                                               Glob&& glob) {
+                                               uint8_t* __restrict__ cnt8row, Glob&& glob) {
   const int2* __restrict__ ikd = Bv.ikd;
   const int32_t* __restrict__ off = Bv.off;
   unsigned kept = 0;
@@ -889,6 +894,8 @@ __device__ __forceinline__ void bfs_chunk_fast(TaskSmem& s, const ViewDev& Bv, i
           }
         }
       }
+      int own = kept;  // stage 2: kept moves (= out-degree in C) of my own state
+      const bool heavy_own = k < stot && deg == 0 && __ldg(&off[ub + 1]) - __ldg(&off[ub]) > kHeavy;
       const int incl = warp_incl_scan(deg);
       const int start = incl - deg;
       const int total = __shfl_sync(0xffffffffu, incl, 31);
@@ -901,9 +908,19 @@ __device__ __forceinline__ void bfs_chunk_fast(TaskSmem& s, const ViewDev& Bv, i
           if (__shfl_sync(0xffffffffu, start, jj + step) <= c) jj += step;
         const int32_t ej = __shfl_sync(0xffffffffu, e, jj) + (c - __shfl_sync(0xffffffffu, start, jj));
         const int32_t uj = __shfl_sync(0xffffffffu, ub, jj);
+        const unsigned k0 = kept;
         if (c < total) fast_arc<kM32>(s, __ldg(&ikd[ej]), ej - uj - 1, cand);
+        if (kStage2) {  // attribute this round's kept moves to their states (owner lanes)
+          const int kc = (int)(kept - k0);
+          const int sc = warp_incl_scan(kc);
+          const int lo = max(start - rr, 0), hi = min(incl - rr, 32) - 1;
+          const int shi = __shfl_sync(0xffffffffu, sc, max(hi, 0));
+          const int slo = __shfl_sync(0xffffffffu, sc, max(lo - 1, 0));
+          if (hi >= lo) own += shi - (lo > 0 ? slo : 0);
+        }
       }
       segkept += kept;
+      if (kStage2 && k < stot) cnt8row[ub] = (uint8_t)(heavy_own ? 255 : min(own, 255));
     }
     if (kStage2) {  // the segment lies inside one 1024-pair block
       const unsigned long long t = warp_sum(segkept);
@@ -1039,6 +1056,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_level(Ctx cx, int level) {
     };
     if (s.small) {  // fast path: compacted source states, one thread per state
       const int32_t cub0 = ch.b0 * kPairsPerBlock, cub1 = min(ch.b1 * kPairsPerBlock, C.VB);
+      uint8_t* cnt8row = cx.cnt8 + ch.rowW * 32;
       auto glob = [&](int slot, int32_t col) -> unsigned {
         const int32_t row = s.slot_row[slot];
         const int64_t gw = C.W + (int64_t)row * wpr + (col >> 5);
@@ -1055,11 +1073,11 @@ __global__ void __launch_bounds__(kThreads, 2) k_level(Ctx cx, int level) {
         return k;
       };
       if (staged) {
-        if (s.mask32) bfs_chunk_fast<kStage2, true, true>(s, Bv, cub0, cub1, nst, wpr, Rs, VS, NW, glob);
-        else bfs_chunk_fast<kStage2, true, false>(s, Bv, cub0, cub1, nst, wpr, Rs, VS, NW, glob);
+        if (s.mask32) bfs_chunk_fast<kStage2, true, true>(s, Bv, cub0, cub1, nst, wpr, Rs, VS, NW, cnt8row, glob);
+        else bfs_chunk_fast<kStage2, true, false>(s, Bv, cub0, cub1, nst, wpr, Rs, VS, NW, cnt8row, glob);
       } else {
-        if (s.mask32) bfs_chunk_fast<kStage2, false, true>(s, Bv, cub0, cub1, nst, wpr, Rs, VS, NW, glob);
-        else bfs_chunk_fast<kStage2, false, false>(s, Bv, cub0, cub1, nst, wpr, Rs, VS, NW, glob);
+        if (s.mask32) bfs_chunk_fast<kStage2, false, true>(s, Bv, cub0, cub1, nst, wpr, Rs, VS, NW, cnt8row, glob);
+        else bfs_chunk_fast<kStage2, false, false>(s, Bv, cub0, cub1, nst, wpr, Rs, VS, NW, cnt8row, glob);
       }
       if (kStage2 && (int)threadIdx.x < ch.b1 - ch.b0 && s.keptc[threadIdx.x])
         cx.kept[C.K + (int64_t)ch.ua * C.bpr + ch.b0 + threadIdx.x] += s.keptc[threadIdx.x];
@@ -1295,8 +1313,9 @@ __global__ void __launch_bounds__(kThreads, 2) k_emit(Ctx cx, const int64_t* __r
           C.is_start[id] = (uint8_t)(stA & __ldg(&C.startB[ub]));
           C.is_accept[id] = (uint8_t)(acA & __ldg(&C.accB[ub]));
         };
-        const int btot = s.mask32 ? emit_block_fast<true>(s, Bv, C, ub0, ub1, lw0, wpr, Vs, wb, run, rk, so)
-                                  : emit_block_fast<false>(s, Bv, C, ub0, ub1, lw0, wpr, Vs, wb, run, rk, so);
+        const uint8_t* cnt8row = cx.cnt8 + ch.rowW * 32;
+        const int btot = s.mask32 ? emit_block_fast<true>(s, Bv, C, ub0, ub1, lw0, wpr, Vs, wb, cnt8row, run, rk, so)
+                                  : emit_block_fast<false>(s, Bv, C, ub0, ub1, lw0, wpr, Vs, wb, cnt8row, run, rk, so);
         if (threadIdx.x == 0 && (unsigned long long)btot != cx.kept[gblk]) atomicAdd(&cx.misc[2], 1ull);
         run += btot;
         __syncthreads();
@@ -1642,6 +1661,7 @@ fst_status compose_impl(int32_t n, const fst_handle* a, const fst_handle* b, cud
   const size_t ohist = take(8 * kMaxLevelStats), omisc = take(8 * 8);
   const size_t ocomps = take(sizeof(CompDev) * n), oseed1 = take(8 * (n + 1)), oseed2 = take(8 * (n + 1));
   const size_t otot = take(8 * 2 * (n + 1));
+  const size_t ocnt8 = take(32 * nwords);
   BufferPtr wb;
   st = alloc_buffer(off, s, &wb);
   if (st) {
@@ -1666,6 +1686,7 @@ fst_status compose_impl(int32_t n, const fst_handle* a, const fst_handle* b, cud
   cx.arcbase = (int64_t*)(base + oarc);
   cx.hist = (unsigned long long*)(base + ohist);
   cx.misc = (unsigned long long*)(base + omisc);
+  cx.cnt8 = (uint8_t*)(base + ocnt8);
   CompDev* d_comps = (CompDev*)(base + ocomps);
   cx.comps = d_comps;
   cx.ncomp = n;
