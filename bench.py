@@ -211,6 +211,8 @@ def run_ours(args):
         pg.barrier()
     fstc.load_library()
     stream = torch.cuda.Stream(device=dev)
+    if args.mode == "sharded":
+        return run_sharded(args, fstc, stream, dev, pg, rank, local_rank, world)
     if args.workload == "c5":
         As, B, mine = c5_shard(rank, world)
         parallelism = (f"{world} rank(s); the {UTTS_PER_GPU * world}-utterance batch LPT-sharded by frames "
@@ -330,6 +332,71 @@ def run_ours(args):
     return 0
 
 
+def run_sharded(args, fstc, stream, dev, pg, rank, local_rank, world):
+    """One composition split over the ranks by rows (fst_compose_sharded, NCCL exchange per level):
+    strong scaling; value = composed arcs of the whole composition / max over ranks of the time."""
+    import torch
+    from paper_2110_02848_b200 import parallel
+    _, V, D, T = WORKLOADS[args.workload]
+    A = fstgen.random_graph(V, D, T, 1000 + V + D)
+    B = fstgen.random_graph(V, D, T, 2000 + V + D)
+    uid = [fstc.Comm.unique_id() if rank == 0 else None]
+    if pg:
+        pg.broadcast_object_list(uid, src=0)
+    comm = fstc.Comm(world, rank, uid[0])
+    a, b = fstc.fst_create(A, stream), fstc.fst_create(B, stream)
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.int32, device=dev)
+    fstc.fst_set_profiling(True)
+
+    def step():
+        with torch.cuda.stream(stream):
+            flush.zero_()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            c = fstc.fst_compose_sharded(a, b, comm, stream)
+            e1.record(stream)
+        e1.synchronize()
+        info = c.shard_info()
+        st = c.stats()
+        c.free()
+        return e0.elapsed_time(e1), info, st
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if pg:
+        pg.barrier()
+    sampler = ClockSampler(local_rank)
+    sampler.start()
+    l0 = fstc.fst_launch_count()
+    times = []
+    for _ in range(args.steps):
+        ms, info, st = step()
+        times.append(ms)
+    launches = fstc.fst_launch_count() - l0
+    clocks = sampler.stop()
+    max_ms, _ = parallel.reduce_timing(sum(times), 0.0, pg, dev)
+    E_C = info["total_arcs"]
+    value = E_C * args.steps / (max_ms / 1e3)
+    line = {"metric": "composed arcs/sec", "value": value, "unit": "arcs/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": max_ms / args.steps, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": WORKLOADS[args.workload][0], "E_C": E_C, "V_C": info["total_states"],
+                       "parallelism": f"one composition sharded by pair-space rows over {world} rank(s); "
+                                      f"per-level NCCL send/recv of claimed row slices, R/V all-reduce"},
+            "phases_ms": {"stage1_backward_bfs": st["ms_stage1"], "stage2_forward_bfs": st["ms_stage2"],
+                          "emit": st["ms_emit"]},
+            "gpu_launches": launches, "clocks": clocks}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    comm.close()
+    if pg:
+        pg.barrier()
+        pg.destroy_process_group()
+    return 0
+
+
 def run_e2e(args, fstc, As, B, stream, dev, pg):
     """Pinned host inputs -> fst_create (FST_MEM_HOST) for every input -> fst_compose[_batch] ->
     fst_copy_to_host of every composed graph into pinned host memory, per step."""
@@ -404,6 +471,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default=os.environ.get("FSTC_BENCH_WORKLOAD", "c4"), choices=sorted(WORKLOADS))
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--mode", default=os.environ.get("FSTC_BENCH_MODE", "replicas"), choices=["replicas", "sharded"],
+                    help="replicas: independent compositions per GPU (weak); sharded: one composition over all GPUs")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()

@@ -150,6 +150,38 @@ fst_status fst_adjacency(fst_handle h, int32_t role, int32_t match_on_olabel, in
  * min(cap, levels) entries to the HOST array `sizes` and returns the number of levels (or -1). */
 int32_t fst_level_sizes(fst_handle c, int32_t stage, int64_t* sizes, int32_t cap);
 
+/* ---- Sharded single composition over several GPUs ----------------------------
+ * The pair-space rows (states of A) are split into `world` contiguous ranges; rank r owns rows
+ * [V_A*r/world, V_A*(r+1)/world).  Each BFS level every rank expands its rows; pairs found in other
+ * ranks' rows are delivered to their owners (NCCL send/recv of bitmap row slices) and claimed there;
+ * R and V are replicated after each stage (NCCL all-reduce, sum of disjoint bits).  Rank r's result
+ * handle holds the states of its rows (a contiguous id range) with GLOBAL state ids in dst; row_ptr
+ * is local to the shard.  Concatenating the shards in rank order gives fst_compose's result. */
+typedef struct fst_comm* fst_comm_handle;
+
+/* 128-byte NCCL unique id, generated on one rank and broadcast by the caller (e.g. with
+ * torch.distributed) before fst_comm_init.  FST_E_NCCL if NCCL cannot be loaded. */
+fst_status fst_comm_unique_id(void* id128);
+/* NCCL communicator over `world` ranks (one per GPU, current CUDA device). */
+fst_status fst_comm_init(int32_t world, int32_t rank, const void* id128, fst_comm_handle* comm);
+void fst_comm_destroy(fst_comm_handle comm); /* NULL-safe */
+/* Collective: every rank calls it with the same inputs; *c_shard receives this rank's shard. */
+fst_status fst_compose_sharded(fst_handle a, fst_handle b, fst_comm_handle comm, void* stream,
+                               fst_handle* c_shard);
+/* The same algorithm with all `world` shards hosted by this process on the current device (the
+ * row-slice exchange is a device copy): c_shards[world].  Used to verify the sharding on one GPU. */
+fst_status fst_compose_sharded_local(fst_handle a, fst_handle b, int32_t world, void* stream,
+                                     fst_handle* c_shards);
+
+typedef struct {
+  int32_t rank, world;      /* -1, 0 for unsharded handles */
+  int64_t state_offset;     /* global id of this shard's first state */
+  int64_t arc_offset;       /* global slot of this shard's first arc */
+  int64_t total_states;     /* states / arcs of the whole composition */
+  int64_t total_arcs;
+} fst_shard_desc;
+fst_status fst_shard_info(fst_handle c, fst_shard_desc* out);
+
 /* Profiling: when on, fst_compose* records CUDA events per phase (fst_compose_stats) and
  * computes |R|.  Off by default. */
 void fst_set_profiling(int32_t on);

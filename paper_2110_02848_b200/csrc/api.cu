@@ -9,6 +9,7 @@
 
 #include "fstc_handle.h"
 #include "fstc_internal.cuh"
+#include "nccl_dl.h"
 
 namespace fstc {
 
@@ -42,6 +43,7 @@ int sm_count() {
 std::vector<int64_t>& level_sizes_slot(fst* h, int stage) { return h->level_sizes[stage == 1 ? 0 : 1]; }
 
 fst_status compose_impl(int32_t n, const fst_handle* a, const fst_handle* b, cudaStream_t s, fst_handle* c);
+fst_status compose_sharded_impl(fst* A, fst* B, int world, fst_comm* comm, cudaStream_t s, fst_handle* c);
 
 fst_status device_ready() {
   int n = 0;
@@ -171,6 +173,91 @@ fst_status fst_adjacency(fst_handle h, int32_t role, int32_t match_on_olabel, in
   if (h->E) FSTC_CUDA_TRY(cudaMemcpy(arc.data(), h->views[k].arc, 4 * h->E, cudaMemcpyDeviceToHost));
   for (int64_t i = 0; i <= h->V; ++i) offsets[i] = off[i];
   for (int64_t i = 0; i < h->E; ++i) arc_ids[i] = arc[i];
+  return FST_OK;
+}
+
+fst_status fst_comm_unique_id(void* id128) {
+  if (!id128) {
+    set_error(FST_E_INVALID_ARG, "fst_comm_unique_id: NULL");
+    return FST_E_INVALID_ARG;
+  }
+  const NcclApi* nc = nccl_api();
+  if (!nc) return FST_E_NCCL;
+  ncclUniqueId id;
+  int r = nc->GetUniqueId(&id);
+  if (r) {
+    set_error(FST_E_NCCL, "ncclGetUniqueId failed: %s", nc->GetErrorString ? nc->GetErrorString(r) : "?");
+    return FST_E_NCCL;
+  }
+  memcpy(id128, &id, sizeof(id));
+  return FST_OK;
+}
+
+fst_status fst_comm_init(int32_t world, int32_t rank, const void* id128, fst_comm_handle* comm) {
+  if (!id128 || !comm || world < 1 || rank < 0 || rank >= world) {
+    set_error(FST_E_INVALID_ARG, "fst_comm_init: bad arguments");
+    return FST_E_INVALID_ARG;
+  }
+  *comm = nullptr;
+  fst_status st = device_ready();
+  if (st) return st;
+  const NcclApi* nc = nccl_api();
+  if (!nc) return FST_E_NCCL;
+  ncclUniqueId id;
+  memcpy(&id, id128, sizeof(id));
+  fst_comm* c = new fst_comm();
+  int r = nc->CommInitRank(&c->comm, world, id, rank);
+  if (r) {
+    delete c;
+    set_error(FST_E_NCCL, "ncclCommInitRank failed: %s", nc->GetErrorString ? nc->GetErrorString(r) : "?");
+    return FST_E_NCCL;
+  }
+  c->world = world;
+  c->rank = rank;
+  *comm = c;
+  return FST_OK;
+}
+
+void fst_comm_destroy(fst_comm_handle comm) {
+  if (!comm) return;
+  const NcclApi* nc = nccl_api();
+  if (nc && comm->comm) nc->CommDestroy(comm->comm);
+  delete comm;
+}
+
+fst_status fst_compose_sharded(fst_handle a, fst_handle b, fst_comm_handle comm, void* stream, fst_handle* c) {
+  if (!a || !b || !comm || !c) {
+    set_error(FST_E_INVALID_ARG, "fst_compose_sharded: NULL argument");
+    return FST_E_INVALID_ARG;
+  }
+  *c = nullptr;
+  fst_status st = device_ready();
+  if (st) return st;
+  return compose_sharded_impl(a, b, comm->world, comm, (cudaStream_t)stream, c);
+}
+
+fst_status fst_compose_sharded_local(fst_handle a, fst_handle b, int32_t world, void* stream, fst_handle* c) {
+  if (!a || !b || !c || world < 1) {
+    set_error(FST_E_INVALID_ARG, "fst_compose_sharded_local: bad arguments");
+    return FST_E_INVALID_ARG;
+  }
+  for (int i = 0; i < world; ++i) c[i] = nullptr;
+  fst_status st = device_ready();
+  if (st) return st;
+  return compose_sharded_impl(a, b, world, nullptr, (cudaStream_t)stream, c);
+}
+
+fst_status fst_shard_info(fst_handle c, fst_shard_desc* out) {
+  if (!c || !out) {
+    set_error(FST_E_INVALID_ARG, "fst_shard_info: NULL argument");
+    return FST_E_INVALID_ARG;
+  }
+  out->rank = c->shard_rank;
+  out->world = c->shard_world;
+  out->state_offset = c->shard_state_offset;
+  out->arc_offset = c->shard_arc_offset;
+  out->total_states = c->shard_rank >= 0 ? c->shard_total_states : c->V;
+  out->total_arcs = c->shard_rank >= 0 ? c->shard_total_arcs : c->E;
   return FST_OK;
 }
 

@@ -68,6 +68,7 @@ struct Ctx {
   unsigned long long* hist;  // per-level frontier sizes
   unsigned long long* misc;  // [0] nonempty levels, [1] |R|, [2] emit consistency errors, [3] staged tasks
   uint8_t* cnt8;             // per pair: out-degree in C recorded by the stage-2 fast path (255 = recount)
+  uint32_t* OUT;             // sharded mode: claims for pairs in rows owned by other shards
   const CompDev* comps;
   const int64_t* seedbase;
   int32_t ncomp;
@@ -959,6 +960,7 @@ __global__ void k_seed(Ctx cx) {
     int32_t nb = kStage2 ? C.nStartB : C.nAccB;
     int32_t va = kStage2 ? C.startListA[i / nb] : C.accListA[i / nb];
     int32_t vb = kStage2 ? C.startListB[i % nb] : C.accListB[i % nb];
+    if (va < C.own_r0 || va >= C.own_r1) continue;  // sharded: another shard seeds it
     const int64_t gw = C.W + (int64_t)va * C.wpr + (vb >> 5);
     const uint32_t bit = 1u << (vb & 31);
     if (kStage2 && !(cx.R[gw] & bit)) continue;
@@ -1048,6 +1050,10 @@ __global__ void __launch_bounds__(kThreads, 2) k_level(Ctx cx, int level) {
           if (!(__ldg(&cx.R[gw]) & bit)) return;
           ++kept;
         }
+        if (c.row < C.own_r0 || c.row >= C.own_r1) {  // sharded: the owner claims it after the exchange
+          atomicOr(&cx.OUT[gw], bit);
+          return;
+        }
         if (vis[gw] & bit) return;  // test before the atomic (bits only get set)
         if (atomicOr(&vis[gw], bit) & bit) return;
         ++nnew;
@@ -1065,6 +1071,10 @@ __global__ void __launch_bounds__(kThreads, 2) k_level(Ctx cx, int level) {
         if (kStage2) {
           if (!(__ldg(&cx.R[gw]) & bit)) return 0u;
           k = 1;
+        }
+        if (row < C.own_r0 || row >= C.own_r1) {  // sharded: the owner claims it after the exchange
+          atomicOr(&cx.OUT[gw], bit);
+          return k;
         }
         if (vis[gw] & bit) return k;
         if (atomicOr(&vis[gw], bit) & bit) return k;
@@ -1148,6 +1158,10 @@ __global__ void __launch_bounds__(kThreads, 2) k_level(Ctx cx, int level) {
         const int r = i / wpr, w = i - r * wpr;
         const int32_t row = s.slot_row[r];
         const int64_t gw = C.W + (int64_t)row * wpr + w;
+        if (row < C.own_r0 || row >= C.own_r1) {  // sharded: the owner claims it after the exchange
+          atomicOr(&cx.OUT[gw], nb);
+          continue;
+        }
         const uint32_t win = nb & ~atomicOr(&vis[gw], nb);
         if (win) {
           nnew += __popc(win);
@@ -1160,6 +1174,48 @@ __global__ void __launch_bounds__(kThreads, 2) k_level(Ctx cx, int level) {
   }
   nnew = warp_sum(nnew);
   if ((threadIdx.x & 31) == 0 && nnew) atomicAdd(&ctrl_nxt->nnew, (unsigned long long)nnew);
+}
+
+// ------------------------------------------------------------------------------ sharded exchange
+// Owner-side claim of the pairs other shards found in this shard's rows during level `level`
+// (the OR of their OUT words over [own_r0, own_r1), received in `in`): new bits become visited and
+// join the next frontier exactly like local claims.  Single composition (ncomp == 1).
+template <bool kStage2>
+__global__ void k_apply_remote(Ctx cx, const uint32_t* __restrict__ in, int level) {
+  const int p = level & 1;
+  LevelCtrl* ctrl_nxt = &cx.ctrl[(level + 1) % 3];
+  uint32_t* Fn = p ? cx.F0 : cx.F1;
+  uint32_t* flagn = p ? cx.flag0 : cx.flag1;
+  int32_t* listn = p ? cx.list0 : cx.list1;
+  uint32_t* vis = kStage2 ? cx.V : cx.R;
+  const CompDev& C = cx.comps[0];
+  const int64_t w0 = C.W + (int64_t)C.own_r0 * C.wpr, w1 = C.W + (int64_t)C.own_r1 * C.wpr;
+  unsigned nnew = 0;
+  for (int64_t gw = w0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; gw < w1;
+       gw += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t nb = in[gw - w0];
+    if (!nb) continue;
+    const uint32_t win = nb & ~atomicOr(&vis[gw], nb);
+    if (!win) continue;
+    nnew += __popc(win);
+    const int64_t local = gw - C.W;
+    const int32_t row = (int32_t)(local / C.wpr);
+    const int32_t col = (int32_t)(local - (int64_t)row * C.wpr) * 32;
+    push_bits(C, row, col, gw, win, Fn, flagn, listn, ctrl_nxt);
+  }
+  nnew = warp_sum(nnew);
+  if ((threadIdx.x & 31) == 0 && nnew) atomicAdd(&ctrl_nxt->nnew, (unsigned long long)nnew);
+}
+
+// dst[i] |= src[i] (merging bitmap / count slices of other shards)
+__global__ void k_or_words(uint32_t* __restrict__ dst, const uint32_t* __restrict__ src, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    if (src[i]) dst[i] |= src[i];
+}
+
+__global__ void k_shift_i64(int64_t* __restrict__ a, int64_t n, int64_t d) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    a[i] -= d;
 }
 
 // ------------------------------------------------------------------------------ numbering
@@ -1223,6 +1279,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_emit(Ctx cx, const int64_t* __r
     const Chunk ch = decode_chunk(cx, q);
     const CompDev& C = cx.comps[ch.comp];
     const int64_t kb0 = C.K + (int64_t)ch.ua * C.bpr;  // global block index of (ua, block 0)
+    if (ch.ua < C.own_r0 || ch.ua >= C.own_r1) continue;            // sharded: another shard emits it
     if (cx.idbase[kb0 + ch.b1] == cx.idbase[kb0 + ch.b0]) continue;  // no states in the chunk
     const ViewDev& Av = C.Af;
     const ViewDev& Bv = C.Bf;
@@ -1633,6 +1690,8 @@ fst_status compose_impl(int32_t n, const fst_handle* a, const fst_handle* b, cud
     C.CB = std::max<int32_t>(1, (C.bpr + cpr - 1) / cpr);
     C.cpr = std::max<int32_t>(1, (C.bpr + C.CB - 1) / C.CB);
     C.smallA = A->max_olabel < 63;
+    C.own_r0 = 0;
+    C.own_r1 = C.VA;
     C.W = W;
     C.K = K;
     C.Q = Q;
@@ -1694,6 +1753,7 @@ fst_status compose_impl(int32_t n, const fst_handle* a, const fst_handle* b, cud
   cx.nblocks = nblocks;
   cx.nchunks = nchunks;
   cx.seedbase = nullptr;
+  cx.OUT = nullptr;
   int64_t* d_seed1 = (int64_t*)(base + oseed1);
   int64_t* d_seed2 = (int64_t*)(base + oseed2);
   int64_t* d_tot = (int64_t*)(base + otot);
@@ -1857,6 +1917,473 @@ fst_status compose_impl(int32_t n, const fst_handle* a, const fst_handle* b, cud
     outs[i]->stats = stats;
     level_sizes_slot(outs[i], 1) = sizes1;
     level_sizes_slot(outs[i], 2) = sizes2;
+    c[i] = outs[i];
+  }
+  return FST_OK;
+}
+
+}  // namespace fstc
+
+// =============================================================================================
+// Sharded single composition: the pair-space rows (states of A) are split into
+// `world` contiguous ranges, one per shard.  Every BFS level each shard expands the frontier of its
+// own rows; claims that land in rows of another shard go to its OUT bitmap, are delivered to the
+// owner (all-to-all of row slices) and claimed there by k_apply_remote.  After each stage the owned
+// slices of R (stage 1) and V + the per-block arc counts (stage 2) are replicated (NCCL: all-reduce
+// sum of disjoint bits == OR), so numbering is global and the emit of each shard's rows is local,
+// with global state ids.  The shards' outputs concatenated in rank order are the unsharded result.
+// Transports: NCCL (one process per GPU; fst_compose_sharded) or all shards in this process on one
+// device (fst_compose_sharded_local, the same kernels and slices moved by device copies).
+#include <dlfcn.h>
+
+#include "nccl_dl.h"
+
+namespace fstc {
+
+const NcclApi* nccl_api() {
+  static NcclApi api;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (h) {
+      api.GetUniqueId = (int (*)(ncclUniqueId*))dlsym(h, "ncclGetUniqueId");
+      api.CommInitRank = (int (*)(ncclComm_t*, int, ncclUniqueId, int))dlsym(h, "ncclCommInitRank");
+      api.CommDestroy = (int (*)(ncclComm_t))dlsym(h, "ncclCommDestroy");
+      api.AllReduce = (int (*)(const void*, void*, size_t, int, int, ncclComm_t, cudaStream_t))dlsym(h, "ncclAllReduce");
+      api.Send = (int (*)(const void*, size_t, int, int, ncclComm_t, cudaStream_t))dlsym(h, "ncclSend");
+      api.Recv = (int (*)(void*, size_t, int, int, ncclComm_t, cudaStream_t))dlsym(h, "ncclRecv");
+      api.GroupStart = (int (*)())dlsym(h, "ncclGroupStart");
+      api.GroupEnd = (int (*)())dlsym(h, "ncclGroupEnd");
+      api.GetErrorString = (const char* (*)(int))dlsym(h, "ncclGetErrorString");
+      api.ok = api.GetUniqueId && api.CommInitRank && api.CommDestroy && api.AllReduce && api.Send && api.Recv &&
+               api.GroupStart && api.GroupEnd;
+    }
+  }
+  if (!api.ok) {
+    set_error(FST_E_NCCL, "NCCL (libnccl.so.2) is not available in this process");
+    return nullptr;
+  }
+  return &api;
+}
+
+#define FSTC_NCCL_TRY(expr)                                                                      \
+  do {                                                                                           \
+    int _r = (expr);                                                                             \
+    if (_r != 0) {                                                                               \
+      set_error(FST_E_NCCL, "%s failed: %s", #expr, nc->GetErrorString ? nc->GetErrorString(_r) : "?"); \
+      return FST_E_NCCL;                                                                         \
+    }                                                                                            \
+  } while (0)
+
+namespace {
+
+struct Shard {
+  int rank = 0;
+  int32_t r0 = 0, r1 = 0;
+  BufferPtr wb;
+  Ctx cx{};
+  CompDev comp{};
+  CompDev* d_comp = nullptr;
+  int64_t *d_seed1 = nullptr, *d_seed2 = nullptr, *d_tot = nullptr, *d_tmp = nullptr;
+  uint32_t* recv = nullptr;  // NCCL: one slice per peer
+  unsigned long long* d_cnt = nullptr;
+  char* base = nullptr;
+  size_t zero_lo = 0, zero_hi = 0, o_ctrl = 0, o_kept = 0, o_misc = 0;
+  std::vector<int64_t> sizes1, sizes2;
+  fst* out = nullptr;
+};
+
+}  // namespace
+
+fst_status compose_sharded_impl(fst* A, fst* B, int world, fst_comm* comm, cudaStream_t s, fst_handle* c) {
+  const bool local = comm == nullptr;
+  const NcclApi* nc = nullptr;
+  if (!local) {
+    nc = nccl_api();
+    if (!nc) return FST_E_NCCL;
+    world = comm->world;
+  }
+  if (world < 1) {
+    set_error(FST_E_INVALID_ARG, "sharded compose: world must be >= 1");
+    return FST_E_INVALID_ARG;
+  }
+  fst_status st = ensure_views(A, s);
+  if (st) return st;
+  st = ensure_views(B, s);
+  if (st) return st;
+  st = init_kernels();
+  if (st) return st;
+  const bool prof = profiling_enabled();
+  EventTimer t_total(prof, s);
+  const int64_t launches0 = fst_launch_count();
+  // ---- layout (one composition), chunks sized for the shard's share of rows
+  CompDev C0;
+  memset(&C0, 0, sizeof(C0));
+  auto vd = [](const View& v) {
+    return ViewDev{v.off, v.key, v.other, v.carry, v.w, v.cw, v.ikd, v.isrc, v.ikcw,
+                   v.lm_other, v.lm_pos, v.seg_node, v.seg_beg, v.lab_val, v.lab_seg, v.nlab};
+  };
+  C0.Af = vd(A->views[kOutByOlabel]);
+  C0.Ab = vd(A->views[kInByOlabel]);
+  C0.Bf = vd(B->views[kOutByIlabel]);
+  C0.Bb = vd(B->views[kInByIlabel]);
+  C0.startA = A->is_start; C0.startB = B->is_start; C0.accA = A->is_accept; C0.accB = B->is_accept;
+  C0.startListA = A->start_list; C0.startListB = B->start_list;
+  C0.accListA = A->accept_list; C0.accListB = B->accept_list;
+  C0.nStartA = A->n_start; C0.nStartB = B->n_start; C0.nAccA = A->n_accept; C0.nAccB = B->n_accept;
+  C0.VA = A->V;
+  C0.VB = B->V;
+  C0.wpr = (B->V + 31) / 32;
+  C0.bpr = (C0.wpr + kWordsPerBlock - 1) / kWordsPerBlock;
+  {
+    const int64_t rows = std::max<int64_t>(1, C0.VA / world);
+    int64_t want = (8ll * g_grid + rows - 1) / rows;
+    int32_t cpr = (int32_t)std::max<int64_t>(1, std::min<int64_t>(want, C0.bpr));
+    cpr = std::max<int32_t>(cpr, (C0.bpr + kChunkMaxBlocks - 1) / kChunkMaxBlocks);
+    C0.CB = std::max<int32_t>(1, (C0.bpr + cpr - 1) / cpr);
+    C0.cpr = std::max<int32_t>(1, (C0.bpr + C0.CB - 1) / C0.CB);
+  }
+  C0.smallA = A->max_olabel < 63;
+  const int64_t nwords = (int64_t)C0.VA * C0.wpr, nblocks = (int64_t)C0.VA * C0.bpr,
+                nchunks = (int64_t)C0.VA * C0.cpr;
+  if (nblocks >= INT32_MAX || nchunks >= INT32_MAX) {
+    set_error(FST_E_CAPACITY, "pair space too large (%lld blocks)", (long long)nblocks);
+    return FST_E_CAPACITY;
+  }
+  const int64_t seed1 = (int64_t)C0.nAccA * C0.nAccB, seed2 = (int64_t)C0.nStartA * C0.nStartB;
+  auto row0 = [&](int q) { return (int32_t)((int64_t)C0.VA * q / world); };
+  int32_t maxrows = 0;
+  for (int q = 0; q < world; ++q) maxrows = std::max(maxrows, row0(q + 1) - row0(q));
+  unsigned long long* hp = pinned_scratch();
+  if (!hp) {
+    set_error(FST_E_CUDA, "cudaMallocHost failed");
+    return FST_E_CUDA;
+  }
+  // ---- shards hosted by this process
+  std::vector<Shard> sh(local ? world : 1);
+  for (size_t i = 0; i < sh.size(); ++i) {
+    Shard& S = sh[i];
+    S.rank = local ? (int)i : comm->rank;
+    S.r0 = row0(S.rank);
+    S.r1 = row0(S.rank + 1);
+    size_t off = 0;
+    auto take = [&](size_t bytes) { size_t o = off; off += (bytes + 255) & ~size_t(255); return o; };
+    const size_t oR = take(4 * nwords), oV = take(4 * nwords), oF0 = take(4 * nwords), oF1 = take(4 * nwords);
+    const size_t ofl0 = take(4 * nchunks), ofl1 = take(4 * nchunks);
+    const size_t oOUT = take(4 * nwords);
+    const size_t ol0 = take(4 * nchunks), ol1 = take(4 * nchunks);
+    const size_t octrl = take(sizeof(LevelCtrl) * 3);
+    const size_t okept = take(8 * nblocks), ovc = take(4 * nblocks), owpre = take(2 * nwords);
+    const size_t oid = take(8 * (nblocks + 1)), oarc = take(8 * (nblocks + 1));
+    const size_t otmp = take(8 * scan_tmp_elems(nblocks));
+    const size_t ohist = take(8 * kMaxLevelStats), omisc = take(8 * 8);
+    const size_t ocomps = take(sizeof(CompDev)), oseed1 = take(16), oseed2 = take(16), otot = take(8 * 4);
+    const size_t ocnt8 = take(32 * nwords), ocnt = take(8);
+    const size_t orecv = take(local ? 4 : 4 * (size_t)world * maxrows * C0.wpr);
+    st = alloc_buffer(off, s, &S.wb);
+    if (st) return st == FST_E_OOM ? FST_E_CAPACITY : st;
+    char* base = (char*)S.wb->ptr;
+    S.base = base;
+    Ctx& cx = S.cx;
+    cx.R = (uint32_t*)(base + oR);
+    cx.V = (uint32_t*)(base + oV);
+    cx.F0 = (uint32_t*)(base + oF0);
+    cx.F1 = (uint32_t*)(base + oF1);
+    cx.flag0 = (uint32_t*)(base + ofl0);
+    cx.flag1 = (uint32_t*)(base + ofl1);
+    cx.OUT = (uint32_t*)(base + oOUT);
+    cx.list0 = (int32_t*)(base + ol0);
+    cx.list1 = (int32_t*)(base + ol1);
+    cx.ctrl = (LevelCtrl*)(base + octrl);
+    cx.kept = (unsigned long long*)(base + okept);
+    cx.vcount = (int32_t*)(base + ovc);
+    cx.wpre = (uint16_t*)(base + owpre);
+    cx.idbase = (int64_t*)(base + oid);
+    cx.arcbase = (int64_t*)(base + oarc);
+    cx.hist = (unsigned long long*)(base + ohist);
+    cx.misc = (unsigned long long*)(base + omisc);
+    cx.cnt8 = (uint8_t*)(base + ocnt8);
+    S.d_comp = (CompDev*)(base + ocomps);
+    cx.comps = S.d_comp;
+    cx.ncomp = 1;
+    cx.nwords = nwords;
+    cx.nblocks = nblocks;
+    cx.nchunks = nchunks;
+    S.d_seed1 = (int64_t*)(base + oseed1);
+    S.d_seed2 = (int64_t*)(base + oseed2);
+    S.d_tot = (int64_t*)(base + otot);
+    S.d_tmp = (int64_t*)(base + otmp);
+    S.d_cnt = (unsigned long long*)(base + ocnt);
+    S.recv = (uint32_t*)(base + orecv);
+    S.zero_lo = oR;
+    S.zero_hi = ol0;
+    S.o_ctrl = octrl;
+    S.o_kept = okept;
+    S.o_misc = omisc;
+    S.comp = C0;
+    S.comp.own_r0 = S.r0;
+    S.comp.own_r1 = S.r1;
+    FSTC_CUDA_TRY(cudaMemsetAsync(base + oR, 0, ol0 - oR, s));  // bitmaps, flags, OUT
+    FSTC_CUDA_TRY(cudaMemsetAsync(base + octrl, 0, sizeof(LevelCtrl) * 3, s));
+    FSTC_CUDA_TRY(cudaMemsetAsync(base + okept, 0, 8 * nblocks, s));
+    FSTC_CUDA_TRY(cudaMemsetAsync(base + omisc, 0, 64, s));
+    FSTC_CUDA_TRY(cudaMemcpyAsync(S.d_comp, &S.comp, sizeof(CompDev), cudaMemcpyHostToDevice, s));
+    int64_t sd1[2] = {0, seed1}, sd2[2] = {0, seed2};
+    FSTC_CUDA_TRY(cudaMemcpyAsync(S.d_seed1, sd1, 16, cudaMemcpyHostToDevice, s));
+    FSTC_CUDA_TRY(cudaMemcpyAsync(S.d_seed2, sd2, 16, cudaMemcpyHostToDevice, s));
+  }
+  const int64_t wlo = 0;
+  (void)wlo;
+  // words of rank q's rows
+  auto wbeg = [&](int q) { return (int64_t)row0(q) * C0.wpr; };
+  auto wcnt = [&](int q) { return (int64_t)(row0(q + 1) - row0(q)) * C0.wpr; };
+  // replicate a bitmap (uint32 words over the whole pair space): every shard gets the owners' rows
+  auto replicate_bits = [&](uint32_t* Shard::*dummy, bool isR) -> fst_status {
+    (void)dummy;
+    if (local) {
+      for (auto& Sr : sh)
+        for (auto& Sq : sh)
+          if (&Sr != &Sq && wcnt(Sq.rank) > 0) {
+            uint32_t* dst = isR ? Sr.cx.R : Sr.cx.V;
+            const uint32_t* src = isR ? Sq.cx.R : Sq.cx.V;
+            FSTC_CUDA_TRY(cudaMemcpyAsync(dst + wbeg(Sq.rank), src + wbeg(Sq.rank), 4 * wcnt(Sq.rank),
+                                          cudaMemcpyDeviceToDevice, s));
+          }
+    } else {
+      uint32_t* p = isR ? sh[0].cx.R : sh[0].cx.V;
+      FSTC_NCCL_TRY(nc->AllReduce(p, p, (size_t)nwords, kNcclUint32, kNcclSum, comm->comm, s));
+    }
+    return FST_OK;
+  };
+  fst_compose_stats stats{};
+  stats.pair_space = (int64_t)C0.VA * C0.VB;
+  stats.num_coaccessible = -1;
+  int64_t level_launches = 0;
+  // ---- one stage: seeds, then levels with an exchange after each
+  auto run_stage_sharded = [&](bool stage2) -> fst_status {
+    for (auto& S : sh) {
+      S.cx.seedbase = stage2 ? S.d_seed2 : S.d_seed1;
+      FSTC_CUDA_TRY(cudaMemsetAsync(S.base + S.o_ctrl, 0, sizeof(LevelCtrl) * 3, s));
+      FSTC_CUDA_TRY(cudaMemsetAsync(S.base + S.o_misc, 0, 8, s));
+      const int64_t ns = stage2 ? seed2 : seed1;
+      if (ns > 0) {
+        if (stage2) k_seed<true><<<nblk(ns, 256), 256, 0, s>>>(S.cx);
+        else k_seed<false><<<nblk(ns, 256), 256, 0, s>>>(S.cx);
+        FSTC_LAUNCH_CHECK();
+      }
+    }
+    if ((stage2 ? seed2 : seed1) == 0 || (stage2 && seed1 == 0)) return FST_OK;
+    for (int level = 0;; ++level) {
+      for (auto& S : sh) {
+        if (stage2) k_level<true><<<g_grid, kThreads, kDynSmem, s>>>(S.cx, level);
+        else k_level<false><<<g_grid, kThreads, kDynSmem, s>>>(S.cx, level);
+        FSTC_LAUNCH_CHECK();
+        ++level_launches;
+      }
+      // deliver the claims in other shards' rows to their owners, who claim them
+      if (local) {
+        for (auto& Sr : sh)
+          for (auto& Sq : sh) {
+            if (&Sr == &Sq || wcnt(Sr.rank) == 0) continue;
+            const uint32_t* in = Sq.cx.OUT + wbeg(Sr.rank);
+            const unsigned grid = (unsigned)std::min<int64_t>(nblk(wcnt(Sr.rank), 256), 8 * sm_count());
+            if (stage2) k_apply_remote<true><<<grid, 256, 0, s>>>(Sr.cx, in, level);
+            else k_apply_remote<false><<<grid, 256, 0, s>>>(Sr.cx, in, level);
+            FSTC_LAUNCH_CHECK();
+          }
+      } else if (world > 1) {
+        Shard& S = sh[0];
+        const int64_t mine = wcnt(S.rank);
+        FSTC_NCCL_TRY(nc->GroupStart());
+        for (int q = 0; q < world; ++q) {
+          if (q == S.rank) continue;
+          FSTC_NCCL_TRY(nc->Send(S.cx.OUT + wbeg(q), (size_t)wcnt(q), kNcclUint32, q, comm->comm, s));
+          FSTC_NCCL_TRY(nc->Recv(S.recv + (size_t)q * maxrows * C0.wpr, (size_t)mine, kNcclUint32, q, comm->comm, s));
+        }
+        FSTC_NCCL_TRY(nc->GroupEnd());
+        for (int q = 0; q < world; ++q) {
+          if (q == S.rank || mine == 0) continue;
+          const unsigned grid = (unsigned)std::min<int64_t>(nblk(mine, 256), 8 * sm_count());
+          const uint32_t* in = S.recv + (size_t)q * maxrows * C0.wpr;
+          if (stage2) k_apply_remote<true><<<grid, 256, 0, s>>>(S.cx, in, level);
+          else k_apply_remote<false><<<grid, 256, 0, s>>>(S.cx, in, level);
+          FSTC_LAUNCH_CHECK();
+        }
+      }
+      for (auto& S : sh) FSTC_CUDA_TRY(cudaMemsetAsync(S.cx.OUT, 0, 4 * nwords, s));
+      // global size of the next frontier
+      unsigned long long total = 0;
+      if (local) {
+        for (auto& S : sh) {
+          FSTC_CUDA_TRY(cudaMemcpyAsync(hp, &S.cx.ctrl[(level + 1) % 3].count, 8, cudaMemcpyDeviceToHost, s));
+          FSTC_CUDA_TRY(cudaStreamSynchronize(s));
+          total += *hp;
+        }
+      } else {
+        Shard& S = sh[0];
+        FSTC_CUDA_TRY(cudaMemcpyAsync(S.d_cnt, &S.cx.ctrl[(level + 1) % 3].count, 8, cudaMemcpyDeviceToDevice, s));
+        FSTC_NCCL_TRY(nc->AllReduce(S.d_cnt, S.d_cnt, 1, kNcclUint64, kNcclSum, comm->comm, s));
+        FSTC_CUDA_TRY(cudaMemcpyAsync(hp, S.d_cnt, 8, cudaMemcpyDeviceToHost, s));
+        FSTC_CUDA_TRY(cudaStreamSynchronize(s));
+        total = *hp;
+      }
+      if (total == 0) {
+        for (auto& S : sh) {  // per-level frontier sizes of this shard
+          FSTC_CUDA_TRY(cudaMemcpyAsync(hp, S.cx.misc, 8, cudaMemcpyDeviceToHost, s));
+          FSTC_CUDA_TRY(cudaStreamSynchronize(s));
+          const int n = (int)std::min<unsigned long long>(*hp, kMaxLevelStats);
+          std::vector<unsigned long long> tmp(n);
+          if (n) {
+            FSTC_CUDA_TRY(cudaMemcpyAsync(tmp.data(), S.cx.hist, 8 * n, cudaMemcpyDeviceToHost, s));
+            FSTC_CUDA_TRY(cudaStreamSynchronize(s));
+          }
+          (stage2 ? S.sizes2 : S.sizes1).assign(tmp.begin(), tmp.end());
+        }
+        break;
+      }
+    }
+    return FST_OK;
+  };
+  {
+    EventTimer t(prof, s);
+    st = run_stage_sharded(false);
+    if (st) return st;
+    st = replicate_bits(nullptr, true);
+    if (st) return st;
+    stats.ms_stage1 = t.stop();
+  }
+  {
+    EventTimer t(prof, s);
+    st = run_stage_sharded(true);
+    if (st) return st;
+    st = replicate_bits(nullptr, false);
+    if (st) return st;
+    // per-block arc counts of the owners' rows
+    if (local) {
+      for (auto& Sr : sh)
+        for (auto& Sq : sh)
+          if (&Sr != &Sq && wcnt(Sq.rank) > 0) {
+            const int64_t b0 = (int64_t)Sq.r0 * C0.bpr, nb = (int64_t)(Sq.r1 - Sq.r0) * C0.bpr;
+            FSTC_CUDA_TRY(cudaMemcpyAsync(Sr.cx.kept + b0, Sq.cx.kept + b0, 8 * nb, cudaMemcpyDeviceToDevice, s));
+          }
+    } else {
+      FSTC_NCCL_TRY(nc->AllReduce(sh[0].cx.kept, sh[0].cx.kept, (size_t)nblocks, kNcclUint64, kNcclSum, comm->comm, s));
+    }
+    stats.ms_stage2 = t.stop();
+    stats.levels_stage1 = (int32_t)sh[0].sizes1.size();
+    stats.levels_stage2 = (int32_t)sh[0].sizes2.size();
+  }
+  // ---- numbering (identical on every shard) and per-shard outputs
+  std::vector<fst*> outs(sh.size(), nullptr);
+  auto cleanup = [&]() {
+    for (auto*& h : outs) {
+      delete h;
+      h = nullptr;
+    }
+  };
+  int64_t total_states = 0, total_arcs = 0;
+  for (size_t i = 0; i < sh.size(); ++i) {
+    Shard& S = sh[i];
+    k_block_counts<<<nblk(nblocks * 32, 256), 256, 0, s>>>(S.cx);
+    FSTC_LAUNCH_CHECK();
+    st = exclusive_scan_i32(S.cx.vcount, nblocks, S.cx.idbase, S.d_tmp, s);
+    if (st) return st;
+    st = exclusive_scan_u64(S.cx.kept, nblocks, S.cx.arcbase, S.d_tmp, s);
+    if (st) return st;
+    int64_t hb[6];
+    const int64_t b0 = (int64_t)S.r0 * C0.bpr, b1 = (int64_t)S.r1 * C0.bpr;
+    FSTC_CUDA_TRY(cudaMemcpyAsync(&hb[0], S.cx.idbase + b0, 8, cudaMemcpyDeviceToHost, s));
+    FSTC_CUDA_TRY(cudaMemcpyAsync(&hb[1], S.cx.idbase + b1, 8, cudaMemcpyDeviceToHost, s));
+    FSTC_CUDA_TRY(cudaMemcpyAsync(&hb[2], S.cx.arcbase + b0, 8, cudaMemcpyDeviceToHost, s));
+    FSTC_CUDA_TRY(cudaMemcpyAsync(&hb[3], S.cx.arcbase + b1, 8, cudaMemcpyDeviceToHost, s));
+    FSTC_CUDA_TRY(cudaMemcpyAsync(&hb[4], S.cx.idbase + nblocks, 8, cudaMemcpyDeviceToHost, s));
+    FSTC_CUDA_TRY(cudaMemcpyAsync(&hb[5], S.cx.arcbase + nblocks, 8, cudaMemcpyDeviceToHost, s));
+    FSTC_CUDA_TRY(cudaStreamSynchronize(s));
+    total_states = hb[4];
+    total_arcs = hb[5];
+    const int64_t nv = hb[1] - hb[0], ne = hb[3] - hb[2];
+    if (total_states >= INT32_MAX) {
+      cleanup();
+      set_error(FST_E_CAPACITY, "composition has %lld states (>= 2^31)", (long long)total_states);
+      return FST_E_CAPACITY;
+    }
+    size_t ob = 0;
+    auto tk = [&](size_t bytes) { size_t o = ob; ob += (bytes + 255) & ~size_t(255); return o; };
+    const size_t o_rp = tk(8 * (nv + 1)), o_il = tk(4 * ne), o_ol = tk(4 * ne), o_d = tk(4 * ne), o_w = tk(4 * ne),
+                 o_st = tk(nv), o_ac = tk(nv), o_pa = tk(4 * nv), o_pb = tk(4 * nv);
+    BufferPtr obuf;
+    st = alloc_buffer(ob, s, &obuf);
+    if (st) {
+      cleanup();
+      return st;
+    }
+    fst* h = new fst();
+    outs[i] = h;
+    h->composed = true;
+    h->V = (int32_t)nv;
+    h->E = ne;
+    h->stream = s;
+    char* pb = (char*)obuf->ptr;
+    h->row_ptr = (int64_t*)(pb + o_rp);
+    h->ilabel = (int32_t*)(pb + o_il);
+    h->olabel = (int32_t*)(pb + o_ol);
+    h->dst = (int32_t*)(pb + o_d);
+    h->weight = (float*)(pb + o_w);
+    h->is_start = (uint8_t*)(pb + o_st);
+    h->is_accept = (uint8_t*)(pb + o_ac);
+    h->pair_a = (int32_t*)(pb + o_pa);
+    h->pair_b = (int32_t*)(pb + o_pb);
+    h->buffers.push_back(obuf);
+    h->shard_rank = S.rank;
+    h->shard_world = world;
+    h->shard_state_offset = hb[0];
+    h->shard_arc_offset = hb[2];
+    // outputs biased so that global state ids / arc slots index the shard's buffers
+    const int64_t ida = hb[0], arca = hb[2];
+    S.comp.row_ptr = h->row_ptr - ida;
+    S.comp.ilabel = h->ilabel - arca;
+    S.comp.olabel = h->olabel - arca;
+    S.comp.dst = h->dst - arca;
+    S.comp.weight = h->weight - arca;
+    S.comp.is_start = h->is_start - ida;
+    S.comp.is_accept = h->is_accept - ida;
+    S.comp.pair_a = h->pair_a - ida;
+    S.comp.pair_b = h->pair_b - ida;
+    FSTC_CUDA_TRY(cudaMemcpyAsync(S.d_comp, &S.comp, sizeof(CompDev), cudaMemcpyHostToDevice, s));
+    int64_t tot[4] = {0, 0, hb[4], hb[5]};
+    FSTC_CUDA_TRY(cudaMemcpyAsync(S.d_tot, tot, sizeof(tot), cudaMemcpyHostToDevice, s));
+    {
+      EventTimer te(prof, s);
+      k_emit<<<g_grid, kThreads, kDynSmem, s>>>(S.cx, S.d_tot);
+      FSTC_LAUNCH_CHECK();
+      stats.ms_emit += te.stop();
+    }
+    if (nv > 0) {  // shard-local row_ptr
+      k_shift_i64<<<nblk(nv, 256), 256, 0, s>>>(h->row_ptr, nv, arca);
+      FSTC_LAUNCH_CHECK();
+    }
+    FSTC_CUDA_TRY(cudaMemcpyAsync(h->row_ptr + nv, &ne, 8, cudaMemcpyHostToDevice, s));
+    FSTC_CUDA_TRY(cudaMemcpyAsync(hp + 2, S.cx.misc + 2, 8, cudaMemcpyDeviceToHost, s));
+    FSTC_CUDA_TRY(cudaStreamSynchronize(s));
+    if (hp[2] != 0) {
+      cleanup();
+      set_error(FST_E_INTERNAL, "sharded emit/count mismatch in %llu blocks", hp[2]);
+      return FST_E_INTERNAL;
+    }
+  }
+  for (auto& S : sh) S.wb.reset();
+  stats.ms_total = t_total.stop();
+  stats.launches = fst_launch_count() - launches0;
+  stats.expand_launches = level_launches;
+  stats.emit_launches = (int64_t)sh.size();
+  for (size_t i = 0; i < sh.size(); ++i) {
+    outs[i]->stats = stats;
+    outs[i]->shard_total_states = total_states;
+    outs[i]->shard_total_arcs = total_arcs;
+    level_sizes_slot(outs[i], 1) = sh[i].sizes1;
+    level_sizes_slot(outs[i], 2) = sh[i].sizes2;
     c[i] = outs[i];
   }
   return FST_OK;

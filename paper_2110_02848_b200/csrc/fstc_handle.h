@@ -76,6 +76,9 @@ struct fst {
   int32_t n_start = 0, n_accept = 0;
   int32_t max_ilabel = -1, max_olabel = -1;
   fst_compose_stats stats{};
+  // sharded compositions: this handle holds rank `shard_rank`'s rows (global state ids in dst)
+  int32_t shard_rank = -1, shard_world = 0;
+  int64_t shard_state_offset = 0, shard_arc_offset = 0, shard_total_states = 0, shard_total_arcs = 0;
   std::vector<int64_t> level_sizes[2];  // frontier size per BFS level, stage 1 / stage 2
   std::vector<fstc::BufferPtr> buffers;  // owned (or shared with a batch) device memory
 };

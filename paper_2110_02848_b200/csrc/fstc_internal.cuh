@@ -64,7 +64,9 @@ struct CompDev {
   int64_t W;         // first word of this composition's pair space
   int64_t K;         // first block
   int64_t Q;         // first chunk
-  // outputs (filled before the emit kernel)
+  int32_t own_r0, own_r1;  // rows (A states) owned by this shard: [own_r0, own_r1) (all rows if unsharded)
+  // outputs (filled before the emit kernel; for a shard they are biased so that a global state id /
+  // arc slot indexes the shard's own buffers)
   int64_t* row_ptr;
   int32_t* ilabel;
   int32_t* olabel;

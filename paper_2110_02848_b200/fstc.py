@@ -27,7 +27,8 @@ STATUS = {0: "FST_OK", 1: "FST_E_INVALID_ARG", 2: "FST_E_INVALID_GRAPH", 3: "FST
 
 EXPORTED = ["fst_create", "fst_compose", "fst_compose_batch", "fst_free", "fst_info", "fst_copy_to_host",
             "fst_get_stats", "fst_level_sizes", "fst_adjacency", "fst_set_profiling", "fst_launch_count",
-            "fst_last_error", "fst_version"]
+            "fst_last_error", "fst_version", "fst_comm_unique_id", "fst_comm_init", "fst_comm_destroy",
+            "fst_compose_sharded", "fst_compose_sharded_local", "fst_shard_info"]
 
 
 class FstError(RuntimeError):
@@ -55,6 +56,14 @@ class fst_compose_stats(C.Structure):
                 ("ms_number", C.c_float), ("ms_alloc", C.c_float), ("ms_emit", C.c_float),
                 ("ms_total", C.c_float), ("launches", C.c_int64), ("emit_launches", C.c_int64),
                 ("expand_launches", C.c_int64), ("staged_tasks", C.c_int64)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+class fst_shard_desc(C.Structure):
+    _fields_ = [("rank", C.c_int32), ("world", C.c_int32), ("state_offset", C.c_int64), ("arc_offset", C.c_int64),
+                ("total_states", C.c_int64), ("total_arcs", C.c_int64)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -90,8 +99,16 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
         lib.fst_launch_count.restype = C.c_int64
         lib.fst_last_error.restype = C.c_char_p
         lib.fst_version.restype = C.c_char_p
+        lib.fst_comm_unique_id.argtypes = [vp]
+        lib.fst_comm_init.argtypes = [C.c_int32, C.c_int32, vp, C.POINTER(vp)]
+        lib.fst_comm_destroy.argtypes = [vp]
+        lib.fst_comm_destroy.restype = None
+        lib.fst_compose_sharded.argtypes = [vp, vp, vp, vp, C.POINTER(vp)]
+        lib.fst_compose_sharded_local.argtypes = [vp, vp, C.c_int32, vp, C.POINTER(vp)]
+        lib.fst_shard_info.argtypes = [vp, C.POINTER(fst_shard_desc)]
         for name in ("fst_create", "fst_compose", "fst_compose_batch", "fst_info", "fst_copy_to_host",
-                     "fst_get_stats", "fst_adjacency"):
+                     "fst_get_stats", "fst_adjacency", "fst_comm_unique_id", "fst_comm_init",
+                     "fst_compose_sharded", "fst_compose_sharded_local", "fst_shard_info"):
             getattr(lib, name).restype = C.c_int
         _lib = lib
         return lib
@@ -165,6 +182,63 @@ def fst_compose_batch(a: Sequence["Fst"], b: Sequence["Fst"], stream=None) -> Li
     return [Fst(C.c_void_p(out[i])) for i in range(n)]
 
 
+def fst_compose_sharded_local(a: "Fst", b: "Fst", world: int, stream=None) -> List["Fst"]:
+    """All `world` shards of the sharded composition in this process (one device)."""
+    lib = load_library()
+    out = (C.c_void_p * world)()
+    _check(lib.fst_compose_sharded_local(a.handle, b.handle, world, _stream_ptr(stream), out))
+    return [Fst(C.c_void_p(out[i])) for i in range(world)]
+
+
+class Comm:
+    """NCCL communicator of the sharded mode (one rank per GPU).  Bootstrap: rank 0 calls
+    ``Comm.unique_id()``, the caller broadcasts the 128 bytes (e.g. torch.distributed), then every
+    rank builds ``Comm(world, rank, uid)``."""
+
+    def __init__(self, world: int, rank: int, uid: bytes):
+        lib = load_library()
+        buf = C.create_string_buffer(bytes(uid), 128)
+        self.handle = C.c_void_p()
+        _check(lib.fst_comm_init(world, rank, buf, C.byref(self.handle)))
+        self.world, self.rank = world, rank
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = C.create_string_buffer(128)
+        _check(load_library().fst_comm_unique_id(buf))
+        return buf.raw
+
+    def close(self):
+        if self.handle and self.handle.value:
+            load_library().fst_comm_destroy(self.handle)
+        self.handle = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def fst_compose_sharded(a: "Fst", b: "Fst", comm: Comm, stream=None) -> "Fst":
+    lib = load_library()
+    h = C.c_void_p()
+    _check(lib.fst_compose_sharded(a.handle, b.handle, comm.handle, _stream_ptr(stream), C.byref(h)))
+    return Fst(h)
+
+
+def merge_shards(parts: Sequence[Dict[str, np.ndarray]], arc_offsets: Sequence[int]) -> Dict[str, np.ndarray]:
+    """Concatenate shard host copies (rank order) into the unsharded graph (numpy; host helper)."""
+    out = {k: np.concatenate([p[k] for p in parts]) for k in ("ilabel", "olabel", "dst", "weight", "is_start",
+                                                              "is_accept", "pair_a", "pair_b")}
+    rps = [p["row_ptr"][:-1] + off for p, off in zip(parts, arc_offsets)]
+    total = sum(int(p["num_arcs"]) for p in parts)
+    out["row_ptr"] = np.concatenate(rps + [np.array([total], np.int64)])
+    out["num_states"] = sum(int(p["num_states"]) for p in parts)
+    out["num_arcs"] = total
+    return out
+
+
 def fst_set_profiling(on: bool):
     load_library().fst_set_profiling(1 if on else 0)
 
@@ -229,6 +303,11 @@ class Fst:
         s = fst_compose_stats()
         _check(load_library().fst_get_stats(self.handle, C.byref(s)))
         return s.as_dict()
+
+    def shard_info(self) -> dict:
+        d = fst_shard_desc()
+        _check(load_library().fst_shard_info(self.handle, C.byref(d)))
+        return d.as_dict()
 
     def level_sizes(self, stage: int) -> List[int]:
         lib = load_library()

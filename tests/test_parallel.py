@@ -63,3 +63,31 @@ def test_gloo_world2_sharding_and_reduction():
     assert sorted(allp0[0] + allp0[1]) == list(range(64)) and not set(allp0[0]) & set(allp0[1])
     for _, _, ms, units in res:
         assert ms == 20.0 and units == 64.0
+
+
+def _uid_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2110_02848_b200 import fstc
+    obj = [fstc.Comm.unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0)  # the sharded mode's NCCL bootstrap (bench.py --mode sharded)
+    q.put((rank, obj[0]))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_gloo_world2_nccl_uid_bootstrap():
+    from paper_2110_02848_b200 import build as b
+    b.build()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_uid_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in range(2))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert len(res[0][1]) == 128 and res[0][1] == res[1][1]
