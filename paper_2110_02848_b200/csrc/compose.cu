@@ -49,6 +49,8 @@ constexpr int kDynSmem = 88 * 1024; // staging area (destination rows)
 constexpr int kSimpleMoves = 4;    // warps whose items have <= this many moves skip the expansion
 constexpr int kHeavy = 64;         // states with more B arcs are walked cooperatively by the CTA
 constexpr int kWCap = 160;         // per-warp output window of the fast emit (arcs)
+constexpr int kOwnerCap = 384;     // per-warp arc-slot owner table of the BFS walk (end of dynamic smem)
+constexpr int kOwnerBytes = kWarps * kOwnerCap;
 
 struct Ctx {
   uint32_t* R;
@@ -242,7 +244,8 @@ __device__ __forceinline__ int item_group(const TaskSmem& s, int i) {
 
 // Stage the A row u_a of view Av: arcs (label-sorted), label masks, destination-row slots.
 // dst_words = shared words needed per destination row; staging succeeds iff m * dst_words fits.
-__device__ void stage_arow(TaskSmem& s, const CompDev& C, const ViewDev& Av, int32_t ua, int dst_words) {
+__device__ void stage_arow(TaskSmem& s, const CompDev& C, const ViewDev& Av, int32_t ua, int dst_words,
+                           int cap_words = kDynSmem / 4) {
   if (threadIdx.x == 0) {
     s.a0 = __ldg(&Av.off[ua]);
     s.a1 = __ldg(&Av.off[ua + 1]);
@@ -285,7 +288,7 @@ __device__ void stage_arow(TaskSmem& s, const CompDev& C, const ViewDev& Av, int
         s.a_slot[k] = j;
       }
       s.m = m;
-      s.dst_staged = ok && (int64_t)m * dst_words <= kDynSmem / 4;
+      s.dst_staged = ok && (int64_t)m * dst_words <= cap_words;
       if (!ok) s.small = 0;  // slots incomplete: the fast paths need a slot for every A arc
     } else {
       s.aeps = lower_bound_g(Av.key, s.a0, s.a1, 0) - s.a0;
@@ -821,6 +824,8 @@ __device__ __forceinline__ void bfs_chunk_fast(TaskSmem& s, const ViewDev& Bv, i
                                                uint8_t* __restrict__ cnt8row, Glob&& glob) {
   const int2* __restrict__ ikd = Bv.ikd;
   const int32_t* __restrict__ off = Bv.off;
+  extern __shared__ uint32_t dyn_bfs[];
+  uint8_t* dynsm = (uint8_t*)dyn_bfs;
   unsigned kept = 0;
   auto cand = [&](int slot, int32_t col, int, int, int32_t) {
     if (kStaged) {
@@ -895,33 +900,56 @@ __device__ __forceinline__ void bfs_chunk_fast(TaskSmem& s, const ViewDev& Bv, i
           }
         }
       }
-      int own = kept;  // stage 2: kept moves (= out-degree in C) of my own state
+      int own_cnt = kept;  // stage 2: kept moves (= out-degree in C) of my own state
       const bool heavy_own = k < stot && deg == 0 && __ldg(&off[ub + 1]) - __ldg(&off[ub]) > kHeavy;
       const int incl = warp_incl_scan(deg);
       const int start = incl - deg;
       const int total = __shfl_sync(0xffffffffu, incl, 31);
       kept = 0;
-      for (int rr = 0; rr < total; rr += 32) {
-        const int c = rr + lane;
+      // arc slot -> owner lane: a per-warp byte table when the batch is small enough, else a
+      // binary search over the lanes' start offsets
+      uint8_t* own = dynsm + (kDynSmem - kOwnerBytes) + (threadIdx.x >> 5) * kOwnerCap;
+      const bool tbl = total <= kOwnerCap;
+      if (tbl)
+        for (int p = start; p < incl; ++p) own[p] = (uint8_t)lane;
+      __syncwarp();
+      auto owner_of = [&](int c) -> int {
+        if (tbl) return c < total ? own[c] : 0;
         int jj = 0;
 #pragma unroll
         for (int step = 16; step > 0; step >>= 1)
           if (__shfl_sync(0xffffffffu, start, jj + step) <= c) jj += step;
-        const int32_t ej = __shfl_sync(0xffffffffu, e, jj) + (c - __shfl_sync(0xffffffffu, start, jj));
-        const int32_t uj = __shfl_sync(0xffffffffu, ub, jj);
+        return jj;
+      };
+      int jn = owner_of(lane);
+      int32_t en = __shfl_sync(0xffffffffu, e, jn) + (lane - __shfl_sync(0xffffffffu, start, jn));
+      int32_t un = __shfl_sync(0xffffffffu, ub, jn);
+      int2 xn = lane < total ? __ldg(&ikd[en]) : make_int2(0, 0);
+      for (int rr = 0; rr < total; rr += 32) {
+        const int c = rr + lane;
+        const int32_t ej = en, uj = un;
+        const int2 xc = xn;
+        if (rr + 32 < total) {  // prefetch the next round's item
+          const int cn = c + 32;
+          jn = owner_of(cn);
+          en = __shfl_sync(0xffffffffu, e, jn) + (cn - __shfl_sync(0xffffffffu, start, jn));
+          un = __shfl_sync(0xffffffffu, ub, jn);
+          if (cn < total) xn = __ldg(&ikd[en]);
+        }
         const unsigned k0 = kept;
-        if (c < total) fast_arc<kM32>(s, __ldg(&ikd[ej]), ej - uj - 1, cand);
+        if (c < total) fast_arc<kM32>(s, xc, ej - uj - 1, cand);
         if (kStage2) {  // attribute this round's kept moves to their states (owner lanes)
           const int kc = (int)(kept - k0);
           const int sc = warp_incl_scan(kc);
           const int lo = max(start - rr, 0), hi = min(incl - rr, 32) - 1;
           const int shi = __shfl_sync(0xffffffffu, sc, max(hi, 0));
           const int slo = __shfl_sync(0xffffffffu, sc, max(lo - 1, 0));
-          if (hi >= lo) own += shi - (lo > 0 ? slo : 0);
+          if (hi >= lo) own_cnt += shi - (lo > 0 ? slo : 0);
         }
       }
       segkept += kept;
-      if (kStage2 && k < stot) cnt8row[ub] = (uint8_t)(heavy_own ? 255 : min(own, 255));
+      __syncwarp();
+      if (kStage2 && k < stot) cnt8row[ub] = (uint8_t)(heavy_own ? 255 : min(own_cnt, 255));
     }
     if (kStage2) {  // the segment lies inside one 1024-pair block
       const unsigned long long t = warp_sum(segkept);
@@ -1011,7 +1039,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_level(Ctx cx, int level) {
     if (nst == 0) continue;
     const int wpr = C.wpr;
     const int per_word = kStage2 ? 3 : 2;  // R, V-snapshot, NEW  |  R-snapshot, NEW
-    stage_arow(s, C, Av, ch.ua, per_word * wpr);
+    stage_arow(s, C, Av, ch.ua, per_word * wpr, (kDynSmem - kOwnerBytes) / 4);
     // stage destination rows only when the chunk has enough work to amortise the staging traffic
     const bool staged = s.dst_staged && (int64_t)nst * 16 >= (int64_t)s.m * wpr;
     uint32_t* Rs = dyn;
