@@ -634,7 +634,7 @@ __device__ __forceinline__ void fast_state4(const TaskSmem& s, const int4* __res
 // stored coalesced.  Returns the block's arc count.
 template <bool kM32, typename Rank, typename StateOut>
 __device__ __forceinline__ int emit_block_fast(TaskSmem& s, const ViewDev& Bv, const CompDev& C, int32_t ub0,
-                                               int32_t ub1, int lw0, int wpr, const uint32_t* Vs, uint32_t* wb,
+                                               int32_t ub1, int lw0, int wpr, const int2* VR, int4* wb4,
                                                const uint8_t* __restrict__ cnt8row, int64_t run, Rank&& rank_of,
                                                StateOut&& state_out) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -642,7 +642,9 @@ __device__ __forceinline__ int emit_block_fast(TaskSmem& s, const ViewDev& Bv, c
   const int4* __restrict__ ikcw = Bv.ikcw;
   const int32_t* __restrict__ boff = Bv.off;
   const int nub = ub1 - ub0;
-  auto present = [&](int slot, int32_t col) -> bool { return (Vs[slot * wpr + (col >> 5)] >> (col & 31)) & 1u; };
+  auto present = [&](int slot, int32_t col) -> bool {
+    return ((uint32_t)VR[slot * wpr + (col >> 5)].x >> (col & 31)) & 1u;
+  };
   // count: states 2t, 2t+1 of thread t; heavy states (> kHeavy arcs) are counted by the whole CTA
   if (threadIdx.x == 0) s.nheavy = 0;
   __syncthreads();
@@ -687,10 +689,6 @@ __device__ __forceinline__ int emit_block_fast(TaskSmem& s, const ViewDev& Bv, c
   s.cur[2 * threadIdx.x + 1] = ex + c0;
   if (threadIdx.x == 0) s.cur[kPairsPerBlock] = btot;
   __syncthreads();
-  int32_t* bd = (int32_t*)wb;
-  int32_t* bi = (int32_t*)(wb + kWCap);
-  int32_t* bo = (int32_t*)(wb + 2 * kWCap);
-  float* bw = (float*)(wb + 3 * kWCap);
   int32_t* __restrict__ od = C.dst;
   int32_t* __restrict__ oi = C.ilabel;
   int32_t* __restrict__ oo = C.olabel;
@@ -735,20 +733,18 @@ __device__ __forceinline__ int emit_block_fast(TaskSmem& s, const ViewDev& Bv, c
           int32_t il, ol;
           float wt;
           fill(kind, a, carry, wbits, il, ol, wt);
-          bd[t] = did;
-          bi[t] = il;
-          bo[t] = ol;
-          bw[t] = wt;
+          wb4[t] = make_int4(did, il, ol, __float_as_int(wt));
         });
       }
       __syncwarp();
       const int n = min(kWCap, q1 - win);
       for (int t = lane; t < n; t += 32) {  // slots of heavy states get overwritten below
         const int64_t pos = run + win + t;
-        __stcs(&od[pos], bd[t]);
-        __stcs(&oi[pos], bi[t]);
-        __stcs(&oo[pos], bo[t]);
-        __stcs(&ow[pos], bw[t]);
+        const int4 v = wb4[t];
+        __stcs(&od[pos], v.x);
+        __stcs(&oi[pos], v.y);
+        __stcs(&oo[pos], v.z);
+        __stcs(&ow[pos], __int_as_float(v.w));
       }
       __syncwarp();
     }
@@ -1317,16 +1313,15 @@ __global__ void __launch_bounds__(kThreads, 2) k_emit(Ctx cx, const int64_t* __r
     load_chunk_bits(s, cx.V, C, ch, false);
     stage_arow(s, C, Av, ch.ua, 2 * wpr);
     const bool staged = s.dst_staged;
-    uint32_t* Vs = dyn;                           // V words of the staged rows
-    int32_t* RB = (int32_t*)(dyn + s.m * wpr);    // rank base of every staged word
+    int2* VR = (int2*)dyn;  // per staged word: (V word, rank of its first pair)
     if (staged) {
       for (int i = threadIdx.x; i < s.m * wpr; i += kThreads) {
         const int r = i / wpr, w = i - r * wpr;
         const int32_t row = s.slot_row[r];
         const int64_t gw = C.W + (int64_t)row * wpr + w;
-        Vs[i] = __ldg(&cx.V[gw]);
         const int64_t blk = C.K + (int64_t)row * C.bpr + (w >> 5);
-        RB[i] = (int32_t)(__ldg(&cx.idbase[blk]) - id_comp + __ldg(&cx.wpre[gw]));
+        VR[i] = make_int2((int32_t)__ldg(&cx.V[gw]),
+                          (int32_t)(__ldg(&cx.idbase[blk]) - id_comp + __ldg(&cx.wpre[gw])));
       }
       __syncthreads();
     }
@@ -1335,10 +1330,9 @@ __global__ void __launch_bounds__(kThreads, 2) k_emit(Ctx cx, const int64_t* __r
       const uint32_t bit = 1u << (col & 31);
       const uint32_t lowmask = bit - 1u;
       if (staged) {
-        const int i = slot * wpr + (col >> 5);
-        const uint32_t w = Vs[i];
-        present = w & bit;
-        return RB[i] + __popc(w & lowmask);
+        const int2 vr = VR[slot * wpr + (col >> 5)];
+        present = (uint32_t)vr.x & bit;
+        return vr.y + __popc((uint32_t)vr.x & lowmask);
       }
       const int64_t gw = C.W + (int64_t)row * wpr + (col >> 5);
       const uint32_t w = __ldg(&cx.V[gw]);
@@ -1374,7 +1368,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_emit(Ctx cx, const int64_t* __r
       __stcs(&C.olabel[pos], ol);
       __stcs(&C.weight[pos], wt);
     };
-    const bool fastE = staged && s.small && (2 * s.m * wpr + kWarps * kWCap * 4) * 4 <= kDynSmem;
+    const bool fastE = staged && s.small && (((2 * s.m * wpr + 3) & ~3) + kWarps * kWCap * 4) * 4 <= kDynSmem;
     if (!fastE) {
       build_groups(s, Bv);
       __syncthreads();
@@ -1387,7 +1381,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_emit(Ctx cx, const int64_t* __r
       const int32_t ub0 = blk * kPairsPerBlock, ub1 = min(ub0 + kPairsPerBlock, C.VB);
       const int lw0 = (blk - ch.b0) * 32;
       if (fastE) {
-        uint32_t* wb = dyn + 2 * s.m * wpr + warp * kWCap * 4;
+        int4* wb = (int4*)(dyn + ((2 * s.m * wpr + 3) & ~3)) + warp * kWCap;
         auto rk = [&](int slot, int32_t col, bool& pr) -> int32_t { return rank_of(slot, 0, col, pr); };
         auto so = [&](int32_t ub, int64_t at) {
           bool pr;
@@ -1399,8 +1393,8 @@ __global__ void __launch_bounds__(kThreads, 2) k_emit(Ctx cx, const int64_t* __r
           C.is_accept[id] = (uint8_t)(acA & __ldg(&C.accB[ub]));
         };
         const uint8_t* cnt8row = cx.cnt8 + ch.rowW * 32;
-        const int btot = s.mask32 ? emit_block_fast<true>(s, Bv, C, ub0, ub1, lw0, wpr, Vs, wb, cnt8row, run, rk, so)
-                                  : emit_block_fast<false>(s, Bv, C, ub0, ub1, lw0, wpr, Vs, wb, cnt8row, run, rk, so);
+        const int btot = s.mask32 ? emit_block_fast<true>(s, Bv, C, ub0, ub1, lw0, wpr, VR, wb, cnt8row, run, rk, so)
+                                  : emit_block_fast<false>(s, Bv, C, ub0, ub1, lw0, wpr, VR, wb, cnt8row, run, rk, so);
         if (threadIdx.x == 0 && (unsigned long long)btot != cx.kept[gblk]) atomicAdd(&cx.misc[2], 1ull);
         run += btot;
         __syncthreads();
