@@ -135,6 +135,10 @@ fst_status fst_copy_to_host(fst_handle h, void* stream, int64_t* row_ptr, int32_
                             int32_t* olabel, int32_t* dst, float* weight, uint8_t* is_start,
                             uint8_t* is_accept, int32_t* pair_a, int32_t* pair_b);
 
+/* Copies arcs [first, first+count) of a handle into HOST buffers (any may be NULL).  Synchronous. */
+fst_status fst_copy_arcs_to_host(fst_handle h, void* stream, int64_t first, int64_t count, int32_t* ilabel,
+                                 int32_t* olabel, int32_t* dst, float* weight);
+
 /* Statistics of the composition that produced handle c (composed handles only). */
 fst_status fst_get_stats(fst_handle c, fst_compose_stats* s);
 

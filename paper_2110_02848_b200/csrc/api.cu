@@ -142,6 +142,23 @@ fst_status fst_copy_to_host(fst_handle h, void* stream, int64_t* row_ptr, int32_
   return FST_OK;
 }
 
+fst_status fst_copy_arcs_to_host(fst_handle h, void* stream, int64_t first, int64_t count, int32_t* ilabel,
+                                 int32_t* olabel, int32_t* dst, float* weight) {
+  if (!h || first < 0 || count < 0 || first + count > h->E) {
+    set_error(FST_E_INVALID_ARG, "fst_copy_arcs_to_host: bad range");
+    return FST_E_INVALID_ARG;
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  if (count > 0) {
+    if (ilabel) FSTC_CUDA_TRY(cudaMemcpyAsync(ilabel, h->ilabel + first, 4 * count, cudaMemcpyDeviceToHost, s));
+    if (olabel) FSTC_CUDA_TRY(cudaMemcpyAsync(olabel, h->olabel + first, 4 * count, cudaMemcpyDeviceToHost, s));
+    if (dst) FSTC_CUDA_TRY(cudaMemcpyAsync(dst, h->dst + first, 4 * count, cudaMemcpyDeviceToHost, s));
+    if (weight) FSTC_CUDA_TRY(cudaMemcpyAsync(weight, h->weight + first, 4 * count, cudaMemcpyDeviceToHost, s));
+  }
+  FSTC_CUDA_TRY(cudaStreamSynchronize(s));
+  return FST_OK;
+}
+
 fst_status fst_get_stats(fst_handle c, fst_compose_stats* s) {
   if (!c || !s || !c->composed) {
     set_error(FST_E_INVALID_ARG, "fst_get_stats: need a composed handle");

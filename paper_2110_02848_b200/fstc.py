@@ -28,7 +28,7 @@ STATUS = {0: "FST_OK", 1: "FST_E_INVALID_ARG", 2: "FST_E_INVALID_GRAPH", 3: "FST
 EXPORTED = ["fst_create", "fst_compose", "fst_compose_batch", "fst_free", "fst_info", "fst_copy_to_host",
             "fst_get_stats", "fst_level_sizes", "fst_adjacency", "fst_set_profiling", "fst_launch_count",
             "fst_last_error", "fst_version", "fst_comm_unique_id", "fst_comm_init", "fst_comm_destroy",
-            "fst_compose_sharded", "fst_compose_sharded_local", "fst_shard_info"]
+            "fst_compose_sharded", "fst_compose_sharded_local", "fst_shard_info", "fst_copy_arcs_to_host"]
 
 
 class FstError(RuntimeError):
@@ -91,6 +91,7 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
         lib.fst_info.argtypes = [vp, C.POINTER(fst_view)]
         lib.fst_copy_to_host.argtypes = [vp, vp] + [vp] * 9
         lib.fst_get_stats.argtypes = [vp, C.POINTER(fst_compose_stats)]
+        lib.fst_copy_arcs_to_host.argtypes = [vp, vp, C.c_int64, C.c_int64, vp, vp, vp, vp]
         lib.fst_level_sizes.argtypes = [vp, C.c_int32, vp, C.c_int32]
         lib.fst_level_sizes.restype = C.c_int32
         lib.fst_adjacency.argtypes = [vp, C.c_int32, C.c_int32, vp, vp]
@@ -108,7 +109,7 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
         lib.fst_shard_info.argtypes = [vp, C.POINTER(fst_shard_desc)]
         for name in ("fst_create", "fst_compose", "fst_compose_batch", "fst_info", "fst_copy_to_host",
                      "fst_get_stats", "fst_adjacency", "fst_comm_unique_id", "fst_comm_init",
-                     "fst_compose_sharded", "fst_compose_sharded_local", "fst_shard_info"):
+                     "fst_compose_sharded", "fst_compose_sharded_local", "fst_shard_info", "fst_copy_arcs_to_host"):
             getattr(lib, name).restype = C.c_int
         _lib = lib
         return lib
@@ -297,6 +298,26 @@ class Fst:
         _check(load_library().fst_copy_to_host(self.handle, _stream_ptr(stream), ptr("row_ptr"), ptr("ilabel"),
                                                ptr("olabel"), ptr("dst"), ptr("weight"), ptr("is_start"),
                                                ptr("is_accept"), ptr("pair_a"), ptr("pair_b")))
+        return out
+
+    def state_arrays(self, stream=None) -> Dict[str, np.ndarray]:
+        """Per-state arrays only (row_ptr, flags, pair_a/pair_b) -- no arcs."""
+        v = self.info()
+        V = int(v.num_states)
+        out = {"num_states": V, "num_arcs": int(v.num_arcs), "row_ptr": np.zeros(V + 1, np.int64),
+               "is_start": np.zeros(V, np.uint8), "is_accept": np.zeros(V, np.uint8),
+               "pair_a": np.zeros(V, np.int32), "pair_b": np.zeros(V, np.int32)}
+        ptr = lambda k: out[k].ctypes.data if out[k].size else None
+        _check(load_library().fst_copy_to_host(self.handle, _stream_ptr(stream), ptr("row_ptr"), None, None, None,
+                                               None, ptr("is_start"), ptr("is_accept"),
+                                               ptr("pair_a") if v.pair_a else None, ptr("pair_b") if v.pair_b else None))
+        return out
+
+    def arcs_range(self, first: int, count: int, stream=None) -> Dict[str, np.ndarray]:
+        out = {"ilabel": np.zeros(count, np.int32), "olabel": np.zeros(count, np.int32),
+               "dst": np.zeros(count, np.int32), "weight": np.zeros(count, np.float32)}
+        p = [out[k].ctypes.data if count else None for k in ("ilabel", "olabel", "dst", "weight")]
+        _check(load_library().fst_copy_arcs_to_host(self.handle, _stream_ptr(stream), first, count, *p))
         return out
 
     def stats(self) -> dict:

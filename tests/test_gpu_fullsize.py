@@ -1,0 +1,53 @@
+"""GPU parity at BASELINE.json's full size, in the configuration bench.py times (configs[3]: random
+acceptors V=20000, D=8, 16 tokens; E_C = 1.44e9 arcs): the oracle cannot compose it in test time, so
+the C oracle computes only the co-accessible set R (Algorithm 1 line 3), and the GPU result is checked
+against it: states = pairs in R only, numbered by ascending key, start/accept flags by definition, and
+2000 sampled rows equal EXACTLY (labels, destinations, weight bits) the N1 moves of their pair whose
+destination is co-accessible (pins.n1_moves: the plain definition)."""
+import numpy as np
+import pytest
+
+import fstgen
+import oracle
+import pins
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def fst():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    from paper_2110_02848_b200 import build as b
+    b.build()
+    import paper_2110_02848_b200 as p
+    p.load_library()
+    return p
+
+
+def test_c4_fullsize_against_oracle_R(fst):
+    A, B = fstgen.config_c4(V=20000, D=8)
+    VB = B.num_states
+    R = oracle.coaccessible(A, B)  # Algorithm 1 line 3 on the CPU
+    c = fst.fst_compose(fst.fst_create(A), fst.fst_create(B))
+    st = c.state_arrays()
+    V_C, E_C = st["num_states"], st["num_arcs"]
+    assert V_C > 3e8 and E_C > 1e9
+    keys = st["pair_a"].astype(np.int64) * VB + st["pair_b"]
+    assert np.all(np.diff(keys) > 0)                      # numbering by ascending pair key
+    assert np.all(R[keys] == 1) and V_C <= int(R.sum())   # every state of C is co-accessible
+    assert np.array_equal(st["is_start"], A.is_start[st["pair_a"]] & B.is_start[st["pair_b"]])
+    assert np.array_equal(st["is_accept"], A.is_accept[st["pair_a"]] & B.is_accept[st["pair_b"]])
+    assert st["row_ptr"][0] == 0 and st["row_ptr"][-1] == E_C and np.all(np.diff(st["row_ptr"]) >= 0)
+    rng = np.random.default_rng(2110)
+    sample = np.unique(np.concatenate([rng.choice(V_C, 2000, replace=False), [0, V_C - 1]]))
+    for sid in sample:
+        a, b = int(st["pair_a"][sid]), int(st["pair_b"][sid])
+        lo, hi = int(st["row_ptr"][sid]), int(st["row_ptr"][sid + 1])
+        got = c.arcs_range(lo, hi - lo)
+        got_rows = sorted((int(keys[d]), int(i), int(o), int(np.float32(w).view(np.uint32)))
+                          for d, i, o, w in zip(got["dst"], got["ilabel"], got["olabel"], got["weight"]))
+        exp_rows = sorted((d[0] * VB + d[1], il, ol, pins.wbits(w)) for d, il, ol, w in pins.n1_moves(A, B, a, b)
+                          if R[d[0] * VB + d[1]])
+        assert got_rows == exp_rows, (sid, a, b)
