@@ -831,7 +831,7 @@ __device__ __forceinline__ void bfs_chunk_fast(TaskSmem& s, const ViewDev& Bv, i
         if (!(Rs[idx] & bit)) return;
         ++kept;
       }
-      if ((VS[idx] | NW[idx]) & bit) return;
+      if (NW[idx] & bit) return;  // NW starts as the visited snapshot
       atomicOr(&NW[idx], bit);
     } else {
       kept += glob(slot, col);
@@ -1046,13 +1046,10 @@ __global__ void __launch_bounds__(kThreads, 2) k_level(Ctx cx, int level) {
       for (int i = threadIdx.x; i < m * wpr; i += kThreads) {
         const int r = i / wpr, w = i - r * wpr;
         const int64_t gw = C.W + (int64_t)s.slot_row[r] * wpr + w;
-        if (kStage2) {
-          Rs[i] = __ldg(&cx.R[gw]);
-          VS[i] = cx.V[gw];
-        } else {
-          VS[i] = cx.R[gw];
-        }
-        NW[i] = 0u;
+        const uint32_t v = kStage2 ? cx.V[gw] : cx.R[gw];
+        if (kStage2) Rs[i] = __ldg(&cx.R[gw]);
+        VS[i] = v;
+        NW[i] = v;  // claims accumulate on top of the snapshot
       }
       __syncthreads();
     }
@@ -1177,7 +1174,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_level(Ctx cx, int level) {
       __syncthreads();
       const int m = s.m;
       for (int i = threadIdx.x; i < m * wpr; i += kThreads) {
-        const uint32_t nb = NW[i];
+        const uint32_t nb = NW[i] & ~VS[i];
         if (!nb) continue;
         const int r = i / wpr, w = i - r * wpr;
         const int32_t row = s.slot_row[r];
