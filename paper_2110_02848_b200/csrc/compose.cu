@@ -862,49 +862,29 @@ __device__ __forceinline__ void bfs_chunk_fast(TaskSmem& s, const ViewDev& Bv, i
     const int wex = winc - pc;
     const int stot = __shfl_sync(0xffffffffu, winc, 31);
     unsigned long long segkept = 0;
-    // the k-th frontier state of the segment (or -1): warp scan over the words + in-word select
-    auto select = [&](int k) -> int32_t {
+    for (int b0 = 0; b0 < stot; b0 += 32) {
+      const int k = b0 + lane;
       int j = 0;
 #pragma unroll
       for (int step = 16; step > 0; step >>= 1)
         if (__shfl_sync(0xffffffffu, wex, j + step) <= k) j += step;
       uint32_t wj = __shfl_sync(0xffffffffu, word, j);
       int r = k - __shfl_sync(0xffffffffu, wex, j);
-      if (k >= stot) return -1;
-      int pos = 0;
-#pragma unroll
-      for (int h = 16; h > 0; h >>= 1) {
-        const int c = __popc(wj & ((1u << h) - 1u));
-        if (r >= c) {
-          r -= c;
-          pos += h;
-          wj >>= h;
-        }
-      }
-      return cub0 + (seg * kSegWords + j) * 32 + pos;
-    };
-    // batches of 32 states; the next batch's state and offsets are loaded one batch ahead
-    int32_t ubN = select(lane), o0N = 0, o1N = 0;
-    if (ubN >= 0) {
-      o0N = __ldg(&off[ubN]);
-      o1N = __ldg(&off[ubN + 1]);
-    }
-    for (int b0 = 0; b0 < stot; b0 += 32) {
-      const int k = b0 + lane;
-      const int32_t ubc = ubN, o0 = o0N, o1 = o1N;
-      if (b0 + 32 < stot) {
-        ubN = select(b0 + 32 + lane);
-        if (ubN >= 0) {
-          o0N = __ldg(&off[ubN]);
-          o1N = __ldg(&off[ubN + 1]);
-        }
-      }
       int32_t ub = 0, e = 0, deg = 0;
-      bool heavy_own = false;
       if (k < stot) {
-        ub = ubc;
-        e = o0 + ub + 1;
-        deg = o1 - o0;
+        int pos = 0;  // r-th set bit of wj (binary search on popcounts)
+#pragma unroll
+        for (int h = 16; h > 0; h >>= 1) {
+          const int c = __popc(wj & ((1u << h) - 1u));
+          if (r >= c) {
+            r -= c;
+            pos += h;
+            wj >>= h;
+          }
+        }
+        ub = cub0 + (seg * kSegWords + j) * 32 + pos;
+        e = __ldg(&off[ub]) + ub + 1;
+        deg = __ldg(&off[ub + 1]) + ub + 1 - e;
         kept = 0;
         for (int a = 0; a < s.aeps; ++a) cand(s.a_slot[a], ub, 2, a, -1);  // M2 moves of the state
         segkept += kept;
@@ -913,11 +893,11 @@ __device__ __forceinline__ void bfs_chunk_fast(TaskSmem& s, const ViewDev& Bv, i
           if (hh < kPairsPerBlock) {
             s.cur[hh] = ub;
             deg = 0;
-            heavy_own = true;
           }
         }
       }
       int own_cnt = kept;  // stage 2: kept moves (= out-degree in C) of my own state
+      const bool heavy_own = k < stot && deg == 0 && __ldg(&off[ub + 1]) - __ldg(&off[ub]) > kHeavy;
       const int incl = warp_incl_scan(deg);
       const int start = incl - deg;
       const int total = __shfl_sync(0xffffffffu, incl, 31);
