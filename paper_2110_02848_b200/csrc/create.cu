@@ -273,6 +273,14 @@ __global__ void __launch_bounds__(1024) k_flag_lists(int32_t V, const uint8_t* _
 
 inline unsigned nblk(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
 
+__global__ void k_view_maxdeg(int32_t V, const int32_t* __restrict__ off, int32_t* __restrict__ out) {
+  int32_t m = 0;
+  for (int32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < V; v += gridDim.x * blockDim.x)
+    m = max(m, off[v + 1] - off[v]);
+  m = __reduce_max_sync(0xffffffffu, (unsigned)m);
+  if ((threadIdx.x & 31) == 0 && m) atomicMax(out, m);
+}
+
 int bits_for(int64_t x) {  // bits to represent values in [0, x]
   int b = 0;
   while (b < 62 && (1ll << b) <= x) ++b;
@@ -438,6 +446,8 @@ fst_status build_views(fst* h, cudaStream_t s, int32_t max_il, int32_t max_ol) {
         FSTC_CUDA_TRY(cudaMemcpyAsync(&lm_counts[slot][0], segi + E, 8, cudaMemcpyDeviceToHost, s));
         FSTC_CUDA_TRY(cudaMemcpyAsync(&lm_counts[slot][1], labi + E, 8, cudaMemcpyDeviceToHost, s));
       }
+      k_view_maxdeg<<<std::min(nblk(V, 256), 1184u), 256, 0, s>>>(V, w.off, counts + 2 + k);
+      FSTC_LAUNCH_CHECK();
     } else {
       FSTC_CUDA_TRY(cudaMemsetAsync(w.off, 0, sizeof(int32_t) * (V + 1), s));
       if (V > 0) {
@@ -460,6 +470,7 @@ fst_status build_views(fst* h, cudaStream_t s, int32_t max_il, int32_t max_ol) {
     h->n_accept = V > 0 ? hc[1] : 0;
     h->max_ilabel = max_il;
     h->max_olabel = max_ol;
+    for (int k = 0; k < 4; ++k) h->views[k].max_deg = E > 0 ? hc[2 + k] : 0;
     h->views[kOutByIlabel].nseg = (int32_t)lm_counts[0][0];
     h->views[kOutByIlabel].nlab = (int32_t)lm_counts[0][1];
     h->views[kInByIlabel].nseg = (int32_t)lm_counts[1][0];

@@ -49,6 +49,7 @@ struct View {
   int32_t* lab_val = nullptr;   // [E] distinct labels, ascending
   int32_t* lab_seg = nullptr;   // [E+1] first segment of each distinct label
   int32_t nseg = 0, nlab = 0;
+  int32_t max_deg = 0;  // largest node degree of the view
 };
 
 }  // namespace fstc

@@ -137,6 +137,36 @@ def test_eps_small_graphs(fst):
         check(fst, A, B, f"eps dag {s}")
 
 
+def hub_graph(V, D, tokens, seed, hub_out, hub_in, n_out, n_in):
+    """random_graph plus a state with ``n_out`` out-arcs and one with ``n_in`` in-arcs (random labels
+    incl. eps, dyadic weights): states above the k_heavy threshold (1024 B arcs) in both stages."""
+    g = fstgen.random_graph(V, D, tokens, seed, acceptor=False, eps_prob=0.1, weights="dyadic64")
+    r = fstgen.SplitMix64(seed + 77)
+    src, dst = list(g.src), list(g.dst)
+    il, ol, w = list(g.ilabel), list(g.olabel), list(g.weight)
+    for k in range(n_out + n_in):
+        src.append(hub_out if k < n_out else r.below(V))
+        dst.append(r.below(V) if k < n_out else hub_in)
+        il.append(r.below(tokens + 1) - 1)
+        ol.append(r.below(tokens + 1) - 1)
+        w.append((r.below(64) - 32) / 16.0)
+    return fstgen.Fst.from_arcs(V, src, dst, il, ol, w, [0], [V - 1, hub_in])
+
+
+@pytest.mark.parametrize("n_hub,a_hub", [(1500, 0), (5000, 40), (2049, 20)])
+def test_heavy_hub_states(fst, n_hub, a_hub):
+    """B states with thousands of arcs (split into grid-wide pieces) x A rows with <= 32 and > 32 arcs."""
+    B = hub_graph(3000, 3, 8, 11 + n_hub, 0, 5, n_hub, n_hub)
+    A = hub_graph(300, 3, 8, 13 + n_hub, 1, 2, a_hub, 0)
+    check(fst, A, B, f"hub {n_hub}/{a_hub}")
+
+
+def test_c3_heavy_lexicon_root(fst):
+    """closure(3000-word lexicon): the root has > 1024 in-arcs (stage 1 pieces)."""
+    A, B = fstgen.config_c3(num_words=3000, T=30)
+    check(fst, A, B, "c3 3000 words")
+
+
 def test_identity_at_scale(fst):
     """A o Id == trim(A) on a config-4-sized A (20k states, degree 8)."""
     A, _ = fstgen.config_c4(V=20000, D=8)
