@@ -150,6 +150,7 @@ struct TaskSmem {
   int32_t mask32;
   int32_t slot_row[kSlotMax];
   int32_t a0, a1, deg, aeps, m, arow_smem, dst_staged, small;
+  unsigned long long repmask;         // stage_arow: A arcs that open a new destination-row slot
   int32_t state[kPairsPerBlock];      // compacted source states of a sparse block (ascending u_b)
   int32_t scan[kPairsPerBlock + 1];   // their item offsets
   int32_t bwpre[33];
@@ -242,6 +243,8 @@ __device__ __forceinline__ int item_group(const TaskSmem& s, int i) {
   return g;
 }
 
+__device__ __forceinline__ bool rep_is(unsigned long long rm, int t) { return (rm >> t) & 1ull; }
+
 // Stage the A row u_a of view Av: arcs (label-sorted), label masks, destination-row slots.
 // dst_words = shared words needed per destination row; staging succeeds iff m * dst_words fits.
 __device__ void stage_arow(TaskSmem& s, const CompDev& C, const ViewDev& Av, int32_t ua, int dst_words,
@@ -253,6 +256,7 @@ __device__ void stage_arow(TaskSmem& s, const CompDev& C, const ViewDev& Av, int
     s.arow_smem = s.deg <= kAMax;
     s.small = s.arow_smem && C.smallA;
     s.aeps = 0;
+    s.repmask = 0ull;
   }
   __syncthreads();
   if (s.arow_smem) {
@@ -262,38 +266,53 @@ __device__ void stage_arow(TaskSmem& s, const CompDev& C, const ViewDev& Av, int
       s.a_carry[k] = __ldg(&Av.carry[s.a0 + k]);
       s.a_w[k] = __ldg(&Av.w[s.a0 + k]);
     }
-    if (threadIdx.x < 64) s.labmask[threadIdx.x] = 0ull;
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
-    if (s.arow_smem) {
-      int aeps = 0;
-      while (aeps < s.deg && s.a_key[aeps] < 0) ++aeps;
-      s.aeps = aeps;
+  const int t = threadIdx.x;
+  if (s.arow_smem) {  // (all in parallel, threads < 64) label masks, eps count, slot-opening arcs
+    const int deg = s.deg;
+    if (t < 64) {
+      unsigned long long lm = 0ull;
       if (s.small)
-        for (int k = 0; k < s.deg; ++k) s.labmask[s.a_key[k] + 1] |= 1ull << k;
-      s.mask32 = s.deg <= 32;
-      for (int l = 0; l < 64; ++l) s.labmask32[l] = (uint32_t)s.labmask[l];
-      // destination-row slots: slot 0 = u_a (M3 moves), then distinct dst rows
-      int m = 1;
-      s.slot_row[0] = ua;
-      bool ok = true;
-      for (int k = 0; k < s.deg; ++k) {
-        int r = s.a_other[k], j = 0;
-        while (j < m && s.slot_row[j] != r) ++j;
-        if (j == m) {
-          if (m == kSlotMax) { ok = false; break; }
-          s.slot_row[m++] = r;
-        }
-        s.a_slot[k] = j;
+        for (int k = 0; k < deg; ++k) lm |= (unsigned long long)(s.a_key[k] + 1 == t) << k;
+      s.labmask[t] = lm;
+      s.labmask32[t] = (uint32_t)lm;
+      if (t < deg) {
+        if (s.a_key[t] < 0 && (t + 1 == deg || s.a_key[t + 1] >= 0)) s.aeps = t + 1;  // eps arcs sort first
+        const int r = s.a_other[t];
+        bool first = r != ua;
+        for (int j = 0; j < t && first; ++j) first = s.a_other[j] != r;
+        if (first) atomicOr(&s.repmask, 1ull << t);
       }
-      s.m = m;
+    }
+  } else if (t == 0) {
+    s.aeps = lower_bound_g(Av.key, s.a0, s.a1, 0) - s.a0;
+    s.m = 0;
+    s.dst_staged = 0;
+  }
+  __syncthreads();
+  if (s.arow_smem) {
+    // destination-row slots: slot 0 = u_a (M3 moves), then the distinct rows in order of first arc
+    const unsigned long long rm = s.repmask;
+    const int m = 1 + __popcll(rm);
+    const bool ok = m <= kSlotMax;
+    if (t < s.deg) {
+      const int r = s.a_other[t];
+      int slot = 0;
+      if (r != ua) {
+        int rep = 0;
+        while (s.a_other[rep] != r) ++rep;
+        slot = 1 + __popcll(rm & ((1ull << rep) - 1ull));
+      }
+      s.a_slot[t] = slot;
+      if (slot > 0 && rep_is(rm, t) && slot < kSlotMax) s.slot_row[slot] = r;
+    }
+    if (t == 0) {
+      s.slot_row[0] = ua;
+      s.m = ok ? m : kSlotMax;
+      s.mask32 = s.deg <= 32;
       s.dst_staged = ok && (int64_t)m * dst_words <= cap_words;
       if (!ok) s.small = 0;  // slots incomplete: the fast paths need a slot for every A arc
-    } else {
-      s.aeps = lower_bound_g(Av.key, s.a0, s.a1, 0) - s.a0;
-      s.m = 0;
-      s.dst_staged = 0;
     }
   }
   __syncthreads();
