@@ -1070,14 +1070,29 @@ __global__ void __launch_bounds__(kThreads, 2) k_level(Ctx cx, int level) {
     uint32_t* VS = kStage2 ? dyn + s.m * wpr : dyn;
     uint32_t* NW = VS + s.m * wpr;
     if (staged) {
-      const int m = s.m;
-      for (int i = threadIdx.x; i < m * wpr; i += kThreads) {
-        const int r = i / wpr, w = i - r * wpr;
-        const int64_t gw = C.W + (int64_t)s.slot_row[r] * wpr + w;
-        const uint32_t v = kStage2 ? cx.V[gw] : cx.R[gw];
-        if (kStage2) Rs[i] = __ldg(&cx.R[gw]);
-        VS[i] = v;
-        NW[i] = v;  // claims accumulate on top of the snapshot
+      const int n = s.m * wpr;
+      for (int i0 = threadIdx.x; i0 < n; i0 += 4 * kThreads) {  // 4 independent loads in flight per thread
+        uint32_t v[4], rv[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int i = i0 + u * kThreads;
+          v[u] = rv[u] = 0u;
+          if (i < n) {
+            const int r = i / wpr, w = i - r * wpr;
+            const int64_t gw = C.W + (int64_t)s.slot_row[r] * wpr + w;
+            v[u] = kStage2 ? cx.V[gw] : cx.R[gw];
+            if (kStage2) rv[u] = __ldg(&cx.R[gw]);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int i = i0 + u * kThreads;
+          if (i < n) {
+            if (kStage2) Rs[i] = rv[u];
+            VS[i] = v[u];
+            NW[i] = v[u];  // claims accumulate on top of the snapshot
+          }
+        }
       }
       __syncthreads();
     }
