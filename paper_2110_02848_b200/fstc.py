@@ -18,7 +18,7 @@ from typing import Dict, List, Optional, Sequence
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libfstc.so")
+LIB_PATH = os.environ.get("FSTC_LIB") or os.path.join(_HERE, "libfstc.so")  # FSTC_LIB: A/B runs (scripts/ab_build.sh)
 
 FST_EPS = -1
 FST_MEM_DEVICE, FST_MEM_HOST = 0, 1

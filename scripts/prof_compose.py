@@ -14,10 +14,25 @@ ap.add_argument("--T", type=int, default=0)
 ap.add_argument("--n", type=int, default=1)
 ap.add_argument("--workload", default="random")
 args = ap.parse_args()
-if args.workload == "lexicon":
+if args.workload == "c5":
+    pass
+elif args.workload == "lexicon":
     A, B = fstgen.config_c3(num_words=10000, T=300)
 else:
     A, B = fstgen.config_c4(V=args.V, D=args.D, tokens=args.T or None)
+if args.workload == "c5":  # the bench's c5 batch (32 utterances, one fst_compose_batch call)
+    import bench  # noqa: E402
+    As, B, _ = bench.c5_shard(0, 1)
+    hb = fstc.fst_create(B)
+    ha = [fstc.fst_create(x) for x in As]
+    fstc.fst_set_profiling(True)
+    for i in range(args.n + 1):
+        cs = fstc.fst_compose_batch(ha, [hb] * len(ha))
+        print(i, sum(c.num_arcs for c in cs), {k: round(v, 3) if isinstance(v, float) else v
+                                               for k, v in cs[0].stats().items()}, flush=True)
+        for c in cs:
+            c.free()
+    sys.exit(0)
 a, b = fstc.fst_create(A), fstc.fst_create(B)
 fstc.fst_set_profiling(True)
 for i in range(args.n + 1):
