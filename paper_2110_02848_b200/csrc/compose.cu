@@ -48,7 +48,6 @@ constexpr int kChunkMaxBlocks = 32; // blocks per chunk (<= 1024 words)
 constexpr int kDynSmem = 88 * 1024; // staging area (destination rows)
 constexpr int kSimpleMoves = 4;    // warps whose items have <= this many moves skip the expansion
 constexpr int kHeavy = 64;         // states with more B arcs are walked cooperatively by the CTA
-constexpr int kDenseBits = 16;     // frontier words with at least this many states take the dense walk
 constexpr int kWCap = 160;         // per-warp output window of the fast emit (arcs)
 constexpr int kOwnerCap = 384;     // per-warp arc-slot owner table of the BFS walk (end of dynamic smem)
 constexpr int kOwnerBytes = kWarps * kOwnerCap;
@@ -870,87 +869,18 @@ __device__ __forceinline__ void bfs_chunk_fast(TaskSmem& s, const ViewDev& Bv, i
   const int lane = threadIdx.x & 31;
   const int nw = (cub1 - cub0 + 31) >> 5;
   constexpr int kSegWords = 8;  // 256-pair segments, handed out dynamically (load balance)
-  // One dense frontier word (local word index lw, bits wj): lane l owns state ub0 + l.  The items of
-  // the word's states [ub0, uend) are walked in rounds of 32 consecutive items; an arc's owner is
-  // the node of the last sentinel at or before it.  Deferred heavy states split the walk into runs.
-  // Returns the word's kept moves (stage 2) and records each state's count in cnt8row.
-  auto dense_word = [&](int lw, uint32_t wj) -> unsigned {
-    const int32_t ub0 = cub0 + lw * 32, uend = min(ub0 + 32, cub1);
-    const int32_t ubl = ub0 + lane;
-    const bool in = (wj >> lane) & 1u;
-    const int32_t ol = __ldg(&off[min(ubl, uend)]);
-    int32_t on = __shfl_down_sync(0xffffffffu, ol, 1);
-    if (lane == 31) on = __ldg(&off[uend]);
-    int deg = on - ol;
-    kept = 0;
-    if (in)
-      for (int a = 0; a < s.aeps; ++a) cand(s.a_slot[a], ubl, 2, a, -1);  // M2 moves of the state
-    int own_cnt = kept;
-    bool heavy_own = false;
-    if (in && deg > kHeavy) {
-      const int hh = atomicAdd(&s.nheavy, 1);
-      if (hh < kPairsPerBlock) {
-        s.cur[hh] = ubl;
-        heavy_own = true;
-      }
-    }
-    const int32_t P = ol + ubl;  // sentinel position of state ubl
-    uint32_t hv = __ballot_sync(0xffffffffu, heavy_own);
-    int lo_state = 0;
-    for (;;) {
-      const int hi_state = hv ? __ffs(hv) - 1 : 32;
-      // items of states [lo_state, hi_state): [P(lo_state), P(hi_state))
-      const int32_t ib = __shfl_sync(0xffffffffu, P, min(lo_state, 31));
-      int32_t ie = __shfl_sync(0xffffffffu, P, min(hi_state, 31));
-      if (hi_state == 32) ie = __shfl_sync(0xffffffffu, on, 31) + uend;  // end of state uend - 1
-      if (lo_state < 32) {
-        int32_t carry = 0;
-        for (int32_t p0 = ib; p0 < ie; p0 += 32) {
-          const int32_t p = p0 + lane;
-          const int2 x = p < ie ? __ldg(&ikd[p]) : make_int2(kSentinel, 0);
-          const uint32_t sm = __ballot_sync(0xffffffffu, p < ie && x.x == kSentinel);
-          const uint32_t le = sm & (0xffffffffu >> (31 - lane));
-          const int32_t nd = __shfl_sync(0xffffffffu, x.y, le ? 31 - __clz(le) : 0);
-          const int32_t owner = le ? nd : carry;
-          carry = __shfl_sync(0xffffffffu, owner, 31);
-          const unsigned k0 = kept;
-          if (p < ie && x.x != kSentinel && ((wj >> (owner - ub0)) & 1u)) fast_arc<kM32>(s, x, p - owner - 1, cand);
-          if (kStage2) {  // attribute the round's kept moves to their states
-            const int kc = (int)(kept - k0);
-            const int sc = warp_incl_scan(kc);
-            const int lo = max(P + 1 - p0, 0), hi = min(P + 1 + deg - p0, 32) - 1;
-            const int shi = __shfl_sync(0xffffffffu, sc, max(hi, 0));
-            const int slo = __shfl_sync(0xffffffffu, sc, max(lo - 1, 0));
-            if (hi >= lo) own_cnt += shi - (lo > 0 ? slo : 0);
-          }
-        }
-      }
-      if (!hv) break;
-      lo_state = hi_state + 1;
-      hv &= hv - 1;
-    }
-    if (kStage2 && in) cnt8row[ubl] = (uint8_t)(heavy_own ? 255 : min(own_cnt, 255));
-    return kept;  // all kept moves walked by this lane
-  };
   for (;;) {
     int seg = 0;
     if (lane == 0) seg = atomicAdd(&s.segnext, 1);
     seg = __shfl_sync(0xffffffffu, seg, 0);
     if (seg * kSegWords >= nw) break;
     const int wi = seg * kSegWords + lane;
-    const uint32_t word0 = (lane < kSegWords && wi < nw) ? s.fw[wi] : 0u;
-    unsigned long long segkept = 0;
-    // dense words: the 32 states' items are one contiguous, coalesced range of B's item array
-    const bool dense = __popc(word0) >= kDenseBits;
-    for (uint32_t dm = __ballot_sync(0xffffffffu, dense); dm; dm &= dm - 1) {
-      const int j = __ffs(dm) - 1;
-      segkept += dense_word(seg * kSegWords + j, __shfl_sync(0xffffffffu, word0, j));
-    }
-    const uint32_t word = dense ? 0u : word0;  // sparse words: select the frontier states 32 at a time
+    const uint32_t word = (lane < kSegWords && wi < nw) ? s.fw[wi] : 0u;
     const int pc = __popc(word);
     const int winc = warp_incl_scan(pc);
     const int wex = winc - pc;
     const int stot = __shfl_sync(0xffffffffu, winc, 31);
+    unsigned long long segkept = 0;
     for (int b0 = 0; b0 < stot; b0 += 32) {
       const int k = b0 + lane;
       int j = 0;
