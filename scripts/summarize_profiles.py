@@ -61,6 +61,15 @@ def main(rnd="r01", workload="c4"):
         for k, (n, ms) in sorted(agg.items(), key=lambda kv: -kv[1][1]):
             lines.append(f"| {k} | {n} | {ms:.3f} | {100 * ms / tot:.1f}% |")
         lines.append("")
+    lp = os.path.join(src, "launches_c5.csv")
+    if os.path.exists(lp):
+        agg = launches(lp)
+        tot = sum(v[1] for v in agg.values())
+        lines += ["## Launch list, configs[4] c5 batch (32 utterances o closure(10k-word lexicon), one "
+                  "fst_compose_batch)", "", "| kernel | launches | total ms | share |", "|---|---|---|---|"]
+        for k, (n, ms) in sorted(agg.items(), key=lambda kv: -kv[1][1])[:12]:
+            lines.append(f"| {k} | {n} | {ms:.3f} | {100 * ms / tot:.1f}% |")
+        lines.append("")
     traffic = {}
     for name, label in (("emit_c4_20k", "k_emit"), ("level14_c4_20k", "k_level (stage 1, level 14 = peak)")):
         rep = os.path.join(src, name + ".ncu-rep")
