@@ -917,6 +917,17 @@ __device__ __forceinline__ void bfs_chunk_fast(TaskSmem& s, const ViewDev& Bv, i
       }
       int own_cnt = kept;  // stage 2: kept moves (= out-degree in C) of my own state
       const bool heavy_own = k < stot && deg == 0 && __ldg(&off[ub + 1]) - __ldg(&off[ub]) > kHeavy;
+      if (__reduce_max_sync(0xffffffffu, (unsigned)deg) <= 2u) {
+        // low-degree batch (e.g. a lexicon trie): every lane walks its own state's <= 2 arcs
+        const int2 x0 = deg > 0 ? __ldg(&ikd[e]) : make_int2(0, 0);
+        const int2 x1 = deg > 1 ? __ldg(&ikd[e + 1]) : make_int2(0, 0);
+        kept = 0;
+        if (deg > 0) fast_arc<kM32>(s, x0, e - ub - 1, cand);
+        if (deg > 1) fast_arc<kM32>(s, x1, e - ub, cand);
+        segkept += kept;
+        if (kStage2 && k < stot) cnt8row[ub] = (uint8_t)(heavy_own ? 255 : min(own_cnt + (int)kept, 255));
+        continue;
+      }
       const int incl = warp_incl_scan(deg);
       const int start = incl - deg;
       const int total = __shfl_sync(0xffffffffu, incl, 31);
