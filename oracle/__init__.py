@@ -7,7 +7,8 @@ binary32 add per M1 arc, no fast-math); this module only marshals numpy arrays t
 Shares no code with the CUDA path.
 
 Functions:
-  compose(A, B)        -> dict of numpy arrays, states in FIFO discovery order (Alg. 1)
+  compose(A, B)        -> dict of numpy arrays, states in FIFO discovery order (Alg. 1), with the
+                          provenance arc_a / arc_b of every arc (-1 = that side stays)
   canonical(A, B)      -> same, canonical form (reading 24)
   coaccessible(A, B)   -> uint8 [V_A * V_B] co-accessible set R (Alg. 1 line 3)
   in_adjacency(g)      -> (inArcOffset, inArcs) per §3.2
@@ -48,7 +49,8 @@ class _Graph(C.Structure):
                 ("dst", C.POINTER(C.c_int32)), ("weight", C.POINTER(C.c_float)),
                 ("is_start", C.POINTER(C.c_uint8)), ("is_accept", C.POINTER(C.c_uint8)),
                 ("pair_a", C.POINTER(C.c_int32)), ("pair_b", C.POINTER(C.c_int32)),
-                ("level", C.POINTER(C.c_int32))]
+                ("level", C.POINTER(C.c_int32)), ("arc_a", C.POINTER(C.c_int32)),
+                ("arc_b", C.POINTER(C.c_int32))]
 
 
 def _load():
@@ -90,6 +92,7 @@ def _to_numpy(g: _Graph):
         "is_start": _take(g.is_start, V, np.uint8), "is_accept": _take(g.is_accept, V, np.uint8),
         "pair_a": _take(g.pair_a, V, np.int32), "pair_b": _take(g.pair_b, V, np.int32),
         "level": _take(g.level, V, np.int32),
+        "arc_a": _take(g.arc_a, E, np.int32), "arc_b": _take(g.arc_b, E, np.int32),
     }
 
 

@@ -19,6 +19,9 @@
  * Data layout follows §3.2: per-arc SoA arrays plus in/out adjacency with
  * offsets; in-adjacency is stable by arc index (the Fig. 1 example).
  *
+ * Provenance (the autodiff use of the composed graph): every
+ * arc also records the arc pair (e_a, e_b) that produced it (-1 for the side that stays).
+ *
  * Pins (tests/test_oracle.py): Fig. 1 arrays, hand fixtures F1-F5, brute-force Eq. (1) path
  * scores on tiny DAGs, Delannoy path counts with eps, plain-definition trim(P_N1), identity and
  * trellis special cases.  Build: gcc -O2 -std=c99 (no -ffast-math: no FTZ/DAZ, SSE float adds).
@@ -54,6 +57,8 @@ typedef struct {
   int32_t* pair_a;
   int32_t* pair_b;
   int32_t* level; /* BFS level of each state (FIFO discovery distance), for Fig. 2 profiles */
+  int32_t* arc_a; /* provenance: the arc pair (e_a, e_b) of Alg. 1 line 13 that */
+  int32_t* arc_b; /* produced each arc; -1 = that side stays (M3 for arc_a, M2 for arc_b) */
 } orc_graph;
 
 /* ---------------------------------------------------------------- adjacency (§3.2) */
@@ -166,11 +171,11 @@ int orc_coaccessible(const orc_fst* A, const orc_fst* B, uint8_t* R) {
 /* ---------------------------------------------------------------- growable output */
 typedef struct {
   int64_t n, cap;
-  int32_t *il, *ol, *dst;
+  int32_t *il, *ol, *dst, *aa, *ab;
   float* w;
 } arcbuf;
 
-static int arc_push(arcbuf* b, int32_t il, int32_t ol, int32_t d, float w) {
+static int arc_push(arcbuf* b, int32_t il, int32_t ol, int32_t d, float w, int32_t aa, int32_t ab) {
   if (b->n == b->cap) {
     int64_t nc = b->cap ? 2 * b->cap : 1024;
     int32_t* a1 = (int32_t*)realloc(b->il, sizeof(int32_t) * (size_t)nc);
@@ -188,12 +193,20 @@ static int arc_push(arcbuf* b, int32_t il, int32_t ol, int32_t d, float w) {
     a4 = (float*)realloc(b->w, sizeof(float) * (size_t)nc);
     if (!a4) return -1;
     b->w = a4;
+    a1 = (int32_t*)realloc(b->aa, sizeof(int32_t) * (size_t)nc);
+    if (!a1) return -1;
+    b->aa = a1;
+    a1 = (int32_t*)realloc(b->ab, sizeof(int32_t) * (size_t)nc);
+    if (!a1) return -1;
+    b->ab = a1;
     b->cap = nc;
   }
   b->il[b->n] = il;
   b->ol[b->n] = ol;
   b->dst[b->n] = d;
   b->w[b->n] = w;
+  b->aa[b->n] = aa;
+  b->ab[b->n] = ab;
   b->n++;
   return 0;
 }
@@ -203,6 +216,7 @@ void orc_free(orc_graph* g) {
   if (!g) return;
   free(g->row_ptr); free(g->ilabel); free(g->olabel); free(g->dst); free(g->weight);
   free(g->is_start); free(g->is_accept); free(g->pair_a); free(g->pair_b); free(g->level);
+  free(g->arc_a); free(g->arc_b);
   memset(g, 0, sizeof(*g));
 }
 
@@ -272,7 +286,7 @@ int orc_compose(const orc_fst* A, const orc_fst* B, orc_graph* C) {
         if (!R[v]) continue;                       /* lines 20-22 */
         if (id[v] < 0) NEW_STATE(va, vb, lv[u] + 1); /* lines 23-28 */
         w = A->weight[ea] + B->weight[eb];         /* line 29-30: one binary32 add */
-        if (arc_push(&arcs, A->ilabel[ea], B->olabel[eb], id[v], w)) return -1;
+        if (arc_push(&arcs, A->ilabel[ea], B->olabel[eb], id[v], w, (int32_t)ea, (int32_t)eb)) return -1;
       }
     }
     /* (ii) M2: e_a with o_a = eps, B stays */
@@ -284,7 +298,7 @@ int orc_compose(const orc_fst* A, const orc_fst* B, orc_graph* C) {
       v = (int64_t)va * VB + ub;
       if (!R[v]) continue;
       if (id[v] < 0) NEW_STATE(va, ub, lv[u] + 1);
-      if (arc_push(&arcs, A->ilabel[ea], ORC_EPS, id[v], A->weight[ea])) return -1;
+      if (arc_push(&arcs, A->ilabel[ea], ORC_EPS, id[v], A->weight[ea], (int32_t)ea, -1)) return -1;
     }
     /* (iii) M3: e_b with i_b = eps, A stays */
     for (eb = B->row_ptr[ub]; eb < B->row_ptr[ub + 1]; ++eb) {
@@ -295,7 +309,7 @@ int orc_compose(const orc_fst* A, const orc_fst* B, orc_graph* C) {
       v = (int64_t)ua * VB + vb;
       if (!R[v]) continue;
       if (id[v] < 0) NEW_STATE(ua, vb, lv[u] + 1);
-      if (arc_push(&arcs, ORC_EPS, B->olabel[eb], id[v], B->weight[eb])) return -1;
+      if (arc_push(&arcs, ORC_EPS, B->olabel[eb], id[v], B->weight[eb], -1, (int32_t)eb)) return -1;
     }
   }
 #undef NEW_STATE
@@ -308,6 +322,8 @@ int orc_compose(const orc_fst* A, const orc_fst* B, orc_graph* C) {
   C->olabel = arcs.ol;
   C->dst = arcs.dst;
   C->weight = arcs.w;
+  C->arc_a = arcs.aa;
+  C->arc_b = arcs.ab;
   C->is_start = st;
   C->is_accept = ac;
   C->pair_a = pa;
@@ -332,6 +348,7 @@ typedef struct {
   int32_t dst, il, ol;
   uint32_t wbits;
   float w;
+  int32_t aa, ab;
 } carc;
 static int cmp_arc(const void* x, const void* y) {
   const carc* a = (const carc*)x;
@@ -340,6 +357,8 @@ static int cmp_arc(const void* x, const void* y) {
   if (a->il != b->il) return a->il < b->il ? -1 : 1;
   if (a->ol != b->ol) return a->ol < b->ol ? -1 : 1;
   if (a->wbits != b->wbits) return a->wbits < b->wbits ? -1 : 1;
+  if (a->aa != b->aa) return a->aa < b->aa ? -1 : 1; /* provenance breaks ties between identical arcs */
+  if (a->ab != b->ab) return a->ab < b->ab ? -1 : 1;
   return 0;
 }
 
@@ -372,6 +391,8 @@ int orc_canonicalize(orc_graph* C, int32_t VB) {
   D.pair_a = (int32_t*)malloc(sizeof(int32_t) * (size_t)(V ? V : 1));
   D.pair_b = (int32_t*)malloc(sizeof(int32_t) * (size_t)(V ? V : 1));
   D.level = (int32_t*)malloc(sizeof(int32_t) * (size_t)(V ? V : 1));
+  D.arc_a = (int32_t*)malloc(sizeof(int32_t) * (size_t)(E ? E : 1));
+  D.arc_b = (int32_t*)malloc(sizeof(int32_t) * (size_t)(E ? E : 1));
   for (s = 0; s < V; ++s) {
     int32_t o = order[s];
     int64_t lo = C->row_ptr[o], hi = C->row_ptr[o + 1], n = hi - lo, e;
@@ -393,6 +414,8 @@ int orc_canonicalize(orc_graph* C, int32_t VB) {
       c->ol = C->olabel[lo + e];
       c->w = C->weight[lo + e];
       memcpy(&c->wbits, &c->w, 4);
+      c->aa = C->arc_a[lo + e];
+      c->ab = C->arc_b[lo + e];
     }
     qsort(tmp, (size_t)n, sizeof(carc), cmp_arc);
     for (e = 0; e < n; ++e) {
@@ -400,6 +423,8 @@ int orc_canonicalize(orc_graph* C, int32_t VB) {
       D.ilabel[k] = tmp[e].il;
       D.olabel[k] = tmp[e].ol;
       D.weight[k] = tmp[e].w;
+      D.arc_a[k] = tmp[e].aa;
+      D.arc_b[k] = tmp[e].ab;
       k++;
     }
   }

@@ -41,21 +41,25 @@ def wbits(w) -> int:
 # ----------------------------------------------------------------------------- canonical builder
 def build_canonical(VB: int, states: Dict[Tuple[int, int], Tuple[int, int]],
                     arcs: List[Tuple[Tuple[int, int], Tuple[int, int], int, int, np.float32]]):
-    """states: {(a,b): (is_start, is_accept)}; arcs: [((a,b),(a',b'), il, ol, w)] -> canonical dict."""
+    """states: {(a,b): (is_start, is_accept)}; arcs: [((a,b),(a',b'), il, ol, w[, (arc_a, arc_b)])]
+    -> canonical dict (with arc_a / arc_b when the arcs carry provenance)."""
     keys = sorted(states, key=lambda p: p[0] * VB + p[1])
     nid = {p: i for i, p in enumerate(keys)}
     rows = collections.defaultdict(list)
-    for s, d, il, ol, w in arcs:
-        rows[nid[s]].append((nid[d], il, ol, wbits(w), np.float32(w)))
+    prov = bool(arcs) and len(arcs[0]) == 6
+    for t in arcs:
+        s, d, il, ol, w = t[:5]
+        pv = t[5] if prov else (0, 0)
+        rows[nid[s]].append((nid[d], il, ol, wbits(w), pv[0], pv[1], np.float32(w)))
     V = len(keys)
     row_ptr = np.zeros(V + 1, np.int64)
-    dst, ilab, olab, wt = [], [], [], []
+    dst, ilab, olab, wt, aa, ab = [], [], [], [], [], []
     for i in range(V):
-        r = sorted(rows[i], key=lambda t: t[:4])
+        r = sorted(rows[i], key=lambda t: t[:6])
         row_ptr[i + 1] = row_ptr[i] + len(r)
-        for d, il, ol, _b, w in r:
-            dst.append(d); ilab.append(il); olab.append(ol); wt.append(w)
-    return {
+        for d, il, ol, _b, xa, xb, w in r:
+            dst.append(d); ilab.append(il); olab.append(ol); wt.append(w); aa.append(xa); ab.append(xb)
+    out = {
         "num_states": V, "num_arcs": int(row_ptr[-1]), "row_ptr": row_ptr,
         "ilabel": np.array(ilab, np.int32), "olabel": np.array(olab, np.int32),
         "dst": np.array(dst, np.int32), "weight": np.array(wt, np.float32).reshape(-1),
@@ -64,6 +68,9 @@ def build_canonical(VB: int, states: Dict[Tuple[int, int], Tuple[int, int]],
         "pair_a": np.array([p[0] for p in keys], np.int32),
         "pair_b": np.array([p[1] for p in keys], np.int32),
     }
+    if prov:
+        out["arc_a"], out["arc_b"] = np.array(aa, np.int32), np.array(ab, np.int32)
+    return out
 
 
 CANON_KEYS = ("row_ptr", "ilabel", "olabel", "dst", "is_start", "is_accept", "pair_a", "pair_b")
@@ -83,6 +90,12 @@ def assert_canonical_equal(got, exp, what=""):
     if not np.array_equal(ga, gb):
         bad = np.flatnonzero(ga != gb)
         raise AssertionError(f"{what}: weight bits differ at {bad[:10]}")
+    for k in ("arc_a", "arc_b"):  # provenance, when both sides carry it
+        if got.get(k) is not None and exp.get(k) is not None:
+            a, b = np.asarray(got[k], np.int64), np.asarray(exp[k], np.int64)
+            if not np.array_equal(a, b):
+                bad = np.flatnonzero(a != b)
+                raise AssertionError(f"{what}: provenance {k} differs at {bad[:10]} ({a[bad[:5]]} vs {b[bad[:5]]})")
 
 
 def canonicalize_rows(g, VB: int):
@@ -96,29 +109,34 @@ def canonicalize_rows(g, VB: int):
         raise AssertionError("states are not numbered by ascending pair key")
     src = np.repeat(np.arange(V, dtype=np.int64), np.diff(row_ptr))
     wb = np.asarray(g["weight"], np.float32).view(np.uint32)
-    order = np.lexsort((wb, np.asarray(g["olabel"]), np.asarray(g["ilabel"]), np.asarray(g["dst"]), src))
+    prov = g.get("arc_a") is not None
+    tie = (np.asarray(g["arc_b"]), np.asarray(g["arc_a"])) if prov else ()  # provenance breaks ties
+    order = np.lexsort(tie + (wb, np.asarray(g["olabel"]), np.asarray(g["ilabel"]), np.asarray(g["dst"]), src))
     out = dict(g)
-    for k in ("dst", "ilabel", "olabel", "weight"):
+    for k in ("dst", "ilabel", "olabel", "weight") + (("arc_a", "arc_b") if prov else ()):
         out[k] = np.asarray(g[k])[order]
     out["num_states"], out["num_arcs"] = V, E
     return out
 
 
 # ----------------------------------------------------------------------------- plain definition
-def n1_moves(A, B, ua, ub):
-    """All moves of N1 from pair (ua, ub): M1 (incl. eps==eps), M2, M3 (SURVEY §8 move table)."""
+def n1_moves(A, B, ua, ub, prov: bool = False):
+    """All moves of N1 from pair (ua, ub): M1 (incl. eps==eps), M2, M3 (SURVEY §8 move table).
+    prov: append the move's arc pair (e_a, e_b), -1 for the side that stays."""
     out = []
     for ea in range(A.row_ptr[ua], A.row_ptr[ua + 1]):
         for eb in range(B.row_ptr[ub], B.row_ptr[ub + 1]):
             if A.olabel[ea] == B.ilabel[eb]:
                 out.append(((int(A.dst[ea]), int(B.dst[eb])), int(A.ilabel[ea]), int(B.olabel[eb]),
-                            f32add(A.weight[ea], B.weight[eb])))
+                            f32add(A.weight[ea], B.weight[eb])) + (((int(ea), int(eb)),) if prov else ()))
     for ea in range(A.row_ptr[ua], A.row_ptr[ua + 1]):
         if A.olabel[ea] == EPS:
-            out.append(((int(A.dst[ea]), ub), int(A.ilabel[ea]), EPS, np.float32(A.weight[ea])))
+            out.append(((int(A.dst[ea]), ub), int(A.ilabel[ea]), EPS, np.float32(A.weight[ea]))
+                       + (((int(ea), -1),) if prov else ()))
     for eb in range(B.row_ptr[ub], B.row_ptr[ub + 1]):
         if B.ilabel[eb] == EPS:
-            out.append(((ua, int(B.dst[eb])), EPS, int(B.olabel[eb]), np.float32(B.weight[eb])))
+            out.append(((ua, int(B.dst[eb])), EPS, int(B.olabel[eb]), np.float32(B.weight[eb]))
+                       + (((-1, int(eb)),) if prov else ()))
     return out
 
 
@@ -134,15 +152,17 @@ def _reach(adj, seeds):
     return seen
 
 
-def plain_trim_product(A, B):
-    """trim(P_N1) built from the definition (tiny inputs only: V_A * V_B <= ~1e4)."""
+def plain_trim_product(A, B, prov: bool = False):
+    """trim(P_N1) built from the definition (tiny inputs only: V_A * V_B <= ~1e4); prov: with the
+    arc pair of every arc."""
     fwd = collections.defaultdict(list)
     bwd = collections.defaultdict(list)
     all_arcs = []
     for ua in range(A.num_states):
         for ub in range(B.num_states):
-            for d, il, ol, w in n1_moves(A, B, ua, ub):
-                all_arcs.append(((ua, ub), d, il, ol, w))
+            for mv in n1_moves(A, B, ua, ub, prov):
+                d = mv[0]
+                all_arcs.append(((ua, ub),) + tuple(mv))
                 fwd[(ua, ub)].append(d)
                 bwd[d].append((ua, ub))
     starts = [(a, b) for a in np.flatnonzero(A.is_start) for b in np.flatnonzero(B.is_start)]

@@ -122,7 +122,7 @@ def test_signed_zero_and_tie_bits():
 # ----------------------------------------------------------------------------- plain definition
 def _check_plain(A, B, what):
     C = oracle.canonical(A, B)
-    P = pins.plain_trim_product(A, B)
+    P = pins.plain_trim_product(A, B, prov=True)  # structure, weights and provenance (arc_a, arc_b)
     pins.assert_canonical_equal(C, P, what)
     R = oracle.coaccessible(A, B)
     assert np.array_equal(R, pins.plain_coaccessible(A, B)), what
@@ -244,3 +244,54 @@ def test_size_bounds_and_R_superset():
     assert C["num_states"] <= A.num_states * B.num_states
     assert C["row_ptr"][-1] == C["num_arcs"] and np.all(np.diff(C["row_ptr"]) >= 0)
     assert pins.is_trim(C)
+
+
+# ----------------------------------------------------------------------------- provenance
+def provenance_consistent(A, B, C, what=""):
+    """Every composed arc agrees with the arc pair it names (the move table of SURVEY §8): source and
+    destination pairs, the matched labels, the carried labels and the weight bits (one binary32 add
+    for M1, a bit copy for M2 / M3).  Vectorised over all arcs; independent of how C was built."""
+    E = int(C["num_arcs"])
+    src = np.repeat(np.arange(C["num_states"]), np.diff(C["row_ptr"]))
+    sa, sb = C["pair_a"][src], C["pair_b"][src]
+    da, db = C["pair_a"][C["dst"]], C["pair_b"][C["dst"]]
+    aa, ab = C["arc_a"].astype(np.int64), C["arc_b"].astype(np.int64)
+    Asrc, Bsrc = A.src, B.src
+    assert np.all((aa >= 0) | (ab >= 0)), what
+    m1, m2, m3 = (aa >= 0) & (ab >= 0), (aa >= 0) & (ab < 0), (aa < 0) & (ab >= 0)
+    assert m1.sum() + m2.sum() + m3.sum() == E, what
+    ia, ib = np.where(aa >= 0, aa, 0), np.where(ab >= 0, ab, 0)
+    # A side moves along arc_a (M1, M2) or stays (M3); the same for B
+    assert np.array_equal(np.where(aa >= 0, Asrc[ia], sa), sa) and np.array_equal(np.where(aa >= 0, A.dst[ia], sa), da), what
+    assert np.array_equal(np.where(ab >= 0, Bsrc[ib], sb), sb) and np.array_equal(np.where(ab >= 0, B.dst[ib], sb), db), what
+    assert np.all(A.olabel[ia][m1] == B.ilabel[ib][m1]), what
+    assert np.all(A.olabel[ia][m2] == pins.EPS) and np.all(B.ilabel[ib][m3] == pins.EPS), what
+    assert np.array_equal(C["ilabel"], np.where(aa >= 0, A.ilabel[ia], pins.EPS)), what
+    assert np.array_equal(C["olabel"], np.where(ab >= 0, B.olabel[ib], pins.EPS)), what
+    wa, wb = A.weight[ia].astype(np.float32), B.weight[ib].astype(np.float32)
+    exp = np.where(m1, wa + wb, np.where(m2, wa, wb)).astype(np.float32)
+    assert np.array_equal(exp.view(np.uint32), np.asarray(C["weight"], np.float32).view(np.uint32)), what
+    # one arc per (source pair, arc pair): no move is emitted twice
+    key = (src.astype(np.int64) * (A.num_arcs + 1) + (aa + 1)) * (B.num_arcs + 1) + (ab + 1)
+    assert len(np.unique(key)) == E, what
+
+
+@pytest.mark.parametrize("seed", [0, 3, 8])
+def test_provenance_consistent_c2(seed):
+    A, B = fstgen.config_c2(seed)
+    provenance_consistent(A, B, oracle.canonical(A, B), f"c2 seed {seed}")
+
+
+def test_provenance_consistent_c3_and_counts():
+    """c3 (lexicon o emissions): consistency, and the M1 count of every state equals the number of
+    label-matched arc pairs whose destination pair is in C (plain definition, per state)."""
+    A, B = fstgen.config_c3(num_words=200, T=30)
+    C = oracle.canonical(A, B)
+    provenance_consistent(A, B, C, "c3")
+    keys = set(zip(C["pair_a"].tolist(), C["pair_b"].tolist()))
+    rp = C["row_ptr"]
+    for s in range(0, C["num_states"], 97):
+        a, b = int(C["pair_a"][s]), int(C["pair_b"][s])
+        exp = sorted(mv[4] for mv in pins.n1_moves(A, B, a, b, prov=True) if mv[0] in keys)
+        got = sorted(zip(C["arc_a"][rp[s]:rp[s + 1]].tolist(), C["arc_b"][rp[s]:rp[s + 1]].tolist()))
+        assert got == exp, s
