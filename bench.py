@@ -230,8 +230,8 @@ def run_ours(args):
 
     def compose_all():
         if len(ha) == 1:
-            return [fstc.fst_compose(ha[0], hb, stream)]
-        return fstc.fst_compose_batch(ha, [hb] * len(ha), stream)
+            return [fstc.fst_compose(ha[0], hb, stream, provenance=args.provenance)]
+        return fstc.fst_compose_batch(ha, [hb] * len(ha), stream, provenance=args.provenance)
 
     def step():
         with torch.cuda.stream(stream):
@@ -280,8 +280,9 @@ def run_ours(args):
     s1 = statistics.mean(s["ms_stage1"] for s in stats)
     s2 = statistics.mean(s["ms_stage2"] for s in stats)
     num = statistics.mean(s["ms_number"] for s in stats)
-    emit_bytes = 16 * E_C + 18 * V_C + P / 8
-    step_bytes = 16 * E_C + 18 * V_C + 2 * k * (R + V_C) + P / 4
+    ab = 24 if args.provenance else 16  # + arc_a / arc_b per arc with provenance
+    emit_bytes = ab * E_C + 18 * V_C + P / 8
+    step_bytes = ab * E_C + 18 * V_C + 2 * k * (R + V_C) + P / 4
     traffic = None
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tp):
@@ -293,10 +294,10 @@ def run_ours(args):
     roof = {"kernel": "k_emit", "bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
             "frac": achieved / hbm, "traffic": traffic, "peak_source": peak_src,
             "algorithmic_bytes_per_launch": emit_bytes,
-            "bytes_formula": "16*E_C + 18*V_C + P/8 (arc SoA + row_ptr/pairs/flags written, V bitmap read)"}
+            "bytes_formula": f"{ab}*E_C + 18*V_C + P/8 (arc SoA + row_ptr/pairs/flags written, V bitmap read)"}
     ms_step = tot_ms / args.steps
     step_roof = {"algorithmic_bytes": step_bytes, "frac_of_hbm": step_bytes / (ms_step / 1e3) / 1e9 / hbm,
-                 "formula": "16*E_C + 18*V_C + 2k(|R|+V_C) + P/4 (SURVEY 8(d) d.4)"}
+                 "formula": f"{ab}*E_C + 18*V_C + 2k(|R|+V_C) + P/4 (SURVEY 8(d) d.4)"}
 
     # ---------------- e2e through the C ABI with host buffers (pinned), copies inside the timed region
     e2e = None
@@ -311,7 +312,7 @@ def run_ours(args):
                    "V_A": sum(A.num_states for A in As), "V_B": B.num_states,
                    "E_A": sum(A.num_arcs for A in As), "E_B": B.num_arcs, "pair_space": P, "V_C": V_C, "E_C": E_C,
                    "coaccessible": R, "levels": [stats[-1]["levels_stage1"], stats[-1]["levels_stage2"]],
-                   "parallelism": parallelism,
+                   "parallelism": parallelism, "provenance": bool(args.provenance),
                    "l2": "flushed before every step (512 MiB write), outside the timed events; the working set "
                          "(pair-space bitmaps + composed graph) exceeds L2"},
         "phases_ms": {"stage1_backward_bfs": s1, "stage2_forward_bfs": s2, "numbering": num, "emit": emit_ms},
@@ -474,6 +475,8 @@ def main():
     ap.add_argument("--mode", default=os.environ.get("FSTC_BENCH_MODE", "replicas"), choices=["replicas", "sharded"],
                     help="replicas: independent compositions per GPU (weak); sharded: one composition over all GPUs")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--provenance", action="store_true",
+                    help="compose with FST_COMPOSE_PROVENANCE (also writes arc_a/arc_b per arc; not the headline)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":

@@ -90,6 +90,8 @@ typedef struct {
   const uint8_t* is_accept;
   const int32_t* pair_a; /* [V] or NULL */
   const int32_t* pair_b; /* [V] or NULL */
+  const int32_t* arc_a;  /* [E] provenance (FST_COMPOSE_PROVENANCE), else NULL: see fst_compose_ex */
+  const int32_t* arc_b;  /* [E] */
 } fst_view;
 
 /* Per-composition statistics (filled by fst_compose*; timings only when profiling is on). */
@@ -122,6 +124,35 @@ fst_status fst_compose(fst_handle a, fst_handle b, void* stream, fst_handle* c);
  * concatenated pair spaces.  All-or-nothing: on error every c[i] is NULL. */
 fst_status fst_compose_batch(int32_t n, const fst_handle* a, const fst_handle* b, void* stream,
                              fst_handle* c);
+
+/* Option flags of fst_compose_ex / fst_compose_batch_ex. */
+#define FST_COMPOSE_PROVENANCE 1u /* also record, per composed arc, the arc pair that produced it */
+
+/* fst_compose / fst_compose_batch with option flags.  FST_COMPOSE_PROVENANCE (
+ * the autodiff use of the composed graph): every arc k of C also gets
+ * arc_a[k] = the index of the A arc e_a of its move in A's input arc order (the order of the
+ * fst_desc passed to fst_create; for a composed A, its own arc order), or -1 for an M3 move
+ * (A stays), and arc_b[k] = the B arc e_b, or -1 for an M2 move (B stays) -- Alg. 1 line 13's
+ * arc pair.  +8 bytes per composed arc.  Unknown flag bits: FST_E_INVALID_ARG. */
+fst_status fst_compose_ex(fst_handle a, fst_handle b, uint32_t flags, void* stream, fst_handle* c);
+fst_status fst_compose_batch_ex(int32_t n, const fst_handle* a, const fst_handle* b, uint32_t flags,
+                                void* stream, fst_handle* c);
+
+/* Copies provenance arcs [first, first+count) of a composed handle into HOST int32 buffers (either
+ * may be NULL).  FST_E_INVALID_ARG if the handle has no provenance or the range is out of bounds. */
+fst_status fst_copy_provenance_to_host(fst_handle c, void* stream, int64_t first, int64_t count,
+                                       int32_t* arc_a, int32_t* arc_b);
+
+/* Gradient scatter through the composition.  Every composed weight is
+ * w_c = w_a + w_b (M1) or a copy of w_a (M2) / w_b (M3), so dL/dw_a[i] = sum of dL/dw_c over the
+ * arcs of C whose arc_a is i, and likewise for B.  grad_c [E_C] is read, grad_a [E_A] and grad_b
+ * [E_B] are ACCUMULATED into (+=; either may be NULL).  All three are DEVICE float arrays; n_a and
+ * n_b are their lengths (checked against the largest index, FST_E_INVALID_ARG if too short).
+ * Needs a handle composed with FST_COMPOSE_PROVENANCE.  The per-element summation order is not
+ * fixed (float atomics): results agree with an exact sum to within E_C-term rounding.
+ * Asynchronous on `stream`. */
+fst_status fst_grad_scatter(fst_handle c, const float* grad_c, float* grad_a, int64_t n_a, float* grad_b,
+                            int64_t n_b, void* stream);
 
 /* Releases a handle and its device memory.  NULL-safe. */
 void fst_free(fst_handle h);

@@ -42,7 +42,10 @@ int sm_count() {
 
 std::vector<int64_t>& level_sizes_slot(fst* h, int stage) { return h->level_sizes[stage == 1 ? 0 : 1]; }
 
-fst_status compose_impl(int32_t n, const fst_handle* a, const fst_handle* b, cudaStream_t s, fst_handle* c);
+fst_status compose_impl(int32_t n, const fst_handle* a, const fst_handle* b, cudaStream_t s, fst_handle* c,
+                        uint32_t flags);
+fst_status grad_scatter_impl(fst* c, const float* grad_c, float* grad_a, int64_t n_a, float* grad_b, int64_t n_b,
+                             cudaStream_t s);
 fst_status compose_sharded_impl(fst* A, fst* B, int world, fst_comm* comm, cudaStream_t s, fst_handle* c);
 
 fst_status device_ready() {
@@ -73,25 +76,64 @@ using namespace fstc;
 
 extern "C" {
 
-fst_status fst_compose(fst_handle a, fst_handle b, void* stream, fst_handle* c) {
+fst_status fst_compose_ex(fst_handle a, fst_handle b, uint32_t flags, void* stream, fst_handle* c) {
   if (!a || !b || !c) {
     set_error(FST_E_INVALID_ARG, "fst_compose: NULL argument");
     return FST_E_INVALID_ARG;
   }
+  if (flags & ~FST_COMPOSE_PROVENANCE) {
+    set_error(FST_E_INVALID_ARG, "fst_compose_ex: unknown flag bits 0x%x", flags);
+    return FST_E_INVALID_ARG;
+  }
   fst_status st = device_ready();
   if (st) return st;
-  return compose_impl(1, &a, &b, (cudaStream_t)stream, c);
+  return compose_impl(1, &a, &b, (cudaStream_t)stream, c, flags);
 }
 
-fst_status fst_compose_batch(int32_t n, const fst_handle* a, const fst_handle* b, void* stream, fst_handle* c) {
+fst_status fst_compose(fst_handle a, fst_handle b, void* stream, fst_handle* c) {
+  return fst_compose_ex(a, b, 0u, stream, c);
+}
+
+fst_status fst_compose_batch_ex(int32_t n, const fst_handle* a, const fst_handle* b, uint32_t flags, void* stream,
+                                fst_handle* c) {
   if (n < 0 || (n > 0 && (!a || !b || !c))) {
     set_error(FST_E_INVALID_ARG, "fst_compose_batch: bad arguments (n=%d)", n);
+    return FST_E_INVALID_ARG;
+  }
+  if (flags & ~FST_COMPOSE_PROVENANCE) {
+    set_error(FST_E_INVALID_ARG, "fst_compose_batch_ex: unknown flag bits 0x%x", flags);
     return FST_E_INVALID_ARG;
   }
   if (n == 0) return FST_OK;
   fst_status st = device_ready();
   if (st) return st;
-  return compose_impl(n, a, b, (cudaStream_t)stream, c);
+  return compose_impl(n, a, b, (cudaStream_t)stream, c, flags);
+}
+
+fst_status fst_compose_batch(int32_t n, const fst_handle* a, const fst_handle* b, void* stream, fst_handle* c) {
+  return fst_compose_batch_ex(n, a, b, 0u, stream, c);
+}
+
+fst_status fst_copy_provenance_to_host(fst_handle c, void* stream, int64_t first, int64_t count, int32_t* arc_a,
+                                       int32_t* arc_b) {
+  if (!c || !c->arc_a || first < 0 || count < 0 || first + count > c->E) {
+    set_error(FST_E_INVALID_ARG, "fst_copy_provenance_to_host: no provenance or bad range");
+    return FST_E_INVALID_ARG;
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  if (count > 0) {
+    if (arc_a) FSTC_CUDA_TRY(cudaMemcpyAsync(arc_a, c->arc_a + first, 4 * count, cudaMemcpyDeviceToHost, s));
+    if (arc_b) FSTC_CUDA_TRY(cudaMemcpyAsync(arc_b, c->arc_b + first, 4 * count, cudaMemcpyDeviceToHost, s));
+  }
+  FSTC_CUDA_TRY(cudaStreamSynchronize(s));
+  return FST_OK;
+}
+
+fst_status fst_grad_scatter(fst_handle c, const float* grad_c, float* grad_a, int64_t n_a, float* grad_b,
+                            int64_t n_b, void* stream) {
+  fst_status st = device_ready();
+  if (st) return st;
+  return grad_scatter_impl(c, grad_c, grad_a, n_a, grad_b, n_b, (cudaStream_t)stream);
 }
 
 void fst_free(fst_handle h) { delete h; }
@@ -112,6 +154,8 @@ fst_status fst_info(fst_handle h, fst_view* v) {
   v->is_accept = h->is_accept;
   v->pair_a = h->composed ? h->pair_a : nullptr;
   v->pair_b = h->composed ? h->pair_b : nullptr;
+  v->arc_a = h->arc_a;
+  v->arc_b = h->arc_b;
   return FST_OK;
 }
 

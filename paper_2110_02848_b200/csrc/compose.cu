@@ -617,41 +617,42 @@ __device__ __forceinline__ void fast_state(const TaskSmem& s, const int2* __rest
   if (e < e1) fast_arc<kM32>(s, __ldg(&ikd[e]), e - ub - 1, f);
 }
 
-// Same walk over the 16-byte items (label, other, carry, weight bits): g(slot, col, kind, a, carry, wbits)
+// Same walk over the 16-byte items (label, other, carry, weight bits):
+// g(slot, col, kind, a, carry, wbits, it) with it = the item index (-1 for M2 moves)
 template <bool kM32, typename G>
 __device__ __forceinline__ void fast_state4(const TaskSmem& s, const int4* __restrict__ ikcw, int32_t ub, int32_t e,
                                             int32_t e1, G&& g) {
-  for (int a = 0; a < s.aeps; ++a) g(s.a_slot[a], ub, 2, a, 0, 0);
-  auto one = [&](const int4 x) {
+  for (int a = 0; a < s.aeps; ++a) g(s.a_slot[a], ub, 2, a, 0, 0, -1);
+  auto one = [&](const int4 x, int32_t it) {
     if (kM32) {
       uint32_t m = (unsigned)(x.x + 1) < 64u ? s.labmask32[x.x + 1] : 0u;
       while (m) {
         const int a = __ffs(m) - 1;
         m &= m - 1;
-        g(s.a_slot[a], x.y, 1, a, x.z, x.w);
+        g(s.a_slot[a], x.y, 1, a, x.z, x.w, it);
       }
     } else {
       unsigned long long m = (unsigned)(x.x + 1) < 64u ? s.labmask[x.x + 1] : 0ull;
       while (m) {
         const int a = __ffsll((long long)m) - 1;
         m &= m - 1;
-        g(s.a_slot[a], x.y, 1, a, x.z, x.w);
+        g(s.a_slot[a], x.y, 1, a, x.z, x.w, it);
       }
     }
-    if (x.x == FST_EPS) g(0, x.y, 3, -1, x.z, x.w);
+    if (x.x == FST_EPS) g(0, x.y, 3, -1, x.z, x.w, it);
   };
   for (; e + 2 <= e1; e += 2) {
     const int4 x0 = __ldg(&ikcw[e]), x1 = __ldg(&ikcw[e + 1]);
-    one(x0);
-    one(x1);
+    one(x0, e);
+    one(x1, e + 1);
   }
-  if (e < e1) one(__ldg(&ikcw[e]));
+  if (e < e1) one(__ldg(&ikcw[e]), e);
 }
 
 // Fast emit of one dense block (staged rows, label masks, no heavy state): per-thread state walks,
 // block scan of per-state counts, then per-warp windows of kWCap slots staged in shared memory and
 // stored coalesced.  Returns the block's arc count.
-template <bool kM32, typename Rank, typename StateOut>
+template <bool kM32, bool kProv, typename Rank, typename StateOut>
 __device__ __forceinline__ int emit_block_fast(TaskSmem& s, const ViewDev& Bv, const CompDev& C, int32_t ub0,
                                                int32_t ub1, int lw0, int wpr, const int2* VR, int4* wb4,
                                                const uint8_t* __restrict__ cnt8row, int64_t run, Rank&& rank_of,
@@ -712,6 +713,12 @@ __device__ __forceinline__ int emit_block_fast(TaskSmem& s, const ViewDev& Bv, c
   int32_t* __restrict__ oi = C.ilabel;
   int32_t* __restrict__ oo = C.olabel;
   float* __restrict__ ow = C.weight;
+  // provenance of the record at slot pos: A arc (A-row position a) unless M3, B arc (view position
+  // eb) unless M2, as input arc indices (FST_COMPOSE_PROVENANCE)
+  auto prov = [&](int64_t pos, int kind, int a, int32_t eb) {
+    __stcs(&C.arc_a[pos], kind != 3 ? __ldg(&C.Af.arc[s.a0 + a]) : -1);
+    __stcs(&C.arc_b[pos], kind != 2 ? __ldg(&Bv.arc[eb]) : -1);
+  };
   auto fill = [&](int kind, int a, int32_t carry, int32_t wbits, int32_t& il, int32_t& ol, float& wt) {
     if (kind == 1) {
       il = s.a_carry[a];
@@ -742,7 +749,8 @@ __device__ __forceinline__ int emit_block_fast(TaskSmem& s, const ViewDev& Bv, c
       if (!__any_sync(0xffffffffu, mine)) continue;  // window entirely inside a heavy state's range
       if (mine) {
         int p = my0;
-        fast_state4<kM32>(s, ikcw, ub, e, e1, [&](int slot, int32_t col, int kind, int a, int32_t carry, int32_t wbits) {
+        fast_state4<kM32>(s, ikcw, ub, e, e1, [&](int slot, int32_t col, int kind, int a, int32_t carry, int32_t wbits,
+                                                 int32_t it) {
           bool pr;
           const int32_t did = rank_of(slot, col, pr);
           if (!pr) return;
@@ -753,6 +761,7 @@ __device__ __forceinline__ int emit_block_fast(TaskSmem& s, const ViewDev& Bv, c
           float wt;
           fill(kind, a, carry, wbits, il, ol, wt);
           wb4[t] = make_int4(did, il, ol, __float_as_int(wt));
+          if (kProv) prov(run + win + t, kind, a, it - ub - 1);
         });
       }
       __syncwarp();
@@ -774,7 +783,7 @@ __device__ __forceinline__ int emit_block_fast(TaskSmem& s, const ViewDev& Bv, c
     const int32_t ub = ub0 + i;
     const int32_t e0 = __ldg(&boff[ub]) + ub + 1, e1 = __ldg(&boff[ub + 1]) + ub + 1;
     int64_t p0 = run + s.cur[i];
-    auto put = [&](int slot, int32_t col, int kind, int a, int32_t carry, int32_t wbits, int64_t pos) {
+    auto put = [&](int slot, int32_t col, int kind, int a, int32_t carry, int32_t wbits, int64_t pos, int32_t eb) {
       bool pr;
       const int32_t did = rank_of(slot, col, pr);
       int32_t il, ol;
@@ -784,13 +793,14 @@ __device__ __forceinline__ int emit_block_fast(TaskSmem& s, const ViewDev& Bv, c
       __stcs(&oi[pos], il);
       __stcs(&oo[pos], ol);
       __stcs(&ow[pos], wt);
+      if (kProv) prov(pos, kind, a, eb);
     };
     int m2 = 0;
     for (int a = 0; a < s.aeps; ++a) m2 += present(s.a_slot[a], ub);
     if (threadIdx.x == 0) {
       int64_t q = p0;
       for (int a = 0; a < s.aeps; ++a)
-        if (present(s.a_slot[a], ub)) put(s.a_slot[a], ub, 2, a, 0, 0, q++);
+        if (present(s.a_slot[a], ub)) put(s.a_slot[a], ub, 2, a, 0, 0, q++, -1);
     }
     p0 += m2;
     for (int32_t eb = e0; eb < e1; eb += kThreads) {
@@ -806,7 +816,7 @@ __device__ __forceinline__ int emit_block_fast(TaskSmem& s, const ViewDev& Bv, c
       if (c) {
         int64_t q = p0 + exh;
         fast_arc<kM32>(s, make_int2(x.x, x.y), 0, [&](int slot, int32_t col, int kind, int a, int32_t) {
-          if (present(slot, col)) put(slot, col, kind, a, x.z, x.w, q++);
+          if (present(slot, col)) put(slot, col, kind, a, x.z, x.w, q++, e - ub - 1);
         });
       }
       p0 += tchunk;
@@ -1394,6 +1404,8 @@ __global__ void __launch_bounds__(kThreads, 2) k_emit(Ctx cx, const int64_t* __r
     };
     const int32_t ua = ch.ua;
     const uint8_t stA = __ldg(&C.startA[ua]), acA = __ldg(&C.accA[ua]);
+    int32_t* const xa = C.arc_a;
+    int32_t* const xb = C.arc_b;
     auto emit_arc = [&](const Cand& c, int64_t pos) {
       bool pr;
       const int32_t did = rank_of(c.slot, c.row, c.col, pr);
@@ -1418,6 +1430,10 @@ __global__ void __launch_bounds__(kThreads, 2) k_emit(Ctx cx, const int64_t* __r
       __stcs(&C.ilabel[pos], il);
       __stcs(&C.olabel[pos], ol);
       __stcs(&C.weight[pos], wt);
+      if (xa) {  // provenance: input arc indices (FST_COMPOSE_PROVENANCE)
+        __stcs(&xa[pos], c.kind != 3 ? __ldg(&Av.arc[s.a0 + c.k]) : -1);
+        __stcs(&xb[pos], c.kind != 2 ? __ldg(&Bv.arc[c.eb]) : -1);
+      }
     };
     const bool fastE = staged && s.small && (((2 * s.m * wpr + 3) & ~3) + kWarps * kWCap * 4) * 4 <= kDynSmem;
     if (!fastE) {
@@ -1444,8 +1460,11 @@ __global__ void __launch_bounds__(kThreads, 2) k_emit(Ctx cx, const int64_t* __r
           C.is_accept[id] = (uint8_t)(acA & __ldg(&C.accB[ub]));
         };
         const uint8_t* cnt8row = cx.cnt8 + ch.rowW * 32;
-        const int btot = s.mask32 ? emit_block_fast<true>(s, Bv, C, ub0, ub1, lw0, wpr, VR, wb, cnt8row, run, rk, so)
-                                  : emit_block_fast<false>(s, Bv, C, ub0, ub1, lw0, wpr, VR, wb, cnt8row, run, rk, so);
+        const int btot =
+            C.arc_a ? (s.mask32 ? emit_block_fast<true, true>(s, Bv, C, ub0, ub1, lw0, wpr, VR, wb, cnt8row, run, rk, so)
+                                : emit_block_fast<false, true>(s, Bv, C, ub0, ub1, lw0, wpr, VR, wb, cnt8row, run, rk, so))
+                    : (s.mask32 ? emit_block_fast<true, false>(s, Bv, C, ub0, ub1, lw0, wpr, VR, wb, cnt8row, run, rk, so)
+                                : emit_block_fast<false, false>(s, Bv, C, ub0, ub1, lw0, wpr, VR, wb, cnt8row, run, rk, so));
         if (threadIdx.x == 0 && (unsigned long long)btot != cx.kept[gblk]) atomicAdd(&cx.misc[2], 1ull);
         run += btot;
         __syncthreads();
@@ -1714,7 +1733,9 @@ unsigned long long* pinned_scratch() {
 
 std::vector<int64_t>& level_sizes_slot(fst* h, int stage);
 
-fst_status compose_impl(int32_t n, const fst_handle* a, const fst_handle* b, cudaStream_t s, fst_handle* c) {
+fst_status compose_impl(int32_t n, const fst_handle* a, const fst_handle* b, cudaStream_t s, fst_handle* c,
+                        uint32_t flags) {
+  const bool want_prov = flags & FST_COMPOSE_PROVENANCE;
   const bool prof = profiling_enabled();
   EventTimer t_total(prof, s);
   for (int i = 0; i < n; ++i) c[i] = nullptr;
@@ -1743,7 +1764,7 @@ fst_status compose_impl(int32_t n, const fst_handle* a, const fst_handle* b, cud
     const fst* B = b[i];
     CompDev& C = comps[i];
     memset(&C, 0, sizeof(C));
-    auto vd = [](const View& v) { return ViewDev{v.off, v.key, v.other, v.carry, v.w, v.cw, v.ikd, v.isrc, v.ikcw, v.lm_other, v.lm_pos, v.seg_node, v.seg_beg, v.lab_val, v.lab_seg, v.nlab}; };
+    auto vd = [](const View& v) { return ViewDev{v.off, v.key, v.other, v.carry, v.w, v.cw, v.ikd, v.isrc, v.ikcw, v.lm_other, v.lm_pos, v.seg_node, v.seg_beg, v.lab_val, v.lab_seg, v.nlab, v.arc}; };
     C.Af = vd(A->views[kOutByOlabel]);
     C.Ab = vd(A->views[kInByOlabel]);
     C.Bf = vd(B->views[kOutByIlabel]);
@@ -1922,6 +1943,7 @@ fst_status compose_impl(int32_t n, const fst_handle* a, const fst_handle* b, cud
       auto tk = [&](size_t bytes) { size_t o = ob; ob += (bytes + 255) & ~size_t(255); return o; };
       const size_t o_rp = tk(8 * (nv + 1)), o_il = tk(4 * ne), o_ol = tk(4 * ne), o_d = tk(4 * ne),
                    o_w = tk(4 * ne), o_st = tk(nv), o_ac = tk(nv), o_pa = tk(4 * nv), o_pb = tk(4 * nv);
+      const size_t o_xa = want_prov ? tk(4 * ne) : 0, o_xb = want_prov ? tk(4 * ne) : 0;
       BufferPtr obuf;
       st = alloc_buffer(ob, s, &obuf);
       if (st) {
@@ -1944,6 +1966,12 @@ fst_status compose_impl(int32_t n, const fst_handle* a, const fst_handle* b, cud
       h->is_accept = (uint8_t*)(pb + o_ac);
       h->pair_a = (int32_t*)(pb + o_pa);
       h->pair_b = (int32_t*)(pb + o_pb);
+      if (want_prov) {
+        h->arc_a = (int32_t*)(pb + o_xa);
+        h->arc_b = (int32_t*)(pb + o_xb);
+      }
+      h->src_arcs_a = a[i]->E;
+      h->src_arcs_b = b[i]->E;
       h->buffers.push_back(obuf);
       CompDev& C = comps[i];
       C.row_ptr = h->row_ptr;
@@ -1955,6 +1983,8 @@ fst_status compose_impl(int32_t n, const fst_handle* a, const fst_handle* b, cud
       C.is_accept = h->is_accept;
       C.pair_a = h->pair_a;
       C.pair_b = h->pair_b;
+      C.arc_a = h->arc_a;
+      C.arc_b = h->arc_b;
     }
     FSTC_CUDA_TRY(cudaMemcpyAsync(d_comps, comps.data(), sizeof(CompDev) * n, cudaMemcpyHostToDevice, s));
     stats.ms_alloc = t.stop();
@@ -1995,6 +2025,38 @@ fst_status compose_impl(int32_t n, const fst_handle* a, const fst_handle* b, cud
   return FST_OK;
 }
 
+}  // namespace fstc
+
+namespace fstc {
+// ------------------------------------------------------------------------------ gradient scatter
+// dL/dw_a[i] += sum of dL/dw_c over the arcs of C with arc_a == i (w_c = w_a + w_b, or a copy), and
+// the same for B.  One thread per composed arc, float atomics.
+__global__ void k_grad_scatter(int64_t E, const int32_t* __restrict__ arc_a, const int32_t* __restrict__ arc_b,
+                               const float* __restrict__ g, float* __restrict__ ga, float* __restrict__ gb) {
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < E; k += (int64_t)gridDim.x * blockDim.x) {
+    const float x = __ldg(&g[k]);
+    const int32_t i = __ldg(&arc_a[k]), j = __ldg(&arc_b[k]);
+    if (ga && i >= 0) atomicAdd(&ga[i], x);
+    if (gb && j >= 0) atomicAdd(&gb[j], x);
+  }
+}
+
+fst_status grad_scatter_impl(fst* c, const float* grad_c, float* grad_a, int64_t n_a, float* grad_b, int64_t n_b,
+                             cudaStream_t s) {
+  if (!c || !c->composed || !c->arc_a) {
+    set_error(FST_E_INVALID_ARG, "fst_grad_scatter: handle was not composed with FST_COMPOSE_PROVENANCE");
+    return FST_E_INVALID_ARG;
+  }
+  if ((c->E > 0 && !grad_c) || (grad_a && n_a < c->src_arcs_a) || (grad_b && n_b < c->src_arcs_b)) {
+    set_error(FST_E_INVALID_ARG, "fst_grad_scatter: NULL grad_c or gradient buffer shorter than the input's arcs");
+    return FST_E_INVALID_ARG;
+  }
+  if (c->E == 0 || (!grad_a && !grad_b)) return FST_OK;
+  const unsigned grid = (unsigned)std::min<int64_t>((c->E + 255) / 256, 148 * 16);
+  k_grad_scatter<<<grid, 256, 0, s>>>(c->E, c->arc_a, c->arc_b, grad_c, grad_a, grad_b);
+  FSTC_LAUNCH_CHECK();
+  return FST_OK;
+}
 }  // namespace fstc
 
 // =============================================================================================
@@ -2096,7 +2158,7 @@ fst_status compose_sharded_impl(fst* A, fst* B, int world, fst_comm* comm, cudaS
   memset(&C0, 0, sizeof(C0));
   auto vd = [](const View& v) {
     return ViewDev{v.off, v.key, v.other, v.carry, v.w, v.cw, v.ikd, v.isrc, v.ikcw,
-                   v.lm_other, v.lm_pos, v.seg_node, v.seg_beg, v.lab_val, v.lab_seg, v.nlab};
+                   v.lm_other, v.lm_pos, v.seg_node, v.seg_beg, v.lab_val, v.lab_seg, v.nlab, v.arc};
   };
   C0.Af = vd(A->views[kOutByOlabel]);
   C0.Ab = vd(A->views[kInByOlabel]);

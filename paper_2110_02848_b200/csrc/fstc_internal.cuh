@@ -41,6 +41,7 @@ struct ViewDev {
   const int32_t* lab_val;
   const int32_t* lab_seg;
   int32_t nlab;
+  const int32_t* arc;     // [E] view position -> input arc index (provenance)
 };
 
 constexpr int32_t kSentinel = INT32_MIN;
@@ -76,6 +77,8 @@ struct CompDev {
   uint8_t* is_accept;
   int32_t* pair_a;
   int32_t* pair_b;
+  int32_t* arc_a;  // provenance outputs (FST_COMPOSE_PROVENANCE), nullptr when off
+  int32_t* arc_b;
 };
 
 // Per-level control block (ring of 3).

@@ -28,7 +28,9 @@ STATUS = {0: "FST_OK", 1: "FST_E_INVALID_ARG", 2: "FST_E_INVALID_GRAPH", 3: "FST
 EXPORTED = ["fst_create", "fst_compose", "fst_compose_batch", "fst_free", "fst_info", "fst_copy_to_host",
             "fst_get_stats", "fst_level_sizes", "fst_adjacency", "fst_set_profiling", "fst_launch_count",
             "fst_last_error", "fst_version", "fst_comm_unique_id", "fst_comm_init", "fst_comm_destroy",
-            "fst_compose_sharded", "fst_compose_sharded_local", "fst_shard_info", "fst_copy_arcs_to_host"]
+            "fst_compose_sharded", "fst_compose_sharded_local", "fst_shard_info", "fst_copy_arcs_to_host",
+            "fst_compose_ex", "fst_compose_batch_ex", "fst_copy_provenance_to_host", "fst_grad_scatter"]
+FST_COMPOSE_PROVENANCE = 1
 
 
 class FstError(RuntimeError):
@@ -47,7 +49,7 @@ class fst_view(C.Structure):
     _fields_ = [("num_states", C.c_int32), ("num_arcs", C.c_int64), ("row_ptr", C.c_void_p),
                 ("ilabel", C.c_void_p), ("olabel", C.c_void_p), ("dst", C.c_void_p), ("weight", C.c_void_p),
                 ("is_start", C.c_void_p), ("is_accept", C.c_void_p), ("pair_a", C.c_void_p),
-                ("pair_b", C.c_void_p)]
+                ("pair_b", C.c_void_p), ("arc_a", C.c_void_p), ("arc_b", C.c_void_p)]
 
 
 class fst_compose_stats(C.Structure):
@@ -92,6 +94,12 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
         lib.fst_copy_to_host.argtypes = [vp, vp] + [vp] * 9
         lib.fst_get_stats.argtypes = [vp, C.POINTER(fst_compose_stats)]
         lib.fst_copy_arcs_to_host.argtypes = [vp, vp, C.c_int64, C.c_int64, vp, vp, vp, vp]
+        if hasattr(lib, "fst_compose_ex"):  # (older builds loaded through FSTC_LIB for A/B runs lack these)
+            lib.fst_compose_ex.argtypes = [vp, vp, C.c_uint32, vp, C.POINTER(vp)]
+            lib.fst_compose_batch_ex.argtypes = [C.c_int32, C.POINTER(vp), C.POINTER(vp), C.c_uint32, vp,
+                                                 C.POINTER(vp)]
+            lib.fst_copy_provenance_to_host.argtypes = [vp, vp, C.c_int64, C.c_int64, vp, vp]
+            lib.fst_grad_scatter.argtypes = [vp, vp, vp, C.c_int64, vp, C.c_int64, vp]
         lib.fst_level_sizes.argtypes = [vp, C.c_int32, vp, C.c_int32]
         lib.fst_level_sizes.restype = C.c_int32
         lib.fst_adjacency.argtypes = [vp, C.c_int32, C.c_int32, vp, vp]
@@ -165,22 +173,48 @@ def fst_create(fst_like, stream=None) -> "Fst":
     return Fst(h)
 
 
-def fst_compose(a: "Fst", b: "Fst", stream=None) -> "Fst":
+def fst_compose(a: "Fst", b: "Fst", stream=None, provenance: bool = False) -> "Fst":
+    """C = trim(A o B); provenance=True also records each arc's (arc_a, arc_b) (fst_compose_ex)."""
     lib = load_library()
     h = C.c_void_p()
-    _check(lib.fst_compose(a.handle, b.handle, _stream_ptr(stream), C.byref(h)))
+    if provenance:
+        _check(lib.fst_compose_ex(a.handle, b.handle, FST_COMPOSE_PROVENANCE, _stream_ptr(stream), C.byref(h)))
+    else:
+        _check(lib.fst_compose(a.handle, b.handle, _stream_ptr(stream), C.byref(h)))
     return Fst(h)
 
 
-def fst_compose_batch(a: Sequence["Fst"], b: Sequence["Fst"], stream=None) -> List["Fst"]:
+def fst_compose_ex(a: "Fst", b: "Fst", flags: int, stream=None) -> "Fst":
+    lib = load_library()
+    h = C.c_void_p()
+    _check(lib.fst_compose_ex(a.handle, b.handle, flags, _stream_ptr(stream), C.byref(h)))
+    return Fst(h)
+
+
+def fst_compose_batch(a: Sequence["Fst"], b: Sequence["Fst"], stream=None, provenance: bool = False) -> List["Fst"]:
     lib = load_library()
     n = len(a)
     assert len(b) == n
     A = (C.c_void_p * n)(*[x.handle for x in a])
     B = (C.c_void_p * n)(*[x.handle for x in b])
     out = (C.c_void_p * n)()
-    _check(lib.fst_compose_batch(n, A, B, _stream_ptr(stream), out))
+    if provenance:
+        _check(lib.fst_compose_batch_ex(n, A, B, FST_COMPOSE_PROVENANCE, _stream_ptr(stream), out))
+    else:
+        _check(lib.fst_compose_batch(n, A, B, _stream_ptr(stream), out))
     return [Fst(C.c_void_p(out[i])) for i in range(n)]
+
+
+def fst_grad_scatter(c: "Fst", grad_c, grad_a=None, grad_b=None, stream=None):
+    """Accumulates dL/dw_c (CUDA float32 tensor [E_C]) into grad_a [E_A] / grad_b [E_B] (CUDA float32
+    tensors, +=) through the provenance of c (composed with provenance=True)."""
+    lib = load_library()
+    for t in (grad_c, grad_a, grad_b):
+        if t is not None and (not t.is_cuda or str(t.dtype) != "torch.float32" or not t.is_contiguous()):
+            raise FstError(1, "fst_grad_scatter: gradients must be contiguous CUDA float32 tensors")
+    ptr = lambda t: t.data_ptr() if t is not None and t.numel() else None
+    _check(lib.fst_grad_scatter(c.handle, ptr(grad_c), ptr(grad_a), 0 if grad_a is None else grad_a.numel(),
+                                ptr(grad_b), 0 if grad_b is None else grad_b.numel(), _stream_ptr(stream)))
 
 
 def fst_compose_sharded_local(a: "Fst", b: "Fst", world: int, stream=None) -> List["Fst"]:
@@ -298,7 +332,18 @@ class Fst:
         _check(load_library().fst_copy_to_host(self.handle, _stream_ptr(stream), ptr("row_ptr"), ptr("ilabel"),
                                                ptr("olabel"), ptr("dst"), ptr("weight"), ptr("is_start"),
                                                ptr("is_accept"), ptr("pair_a"), ptr("pair_b")))
+        if v.arc_a:
+            out["arc_a"], out["arc_b"] = self.provenance(stream)
         return out
+
+    def provenance(self, stream=None):
+        """(arc_a, arc_b) int32 arrays [E] (handles composed with provenance=True)."""
+        E = self.num_arcs
+        aa, ab = np.zeros(E, np.int32), np.zeros(E, np.int32)
+        _check(load_library().fst_copy_provenance_to_host(self.handle, _stream_ptr(stream), 0, E,
+                                                          aa.ctypes.data if E else None,
+                                                          ab.ctypes.data if E else None))
+        return aa, ab
 
     def state_arrays(self, stream=None) -> Dict[str, np.ndarray]:
         """Per-state arrays only (row_ptr, flags, pair_a/pair_b) -- no arcs."""
@@ -348,9 +393,9 @@ class Fst:
         return off, arcs[: int(v.num_arcs)]
 
 
-def compose(A, B, stream=None) -> Dict[str, np.ndarray]:
+def compose(A, B, stream=None, provenance: bool = False) -> Dict[str, np.ndarray]:
     """Convenience: host arrays in, composed graph (numpy, GPU numbering) out."""
     a = fst_create(A, stream)
     b = fst_create(B, stream)
-    c = fst_compose(a, b, stream)
+    c = fst_compose(a, b, stream, provenance=provenance)
     return c.to_host(stream)
