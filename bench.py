@@ -36,10 +36,12 @@ WORKLOADS = {
     "c4": ("configs[3] large random composition: acceptors V=20000, D=8, 16 tokens", 20000, 8, 16),
     "c4-d4": ("configs[3] large random composition: acceptors V=20000, D=4, 8 tokens", 20000, 4, 8),
     "c4-paper": ("paper point PAPER.md:316-325: acceptors V=8192, D=5, 10 tokens", 8192, 5, 10),
+    "fig3b-d16": ("Fig. 3b degree sweep point PAPER.md:285-288: acceptors V=256, D=16, 32 tokens", 256, 16, 32),
+    "fig3b-d64": ("Fig. 3b degree sweep point PAPER.md:285-288: acceptors V=256, D=64, 128 tokens", 256, 64, 128),
     "c5": ("configs[4] batched lexicon x emissions: closure(10k-word letter lexicon) composed with "
            "32 emissions graphs per GPU (T_i = 100 + rand(401), 28 tokens), fst_compose_batch", 0, 0, 28),
 }
-REF_SAMPLE_V = {"c4": 1024, "c4-d4": 2048, "c4-paper": 1024}  # oracle sample sizes (~2-8 s per step)
+REF_SAMPLE_V = {"c4": 1024, "c4-d4": 2048, "c4-paper": 1024, "fig3b-d16": 256, "fig3b-d64": 256}  # oracle sample sizes (~2-8 s per step)
 UTTS_PER_GPU = 32
 L2_FLUSH_BYTES = 512 << 20
 

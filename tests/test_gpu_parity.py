@@ -126,6 +126,16 @@ def test_c4_random_acceptors(fst, V, D):
     check(fst, A, B, f"c4 {V}/{D}")
 
 
+@pytest.mark.parametrize("D", [4, 8, 16, 32, 64])
+def test_fig3b_degree_sweep(fst, D):
+    """Fig. 3b: V=256, out-degree D, 2D tokens -- up to 4096 arc pairs and ~32
+    matches per state pair; D >= 32 has labels >= 63 (no label masks: the general paths)."""
+    A = fstgen.random_graph(256, D, 2 * D, 1000 + 256 + D)
+    B = fstgen.random_graph(256, D, 2 * D, 2000 + 256 + D)
+    got = check(fst, A, B, f"fig3b D={D}")
+    assert got["num_arcs"] > 0
+
+
 def test_eps_small_graphs(fst):
     for s in range(100):
         A = fstgen.random_graph(12, 3, 4, 500 + s, acceptor=False, eps_prob=0.3, weights="dyadic64")
