@@ -6,6 +6,7 @@ brute-force Eq. (1) path scores, Delannoy path counts, the trellis closed form, 
 special case and invariants.  See DESIGN.md "Oracle and pins".
 """
 import collections
+import math
 
 import numpy as np
 import pytest
@@ -295,3 +296,51 @@ def test_provenance_consistent_c3_and_counts():
         exp = sorted(mv[4] for mv in pins.n1_moves(A, B, a, b, prov=True) if mv[0] in keys)
         got = sorted(zip(C["arc_a"][rp[s]:rp[s + 1]].tolist(), C["arc_b"][rp[s]:rp[s + 1]].tolist()))
         assert got == exp, s
+
+
+# ----------------------------------------------------------------------------- forward score
+def _lse(vals):
+    vals = list(vals)
+    if not vals:
+        return float("-inf")
+    m = max(vals)
+    return m + math.log(sum(math.exp(v - m) for v in vals))
+
+
+@pytest.mark.parametrize("seed", range(40))
+def test_forward_score_bruteforce(seed):
+    """total = logsumexp over every accepting path of C of its weight (path enumeration of the DAG),
+    and = logsumexp over the Eq. (1) table of matched A/B path pairs with Delannoy multiplicities:
+    two pins independent of the forward recursion."""
+    from oracle import forward as fw
+    eps = 0.2 if seed % 2 else 0.3
+    A = fstgen.random_dag(7, 3, 3, eps, 7919 * seed + 11)
+    B = fstgen.random_dag(7, 3, 3, eps, 7919 * seed + 13)
+    C = oracle.compose(A, B)
+    alpha, total = fw.forward(C)
+    w = np.asarray(C["weight"], np.float64)
+    class G:  # accepting_paths wants attribute access
+        row_ptr, dst = C["row_ptr"], C["dst"]
+        is_start, is_accept = C["is_start"], C["is_accept"]
+    exp = _lse(sum(w[e] for e in p) for p in pins.accepting_paths(G))
+    eq1 = _lse(s + math.log(c) for cnt in pins.eq1_bruteforce(A, B).values() for s, c in cnt.items())
+    for ref in (exp, eq1):
+        if ref == float("-inf"):
+            assert total == ref
+        else:
+            assert abs(total - ref) <= 1e-9 * max(1.0, abs(ref)), (seed, total, ref)
+
+
+def test_forward_score_trellis_and_cycles():
+    """lexicon o emissions (a DAG): every state has a finite alpha (C is trim, so every state is
+    reachable from a start), and a cyclic graph is rejected."""
+    from oracle import forward as fw
+    A, B = fstgen.config_c3(num_words=100, T=20)
+    C = oracle.compose(A, B)
+    alpha, total = fw.forward(C)
+    assert np.all(np.isfinite(alpha)) and math.isfinite(total)
+    A, B = fstgen.config_c1(0)  # random graphs with cycles
+    C = oracle.compose(A, B)
+    if C["num_states"]:
+        with pytest.raises(ValueError):
+            fw.forward(C)
