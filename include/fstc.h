@@ -154,6 +154,16 @@ fst_status fst_copy_provenance_to_host(fst_handle c, void* stream, int64_t first
 fst_status fst_grad_scatter(fst_handle c, const float* grad_c, float* grad_a, int64_t n_a, float* grad_b,
                             int64_t n_b, void* stream);
 
+/* Forward score of an ACYCLIC graph in the log semiring (PAPER.md:368-370,
+ * semiring PAPER.md:89-91): alpha(v) = logsumexp([0 if v is a start state] + {alpha(u) + w(e) :
+ * e = u -> v}), *total = logsumexp of alpha over the accept states (-inf if none is reachable; an
+ * empty graph gives -inf).  total: HOST double (required).  alpha: optional DEVICE double array
+ * [num_states] that receives alpha (NULL to skip).  Works on any handle (composed or created).
+ * Float64 throughout; the fold order of a state's in-arcs is not fixed, so results agree with an
+ * exact evaluation to float64 rounding.  A cyclic graph returns FST_E_INVALID_GRAPH (the sum over
+ * paths is an infinite series).  Synchronises `stream`. */
+fst_status fst_forward_score(fst_handle h, void* stream, double* total, double* alpha);
+
 /* Releases a handle and its device memory.  NULL-safe. */
 void fst_free(fst_handle h);
 

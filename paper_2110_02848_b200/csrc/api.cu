@@ -47,6 +47,7 @@ fst_status compose_impl(int32_t n, const fst_handle* a, const fst_handle* b, cud
 fst_status grad_scatter_impl(fst* c, const float* grad_c, float* grad_a, int64_t n_a, float* grad_b, int64_t n_b,
                              cudaStream_t s);
 fst_status compose_sharded_impl(fst* A, fst* B, int world, fst_comm* comm, cudaStream_t s, fst_handle* c);
+fst_status forward_score_impl(fst* h, cudaStream_t s, double* total, double* alpha_out);
 
 fst_status device_ready() {
   int n = 0;
@@ -134,6 +135,16 @@ fst_status fst_grad_scatter(fst_handle c, const float* grad_c, float* grad_a, in
   fst_status st = device_ready();
   if (st) return st;
   return grad_scatter_impl(c, grad_c, grad_a, n_a, grad_b, n_b, (cudaStream_t)stream);
+}
+
+fst_status fst_forward_score(fst_handle h, void* stream, double* total, double* alpha) {
+  if (!h || !total) {
+    set_error(FST_E_INVALID_ARG, "fst_forward_score: NULL argument");
+    return FST_E_INVALID_ARG;
+  }
+  fst_status st = device_ready();
+  if (st) return st;
+  return forward_score_impl(h, (cudaStream_t)stream, total, alpha);
 }
 
 void fst_free(fst_handle h) { delete h; }

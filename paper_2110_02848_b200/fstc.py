@@ -29,7 +29,8 @@ EXPORTED = ["fst_create", "fst_compose", "fst_compose_batch", "fst_free", "fst_i
             "fst_get_stats", "fst_level_sizes", "fst_adjacency", "fst_set_profiling", "fst_launch_count",
             "fst_last_error", "fst_version", "fst_comm_unique_id", "fst_comm_init", "fst_comm_destroy",
             "fst_compose_sharded", "fst_compose_sharded_local", "fst_shard_info", "fst_copy_arcs_to_host",
-            "fst_compose_ex", "fst_compose_batch_ex", "fst_copy_provenance_to_host", "fst_grad_scatter"]
+            "fst_compose_ex", "fst_compose_batch_ex", "fst_copy_provenance_to_host", "fst_grad_scatter",
+            "fst_forward_score"]
 FST_COMPOSE_PROVENANCE = 1
 
 
@@ -100,6 +101,8 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
                                                  C.POINTER(vp)]
             lib.fst_copy_provenance_to_host.argtypes = [vp, vp, C.c_int64, C.c_int64, vp, vp]
             lib.fst_grad_scatter.argtypes = [vp, vp, vp, C.c_int64, vp, C.c_int64, vp]
+        if hasattr(lib, "fst_forward_score"):
+            lib.fst_forward_score.argtypes = [vp, vp, C.POINTER(C.c_double), vp]
         lib.fst_level_sizes.argtypes = [vp, C.c_int32, vp, C.c_int32]
         lib.fst_level_sizes.restype = C.c_int32
         lib.fst_adjacency.argtypes = [vp, C.c_int32, C.c_int32, vp, vp]
@@ -203,6 +206,19 @@ def fst_compose_batch(a: Sequence["Fst"], b: Sequence["Fst"], stream=None, prove
     else:
         _check(lib.fst_compose_batch(n, A, B, _stream_ptr(stream), out))
     return [Fst(C.c_void_p(out[i])) for i in range(n)]
+
+
+def fst_forward_score(h: "Fst", alpha=None, stream=None) -> float:
+    """Log-semiring forward score of an acyclic graph (float64); alpha: optional CUDA float64 tensor
+    [num_states] receiving alpha."""
+    lib = load_library()
+    if alpha is not None and (not alpha.is_cuda or str(alpha.dtype) != "torch.float64" or not alpha.is_contiguous()
+                              or alpha.numel() < h.num_states):
+        raise FstError(1, "fst_forward_score: alpha must be a contiguous CUDA float64 tensor [num_states]")
+    tot = C.c_double()
+    _check(lib.fst_forward_score(h.handle, _stream_ptr(stream), C.byref(tot),
+                                 alpha.data_ptr() if alpha is not None and alpha.numel() else None))
+    return float(tot.value)
 
 
 def fst_grad_scatter(c: "Fst", grad_c, grad_a=None, grad_b=None, stream=None):

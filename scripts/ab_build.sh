@@ -12,7 +12,7 @@ for f in $(git -C "$ROOT" ls-tree --name-only "$REV" paper_2110_02848_b200/csrc/
 done
 git -C "$ROOT" show "$REV:include/fstc.h" > "$TMP/include/fstc.h"
 FLAGS="-gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC --expt-relaxed-constexpr --extended-lambda -I $TMP/include"
-for s in api create compose scan memory; do
+for s in $(git -C "$ROOT" ls-tree --name-only "$REV" paper_2110_02848_b200/csrc/ | grep "\.cu$" | xargs -n1 basename | sed "s/\.cu$//"); do
   /usr/local/cuda/bin/nvcc $FLAGS -c "$TMP/p/csrc/$s.cu" -o "$TMP/$s.o" &
 done
 wait
