@@ -271,6 +271,24 @@ def run_ours(args):
     clocks = sampler.stop()
     tot_ms = sum(times)
     V_C, E_C = info
+    fwd = None
+    if args.forward:  # forward score over the composed graphs, timed separately
+        with torch.cuda.stream(stream):
+            cs = compose_all()
+            fstc.fst_forward_score(cs[0], stream=stream)  # warm-up
+            torch.cuda.synchronize()
+            f0 = torch.cuda.Event(enable_timing=True)
+            f1 = torch.cuda.Event(enable_timing=True)
+            f0.record(stream)
+            tots = [fstc.fst_forward_score(c, stream=stream) for c in cs]
+            f1.record(stream)
+        f1.synchronize()
+        fms = f0.elapsed_time(f1)
+        fwd = {"metric": "forward-score arcs/sec", "value": E_C / (fms / 1e3), "unit": "arcs/s", "ms": fms,
+               "graphs": len(cs), "total_of_first": tots[0],
+               "note": "fst_forward_score over every composed graph of one step (log semiring, float64)"}
+        for c in cs:
+            c.free()
     max_ms, arcs_all = parallel.reduce_timing(tot_ms, float(E_C), pg, dev)
     value = arcs_all * args.steps / (max_ms / 1e3)
 
@@ -319,6 +337,7 @@ def run_ours(args):
                          "(pair-space bitmaps + composed graph) exceeds L2"},
         "phases_ms": {"stage1_backward_bfs": s1, "stage2_forward_bfs": s2, "numbering": num, "emit": emit_ms},
         "roofline": roof,
+        **({"forward_score": fwd} if fwd else {}),
         "step_roofline": step_roof,
         "gpu_launches": launches,
         "clocks": clocks,
@@ -477,6 +496,8 @@ def main():
     ap.add_argument("--mode", default=os.environ.get("FSTC_BENCH_MODE", "replicas"), choices=["replicas", "sharded"],
                     help="replicas: independent compositions per GPU (weak); sharded: one composition over all GPUs")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--forward", action="store_true",
+                    help="also time fst_forward_score over the composed graphs (c5: lexicon o emissions DAGs)")
     ap.add_argument("--provenance", action="store_true",
                     help="compose with FST_COMPOSE_PROVENANCE (also writes arc_a/arc_b per arc; not the headline)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
