@@ -10,6 +10,9 @@ Functions:
   compose(A, B)        -> dict of numpy arrays, states in FIFO discovery order (Alg. 1), with the
                           provenance arc_a / arc_b of every arc (-1 = that side stays)
   canonical(A, B)      -> same, canonical form (reading 24)
+  compose_filtered(A, B) -> the eps-filtered variant (three-state filter),
+                          states (pair_a, pair_b, pair_f)
+  compose_chain(gs)    -> N-way composition as a left fold of compose
   coaccessible(A, B)   -> uint8 [V_A * V_B] co-accessible set R (Alg. 1 line 3)
   in_adjacency(g)      -> (inArcOffset, inArcs) per §3.2
 """
@@ -50,7 +53,7 @@ class _Graph(C.Structure):
                 ("is_start", C.POINTER(C.c_uint8)), ("is_accept", C.POINTER(C.c_uint8)),
                 ("pair_a", C.POINTER(C.c_int32)), ("pair_b", C.POINTER(C.c_int32)),
                 ("level", C.POINTER(C.c_int32)), ("arc_a", C.POINTER(C.c_int32)),
-                ("arc_b", C.POINTER(C.c_int32))]
+                ("arc_b", C.POINTER(C.c_int32)), ("pair_f", C.POINTER(C.c_int32))]
 
 
 def _load():
@@ -59,6 +62,7 @@ def _load():
         if _lib is None:
             lib = C.CDLL(build())
             lib.orc_compose.argtypes = [C.POINTER(_Fst), C.POINTER(_Fst), C.POINTER(_Graph)]
+            lib.orc_compose_filtered.argtypes = [C.POINTER(_Fst), C.POINTER(_Fst), C.POINTER(_Graph)]
             lib.orc_canonicalize.argtypes = [C.POINTER(_Graph), C.c_int32]
             lib.orc_coaccessible.argtypes = [C.POINTER(_Fst), C.POINTER(_Fst), C.c_void_p]
             lib.orc_in_adjacency.argtypes = [C.POINTER(_Fst), C.c_void_p, C.c_void_p]
@@ -82,9 +86,9 @@ def _take(ptr, n, dtype):
     return np.ctypeslib.as_array(ptr, shape=(n,)).astype(dtype, copy=True)
 
 
-def _to_numpy(g: _Graph):
+def _to_numpy(g: _Graph, filtered: bool = False):
     V, E = g.V, g.E
-    return {
+    out = {
         "num_states": V, "num_arcs": E,
         "row_ptr": _take(g.row_ptr, V + 1, np.int64),
         "ilabel": _take(g.ilabel, E, np.int32), "olabel": _take(g.olabel, E, np.int32),
@@ -94,26 +98,54 @@ def _to_numpy(g: _Graph):
         "level": _take(g.level, V, np.int32),
         "arc_a": _take(g.arc_a, E, np.int32), "arc_b": _take(g.arc_b, E, np.int32),
     }
+    if filtered:
+        out["pair_f"] = _take(g.pair_f, V, np.int32)
+    return out
 
 
-def compose(A, B, canonicalize: bool = False):
+def compose(A, B, canonicalize: bool = False, eps_filter: bool = False):
     lib = _load()
     da, ka = _desc(A)
     db, kb = _desc(B)
     out = _Graph()
-    if lib.orc_compose(C.byref(da), C.byref(db), C.byref(out)) != 0:
+    fn = lib.orc_compose_filtered if eps_filter else lib.orc_compose
+    if fn(C.byref(da), C.byref(db), C.byref(out)) != 0:
         raise MemoryError("oracle compose failed")
     try:
         if canonicalize and lib.orc_canonicalize(C.byref(out), int(B.num_states)) != 0:
             raise MemoryError("oracle canonicalize failed")
-        return _to_numpy(out)
+        return _to_numpy(out, eps_filter)
     finally:
         lib.orc_free(C.byref(out))
         del ka, kb
 
 
-def canonical(A, B):
-    return compose(A, B, canonicalize=True)
+def canonical(A, B, eps_filter: bool = False):
+    return compose(A, B, canonicalize=True, eps_filter=eps_filter)
+
+
+def compose_filtered(A, B, canonicalize: bool = False):
+    """eps-filtered variant (SPEC.md S:150-177 three-state filter): states are
+    triples (pair_a, pair_b, pair_f), f in {0 MATCH, 1 A_EPS, 2 B_EPS}; canonical key
+    (a * V_B + b) * 3 + f."""
+    return compose(A, B, canonicalize=canonicalize, eps_filter=True)
+
+
+def compose_chain(graphs, canonicalize: bool = False):
+    """N-way composition as the left fold ((G0 o G1) o G2) o ... (PAPER.md:366-368 names N-way
+    composition as future work; Algorithm 1 applied N-1 times).  Returns the last composition (as
+    numpy dict); with canonicalize, states are keyed by the last fold's (pair_a, pair_b)."""
+    from types import SimpleNamespace
+    cur = graphs[0]
+    out = None
+    for k, g in enumerate(graphs[1:]):
+        last = k == len(graphs) - 2
+        out = compose(cur, g, canonicalize=canonicalize and last)
+        if not last:
+            cur = SimpleNamespace(num_states=int(out["num_states"]), num_arcs=int(out["num_arcs"]),
+                                  **{k: out[k] for k in ("row_ptr", "ilabel", "olabel", "dst", "weight",
+                                                         "is_start", "is_accept")})
+    return out
 
 
 def coaccessible(A, B) -> np.ndarray:

@@ -59,6 +59,7 @@ typedef struct {
   int32_t* level; /* BFS level of each state (FIFO discovery distance), for Fig. 2 profiles */
   int32_t* arc_a; /* provenance: the arc pair (e_a, e_b) of Alg. 1 line 13 that */
   int32_t* arc_b; /* produced each arc; -1 = that side stays (M3 for arc_a, M2 for arc_b) */
+  int32_t* pair_f; /* eps-filter state of each state (orc_compose_filtered only; NULL otherwise) */
 } orc_graph;
 
 /* ---------------------------------------------------------------- adjacency (§3.2) */
@@ -216,7 +217,7 @@ void orc_free(orc_graph* g) {
   if (!g) return;
   free(g->row_ptr); free(g->ilabel); free(g->olabel); free(g->dst); free(g->weight);
   free(g->is_start); free(g->is_accept); free(g->pair_a); free(g->pair_b); free(g->level);
-  free(g->arc_a); free(g->arc_b);
+  free(g->arc_a); free(g->arc_b); free(g->pair_f);
   memset(g, 0, sizeof(*g));
 }
 
@@ -336,6 +337,184 @@ int orc_compose(const orc_fst* A, const orc_fst* B, orc_graph* C) {
   return 0;
 }
 
+/* ---------------------------------------------------------------- eps-filtered variant */
+/* The paper claims eps support but gives no redundancy filter; without one,
+ * interleaved eps moves duplicate paths (the Delannoy inflation of reading N1).  This is the standard
+ * three-state eps filter as SPEC.md states it (S:150-153 FilterState, S:168-177 match_moves), run
+ * through Algorithm 1's structure over triples (u_a, u_b, f), f in
+ * {0 = MATCH, 1 = A_EPS, 2 = B_EPS}:
+ *   (1) MATCH     e_a x e_b, o_a == i_b != eps, from any f          -> (dst e_a, dst e_b, 0), w_a + w_b
+ *   (2) EPS-BOTH  e_a x e_b, o_a == i_b == eps, only from f = 0      -> (dst e_a, dst e_b, 0), w_a + w_b
+ *   (3) EPS-A     e_a with o_a = eps, B stays, from f in {0, 1}      -> (dst e_a, u_b, 1),     w_a
+ *   (4) EPS-B     e_b with i_b = eps, A stays, from f in {0, 2}      -> (u_a, dst e_b, 2),     w_b
+ * Start triples (s_a, s_b, 0); accept triples (f_a, f_b, any f).  R (line 3) is computed exactly on
+ * the triple space by the reversed moves (SPEC's unfiltered R + final trim sweep gives the same
+ * trim graph).  Labels, weights and provenance as in orc_compose. */
+#define FK(a_, b_, f_) ((((int64_t)(a_)) * VB + (b_)) * 3 + (f_))
+
+static int coaccessible_filtered(const orc_fst* A, const orc_fst* B, const orc_adj* aA, const orc_adj* aB,
+                                 uint8_t* R) {
+  int64_t VB = B->V, P3 = (int64_t)A->V * B->V * 3;
+  int64_t* Q = (int64_t*)malloc(sizeof(int64_t) * (size_t)(P3 ? P3 : 1));
+  int64_t head = 0, tail = 0;
+  int32_t fa, fb, f;
+  if (!Q) return -1;
+  memset(R, 0, (size_t)P3);
+#define MARK(p_) do { int64_t q_ = (p_); if (!R[q_]) { R[q_] = 1; Q[tail++] = q_; } } while (0)
+  for (fa = 0; fa < A->V; ++fa) {
+    if (!A->is_accept[fa]) continue;
+    for (fb = 0; fb < B->V; ++fb)
+      if (B->is_accept[fb])
+        for (f = 0; f < 3; ++f) MARK(FK(fa, fb, f));
+  }
+  while (head < tail) {
+    int64_t v = Q[head++];
+    int32_t vf = (int32_t)(v % 3), va = (int32_t)(v / 3 / VB), vb = (int32_t)(v / 3 % VB);
+    int64_t i, j;
+    if (vf == 0) { /* reversed (1) from any f, reversed (2) from f = 0 */
+      for (i = aA->in_off[va]; i < aA->in_off[va + 1]; ++i) {
+        int64_t ea = aA->in_arcs[i];
+        for (j = aB->in_off[vb]; j < aB->in_off[vb + 1]; ++j) {
+          int64_t eb = aB->in_arcs[j];
+          if (A->olabel[ea] != B->ilabel[eb]) continue;
+          if (A->olabel[ea] != ORC_EPS) {
+            for (f = 0; f < 3; ++f) MARK(FK(aA->src[ea], aB->src[eb], f));
+          } else {
+            MARK(FK(aA->src[ea], aB->src[eb], 0));
+          }
+        }
+      }
+    } else if (vf == 1) { /* reversed (3): from f in {0, 1} */
+      for (i = aA->in_off[va]; i < aA->in_off[va + 1]; ++i) {
+        int64_t ea = aA->in_arcs[i];
+        if (A->olabel[ea] != ORC_EPS) continue;
+        MARK(FK(aA->src[ea], vb, 0));
+        MARK(FK(aA->src[ea], vb, 1));
+      }
+    } else { /* reversed (4): from f in {0, 2} */
+      for (j = aB->in_off[vb]; j < aB->in_off[vb + 1]; ++j) {
+        int64_t eb = aB->in_arcs[j];
+        if (B->ilabel[eb] != ORC_EPS) continue;
+        MARK(FK(va, aB->src[eb], 0));
+        MARK(FK(va, aB->src[eb], 2));
+      }
+    }
+  }
+#undef MARK
+  free(Q);
+  return 0;
+}
+
+int orc_compose_filtered(const orc_fst* A, const orc_fst* B, orc_graph* C) {
+  int64_t VB = B->V, P3 = (int64_t)A->V * B->V * 3;
+  orc_adj aA, aB;
+  uint8_t* R;
+  int32_t* id; /* V_A x V_B x 3 state-index table */
+  int32_t *pa = NULL, *pb = NULL, *pf = NULL, *lv = NULL;
+  uint8_t *st = NULL, *ac = NULL;
+  int64_t* rp = NULL;
+  int64_t ns = 0, capS = 0, u, i;
+  arcbuf arcs;
+  int32_t sa, sb;
+  memset(C, 0, sizeof(*C));
+  memset(&arcs, 0, sizeof(arcs));
+  if (adj_build(A, &aA) || adj_build(B, &aB)) return -1;
+  R = (uint8_t*)malloc((size_t)(P3 ? P3 : 1));
+  id = (int32_t*)malloc(sizeof(int32_t) * (size_t)(P3 ? P3 : 1));
+  if (!R || !id) return -1;
+  if (coaccessible_filtered(A, B, &aA, &aB, R)) return -1;
+  for (i = 0; i < P3; ++i) id[i] = -1;
+
+#define NEW_STATE3(va_, vb_, vf_, lev_)                                                   \
+  do {                                                                                    \
+    if (ns == capS) {                                                                     \
+      capS = capS ? 2 * capS : 1024;                                                      \
+      pa = (int32_t*)realloc(pa, sizeof(int32_t) * (size_t)capS);                        \
+      pb = (int32_t*)realloc(pb, sizeof(int32_t) * (size_t)capS);                        \
+      pf = (int32_t*)realloc(pf, sizeof(int32_t) * (size_t)capS);                        \
+      lv = (int32_t*)realloc(lv, sizeof(int32_t) * (size_t)capS);                        \
+      st = (uint8_t*)realloc(st, (size_t)capS);                                          \
+      ac = (uint8_t*)realloc(ac, (size_t)capS);                                          \
+      rp = (int64_t*)realloc(rp, sizeof(int64_t) * (size_t)(capS + 1));                  \
+      if (!pa || !pb || !pf || !lv || !st || !ac || !rp) return -1;                      \
+    }                                                                                     \
+    id[FK(va_, vb_, vf_)] = (int32_t)ns;                                                  \
+    pa[ns] = (va_); pb[ns] = (vb_); pf[ns] = (vf_); lv[ns] = (lev_); st[ns] = 0;         \
+    ac[ns] = (uint8_t)(A->is_accept[(va_)] && B->is_accept[(vb_)]);                      \
+    ns++;                                                                                 \
+  } while (0)
+#define ADD_MOVE(va_, vb_, vf_, il_, ol_, w_, xa_, xb_)                                   \
+  do {                                                                                    \
+    int64_t v_ = FK(va_, vb_, vf_);                                                       \
+    if (R[v_]) {                                                                          \
+      if (id[v_] < 0) NEW_STATE3(va_, vb_, vf_, lv[u] + 1);                               \
+      if (arc_push(&arcs, il_, ol_, id[v_], w_, xa_, xb_)) return -1;                     \
+    }                                                                                     \
+  } while (0)
+
+  /* lines 4-11: start triples (s_a, s_b, MATCH) in R */
+  for (sa = 0; sa < A->V; ++sa) {
+    if (!A->is_start[sa]) continue;
+    for (sb = 0; sb < B->V; ++sb) {
+      if (!B->is_start[sb] || !R[FK(sa, sb, 0)]) continue;
+      NEW_STATE3(sa, sb, 0, 0);
+      st[ns - 1] = 1;
+    }
+  }
+  /* lines 12-31 */
+  for (u = 0; u < ns; ++u) {
+    int32_t ua = pa[u], ub = pb[u], uf = pf[u];
+    int64_t ea, eb;
+    rp[u] = arcs.n;
+    /* (1) MATCH and (2) EPS-BOTH: arc pairs in arc order */
+    for (ea = A->row_ptr[ua]; ea < A->row_ptr[ua + 1]; ++ea) {
+      for (eb = B->row_ptr[ub]; eb < B->row_ptr[ub + 1]; ++eb) {
+        int32_t oa = A->olabel[ea];
+        float w;
+        if (oa != B->ilabel[eb]) continue;
+        if (oa == ORC_EPS && uf != 0) continue; /* EPS-BOTH only from MATCH */
+        w = A->weight[ea] + B->weight[eb];      /* one binary32 add */
+        ADD_MOVE(A->dst[ea], B->dst[eb], 0, A->ilabel[ea], B->olabel[eb], w, (int32_t)ea, (int32_t)eb);
+      }
+    }
+    /* (3) EPS-A from f in {MATCH, A_EPS} */
+    if (uf != 2)
+      for (ea = A->row_ptr[ua]; ea < A->row_ptr[ua + 1]; ++ea)
+        if (A->olabel[ea] == ORC_EPS)
+          ADD_MOVE(A->dst[ea], ub, 1, A->ilabel[ea], ORC_EPS, A->weight[ea], (int32_t)ea, -1);
+    /* (4) EPS-B from f in {MATCH, B_EPS} */
+    if (uf != 1)
+      for (eb = B->row_ptr[ub]; eb < B->row_ptr[ub + 1]; ++eb)
+        if (B->ilabel[eb] == ORC_EPS)
+          ADD_MOVE(ua, B->dst[eb], 2, ORC_EPS, B->olabel[eb], B->weight[eb], -1, (int32_t)eb);
+  }
+#undef ADD_MOVE
+#undef NEW_STATE3
+  if (!rp) rp = (int64_t*)malloc(sizeof(int64_t));
+  rp[ns] = arcs.n;
+  C->V = (int32_t)ns;
+  C->E = arcs.n;
+  C->row_ptr = rp;
+  C->ilabel = arcs.il;
+  C->olabel = arcs.ol;
+  C->dst = arcs.dst;
+  C->weight = arcs.w;
+  C->arc_a = arcs.aa;
+  C->arc_b = arcs.ab;
+  C->is_start = st;
+  C->is_accept = ac;
+  C->pair_a = pa;
+  C->pair_b = pb;
+  C->pair_f = pf;
+  C->level = lv;
+  free(R);
+  free(id);
+  adj_free(&aA);
+  adj_free(&aB);
+  return 0;
+}
+#undef FK
+
 /* ---------------------------------------------------------------- canonical form (reading 24) */
 /* States renumbered by ascending key(a,b) = a*V_B + b; arcs of a row sorted by
  * (dst key, ilabel, olabel, weight bits as uint32). */
@@ -374,6 +553,7 @@ int orc_canonicalize(orc_graph* C, int32_t VB) {
   if (!keys || !order || !newid) return -1;
   for (s = 0; s < V; ++s) {
     keys[s] = (int64_t)C->pair_a[s] * VB + C->pair_b[s];
+    if (C->pair_f) keys[s] = keys[s] * 3 + C->pair_f[s]; /* SPEC PairState key (a*V_B + b)*3 + f */
     order[s] = s;
   }
   g_keys = keys;
@@ -393,6 +573,7 @@ int orc_canonicalize(orc_graph* C, int32_t VB) {
   D.level = (int32_t*)malloc(sizeof(int32_t) * (size_t)(V ? V : 1));
   D.arc_a = (int32_t*)malloc(sizeof(int32_t) * (size_t)(E ? E : 1));
   D.arc_b = (int32_t*)malloc(sizeof(int32_t) * (size_t)(E ? E : 1));
+  if (C->pair_f) D.pair_f = (int32_t*)malloc(sizeof(int32_t) * (size_t)(V ? V : 1));
   for (s = 0; s < V; ++s) {
     int32_t o = order[s];
     int64_t lo = C->row_ptr[o], hi = C->row_ptr[o + 1], n = hi - lo, e;
@@ -402,6 +583,7 @@ int orc_canonicalize(orc_graph* C, int32_t VB) {
     D.pair_a[s] = C->pair_a[o];
     D.pair_b[s] = C->pair_b[o];
     D.level[s] = C->level[o];
+    if (C->pair_f) D.pair_f[s] = C->pair_f[o];
     if (n > tcap) {
       tcap = n;
       tmp = (carc*)realloc(tmp, sizeof(carc) * (size_t)tcap);

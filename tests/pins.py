@@ -39,11 +39,17 @@ def wbits(w) -> int:
 
 
 # ----------------------------------------------------------------------------- canonical builder
+def state_key(p, VB: int) -> int:
+    """Canonical state key: a * V_B + b for pairs, (a * V_B + b) * 3 + f for eps-filter triples."""
+    return p[0] * VB + p[1] if len(p) == 2 else (p[0] * VB + p[1]) * 3 + p[2]
+
+
 def build_canonical(VB: int, states: Dict[Tuple[int, int], Tuple[int, int]],
-                    arcs: List[Tuple[Tuple[int, int], Tuple[int, int], int, int, np.float32]]):
-    """states: {(a,b): (is_start, is_accept)}; arcs: [((a,b),(a',b'), il, ol, w[, (arc_a, arc_b)])]
-    -> canonical dict (with arc_a / arc_b when the arcs carry provenance)."""
-    keys = sorted(states, key=lambda p: p[0] * VB + p[1])
+                    arcs: List[Tuple[Tuple[int, int], Tuple[int, int], int, int, np.float32]],
+                    triples: bool = False):
+    """states: {(a,b) or (a,b,f): (is_start, is_accept)}; arcs: [(src, dst, il, ol, w[, (arc_a, arc_b)])]
+    -> canonical dict (with arc_a / arc_b when the arcs carry provenance, pair_f for triples)."""
+    keys = sorted(states, key=lambda p: state_key(p, VB))
     nid = {p: i for i, p in enumerate(keys)}
     rows = collections.defaultdict(list)
     prov = bool(arcs) and len(arcs[0]) == 6
@@ -68,6 +74,8 @@ def build_canonical(VB: int, states: Dict[Tuple[int, int], Tuple[int, int]],
         "pair_a": np.array([p[0] for p in keys], np.int32),
         "pair_b": np.array([p[1] for p in keys], np.int32),
     }
+    if triples:
+        out["pair_f"] = np.array([p[2] for p in keys], np.int32)
     if prov:
         out["arc_a"], out["arc_b"] = np.array(aa, np.int32), np.array(ab, np.int32)
     return out
@@ -80,7 +88,8 @@ def assert_canonical_equal(got, exp, what=""):
     """Element-by-element equality of two canonical graphs; weights compared BIT-exactly."""
     assert int(got["num_states"]) == int(exp["num_states"]), f"{what}: V {got['num_states']} != {exp['num_states']}"
     assert int(got["num_arcs"]) == int(exp["num_arcs"]), f"{what}: E {got['num_arcs']} != {exp['num_arcs']}"
-    for k in CANON_KEYS:
+    keys = CANON_KEYS + (("pair_f",) if "pair_f" in exp or "pair_f" in got else ())
+    for k in keys:
         a, b = np.asarray(got[k]), np.asarray(exp[k])
         if not np.array_equal(a.astype(np.int64), b.astype(np.int64)):
             bad = np.flatnonzero(a.astype(np.int64) != b.astype(np.int64))
@@ -119,6 +128,37 @@ def canonicalize_rows(g, VB: int):
     return out
 
 
+def canonicalize_any(g, VB: int):
+    """Canonicalise a graph with ANY state numbering: states sorted by their key (pairs, or triples
+    when g has pair_f), dst remapped, rows sorted as in canonicalize_rows.  Comparator only."""
+    V = int(g["num_states"])
+    keys = np.asarray(g["pair_a"], np.int64) * VB + np.asarray(g["pair_b"], np.int64)
+    if "pair_f" in g and g["pair_f"] is not None:
+        keys = keys * 3 + np.asarray(g["pair_f"], np.int64)
+    order = np.argsort(keys, kind="stable")
+    newid = np.empty(V, np.int64)
+    newid[order] = np.arange(V)
+    rp = np.asarray(g["row_ptr"], np.int64)
+    deg = np.diff(rp)[order]
+    nrp = np.zeros(V + 1, np.int64)
+    np.cumsum(deg, out=nrp[1:])
+    arc_idx = np.concatenate([np.arange(rp[o], rp[o + 1]) for o in order]) if V else np.zeros(0, np.int64)
+    out = dict(g)
+    out["row_ptr"] = nrp
+    for k in ("is_start", "is_accept", "pair_a", "pair_b") + (("pair_f",) if "pair_f" in g else ()):
+        out[k] = np.asarray(g[k])[order]
+    for k in ("ilabel", "olabel", "weight") + (("arc_a", "arc_b") if g.get("arc_a") is not None else ()):
+        out[k] = np.asarray(g[k])[arc_idx]
+    out["dst"] = newid[np.asarray(g["dst"], np.int64)[arc_idx]].astype(np.int32) if len(arc_idx) else np.zeros(0, np.int32)
+    out["pair_a"] = np.asarray(out["pair_a"])
+    fake = dict(out)
+    fake["pair_a"] = np.arange(V, dtype=np.int64)  # rows are now in key order
+    fake["pair_b"] = np.zeros(V, np.int64)
+    res = canonicalize_rows(fake, 1)
+    res["pair_a"], res["pair_b"] = out["pair_a"], out["pair_b"]
+    return res
+
+
 # ----------------------------------------------------------------------------- plain definition
 def n1_moves(A, B, ua, ub, prov: bool = False):
     """All moves of N1 from pair (ua, ub): M1 (incl. eps==eps), M2, M3 (SURVEY §8 move table).
@@ -138,6 +178,50 @@ def n1_moves(A, B, ua, ub, prov: bool = False):
             out.append(((ua, int(B.dst[eb])), EPS, int(B.olabel[eb]), np.float32(B.weight[eb]))
                        + (((-1, int(eb)),) if prov else ()))
     return out
+
+
+def filtered_moves(A, B, ua, ub, uf):
+    """Moves of the three-state eps filter from triple (ua, ub, uf): MATCH
+    (o_a == i_b != eps, any f -> 0), EPS-BOTH (o_a == i_b == eps, only f = 0 -> 0), EPS-A (o_a = eps,
+    f in {0,1} -> 1), EPS-B (i_b = eps, f in {0,2} -> 2)."""
+    out = []
+    for ea in range(A.row_ptr[ua], A.row_ptr[ua + 1]):
+        for eb in range(B.row_ptr[ub], B.row_ptr[ub + 1]):
+            if A.olabel[ea] != B.ilabel[eb] or (A.olabel[ea] == EPS and uf != 0):
+                continue
+            out.append(((int(A.dst[ea]), int(B.dst[eb]), 0), int(A.ilabel[ea]), int(B.olabel[eb]),
+                        f32add(A.weight[ea], B.weight[eb])))
+    if uf in (0, 1):
+        for ea in range(A.row_ptr[ua], A.row_ptr[ua + 1]):
+            if A.olabel[ea] == EPS:
+                out.append(((int(A.dst[ea]), ub, 1), int(A.ilabel[ea]), EPS, np.float32(A.weight[ea])))
+    if uf in (0, 2):
+        for eb in range(B.row_ptr[ub], B.row_ptr[ub + 1]):
+            if B.ilabel[eb] == EPS:
+                out.append(((ua, int(B.dst[eb]), 2), EPS, int(B.olabel[eb]), np.float32(B.weight[eb])))
+    return out
+
+
+def plain_trim_product_filtered(A, B):
+    """trim of the full eps-filtered product over V_A x V_B x 3 (tiny inputs only)."""
+    fwd = collections.defaultdict(list)
+    bwd = collections.defaultdict(list)
+    all_arcs = []
+    for ua in range(A.num_states):
+        for ub in range(B.num_states):
+            for uf in range(3):
+                for mv in filtered_moves(A, B, ua, ub, uf):
+                    all_arcs.append(((ua, ub, uf),) + tuple(mv))
+                    fwd[(ua, ub, uf)].append(mv[0])
+                    bwd[mv[0]].append((ua, ub, uf))
+    starts = [(int(a), int(b), 0) for a in np.flatnonzero(A.is_start) for b in np.flatnonzero(B.is_start)]
+    accepts = [(int(a), int(b), f) for a in np.flatnonzero(A.is_accept) for b in np.flatnonzero(B.is_accept)
+               for f in range(3)]
+    keep = _reach(fwd, starts) & _reach(bwd, accepts)
+    sset = set(starts)
+    states = {p: (int(p in sset), int(A.is_accept[p[0]] and B.is_accept[p[1]])) for p in keep}
+    arcs = [t for t in all_arcs if t[0] in keep and t[1] in keep]
+    return build_canonical(B.num_states, states, arcs, triples=True)
 
 
 def _reach(adj, seeds):
@@ -226,12 +310,14 @@ def _runs(labels):
     return tuple(seq), runs
 
 
-def eq1_bruteforce(A, B, max_len: int = 64):
+def eq1_bruteforce(A, B, max_len: int = 64, filtered: bool = False):
     """Expected multiset of composed accepting-path scores per (x, z) under N1.
 
     Each matched path pair (pi_a labelled (x, y), pi_b labelled (y, z)) contributes the score
     s_a + s_b (float64; exact for dyadic weights) with multiplicity prod_i D(k_i, m_i)
-    (Delannoy; = 1 for every pair when A has no eps outputs or B no eps inputs).
+    (Delannoy; = 1 for every pair when A has no eps outputs or B no eps inputs).  filtered: the
+    eps-filtered composition's target -- exactly ONE composed path per matched path pair (SPEC.md
+    "Path bijection"), i.e. Eq. (1) itself with no duplicated terms.
     """
     pa = collections.defaultdict(list)
     for p in accepting_paths(A, max_len):
@@ -245,8 +331,9 @@ def eq1_bruteforce(A, B, max_len: int = 64):
         sb = sum(float(B.weight[e]) for e in p)
         for x, ka, sa in pa.get(y, ()):
             mult = 1
-            for k, m in zip(ka, mb):
-                mult *= delannoy(k, m)
+            if not filtered:
+                for k, m in zip(ka, mb):
+                    mult *= delannoy(k, m)
             table[(x, z)][sa + sb] += mult
     return table
 

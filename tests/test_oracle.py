@@ -349,3 +349,121 @@ def test_forward_score_trellis_and_cycles():
     if C["num_states"]:
         with pytest.raises(ValueError):
             fw.forward(C)
+
+
+# ----------------------------------------------------------------------------- eps-filtered variant
+# the three-state eps filter.  Pins: hand-worked
+# fixtures, the path bijection of Eq. (1) with eps (one composed path per matched path pair, no
+# Delannoy inflation), the plain-definition trim of the filtered product, and reduction to the
+# unfiltered composition when there is no eps.
+@pytest.mark.parametrize("name", golden_io.FILTER_FIXTURES)
+def test_filtered_golden_fixture(name):
+    g = golden_io.load(name)
+    C = oracle.canonical(g["A"], g["B"], eps_filter=True)
+    pins.assert_canonical_equal(C, g["CF"], name)
+    assert pins.is_trim(C)
+
+
+@pytest.mark.parametrize("seed", range(100))
+def test_filtered_eq1_bijection_eps_dags(seed):
+    """eps DAGs: per (x, z) the multiset of composed path scores equals {s_a + s_b} over matched path
+    pairs with multiplicity ONE (Eq. (1), as a sum without duplicated terms)."""
+    eps = 0.2 if seed % 2 else 0.3
+    A = fstgen.random_dag(7, 3, 3, eps, 7919 * seed + 11)
+    B = fstgen.random_dag(7, 3, 3, eps, 7919 * seed + 13)
+    C = oracle.compose_filtered(A, B)
+    exp = pins.eq1_bruteforce(A, B, filtered=True)
+    got = pins.composed_path_table(C)
+    assert set(got) == set(exp)
+    for k in exp:
+        assert got[k] == exp[k], k
+    lg, le = pins.logsumexp_table(got), pins.logsumexp_table(exp)
+    for k in le:
+        assert abs(lg[k] - le[k]) <= 1e-12 * max(1.0, abs(le[k]))
+
+
+def test_filtered_bijection_differs_from_n1():
+    """The filter matters on these inputs: some matched pair has Delannoy multiplicity > 1 under N1
+    while the filtered composition has exactly one path for it."""
+    hit = 0
+    for seed in range(60):
+        A = fstgen.random_dag(7, 3, 3, 0.3, 7919 * seed + 11)
+        B = fstgen.random_dag(7, 3, 3, 0.3, 7919 * seed + 13)
+        n1 = pins.composed_path_table(oracle.compose(A, B))
+        fl = pins.composed_path_table(oracle.compose_filtered(A, B))
+        hit += sum(n1[k].total() > fl[k].total() for k in fl)
+    assert hit > 0
+
+
+@pytest.mark.parametrize("seed", range(40))
+def test_filtered_vs_plain_definition(seed):
+    """eps DAGs and cyclic eps transducers: the oracle's FIFO construction equals trim of the full
+    filtered product over V_A x V_B x 3."""
+    if seed % 2:
+        A = fstgen.random_dag(7, 3, 3, 0.3, 104729 * seed + 1)
+        B = fstgen.random_dag(7, 3, 3, 0.3, 104729 * seed + 2)
+    else:
+        A = fstgen.random_graph(9, 2, 3, 5000 + seed, acceptor=False, eps_prob=0.3)
+        B = fstgen.random_graph(9, 2, 3, 6000 + seed, acceptor=False, eps_prob=0.3)
+    got = oracle.canonical(A, B, eps_filter=True)
+    pins.assert_canonical_equal(got, pins.plain_trim_product_filtered(A, B), f"seed {seed}")
+    assert pins.is_trim(got)
+
+
+@pytest.mark.parametrize("seed", range(0, 1000, 50))
+def test_filtered_eps_free_reduces_to_unfiltered(seed):
+    """Without eps every move is MATCH: the filtered graph is the unfiltered one with f = 0."""
+    A, B = fstgen.config_c1(seed)
+    got = oracle.canonical(A, B, eps_filter=True)
+    exp = oracle.canonical(A, B)
+    assert np.all(got["pair_f"] == 0)
+    got = dict(got)
+    del got["pair_f"]
+    pins.assert_canonical_equal(got, exp, f"c1 seed {seed}")
+
+
+def test_filtered_c2_sizes():
+    """configs[1] (eps-1k): the filtered graph is trim, its pair set covers at most 3 copies of the
+    unfiltered pairs, and (a, b) projections are states of the unfiltered trim graph."""
+    A, B = fstgen.config_c2(1, V=200)
+    got = oracle.canonical(A, B, eps_filter=True)
+    unf = oracle.canonical(A, B)
+    assert pins.is_trim(got)
+    pairs = set(zip(unf["pair_a"].tolist(), unf["pair_b"].tolist()))
+    assert set(zip(got["pair_a"].tolist(), got["pair_b"].tolist())) <= pairs
+    assert got["num_states"] <= 3 * unf["num_states"]
+
+
+# ----------------------------------------------------------------------------- N-way (left fold)
+@pytest.mark.parametrize("seed", range(30))
+def test_chain_eq1_three_way_eps_free(seed):
+    """N-way composition as ((A o B) o D): per (x, w) the
+    multiset of path scores equals {s_a + s_b + s_d} over path triples matched on y and z
+    (Eq. (1) applied twice); eps-free inputs, exact dyadic sums."""
+    A = fstgen.random_dag(6, 3, 3, 0.0, 31 * seed + 1)
+    B = fstgen.random_dag(6, 3, 3, 0.0, 31 * seed + 2)
+    D = fstgen.random_dag(6, 3, 3, 0.0, 31 * seed + 3)
+    C = oracle.compose_chain([A, B, D])
+
+    def paths(g):
+        out = []
+        for p in pins.accepting_paths(g):
+            out.append((tuple(int(g.ilabel[e]) for e in p), tuple(int(g.olabel[e]) for e in p),
+                        sum(float(g.weight[e]) for e in p)))
+        return out
+
+    exp = collections.defaultdict(collections.Counter)
+    pb = collections.defaultdict(list)
+    for y, z, s in paths(B):
+        pb[y].append((z, s))
+    pd = collections.defaultdict(list)
+    for z, w, s in paths(D):
+        pd[z].append((w, s))
+    for x, y, sa in paths(A):
+        for z, sb in pb.get(y, ()):
+            for w, sd in pd.get(z, ()):
+                exp[(x, w)][sa + sb + sd] += 1
+    got = pins.composed_path_table(C)
+    assert set(got) == set(exp)
+    for k in exp:
+        assert got[k] == exp[k], k
