@@ -92,6 +92,7 @@ typedef struct {
   const int32_t* pair_b; /* [V] or NULL */
   const int32_t* arc_a;  /* [E] provenance (FST_COMPOSE_PROVENANCE), else NULL: see fst_compose_ex */
   const int32_t* arc_b;  /* [E] */
+  const int32_t* pair_f; /* [V] eps-filter state f of every state (FST_COMPOSE_EPS_FILTER), else NULL */
 } fst_view;
 
 /* Per-composition statistics (filled by fst_compose*; timings only when profiling is on). */
@@ -127,6 +128,7 @@ fst_status fst_compose_batch(int32_t n, const fst_handle* a, const fst_handle* b
 
 /* Option flags of fst_compose_ex / fst_compose_batch_ex. */
 #define FST_COMPOSE_PROVENANCE 1u /* also record, per composed arc, the arc pair that produced it */
+#define FST_COMPOSE_EPS_FILTER 2u /* three-state eps filter: no duplicated eps paths (see below) */
 
 /* fst_compose / fst_compose_batch with option flags.  FST_COMPOSE_PROVENANCE (
  * the autodiff use of the composed graph): every arc k of C also gets
@@ -134,9 +136,32 @@ fst_status fst_compose_batch(int32_t n, const fst_handle* a, const fst_handle* b
  * fst_desc passed to fst_create; for a composed A, its own arc order), or -1 for an M3 move
  * (A stays), and arc_b[k] = the B arc e_b, or -1 for an M2 move (B stays) -- Alg. 1 line 13's
  * arc pair.  +8 bytes per composed arc.  Unknown flag bits: FST_E_INVALID_ARG. */
+/* FST_COMPOSE_EPS_FILTER (R25): C is
+ * the trim product over TRIPLES (a, b, f), f in {0 MATCH, 1 A_EPS, 2 B_EPS}, with the moves
+ *     MATCH     e_a x e_b, olabel(e_a) == ilabel(e_b) != eps, from any f -> (dst e_a, dst e_b, 0)
+ *     EPS-BOTH  e_a x e_b, olabel(e_a) == ilabel(e_b) == eps, only from f = 0 -> (dst, dst, 0)
+ *     EPS-A     e_a with olabel eps, B stays, from f in {0, 1} -> (dst e_a, u_b, 1)
+ *     EPS-B     e_b with ilabel eps, A stays, from f in {0, 2} -> (u_a, dst e_b, 2)
+ * (labels and weights as M1 / M2 / M3 above); start triples (s_a, s_b, 0), accept triples
+ * (f_a, f_b, any f).  Every matched path pair of Eq. (1) then yields exactly ONE
+ * composed path, so log-semiring scores are exact with eps on both tapes.  pair_a / pair_b / pair_f
+ * (fst_info, fst_copy_pair_f_to_host) give every state's triple; state numbering is ascending
+ * (a, f, b).  Costs two passes of the binary kernels (A~ o F, then o B~; filter.cu) over a pair space
+ * of about 3 V_A x V_B.  Requires labels < 2^24 and E + V < 2^31 per input (FST_E_CAPACITY).
+ * Combines with FST_COMPOSE_PROVENANCE (arc_a / arc_b index the original A and B arcs). */
 fst_status fst_compose_ex(fst_handle a, fst_handle b, uint32_t flags, void* stream, fst_handle* c);
 fst_status fst_compose_batch_ex(int32_t n, const fst_handle* a, const fst_handle* b, uint32_t flags,
                                 void* stream, fst_handle* c);
+
+/* Copies pair_f [V] of a handle composed with FST_COMPOSE_EPS_FILTER into a HOST int32 buffer.
+ * FST_E_INVALID_ARG for any other handle.  Synchronous. */
+fst_status fst_copy_pair_f_to_host(fst_handle c, void* stream, int32_t* pair_f);
+
+/* N-way composition: *c = (((g[0] o g[1]) o g[2]) ... o g[n-1]),
+ * a left fold of trimmed compositions (each step filtered when flags has FST_COMPOSE_EPS_FILTER;
+ * FST_COMPOSE_PROVENANCE is not supported here: FST_E_INVALID_ARG).  n >= 2; intermediates are freed.
+ * The result's pair_a indexes the states of the previous fold step, pair_b the states of g[n-1]. */
+fst_status fst_compose_chain(int32_t n, const fst_handle* g, uint32_t flags, void* stream, fst_handle* c);
 
 /* Copies provenance arcs [first, first+count) of a composed handle into HOST int32 buffers (either
  * may be NULL).  FST_E_INVALID_ARG if the handle has no provenance or the range is out of bounds. */

@@ -134,13 +134,14 @@ def compose_filtered(A, B, canonicalize: bool = False):
 def compose_chain(graphs, canonicalize: bool = False):
     """N-way composition as the left fold ((G0 o G1) o G2) o ... (PAPER.md:366-368 names N-way
     composition as future work; Algorithm 1 applied N-1 times).  Returns the last composition (as
-    numpy dict); with canonicalize, states are keyed by the last fold's (pair_a, pair_b)."""
+    numpy dict); with canonicalize, EVERY step is canonicalised, so each intermediate's states are
+    numbered by ascending pair key and the result's pair_a indexes them in that order."""
     from types import SimpleNamespace
     cur = graphs[0]
     out = None
     for k, g in enumerate(graphs[1:]):
         last = k == len(graphs) - 2
-        out = compose(cur, g, canonicalize=canonicalize and last)
+        out = compose(cur, g, canonicalize=canonicalize)
         if not last:
             cur = SimpleNamespace(num_states=int(out["num_states"]), num_arcs=int(out["num_arcs"]),
                                   **{k: out[k] for k in ("row_ptr", "ilabel", "olabel", "dst", "weight",

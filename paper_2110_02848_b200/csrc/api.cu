@@ -48,6 +48,9 @@ fst_status grad_scatter_impl(fst* c, const float* grad_c, float* grad_a, int64_t
                              cudaStream_t s);
 fst_status compose_sharded_impl(fst* A, fst* B, int world, fst_comm* comm, cudaStream_t s, fst_handle* c);
 fst_status forward_score_impl(fst* h, cudaStream_t s, double* total, double* alpha_out);
+fst_status compose_filtered_impl(int32_t n, const fst_handle* a, const fst_handle* b, cudaStream_t s, fst_handle* c,
+                                 uint32_t flags);
+fst_status compose_chain_impl(int32_t n, const fst_handle* g, uint32_t flags, cudaStream_t s, fst_handle* out);
 
 fst_status device_ready() {
   int n = 0;
@@ -82,12 +85,13 @@ fst_status fst_compose_ex(fst_handle a, fst_handle b, uint32_t flags, void* stre
     set_error(FST_E_INVALID_ARG, "fst_compose: NULL argument");
     return FST_E_INVALID_ARG;
   }
-  if (flags & ~FST_COMPOSE_PROVENANCE) {
+  if (flags & ~(FST_COMPOSE_PROVENANCE | FST_COMPOSE_EPS_FILTER)) {
     set_error(FST_E_INVALID_ARG, "fst_compose_ex: unknown flag bits 0x%x", flags);
     return FST_E_INVALID_ARG;
   }
   fst_status st = device_ready();
   if (st) return st;
+  if (flags & FST_COMPOSE_EPS_FILTER) return compose_filtered_impl(1, &a, &b, (cudaStream_t)stream, c, flags);
   return compose_impl(1, &a, &b, (cudaStream_t)stream, c, flags);
 }
 
@@ -101,13 +105,19 @@ fst_status fst_compose_batch_ex(int32_t n, const fst_handle* a, const fst_handle
     set_error(FST_E_INVALID_ARG, "fst_compose_batch: bad arguments (n=%d)", n);
     return FST_E_INVALID_ARG;
   }
-  if (flags & ~FST_COMPOSE_PROVENANCE) {
+  if (flags & ~(FST_COMPOSE_PROVENANCE | FST_COMPOSE_EPS_FILTER)) {
     set_error(FST_E_INVALID_ARG, "fst_compose_batch_ex: unknown flag bits 0x%x", flags);
     return FST_E_INVALID_ARG;
   }
   if (n == 0) return FST_OK;
   fst_status st = device_ready();
   if (st) return st;
+  for (int i = 0; i < n; ++i)
+    if (!a[i] || !b[i]) {
+      set_error(FST_E_INVALID_ARG, "fst_compose_batch: NULL handle at %d", i);
+      return FST_E_INVALID_ARG;
+    }
+  if (flags & FST_COMPOSE_EPS_FILTER) return compose_filtered_impl(n, a, b, (cudaStream_t)stream, c, flags);
   return compose_impl(n, a, b, (cudaStream_t)stream, c, flags);
 }
 
@@ -128,6 +138,37 @@ fst_status fst_copy_provenance_to_host(fst_handle c, void* stream, int64_t first
   }
   FSTC_CUDA_TRY(cudaStreamSynchronize(s));
   return FST_OK;
+}
+
+fst_status fst_copy_pair_f_to_host(fst_handle c, void* stream, int32_t* pair_f) {
+  if (!c || !c->pair_f || (c->V > 0 && !pair_f)) {
+    set_error(FST_E_INVALID_ARG, "fst_copy_pair_f_to_host: not an eps-filtered composition or NULL buffer");
+    return FST_E_INVALID_ARG;
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  if (c->V > 0) FSTC_CUDA_TRY(cudaMemcpyAsync(pair_f, c->pair_f, 4 * (size_t)c->V, cudaMemcpyDeviceToHost, s));
+  FSTC_CUDA_TRY(cudaStreamSynchronize(s));
+  return FST_OK;
+}
+
+fst_status fst_compose_chain(int32_t n, const fst_handle* g, uint32_t flags, void* stream, fst_handle* c) {
+  if (!c || n < 2 || !g) {
+    set_error(FST_E_INVALID_ARG, "fst_compose_chain: need n >= 2 handles and an output");
+    return FST_E_INVALID_ARG;
+  }
+  *c = nullptr;
+  for (int i = 0; i < n; ++i)
+    if (!g[i]) {
+      set_error(FST_E_INVALID_ARG, "fst_compose_chain: NULL handle at %d", i);
+      return FST_E_INVALID_ARG;
+    }
+  if (flags & ~FST_COMPOSE_EPS_FILTER) {
+    set_error(FST_E_INVALID_ARG, "fst_compose_chain: unsupported flag bits 0x%x", flags);
+    return FST_E_INVALID_ARG;
+  }
+  fst_status st = device_ready();
+  if (st) return st;
+  return compose_chain_impl(n, g, flags, (cudaStream_t)stream, c);
 }
 
 fst_status fst_grad_scatter(fst_handle c, const float* grad_c, float* grad_a, int64_t n_a, float* grad_b,
@@ -167,6 +208,7 @@ fst_status fst_info(fst_handle h, fst_view* v) {
   v->pair_b = h->composed ? h->pair_b : nullptr;
   v->arc_a = h->arc_a;
   v->arc_b = h->arc_b;
+  v->pair_f = h->pair_f;
   return FST_OK;
 }
 

@@ -71,6 +71,8 @@ struct fst {
   int32_t* pair_b = nullptr;
   int32_t* arc_a = nullptr;  // provenance (composed with FST_COMPOSE_PROVENANCE)
   int32_t* arc_b = nullptr;
+  int32_t* pair_f = nullptr;  // eps-filter state of every state (FST_COMPOSE_EPS_FILTER), else nullptr
+  bool filtered = false;
   int64_t src_arcs_a = 0, src_arcs_b = 0;  // arc counts of the inputs (grad_a / grad_b lengths)
   // label-sorted views (built by fst_create, lazily for composed handles)
   bool has_views = false;

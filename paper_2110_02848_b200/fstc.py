@@ -30,8 +30,9 @@ EXPORTED = ["fst_create", "fst_compose", "fst_compose_batch", "fst_free", "fst_i
             "fst_last_error", "fst_version", "fst_comm_unique_id", "fst_comm_init", "fst_comm_destroy",
             "fst_compose_sharded", "fst_compose_sharded_local", "fst_shard_info", "fst_copy_arcs_to_host",
             "fst_compose_ex", "fst_compose_batch_ex", "fst_copy_provenance_to_host", "fst_grad_scatter",
-            "fst_forward_score"]
+            "fst_forward_score", "fst_copy_pair_f_to_host", "fst_compose_chain"]
 FST_COMPOSE_PROVENANCE = 1
+FST_COMPOSE_EPS_FILTER = 2
 
 
 class FstError(RuntimeError):
@@ -50,7 +51,7 @@ class fst_view(C.Structure):
     _fields_ = [("num_states", C.c_int32), ("num_arcs", C.c_int64), ("row_ptr", C.c_void_p),
                 ("ilabel", C.c_void_p), ("olabel", C.c_void_p), ("dst", C.c_void_p), ("weight", C.c_void_p),
                 ("is_start", C.c_void_p), ("is_accept", C.c_void_p), ("pair_a", C.c_void_p),
-                ("pair_b", C.c_void_p), ("arc_a", C.c_void_p), ("arc_b", C.c_void_p)]
+                ("pair_b", C.c_void_p), ("arc_a", C.c_void_p), ("arc_b", C.c_void_p), ("pair_f", C.c_void_p)]
 
 
 class fst_compose_stats(C.Structure):
@@ -101,6 +102,9 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
                                                  C.POINTER(vp)]
             lib.fst_copy_provenance_to_host.argtypes = [vp, vp, C.c_int64, C.c_int64, vp, vp]
             lib.fst_grad_scatter.argtypes = [vp, vp, vp, C.c_int64, vp, C.c_int64, vp]
+        if hasattr(lib, "fst_compose_chain"):
+            lib.fst_copy_pair_f_to_host.argtypes = [vp, vp, vp]
+            lib.fst_compose_chain.argtypes = [C.c_int32, C.POINTER(vp), C.c_uint32, vp, C.POINTER(vp)]
         if hasattr(lib, "fst_forward_score"):
             lib.fst_forward_score.argtypes = [vp, vp, C.POINTER(C.c_double), vp]
         lib.fst_level_sizes.argtypes = [vp, C.c_int32, vp, C.c_int32]
@@ -176,12 +180,18 @@ def fst_create(fst_like, stream=None) -> "Fst":
     return Fst(h)
 
 
-def fst_compose(a: "Fst", b: "Fst", stream=None, provenance: bool = False) -> "Fst":
-    """C = trim(A o B); provenance=True also records each arc's (arc_a, arc_b) (fst_compose_ex)."""
+def _flags(provenance: bool, eps_filter: bool) -> int:
+    return (FST_COMPOSE_PROVENANCE if provenance else 0) | (FST_COMPOSE_EPS_FILTER if eps_filter else 0)
+
+
+def fst_compose(a: "Fst", b: "Fst", stream=None, provenance: bool = False, eps_filter: bool = False) -> "Fst":
+    """C = trim(A o B); provenance=True also records each arc's (arc_a, arc_b); eps_filter=True runs
+    the three-state eps-filtered variant (states (pair_a, pair_b, pair_f)) (fst_compose_ex)."""
     lib = load_library()
     h = C.c_void_p()
-    if provenance:
-        _check(lib.fst_compose_ex(a.handle, b.handle, FST_COMPOSE_PROVENANCE, _stream_ptr(stream), C.byref(h)))
+    if provenance or eps_filter:
+        _check(lib.fst_compose_ex(a.handle, b.handle, _flags(provenance, eps_filter), _stream_ptr(stream),
+                                  C.byref(h)))
     else:
         _check(lib.fst_compose(a.handle, b.handle, _stream_ptr(stream), C.byref(h)))
     return Fst(h)
@@ -194,18 +204,29 @@ def fst_compose_ex(a: "Fst", b: "Fst", flags: int, stream=None) -> "Fst":
     return Fst(h)
 
 
-def fst_compose_batch(a: Sequence["Fst"], b: Sequence["Fst"], stream=None, provenance: bool = False) -> List["Fst"]:
+def fst_compose_batch(a: Sequence["Fst"], b: Sequence["Fst"], stream=None, provenance: bool = False,
+                      eps_filter: bool = False) -> List["Fst"]:
     lib = load_library()
     n = len(a)
     assert len(b) == n
     A = (C.c_void_p * n)(*[x.handle for x in a])
     B = (C.c_void_p * n)(*[x.handle for x in b])
     out = (C.c_void_p * n)()
-    if provenance:
-        _check(lib.fst_compose_batch_ex(n, A, B, FST_COMPOSE_PROVENANCE, _stream_ptr(stream), out))
+    if provenance or eps_filter:
+        _check(lib.fst_compose_batch_ex(n, A, B, _flags(provenance, eps_filter), _stream_ptr(stream), out))
     else:
         _check(lib.fst_compose_batch(n, A, B, _stream_ptr(stream), out))
     return [Fst(C.c_void_p(out[i])) for i in range(n)]
+
+
+def fst_compose_chain(graphs: Sequence["Fst"], stream=None, eps_filter: bool = False) -> "Fst":
+    """N-way composition: ((g0 o g1) o g2) o ... (left fold on the GPU, intermediates freed)."""
+    lib = load_library()
+    n = len(graphs)
+    G = (C.c_void_p * n)(*[x.handle for x in graphs])
+    h = C.c_void_p()
+    _check(lib.fst_compose_chain(n, G, _flags(False, eps_filter), _stream_ptr(stream), C.byref(h)))
+    return Fst(h)
 
 
 def fst_forward_score(h: "Fst", alpha=None, stream=None) -> float:
@@ -350,6 +371,15 @@ class Fst:
                                                ptr("is_accept"), ptr("pair_a"), ptr("pair_b")))
         if v.arc_a:
             out["arc_a"], out["arc_b"] = self.provenance(stream)
+        if v.pair_f:
+            out["pair_f"] = self.pair_f(stream)
+        return out
+
+    def pair_f(self, stream=None) -> np.ndarray:
+        """eps-filter state of every state (handles composed with eps_filter=True)."""
+        V = self.num_states
+        out = np.zeros(V, np.int32)
+        _check(load_library().fst_copy_pair_f_to_host(self.handle, _stream_ptr(stream), out.ctypes.data if V else None))
         return out
 
     def provenance(self, stream=None):
@@ -409,9 +439,9 @@ class Fst:
         return off, arcs[: int(v.num_arcs)]
 
 
-def compose(A, B, stream=None, provenance: bool = False) -> Dict[str, np.ndarray]:
+def compose(A, B, stream=None, provenance: bool = False, eps_filter: bool = False) -> Dict[str, np.ndarray]:
     """Convenience: host arrays in, composed graph (numpy, GPU numbering) out."""
     a = fst_create(A, stream)
     b = fst_create(B, stream)
-    c = fst_compose(a, b, stream, provenance=provenance)
+    c = fst_compose(a, b, stream, provenance=provenance, eps_filter=eps_filter)
     return c.to_host(stream)

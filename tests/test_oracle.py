@@ -467,3 +467,16 @@ def test_chain_eq1_three_way_eps_free(seed):
     assert set(got) == set(exp)
     for k in exp:
         assert got[k] == exp[k], k
+
+
+@pytest.mark.parametrize("seed", range(10))
+def test_canonicalize_any_comparator(seed):
+    """The GPU-side comparator (pins.canonicalize_any: any state numbering -> canonical) maps the
+    oracle's FIFO-numbered output onto the oracle's own canonical form (pairs and triples)."""
+    A = fstgen.random_graph(30, 3, 4, 300 + seed, acceptor=False, eps_prob=0.3)
+    B = fstgen.random_graph(30, 3, 4, 400 + seed, acceptor=False, eps_prob=0.3)
+    for filt in (False, True):
+        raw = oracle.compose(A, B, eps_filter=filt)
+        raw = {k: v for k, v in raw.items() if k not in ("arc_a", "arc_b")}
+        exp = {k: v for k, v in oracle.canonical(A, B, eps_filter=filt).items() if k not in ("arc_a", "arc_b")}
+        pins.assert_canonical_equal(pins.canonicalize_any(raw, B.num_states), exp, f"seed {seed} filter {filt}")
