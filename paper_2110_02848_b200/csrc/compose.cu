@@ -879,6 +879,11 @@ __device__ __forceinline__ void bfs_chunk_fast(TaskSmem& s, const ViewDev& Bv, i
   const int lane = threadIdx.x & 31;
   const int nw = (cub1 - cub0 + 31) >> 5;
   constexpr int kSegWords = 8;  // 256-pair segments, handed out dynamically (load balance)
+  // stage 2: per-warp kept-move counters of the batch's 32 states, indexed by owner lane (the
+  // compacted-state scratch s.state is unused on this path)
+  int32_t* cntw = s.state + (threadIdx.x >> 5) * 32;
+  if (kStage2) cntw[lane] = 0;
+  __syncwarp();
   for (;;) {
     int seg = 0;
     if (lane == 0) seg = atomicAdd(&s.segnext, 1);
@@ -964,6 +969,7 @@ __device__ __forceinline__ void bfs_chunk_fast(TaskSmem& s, const ViewDev& Bv, i
       for (int rr = 0; rr < total; rr += 32) {
         const int c = rr + lane;
         const int32_t ej = en, uj = un;
+        const int jc = jn;  // owner lane of this round's item
         const int2 xc = xn;
         if (rr + 32 < total) {  // prefetch the next round's item
           const int cn = c + 32;
@@ -974,18 +980,15 @@ __device__ __forceinline__ void bfs_chunk_fast(TaskSmem& s, const ViewDev& Bv, i
         }
         const unsigned k0 = kept;
         if (c < total) fast_arc<kM32>(s, xc, ej - uj - 1, cand);
-        if (kStage2) {  // attribute this round's kept moves to their states (owner lanes)
-          const int kc = (int)(kept - k0);
-          const int sc = warp_incl_scan(kc);
-          const int lo = max(start - rr, 0), hi = min(incl - rr, 32) - 1;
-          const int shi = __shfl_sync(0xffffffffu, sc, max(hi, 0));
-          const int slo = __shfl_sync(0xffffffffu, sc, max(lo - 1, 0));
-          if (hi >= lo) own_cnt += shi - (lo > 0 ? slo : 0);
-        }
+        if (kStage2 && kept != k0) atomicAdd(&cntw[jc], (int)(kept - k0));  // credit the owner state
       }
       segkept += kept;
       __syncwarp();
-      if (kStage2 && k < stot) cnt8row[ub] = (uint8_t)(heavy_own ? 255 : min(own_cnt, 255));
+      if (kStage2) {
+        if (k < stot) cnt8row[ub] = (uint8_t)(heavy_own ? 255 : min(own_cnt + cntw[lane], 255));
+        cntw[lane] = 0;
+        __syncwarp();
+      }
     }
     if (kStage2) {  // the segment lies inside one 1024-pair block
       const unsigned long long t = warp_sum(segkept);
