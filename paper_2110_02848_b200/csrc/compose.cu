@@ -856,9 +856,13 @@ __device__ __forceinline__ void bfs_chunk_fast(TaskSmem& s, const ViewDev& Bv, i
     if (kStaged) {
       const int idx = slot * wpr + (col >> 5);
       const uint32_t bit = 1u << (col & 31);
-      if (kStage2) {
-        if (!(Rs[idx] & bit)) return;
+      if (kStage2) {  // (R word, NEW word) pairs: one 64-bit shared load per candidate
+        const uint2 rn = reinterpret_cast<const uint2*>(Rs)[idx];
+        if (!(rn.x & bit)) return;
         ++kept;
+        if (rn.y & bit) return;  // NEW starts as the visited snapshot
+        atomicOr(&NW[2 * idx], bit);
+        return;
       }
       if (NW[idx] & bit) return;  // NW starts as the visited snapshot
       atomicOr(&NW[idx], bit);
@@ -1090,9 +1094,12 @@ __global__ void __launch_bounds__(kThreads, 2) k_level(Ctx cx, int level) {
     stage_arow(s, C, Av, ch.ua, per_word * wpr, (kDynSmem - kOwnerBytes) / 4);
     // stage destination rows only when the chunk has enough work to amortise the staging traffic
     const bool staged = s.dst_staged && (int64_t)nst * 16 >= (int64_t)s.m * wpr;
+    // stage 2: (R, NEW) word pairs interleaved, then the V snapshot; stage 1: R snapshot, then NEW.
+    // NEW word of pair-word i: NW[kNS * i].
+    constexpr int kNS = kStage2 ? 2 : 1;
     uint32_t* Rs = dyn;
-    uint32_t* VS = kStage2 ? dyn + s.m * wpr : dyn;
-    uint32_t* NW = VS + s.m * wpr;
+    uint32_t* VS = kStage2 ? dyn + 2 * s.m * wpr : dyn;
+    uint32_t* NW = kStage2 ? dyn + 1 : VS + s.m * wpr;
     if (staged) {
       const int n = s.m * wpr;
       for (int i0 = threadIdx.x; i0 < n; i0 += 4 * kThreads) {  // 4 independent loads in flight per thread
@@ -1112,9 +1119,9 @@ __global__ void __launch_bounds__(kThreads, 2) k_level(Ctx cx, int level) {
         for (int u = 0; u < 4; ++u) {
           const int i = i0 + u * kThreads;
           if (i < n) {
-            if (kStage2) Rs[i] = rv[u];
+            if (kStage2) Rs[2 * i] = rv[u];
             VS[i] = v[u];
-            NW[i] = v[u];  // claims accumulate on top of the snapshot
+            NW[kNS * i] = v[u];  // claims accumulate on top of the snapshot
           }
         }
       }
@@ -1127,11 +1134,11 @@ __global__ void __launch_bounds__(kThreads, 2) k_level(Ctx cx, int level) {
       if (staged) {
         const int i = c.slot * wpr + (c.col >> 5);
         if (kStage2) {
-          if (!(Rs[i] & bit)) return;
+          if (!(Rs[2 * i] & bit)) return;
           ++kept;
         }
-        if ((VS[i] | NW[i]) & bit) return;
-        atomicOr(&NW[i], bit);
+        if (NW[kNS * i] & bit) return;  // NEW starts as the visited snapshot
+        atomicOr(&NW[kNS * i], bit);
       } else {
         const int64_t gw = C.W + (int64_t)c.row * wpr + (c.col >> 5);
         if (kStage2) {
@@ -1241,7 +1248,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_level(Ctx cx, int level) {
       __syncthreads();
       const int m = s.m;
       for (int i = threadIdx.x; i < m * wpr; i += kThreads) {
-        const uint32_t nb = NW[i] & ~VS[i];
+        const uint32_t nb = NW[kNS * i] & ~VS[i];
         if (!nb) continue;
         const int r = i / wpr, w = i - r * wpr;
         const int32_t row = s.slot_row[r];
