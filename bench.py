@@ -232,8 +232,9 @@ def run_ours(args):
 
     def compose_all():
         if len(ha) == 1:
-            return [fstc.fst_compose(ha[0], hb, stream, provenance=args.provenance)]
-        return fstc.fst_compose_batch(ha, [hb] * len(ha), stream, provenance=args.provenance)
+            return [fstc.fst_compose(ha[0], hb, stream, provenance=args.provenance, eps_filter=args.eps_filter)]
+        return fstc.fst_compose_batch(ha, [hb] * len(ha), stream, provenance=args.provenance,
+                                      eps_filter=args.eps_filter)
 
     def step():
         with torch.cuda.stream(stream):
@@ -333,6 +334,8 @@ def run_ours(args):
                    "E_A": sum(A.num_arcs for A in As), "E_B": B.num_arcs, "pair_space": P, "V_C": V_C, "E_C": E_C,
                    "coaccessible": R, "levels": [stats[-1]["levels_stage1"], stats[-1]["levels_stage2"]],
                    "parallelism": parallelism, "provenance": bool(args.provenance),
+                   **({"eps_filter": "three-state eps filter (A~ o F, then o B~); phases_ms / roofline are "
+                                     "the second pass's, ms_per_step covers both"} if args.eps_filter else {}),
                    "l2": "flushed before every step (512 MiB write), outside the timed events; the working set "
                          "(pair-space bitmaps + composed graph) exceeds L2"},
         "phases_ms": {"stage1_backward_bfs": s1, "stage2_forward_bfs": s2, "numbering": num, "emit": emit_ms},
@@ -500,6 +503,8 @@ def main():
                     help="also time fst_forward_score over the composed graphs (c5: lexicon o emissions DAGs)")
     ap.add_argument("--provenance", action="store_true",
                     help="compose with FST_COMPOSE_PROVENANCE (also writes arc_a/arc_b per arc; not the headline)")
+    ap.add_argument("--eps-filter", action="store_true",
+                    help="compose with FST_COMPOSE_EPS_FILTER (the eps-filtered variant; not the headline)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":

@@ -10,6 +10,8 @@ ncu --set full --clock-control none --import-source on -k regex:"k_emit" -c 1 -o
     python scripts/prof_compose.py --V 20000 --D 8 --n 0 > gpurun_out/$R/ncu_emit.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:"k_level" -s 14 -c 1 -o gpurun_out/$R/level14_c4_20k \
     python scripts/prof_compose.py --V 20000 --D 8 --n 0 > gpurun_out/$R/ncu_level.log 2>&1
+ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k regex:"k_level<\(bool\)1>" -s 13 -c 1 \
+    -o gpurun_out/$R/level2_c4_20k python scripts/prof_compose.py --V 20000 --D 8 --n 0 > gpurun_out/$R/ncu_level2.log 2>&1
 ls -la gpurun_out/$R
 # c5 (batched lexicon): launch list only
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/$R/launches_c5.csv \

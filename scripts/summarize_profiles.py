@@ -71,7 +71,8 @@ def main(rnd="r01", workload="c4"):
             lines.append(f"| {k} | {n} | {ms:.3f} | {100 * ms / tot:.1f}% |")
         lines.append("")
     traffic = {}
-    for name, label in (("emit_c4_20k", "k_emit"), ("level14_c4_20k", "k_level (stage 1, level 14 = peak)")):
+    for name, label in (("emit_c4_20k", "k_emit"), ("level14_c4_20k", "k_level (stage 1, level 14 = peak)"),
+                        ("level2_c4_20k", "k_level (stage 2, 14th launch = peak)")):
         rep = os.path.join(src, name + ".ncu-rep")
         if not os.path.exists(rep):
             continue
