@@ -256,3 +256,20 @@ def test_compose_of_composed(fst):
                       C1["is_start"], C1["is_accept"])
     got = pins.canonicalize_rows(c2, 1)
     pins.assert_canonical_equal(got, oracle.canonical(Cfst, fstgen.identity_fst(labels)), "(A o B) o Id")
+
+
+@pytest.mark.parametrize("T", [40, 150, 400])
+def test_deep_bfs_level_profile(fst, T):
+    """Lexicon o emissions is a trellis: one BFS level per frame, so T = 150 / 400 run most levels in the
+    graph-driven level loop (levels >= 64).  Per-level frontier sizes of stage 2 equal the oracle's
+    FIFO discovery levels (Alg. 1, PAPER.md:207-213 round profile); stage 1 sizes sum to |R|; the graph
+    itself equals the oracle's."""
+    A, B = fstgen.config_c3(num_words=300, T=T)
+    a, b = fst.fst_create(A), fst.fst_create(B)
+    c = fst.fst_compose(a, b)
+    exp = oracle.compose(A, B)
+    lv = np.bincount(exp["level"]) if exp["num_states"] else np.zeros(0, np.int64)
+    assert c.level_sizes(2) == [int(x) for x in lv]
+    assert sum(c.level_sizes(1)) == int(oracle.coaccessible(A, B).sum())
+    assert len(c.level_sizes(2)) > (64 if T > 64 else 0)
+    pins.assert_canonical_equal(pins.canonicalize_rows(c.to_host(), B.num_states), oracle.canonical(A, B), f"c3 T={T}")
