@@ -48,7 +48,8 @@ constexpr int kChunkMaxBlocks = 32; // blocks per chunk (<= 1024 words)
 constexpr int kDynSmem = 88 * 1024; // staging area (destination rows)
 constexpr int kSimpleMoves = 4;    // warps whose items have <= this many moves skip the expansion
 constexpr int kHeavy = 64;         // states with more B arcs are walked cooperatively by the CTA
-constexpr int kWCap = 160;         // per-warp output window of the fast emit (arcs)
+constexpr int kWCap = 160;         // per-warp output window of the fast emit (arcs), at most
+constexpr int kWCapMin = 64;       // ... and at least (smaller when the staged rows take the space)
 constexpr int kOwnerCap = 384;     // per-warp arc-slot owner table of the BFS walk (end of dynamic smem)
 constexpr int kOwnerBytes = kWarps * kOwnerCap;
 
@@ -75,6 +76,7 @@ struct Ctx {
   const int64_t* seedbase;
   int32_t ncomp;
   int64_t nwords, nblocks, nchunks;
+  int32_t* level_dev;  // graph-driven level loop: the true level number (hist index), advanced by block 0
 };
 
 struct Chunk {
@@ -650,11 +652,11 @@ __device__ __forceinline__ void fast_state4(const TaskSmem& s, const int4* __res
 }
 
 // Fast emit of one dense block (staged rows, label masks, no heavy state): per-thread state walks,
-// block scan of per-state counts, then per-warp windows of kWCap slots staged in shared memory and
+// block scan of per-state counts, then per-warp windows of wcap slots staged in shared memory and
 // stored coalesced.  Returns the block's arc count.
 template <bool kM32, bool kProv, typename Rank, typename StateOut>
 __device__ __forceinline__ int emit_block_fast(TaskSmem& s, const ViewDev& Bv, const CompDev& C, int32_t ub0,
-                                               int32_t ub1, int lw0, int wpr, const int2* VR, int4* wb4,
+                                               int32_t ub1, int lw0, int wpr, const int2* VR, int4* wb4, int wcap,
                                                const uint8_t* __restrict__ cnt8row, int64_t run, Rank&& rank_of,
                                                StateOut&& state_out) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -744,8 +746,8 @@ __device__ __forceinline__ int emit_block_fast(TaskSmem& s, const ViewDev& Bv, c
     if (has) state_out(ub, run + my0);
     const int32_t e = has ? __ldg(&boff[ub]) + ub + 1 : 0, e1 = has ? __ldg(&boff[ub + 1]) + ub + 1 : 0;
     const bool walk = has && e1 - e <= kHeavy;  // heavy states are written by the whole CTA below
-    for (int win = q0; win < q1; win += kWCap) {
-      const bool mine = walk && my1 > win && my0 < win + kWCap;
+    for (int win = q0; win < q1; win += wcap) {
+      const bool mine = walk && my1 > win && my0 < win + wcap;
       if (!__any_sync(0xffffffffu, mine)) continue;  // window entirely inside a heavy state's range
       if (mine) {
         int p = my0;
@@ -756,7 +758,7 @@ __device__ __forceinline__ int emit_block_fast(TaskSmem& s, const ViewDev& Bv, c
           if (!pr) return;
           const int t = p - win;
           ++p;
-          if ((unsigned)t >= (unsigned)kWCap) return;
+          if ((unsigned)t >= (unsigned)wcap) return;
           int32_t il, ol;
           float wt;
           fill(kind, a, carry, wbits, il, ol, wt);
@@ -765,7 +767,7 @@ __device__ __forceinline__ int emit_block_fast(TaskSmem& s, const ViewDev& Bv, c
         });
       }
       __syncwarp();
-      const int n = min(kWCap, q1 - win);
+      const int n = min(wcap, q1 - win);
       for (int t = lane; t < n; t += 32) {  // slots of heavy states get overwritten below
         const int64_t pos = run + win + t;
         const int4 v = wb4[t];
@@ -1065,9 +1067,14 @@ __global__ void __launch_bounds__(kThreads, 2) k_level(Ctx cx, int level) {
     LevelCtrl* z = &cx.ctrl[(level + 2) % 3];
     z->count = 0;
     z->nnew = 0;
+    int hl = level;  // graph-driven loop: `level` is only right modulo 6 (ring phase); the true level
+    if (cx.level_dev) {  // number lives in device memory and is advanced here
+      hl = *cx.level_dev;
+      *cx.level_dev = hl + 1;
+    }
     if (nlist) {
       cx.misc[0] += 1;
-      if (level < kMaxLevelStats) cx.hist[level] = ctrl_cur->nnew;
+      if (hl < kMaxLevelStats) cx.hist[hl] = ctrl_cur->nnew;
     }
   }
   unsigned nnew = 0;
@@ -1445,7 +1452,10 @@ __global__ void __launch_bounds__(kThreads, 2) k_emit(Ctx cx, const int64_t* __r
         __stcs(&xb[pos], c.kind != 2 ? __ldg(&Bv.arc[c.eb]) : -1);
       }
     };
-    const bool fastE = staged && s.small && (((2 * s.m * wpr + 3) & ~3) + kWarps * kWCap * 4) * 4 <= kDynSmem;
+    // output window per warp: what the staged (V word, rank) rows leave of the dynamic shared memory
+    const int vr_words = (2 * s.m * wpr + 3) & ~3;
+    const int wcap = min(kWCap, ((kDynSmem / 4 - vr_words) / (kWarps * 4)) & ~31);
+    const bool fastE = staged && s.small && wcap >= kWCapMin;
     if (!fastE) {
       build_groups(s, Bv);
       __syncthreads();
@@ -1458,7 +1468,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_emit(Ctx cx, const int64_t* __r
       const int32_t ub0 = blk * kPairsPerBlock, ub1 = min(ub0 + kPairsPerBlock, C.VB);
       const int lw0 = (blk - ch.b0) * 32;
       if (fastE) {
-        int4* wb = (int4*)(dyn + ((2 * s.m * wpr + 3) & ~3)) + warp * kWCap;
+        int4* wb = (int4*)(dyn + vr_words) + warp * wcap;
         auto rk = [&](int slot, int32_t col, bool& pr) -> int32_t { return rank_of(slot, 0, col, pr); };
         auto so = [&](int32_t ub, int64_t at) {
           bool pr;
@@ -1471,10 +1481,10 @@ __global__ void __launch_bounds__(kThreads, 2) k_emit(Ctx cx, const int64_t* __r
         };
         const uint8_t* cnt8row = cx.cnt8 + ch.rowW * 32;
         const int btot =
-            C.arc_a ? (s.mask32 ? emit_block_fast<true, true>(s, Bv, C, ub0, ub1, lw0, wpr, VR, wb, cnt8row, run, rk, so)
-                                : emit_block_fast<false, true>(s, Bv, C, ub0, ub1, lw0, wpr, VR, wb, cnt8row, run, rk, so))
-                    : (s.mask32 ? emit_block_fast<true, false>(s, Bv, C, ub0, ub1, lw0, wpr, VR, wb, cnt8row, run, rk, so)
-                                : emit_block_fast<false, false>(s, Bv, C, ub0, ub1, lw0, wpr, VR, wb, cnt8row, run, rk, so));
+            C.arc_a ? (s.mask32 ? emit_block_fast<true, true>(s, Bv, C, ub0, ub1, lw0, wpr, VR, wb, wcap, cnt8row, run, rk, so)
+                                : emit_block_fast<false, true>(s, Bv, C, ub0, ub1, lw0, wpr, VR, wb, wcap, cnt8row, run, rk, so))
+                    : (s.mask32 ? emit_block_fast<true, false>(s, Bv, C, ub0, ub1, lw0, wpr, VR, wb, wcap, cnt8row, run, rk, so)
+                                : emit_block_fast<false, false>(s, Bv, C, ub0, ub1, lw0, wpr, VR, wb, wcap, cnt8row, run, rk, so));
         if (threadIdx.x == 0 && (unsigned long long)btot != cx.kept[gblk]) atomicAdd(&cx.misc[2], 1ull);
         run += btot;
         __syncthreads();
@@ -1702,7 +1712,88 @@ struct EventTimer {
   }
 };
 
-// Runs one BFS stage (level loop); fills the per-level frontier sizes.
+// Body tail of the graph-driven level loop: advance the device level counter and keep looping
+// while the next level has active chunks (CUDA graph while-node, set from the device).
+__global__ void k_level_advance(Ctx cx, const int32_t* level_dev, cudaGraphConditionalHandle h) {
+  const int32_t l = *level_dev;  // the next level to run
+  const bool more = *((volatile unsigned long long*)&cx.ctrl[l % 3].count) != 0ull;
+  cudaGraphSetConditional(h, more ? 1u : 0u);
+}
+
+int32_t* level_scratch() {
+  static thread_local int32_t* p = nullptr;
+  if (!p && cudaMalloc(&p, 256) != cudaSuccess) p = nullptr;
+  return p;
+}
+
+cudaStream_t capture_stream() {
+  static thread_local cudaStream_t cs = nullptr;
+  if (!cs && cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking) != cudaSuccess) cs = nullptr;
+  return cs;
+}
+
+// Levels [level, ...) of a deep BFS in ONE graph launch: a while-node whose body is 6 k_level
+// launches (one period of the frontier / control-block rings: the captured level arguments are
+// right modulo 6) + the advance kernel that tests the next level's list, so there is no host round
+// trip per level batch (lexicon trellises run hundreds of levels).  Up to 5 trailing levels are
+// no-op launches, as in the host loop's speculative batches.
+template <bool kStage2>
+fst_status run_levels_graph(const Ctx& cx, cudaStream_t s, int* level, int64_t* level_launches) {
+  int32_t* d_level = level_scratch();
+  cudaStream_t cs = capture_stream();
+  if (!d_level || !cs) {
+    set_error(FST_E_CUDA, "level loop: scratch allocation failed");
+    return FST_E_CUDA;
+  }
+  const int32_t l0 = *level;
+  FSTC_CUDA_TRY(cudaMemcpyAsync(d_level, &l0, sizeof(int32_t), cudaMemcpyHostToDevice, s));
+  cudaGraph_t g = nullptr;
+  cudaGraphExec_t ge = nullptr;
+  FSTC_CUDA_TRY(cudaGraphCreate(&g, 0));
+  cudaGraphConditionalHandle h;
+  cudaGraphNodeParams cp = {};
+  cudaGraphNode_t node;
+  cudaGraph_t body;
+  cudaError_t e = cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault);
+  if (e == cudaSuccess) {
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = h;
+    cp.conditional.type = cudaGraphCondTypeWhile;
+    cp.conditional.size = 1;
+    e = cudaGraphAddNode(&node, g, nullptr, 0, &cp);
+  }
+  if (e == cudaSuccess) {
+    body = cp.conditional.phGraph_out[0];
+    e = cudaStreamBeginCaptureToGraph(cs, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed);
+    if (e == cudaSuccess) {
+      Ctx cg = cx;
+      cg.level_dev = d_level;
+      for (int j = 0; j < 6; ++j) k_level<kStage2><<<g_grid, kThreads, kDynSmem, cs>>>(cg, l0 + j);
+      k_level_advance<<<1, 1, 0, cs>>>(cx, d_level, h);
+      e = cudaStreamEndCapture(cs, &body);
+    }
+  }
+  if (e == cudaSuccess) e = cudaGraphInstantiate(&ge, g, 0);
+  if (e == cudaSuccess) e = cudaGraphLaunch(ge, s);
+  int32_t lend = l0;
+  if (e == cudaSuccess) e = cudaMemcpyAsync(&lend, d_level, sizeof(int32_t), cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (ge) cudaGraphExecDestroy(ge);
+  cudaGraphDestroy(g);
+  if (e != cudaSuccess) {
+    set_error(FST_E_CUDA, "graph level loop: %s", cudaGetErrorString(e));
+    return FST_E_CUDA;
+  }
+  count_launch((int64_t)(lend - l0) * 7 / 6);
+  *level_launches += lend - l0;
+  *level = lend;
+  return FST_OK;
+}
+
+// Runs one BFS stage (level loop); fills the per-level frontier sizes.  The first levels run as
+// host-driven speculative batches; a BFS still going after kHostLevels levels continues in one
+// graph launch (run_levels_graph).
+constexpr int kHostLevels = 64;
 template <bool kStage2>
 fst_status run_stage(const Ctx& cx, cudaStream_t s, unsigned long long* h_pinned, int64_t* level_launches,
                      std::vector<int64_t>* sizes) {
@@ -1718,7 +1809,12 @@ fst_status run_stage(const Ctx& cx, cudaStream_t s, unsigned long long* h_pinned
                                   cudaMemcpyDeviceToHost, s));
     FSTC_CUDA_TRY(cudaStreamSynchronize(s));
     if (*h_pinned == 0) break;
-    batch = std::min(batch * 2, 8);  // speculative level batches: empty levels are no-op launches
+    if (level >= kHostLevels) {  // deep BFS: the rest in one graph launch
+      fst_status st = run_levels_graph<kStage2>(cx, s, &level, level_launches);
+      if (st) return st;
+      break;
+    }
+    batch = std::min(batch * 2, 32);  // speculative level batches: empty levels are no-op launches
   }
   FSTC_CUDA_TRY(cudaMemcpyAsync(h_pinned, cx.misc, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
   FSTC_CUDA_TRY(cudaStreamSynchronize(s));
@@ -1832,7 +1928,7 @@ fst_status compose_impl(int32_t n, const fst_handle* a, const fst_handle* b, cud
     return st == FST_E_OOM ? FST_E_CAPACITY : st;
   }
   char* base = (char*)wb->ptr;
-  Ctx cx;
+  Ctx cx{};
   cx.R = (uint32_t*)(base + oR);
   cx.V = (uint32_t*)(base + oV);
   cx.F0 = (uint32_t*)(base + oF0);

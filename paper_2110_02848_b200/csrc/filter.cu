@@ -24,6 +24,9 @@
 // every (a, f) on an accepted triple path (F is all-final), so trim(C1 o B~) = the trim filtered
 // product; state (c1, b) maps to the triple (C1.pair_a[c1], b, C1.pair_b[c1]).
 //
+// Shortcut: when no A arc has an eps output and no B arc an eps input, every move is MATCH and the
+// filtered graph is the plain composition with f = 0 (one pass, no marked copies).
+//
 // N-way ("N-way composition instead of just two inputs"): a left fold
 // ((G0 o G1) o G2) o ... of full trimmed compositions; intermediates are freed as the fold goes.
 #include <stdio.h>
@@ -110,6 +113,13 @@ __global__ void k_filter_prov(int64_t E, int32_t* __restrict__ arc_a, int32_t* _
   }
 }
 
+__global__ void k_any_eps(const int32_t* __restrict__ lab, int64_t E, int32_t* __restrict__ flag) {
+  bool hit = false;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < E; e += (int64_t)gridDim.x * blockDim.x)
+    hit |= lab[e] == FST_EPS;
+  if (__any_sync(0xffffffffu, hit) && (threadIdx.x & 31) == 0) *flag = 1;
+}
+
 struct Marked {
   fst_handle h = nullptr;
   BufferPtr map;  // [E+V] marked arc -> input arc (-1 = self-loop)
@@ -189,17 +199,85 @@ fst_status make_filter(int32_t L, cudaStream_t s, fst_handle* out) {
 
 }  // namespace
 
+// Does any arc of a side carry eps on the matched tape (A: olabel, B: ilabel)?  Without eps there
+// the filter never leaves MATCH and the filtered graph is the plain one with f = 0.
+fst_status matched_tape_has_eps(const fst* g, bool a_side, cudaStream_t s, bool* out) {
+  *out = false;
+  if (g->E == 0) return FST_OK;
+  BufferPtr fb;
+  fst_status st = alloc_buffer(256, s, &fb);
+  if (st) return st;
+  int32_t* flag = (int32_t*)fb->ptr;
+  FSTC_CUDA_TRY(cudaMemsetAsync(flag, 0, 4, s));
+  k_any_eps<<<std::min(nblk(g->E, 256), 1184u), 256, 0, s>>>(a_side ? g->olabel : g->ilabel, g->E, flag);
+  FSTC_LAUNCH_CHECK();
+  int32_t h = 0;
+  FSTC_CUDA_TRY(cudaMemcpyAsync(&h, flag, 4, cudaMemcpyDeviceToHost, s));
+  FSTC_CUDA_TRY(cudaStreamSynchronize(s));
+  *out = h != 0;
+  return FST_OK;
+}
+
 fst_status compose_filtered_impl(int32_t n, const fst_handle* a, const fst_handle* b, cudaStream_t s, fst_handle* c,
                                  uint32_t flags) {
   const bool want_prov = flags & FST_COMPOSE_PROVENANCE;
   for (int i = 0; i < n; ++i) c[i] = nullptr;
-  std::vector<Marked> am(n), bm(n);
+  {  // eps-free matched tapes everywhere: one plain pass, f = 0 for every state
+    std::map<std::pair<const fst*, bool>, bool> seen;
+    bool any = false;
+    for (int i = 0; i < n && !any; ++i) {
+      for (int side = 0; side < 2 && !any; ++side) {
+        const fst* g = side == 0 ? a[i] : b[i];
+        auto key = std::make_pair(g, side == 0);
+        auto it = seen.find(key);
+        bool has;
+        if (it != seen.end()) {
+          has = it->second;
+        } else {
+          fst_status st = matched_tape_has_eps(g, side == 0, s, &has);
+          if (st) return st;
+          seen[key] = has;
+        }
+        any |= has;
+      }
+    }
+    if (!any) {
+      fst_status st = compose_impl(n, a, b, s, c, flags & FST_COMPOSE_PROVENANCE);
+      if (st) return st;
+      for (int i = 0; i < n && !st; ++i) {
+        fst* h = c[i];
+        BufferPtr pf;
+        st = alloc_buffer((size_t)std::max<int32_t>(h->V, 1) * 4, s, &pf);
+        if (st) break;
+        h->pair_f = (int32_t*)pf->ptr;
+        h->buffers.push_back(pf);
+        h->filtered = true;
+        if (h->V > 0 && cudaMemsetAsync(h->pair_f, 0, 4 * (size_t)h->V, s) != cudaSuccess) {
+          set_error(FST_E_CUDA, "eps filter: memset failed");
+          st = FST_E_CUDA;
+        }
+      }
+      if (!st && cudaStreamSynchronize(s) != cudaSuccess) {
+        set_error(FST_E_CUDA, "eps filter: synchronize failed");
+        st = FST_E_CUDA;
+      }
+      if (st)
+        for (int i = 0; i < n; ++i) {
+          fst_free(c[i]);
+          c[i] = nullptr;
+        }
+      return st;
+    }
+  }
+  // marked copies are built once per distinct input handle (a batch usually repeats its B)
+  std::map<std::pair<const fst*, int32_t>, Marked> amk, bmk;
+  std::vector<Marked*> am(n), bm(n);
   std::map<int32_t, fst_handle> filters;
   std::vector<fst_handle> fa(n), c1(n, nullptr), am_h(n), bm_h(n);
   fst_status st = FST_OK;
   auto cleanup = [&]() {
-    for (auto& m : am) fst_free(m.h);
-    for (auto& m : bm) fst_free(m.h);
+    for (auto& kv : amk) fst_free(kv.second.h);
+    for (auto& kv : bmk) fst_free(kv.second.h);
     for (auto& kv : filters) fst_free(kv.second);
     for (auto h : c1) fst_free(h);
   };
@@ -214,17 +292,20 @@ fst_status compose_filtered_impl(int32_t n, const fst_handle* a, const fst_handl
       break;
     }
     const int32_t E1 = (int32_t)L, E2 = (int32_t)L + 1;
-    st = make_marked(a[i], 0, E2, E1, s, &am[i]);
-    if (!st) st = make_marked(b[i], 1, E1, E2, s, &bm[i]);
+    const auto ka = std::make_pair((const fst*)a[i], E1), kb = std::make_pair((const fst*)b[i], E1);
+    if (!amk.count(ka)) st = make_marked(a[i], 0, E2, E1, s, &amk[ka]);
+    if (!st && !bmk.count(kb)) st = make_marked(b[i], 1, E1, E2, s, &bmk[kb]);
     if (!st && !filters.count(E1)) {
       fst_handle f = nullptr;
       st = make_filter(E1, s, &f);
       if (!st) filters[E1] = f;
     }
     if (!st) {
+      am[i] = &amk[ka];
+      bm[i] = &bmk[kb];
       fa[i] = filters[E1];
-      am_h[i] = am[i].h;
-      bm_h[i] = bm[i].h;
+      am_h[i] = am[i]->h;
+      bm_h[i] = bm[i]->h;
     }
   }
   if (!st) st = compose_impl(n, am_h.data(), fa.data(), s, c1.data(), flags);
@@ -242,7 +323,7 @@ fst_status compose_filtered_impl(int32_t n, const fst_handle* a, const fst_handl
     }
     if (want_prov && h->E > 0) {
       k_filter_prov<<<nblk(h->E, 256), 256, 0, s>>>(h->E, h->arc_a, h->arc_b, c1[i]->arc_a,
-                                                    (const int32_t*)am[i].map->ptr, (const int32_t*)bm[i].map->ptr);
+                                                    (const int32_t*)am[i]->map->ptr, (const int32_t*)bm[i]->map->ptr);
       count_launch();
     }
     h->src_arcs_a = a[i]->E;
