@@ -827,20 +827,6 @@ __device__ __forceinline__ int emit_block_fast(TaskSmem& s, const ViewDev& Bv, c
   return btot;
 }
 
-// Compact the set bits of s.fw[w0, w1) (at most 1024 of them) into s.state; word w0 holds states
-// ub_w0 ..  Returns the count (all threads).
-__device__ __forceinline__ int compact_words(TaskSmem& s, int w0, int w1, int32_t ub_w0) {
-  const int wa = w0 + 2 * threadIdx.x;
-  const uint32_t x0 = wa < w1 ? s.fw[wa] : 0u, x1 = wa + 1 < w1 ? s.fw[wa + 1] : 0u;
-  int tot;
-  const int ex = block_excl_scan(__popc(x0) + __popc(x1), s.red32, &tot);
-  int pos = ex;
-  for (uint32_t m = x0; m; m &= m - 1) s.state[pos++] = ub_w0 + 64 * threadIdx.x + __ffs(m) - 1;
-  for (uint32_t m = x1; m; m &= m - 1) s.state[pos++] = ub_w0 + 64 * threadIdx.x + 32 + __ffs(m) - 1;
-  __syncthreads();
-  return tot;
-}
-
 
 // Whole-chunk BFS walk (fast path): one thread per source state of the chunk, no per-block barriers.
 // kStaged: candidates claimed in the staged NEW bits; else test-and-set on the global bitmaps.
@@ -1310,10 +1296,6 @@ __global__ void k_apply_remote(Ctx cx, const uint32_t* __restrict__ in, int leve
 }
 
 // dst[i] |= src[i] (merging bitmap / count slices of other shards)
-__global__ void k_or_words(uint32_t* __restrict__ dst, const uint32_t* __restrict__ src, int64_t n) {
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    if (src[i]) dst[i] |= src[i];
-}
 
 __global__ void k_shift_i64(int64_t* __restrict__ a, int64_t n, int64_t d) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)

@@ -323,6 +323,15 @@ def fst_version() -> str:
     return load_library().fst_version().decode()
 
 
+class _DeviceArray:
+    """__cuda_array_interface__ over library-owned device memory; holds its Fst alive."""
+
+    def __init__(self, owner: "Fst", ptr: int, n: int, typestr: str):
+        self._owner = owner
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": typestr, "data": (ptr if n else 0, True),
+                                         "version": 3, "strides": None}
+
+
 class Fst:
     """Owning wrapper of an fst_handle (freed on garbage collection or ``free()``)."""
 
@@ -380,6 +389,25 @@ class Fst:
         V = self.num_states
         out = np.zeros(V, np.int32)
         _check(load_library().fst_copy_pair_f_to_host(self.handle, _stream_ptr(stream), out.ctypes.data if V else None))
+        return out
+
+    def device_tensors(self) -> Dict[str, "object"]:
+        """Zero-copy torch CUDA tensors over the handle's device arrays (fst_info pointers).  Each tensor
+        keeps this handle alive (the library owns the memory until every view and the handle are gone);
+        treat them as read-only.  Keys: row_ptr, ilabel, olabel, dst, weight, is_start, is_accept, and
+        pair_a / pair_b / pair_f / arc_a / arc_b when present."""
+        import torch
+        v = self.info()
+        V, E = int(v.num_states), int(v.num_arcs)
+        spec = [("row_ptr", v.row_ptr, V + 1, "<i8"), ("ilabel", v.ilabel, E, "<i4"), ("olabel", v.olabel, E, "<i4"),
+                ("dst", v.dst, E, "<i4"), ("weight", v.weight, E, "<f4"), ("is_start", v.is_start, V, "|u1"),
+                ("is_accept", v.is_accept, V, "|u1"), ("pair_a", v.pair_a, V, "<i4"), ("pair_b", v.pair_b, V, "<i4"),
+                ("pair_f", v.pair_f, V, "<i4"), ("arc_a", v.arc_a, E, "<i4"), ("arc_b", v.arc_b, E, "<i4")]
+        out = {}
+        for name, ptr, n, typestr in spec:
+            if not ptr and n > 0:
+                continue
+            out[name] = torch.as_tensor(_DeviceArray(self, ptr or 0, n, typestr), device="cuda")
         return out
 
     def provenance(self, stream=None):

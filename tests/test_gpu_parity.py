@@ -273,3 +273,20 @@ def test_deep_bfs_level_profile(fst, T):
     assert sum(c.level_sizes(1)) == int(oracle.coaccessible(A, B).sum())
     assert len(c.level_sizes(2)) > (64 if T > 64 else 0)
     pins.assert_canonical_equal(pins.canonicalize_rows(c.to_host(), B.num_states), oracle.canonical(A, B), f"c3 T={T}")
+
+
+def test_device_tensors_zero_copy(fst):
+    """Fst.device_tensors(): zero-copy torch views of the composed graph equal fst_copy_to_host and keep
+    the handle alive after the Python wrapper is dropped."""
+    import torch
+    A, B = fstgen.config_c2(2, V=300)
+    c = fst.fst_compose(fst.fst_create(A), fst.fst_create(B), eps_filter=True)
+    host = c.to_host()
+    t = c.device_tensors()
+    del c
+    import gc
+    gc.collect()
+    torch.cuda.synchronize()
+    for k in ("row_ptr", "ilabel", "olabel", "dst", "is_start", "is_accept", "pair_a", "pair_b", "pair_f"):
+        assert np.array_equal(t[k].cpu().numpy(), host[k]), k
+    assert np.array_equal(t["weight"].cpu().numpy().view(np.uint32), host["weight"].view(np.uint32))
