@@ -23,6 +23,7 @@
 // time.  Sparse chunks and rows whose staging does not fit fall back to compacted per-state work
 // with global test-and-set.
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
@@ -993,7 +994,17 @@ __device__ __forceinline__ void bfs_chunk_fast(TaskSmem& s, const ViewDev& Bv, i
     const int32_t ub = s.cur[h];
     const int32_t e0 = __ldg(&off[ub]) + ub + 1, e1 = __ldg(&off[ub + 1]) + ub + 1;
     kept = 0;
-    for (int32_t e = e0 + threadIdx.x; e < e1; e += kThreads) fast_arc<kM32>(s, __ldg(&ikd[e]), e - ub - 1, cand);
+    // 4 coalesced item loads in flight per thread (a lexicon root has ~10^4 arcs: 20 dependent
+    // rounds of 512 would sit on the level's critical path)
+    constexpr int kHU = 4;
+    for (int32_t e = e0 + threadIdx.x; e < e1; e += kHU * kThreads) {
+      int2 x[kHU];
+#pragma unroll
+      for (int u = 0; u < kHU; ++u) x[u] = e + u * kThreads < e1 ? __ldg(&ikd[e + u * kThreads]) : make_int2(0, 0);
+#pragma unroll
+      for (int u = 0; u < kHU; ++u)
+        if (e + u * kThreads < e1) fast_arc<kM32>(s, x[u], e + u * kThreads - ub - 1, cand);
+    }
     if (kStage2) {
       const unsigned long long k = warp_sum((unsigned long long)kept);
       if ((threadIdx.x & 31) == 0 && k) atomicAdd(&s.keptc[(ub - cub0) >> 10], k);
@@ -1772,6 +1783,16 @@ fst_status run_levels_graph(const Ctx& cx, cudaStream_t s, int* level, int64_t* 
   return FST_OK;
 }
 
+// FSTC_NO_GRAPH_LOOP=1 keeps every level on the host loop (ncu cannot profile kernels inside a graph
+// with conditional nodes).
+bool graph_loop_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("FSTC_NO_GRAPH_LOOP");
+    return !(e && e[0] == '1');
+  }();
+  return on;
+}
+
 // Runs one BFS stage (level loop); fills the per-level frontier sizes.  The first levels run as
 // host-driven speculative batches; a BFS still going after kHostLevels levels continues in one
 // graph launch (run_levels_graph).
@@ -1791,7 +1812,7 @@ fst_status run_stage(const Ctx& cx, cudaStream_t s, unsigned long long* h_pinned
                                   cudaMemcpyDeviceToHost, s));
     FSTC_CUDA_TRY(cudaStreamSynchronize(s));
     if (*h_pinned == 0) break;
-    if (level >= kHostLevels) {  // deep BFS: the rest in one graph launch
+    if (level >= kHostLevels && graph_loop_enabled()) {  // deep BFS: the rest in one graph launch
       fst_status st = run_levels_graph<kStage2>(cx, s, &level, level_launches);
       if (st) return st;
       break;

@@ -14,6 +14,6 @@ ncu --set full --clock-control none --import-source on --kernel-name-base demang
     -o gpurun_out/$R/level2_c4_20k python scripts/prof_compose.py --V 20000 --D 8 --n 0 > gpurun_out/$R/ncu_level2.log 2>&1
 ls -la gpurun_out/$R
 # c5 (batched lexicon): launch list only
-ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/$R/launches_c5.csv \
+FSTC_NO_GRAPH_LOOP=1 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/$R/launches_c5.csv \
     python scripts/prof_compose.py --workload c5 --n 0 > gpurun_out/$R/launches_c5_run.log 2>&1
 ls -la gpurun_out/$R
