@@ -54,6 +54,8 @@ constexpr int kWCapMin = 64;       // ... and at least (smaller when the staged 
 constexpr int kOwnerCap = 384;     // per-warp arc-slot owner table of the BFS walk (end of dynamic smem)
 constexpr int kOwnerBytes = kWarps * kOwnerCap;
 
+constexpr int kCompQ = 64;
+
 struct Ctx {
   uint32_t* R;
   uint32_t* V;
@@ -78,6 +80,9 @@ struct Ctx {
   int32_t ncomp;
   int64_t nwords, nblocks, nchunks;
   int32_t* level_dev;  // graph-driven level loop: the true level number (hist index), advanced by block 0
+  // first chunk of every composition (batches of <= kCompQ): kernel-parameter copy, so a task's
+  // composition is found in the constant bank instead of by dependent global loads every level
+  int64_t compQ[kCompQ];
 };
 
 struct Chunk {
@@ -98,7 +103,18 @@ __device__ __forceinline__ int find_comp_q(const CompDev* __restrict__ comps, in
 
 __device__ __forceinline__ Chunk decode_chunk(const Ctx& cx, int64_t q) {
   Chunk ch;
-  ch.comp = cx.ncomp == 1 ? 0 : find_comp_q(cx.comps, cx.ncomp, q);
+  if (cx.ncomp == 1) {
+    ch.comp = 0;
+  } else if (cx.ncomp <= kCompQ) {
+    int lo = 0, hi = cx.ncomp - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (cx.compQ[mid] <= q) lo = mid; else hi = mid - 1;
+    }
+    ch.comp = lo;
+  } else {
+    ch.comp = find_comp_q(cx.comps, cx.ncomp, q);
+  }
   const CompDev& C = cx.comps[ch.comp];
   int64_t local = q - C.Q;
   ch.ua = (int32_t)(local / C.cpr);
@@ -1952,6 +1968,7 @@ fst_status compose_impl(int32_t n, const fst_handle* a, const fst_handle* b, cud
   CompDev* d_comps = (CompDev*)(base + ocomps);
   cx.comps = d_comps;
   cx.ncomp = n;
+  for (int i = 0; i < n && i < kCompQ; ++i) cx.compQ[i] = comps[i].Q;
   cx.nwords = nwords;
   cx.nblocks = nblocks;
   cx.nchunks = nchunks;
