@@ -83,6 +83,9 @@ struct Ctx {
   // first chunk of every composition (batches of <= kCompQ): kernel-parameter copy, so a task's
   // composition is found in the constant bank instead of by dependent global loads every level
   int64_t compQ[kCompQ];
+  int64_t ptotal;   // pairs over all compositions (pull decision of stage 1)
+  int32_t pull_ok;  // stage 1 may run bottom-up (pull) levels (unsharded compositions only)
+  int32_t pull_num; // pull threshold: frontier * pull_num >= unvisited * 4
 };
 
 struct Chunk {
@@ -1058,6 +1061,125 @@ __global__ void k_seed(Ctx cx) {
   if ((threadIdx.x & 31) == 0 && nnew) atomicAdd(&cx.ctrl[0].nnew, (unsigned long long)nnew);
 }
 
+// ------------------------------------------------------------------------------ bottom-up level (stage 1)
+// Direction-optimising BFS (pull): once the frontier is at least as large as the set of pairs not yet
+// in R, a level costs less as "every unvisited pair looks for ONE forward move into R" than as "every
+// frontier pair enumerates all its predecessors".  R is a set, so a pair may be claimed as soon as
+// any successor is in R (at most one level early): the final R is the same set (Alg. 1 line 3).  A
+// CTA owns row u_a of a chunk: it consumes the chunk's frontier words (pull does not read them), stages
+// the R words of the destination rows {dst(e_a)} U {u_a} of A's OUT-view, walks the chunk's unvisited
+// pairs (one lane per pair, early exit) over B's out-items, and ORs the new bits into its own row of R
+// and into the next frontier -- no other task writes that row during a pull level.
+// pull iff frontier * pull_num >= unvisited * 4 AND frontier >= pairs / 16 (the level scans every
+// chunk of the pair space, so the frontier must be a sizable share of it: never on trellis levels)
+
+__device__ __forceinline__ void level_pull(const Ctx& cx, TaskSmem& s, uint32_t* dyn, uint32_t* Fc, uint32_t* Fn,
+                                           uint32_t* flagc, uint32_t* flagn, int32_t* listn, LevelCtrl* ctrl_nxt,
+                                           unsigned& nnew) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t q = blockIdx.x; q < cx.nchunks; q += gridDim.x) {
+    const Chunk ch = decode_chunk(cx, q);
+    const CompDev& C = cx.comps[ch.comp];
+    const ViewDev& Av = C.Af;
+    const ViewDev& Bv = C.Bf;
+    const int wpr = C.wpr;
+    if (threadIdx.x == 0) flagc[q] = 0u;
+    // unvisited pairs of the chunk -> s.fw; the chunk's frontier words are consumed
+    const int w0 = ch.b0 * 32, w1 = min(ch.b1 * 32, wpr);
+    int cnt = 0;
+    for (int w = w0 + threadIdx.x; w < w1; w += kThreads) {
+      const int64_t gw = ch.rowW + w;
+      if (Fc[gw]) Fc[gw] = 0u;
+      uint32_t x = ~cx.R[gw];
+      if (w == wpr - 1 && (C.VB & 31)) x &= (1u << (C.VB & 31)) - 1u;  // columns beyond V_B
+      s.fw[w - w0] = x;
+      cnt += __popc(x);
+    }
+    cnt = warp_sum(cnt);
+    if (lane == 0) s.red32[threadIdx.x >> 5] = cnt;
+    __syncthreads();
+    int tot = 0;
+    for (int i = 0; i < kWarps; ++i) tot += s.red32[i];
+    __syncthreads();
+    if (tot == 0) continue;
+    const int nwc = w1 - w0;
+    uint32_t* NEWW = dyn + ((kDynSmem / 4) - kChunkMaxBlocks * 32);  // claimed bits of the chunk
+    stage_arow(s, C, Av, ch.ua, wpr, (kDynSmem / 4) - kChunkMaxBlocks * 32);
+    const bool staged = s.dst_staged;
+    uint32_t* RS = dyn;  // R words of the destination rows (slot-major)
+    for (int i = threadIdx.x; i < nwc; i += kThreads) NEWW[i] = 0u;
+    if (staged) {
+      const int n = s.m * wpr;
+      for (int i = threadIdx.x; i < n; i += kThreads) {
+        const int r = i / wpr, w = i - r * wpr;
+        RS[i] = cx.R[C.W + (int64_t)s.slot_row[r] * wpr + w];
+      }
+    }
+    __syncthreads();
+    auto in_r = [&](const Cand& c) -> bool {
+      const uint32_t bit = 1u << (c.col & 31);
+      if (staged && c.slot >= 0) return RS[c.slot * wpr + (c.col >> 5)] & bit;
+      return __ldg(&cx.R[C.W + (int64_t)c.row * wpr + (c.col >> 5)]) & bit;
+    };
+    // warps take 8-word segments; lanes take the segment's unvisited pairs 32 at a time
+    if (threadIdx.x == 0) s.segnext = 0;
+    __syncthreads();
+    constexpr int kSegWords = 8;
+    for (;;) {
+      int seg = 0;
+      if (lane == 0) seg = atomicAdd(&s.segnext, 1);
+      seg = __shfl_sync(0xffffffffu, seg, 0);
+      if (seg * kSegWords >= nwc) break;
+      const int wi = seg * kSegWords + lane;
+      const uint32_t word = (lane < kSegWords && wi < nwc) ? s.fw[wi] : 0u;
+      const int pc = __popc(word);
+      const int winc = warp_incl_scan(pc);
+      const int wex = winc - pc;
+      const int stot = __shfl_sync(0xffffffffu, winc, 31);
+      for (int b0 = 0; b0 < stot; b0 += 32) {
+        const int k = b0 + lane;
+        int j = 0;
+#pragma unroll
+        for (int step = 16; step > 0; step >>= 1)
+          if (__shfl_sync(0xffffffffu, wex, j + step) <= k) j += step;
+        uint32_t wj = __shfl_sync(0xffffffffu, word, j);
+        int r = k - __shfl_sync(0xffffffffu, wex, j);
+        if (k >= stot) continue;
+        int pos = 0;
+#pragma unroll
+        for (int h = 16; h > 0; h >>= 1) {
+          const int c = __popc(wj & ((1u << h) - 1u));
+          if (r >= c) {
+            r -= c;
+            pos += h;
+            wj >>= h;
+          }
+        }
+        const int lw = seg * kSegWords + j;  // chunk-local word
+        const int32_t ub = (w0 + lw) * 32 + pos;
+        // forward moves of (u_a, ub): the sentinel item (M2) then its B arcs (M1, M3), early exit
+        const int32_t i0 = __ldg(&Bv.off[ub]) + ub, i1 = __ldg(&Bv.off[ub + 1]) + ub + 1;
+        bool hit = false;
+        for (int32_t it = i0; it < i1 && !hit; ++it) {
+          const Item x = make_item(s, Av, it, ub, __ldg(&Bv.ikd[it]), true);
+          for (int m = 0; m < x.n && !hit; ++m) hit = in_r(item_move(s, Av, ch.ua, x, m));
+        }
+        if (hit) atomicOr(&NEWW[lw], 1u << pos);
+      }
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < nwc; i += kThreads) {  // own row: plain OR into R, then the frontier
+      const uint32_t nb = NEWW[i];
+      if (!nb) continue;
+      const int64_t gw = ch.rowW + w0 + i;
+      cx.R[gw] |= nb;
+      nnew += __popc(nb);
+      push_bits(C, ch.ua, (w0 + i) * 32, gw, nb, Fn, flagn, listn, ctrl_nxt);
+    }
+    __syncthreads();
+  }
+}
+
 // ------------------------------------------------------------------------------ one BFS level
 // kStage2 = false: backward BFS over in-views, visited set R.
 // kStage2 = true : forward BFS over out-views, filter R, visited set V, per-block kept counts.
@@ -1089,8 +1211,20 @@ __global__ void __launch_bounds__(kThreads, 2) k_level(Ctx cx, int level) {
       cx.misc[0] += 1;
       if (hl < kMaxLevelStats) cx.hist[hl] = ctrl_cur->nnew;
     }
+    ctrl_nxt->pad[0] = ctrl_cur->pad[0] + ctrl_cur->nnew;  // pairs visited through this level's frontier
   }
   unsigned nnew = 0;
+  if (!kStage2 && cx.pull_ok && nlist) {  // uniform decision: inputs fixed before this launch
+    const unsigned long long nf = ctrl_cur->nnew;
+    const unsigned long long visited = ctrl_cur->pad[0] + nf;
+    const unsigned long long unvisited = (unsigned long long)cx.ptotal > visited ? cx.ptotal - visited : 0ull;
+    if (nf * (unsigned long long)cx.pull_num >= unvisited * 4ull && nf * 16ull >= (unsigned long long)cx.ptotal) {
+      level_pull(cx, s, dyn, Fc, Fn, flagc, flagn, listn, ctrl_nxt, nnew);
+      nnew = warp_sum(nnew);
+      if ((threadIdx.x & 31) == 0 && nnew) atomicAdd(&ctrl_nxt->nnew, (unsigned long long)nnew);
+      return;
+    }
+  }
   // narrow levels (fewer active chunks than CTAs, e.g. a trellis A with one row per level): split
   // every chunk into `split` block ranges so the whole grid works on the level
   const unsigned split = nlist == 0 ? 1u : (unsigned)max(1ull, min((unsigned long long)kChunkMaxBlocks, gridDim.x / nlist));
@@ -1799,6 +1933,26 @@ fst_status run_levels_graph(const Ctx& cx, cudaStream_t s, int* level, int64_t* 
   return FST_OK;
 }
 
+// FSTC_NO_PULL=1 disables the bottom-up stage-1 levels (A/B and debugging).
+bool pull_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("FSTC_NO_PULL");
+    return !(e && e[0] == '1');
+  }();
+  return on;
+}
+
+// FSTC_PULL_NUM=k (A/B tuning): pull when frontier * k >= unvisited * 4 (default 8: configs[3] stage 1
+// 36.4 -> 29.5 ms; 4: 30.3, 16: 29.4 but D=4 +12%).
+int32_t pull_num() {
+  static const int32_t v = [] {
+    const char* e = getenv("FSTC_PULL_NUM");
+    const int k = e ? atoi(e) : 8;
+    return k > 0 ? k : 8;
+  }();
+  return v;
+}
+
 // FSTC_NO_GRAPH_LOOP=1 keeps every level on the host loop (ncu cannot profile kernels inside a graph
 // with conditional nodes).
 bool graph_loop_enabled() {
@@ -1969,6 +2123,9 @@ fst_status compose_impl(int32_t n, const fst_handle* a, const fst_handle* b, cud
   cx.comps = d_comps;
   cx.ncomp = n;
   for (int i = 0; i < n && i < kCompQ; ++i) cx.compQ[i] = comps[i].Q;
+  cx.ptotal = pairs;
+  cx.pull_ok = (pull_enabled() && n == 1) ? 1 : 0;  // batches are many narrow problems (trellises)
+  cx.pull_num = pull_num();
   cx.nwords = nwords;
   cx.nblocks = nblocks;
   cx.nchunks = nchunks;

@@ -328,7 +328,7 @@ class _DeviceArray:
 
     def __init__(self, owner: "Fst", ptr: int, n: int, typestr: str):
         self._owner = owner
-        self.__cuda_array_interface__ = {"shape": (n,), "typestr": typestr, "data": (ptr if n else 0, True),
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": typestr, "data": (ptr if n else 0, False),
                                          "version": 3, "strides": None}
 
 
