@@ -1158,10 +1158,14 @@ __device__ __forceinline__ void level_pull(const Ctx& cx, TaskSmem& s, uint32_t*
         const int lw = seg * kSegWords + j;  // chunk-local word
         const int32_t ub = (w0 + lw) * 32 + pos;
         // forward moves of (u_a, ub): the sentinel item (M2) then its B arcs (M1, M3), early exit
-        const int32_t i0 = __ldg(&Bv.off[ub]) + ub, i1 = __ldg(&Bv.off[ub + 1]) + ub + 1;
+        // (the sentinel carries only M2 moves: skipped when the A row has no eps outputs)
+        const int32_t i0 = __ldg(&Bv.off[ub]) + ub + (s.aeps == 0 ? 1 : 0), i1 = __ldg(&Bv.off[ub + 1]) + ub + 1;
         bool hit = false;
+        int2 kn = i0 < i1 ? __ldg(&Bv.ikd[i0]) : make_int2(0, 0);
         for (int32_t it = i0; it < i1 && !hit; ++it) {
-          const Item x = make_item(s, Av, it, ub, __ldg(&Bv.ikd[it]), true);
+          const int2 kd = kn;
+          if (it + 1 < i1) kn = __ldg(&Bv.ikd[it + 1]);  // next item in flight while this one is tested
+          const Item x = make_item(s, Av, it, ub, kd, true);
           for (int m = 0; m < x.n && !hit; ++m) hit = in_r(item_move(s, Av, ch.ua, x, m));
         }
         if (hit) atomicOr(&NEWW[lw], 1u << pos);
