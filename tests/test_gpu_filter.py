@@ -155,3 +155,35 @@ def test_chain_lexicon_pipeline(fst):
     got = pins.canonicalize_rows(c3.to_host(), Id.num_states)
     exp = {k: v for k, v in oracle.compose_chain([A, B, Id], canonicalize=True).items() if k not in ("arc_a", "arc_b")}
     pins.assert_canonical_equal(got, exp, "lexicon chain")
+
+
+def test_chain_eps_filtered_three_way_bijection(fst):
+    """fst_compose_chain with the eps filter on three eps DAGs: every matched path triple
+    (pi_a: x->y, pi_b: y->z, pi_d: z->w, eps-free label strings) yields exactly ONE composed path of
+    score s_a + s_b + s_d (Eq. (1) applied twice, no duplicated terms)."""
+    import collections
+
+    def paths(g):
+        out = []
+        for p in pins.accepting_paths(g):
+            il = tuple(int(g.ilabel[e]) for e in p if g.ilabel[e] != pins.EPS)
+            ol = tuple(int(g.olabel[e]) for e in p if g.olabel[e] != pins.EPS)
+            out.append((il, ol, sum(float(g.weight[e]) for e in p)))
+        return out
+
+    for seed in range(20):
+        gs = [fstgen.random_dag(6, 3, 3, 0.25, 104729 * seed + k) for k in (5, 6, 7)]
+        c = fst.fst_compose_chain([fst.fst_create(g) for g in gs], eps_filter=True)
+        got = pins.composed_path_table(c.to_host())
+        pb = collections.defaultdict(list)
+        for y, z, sb in paths(gs[1]):
+            pb[y].append((z, sb))
+        pd = collections.defaultdict(list)
+        for z, w, sd in paths(gs[2]):
+            pd[z].append((w, sd))
+        exp = collections.defaultdict(collections.Counter)
+        for x, y, sa in paths(gs[0]):
+            for z, sb in pb.get(y, ()):
+                for w, sd in pd.get(z, ()):
+                    exp[(x, w)][sa + sb + sd] += 1
+        assert got == exp, f"seed {seed}"

@@ -480,3 +480,35 @@ def test_canonicalize_any_comparator(seed):
         raw = {k: v for k, v in raw.items() if k not in ("arc_a", "arc_b")}
         exp = {k: v for k, v in oracle.canonical(A, B, eps_filter=filt).items() if k not in ("arc_a", "arc_b")}
         pins.assert_canonical_equal(pins.canonicalize_any(raw, B.num_states), exp, f"seed {seed} filter {filt}")
+
+
+@pytest.mark.parametrize("seed", range(20))
+def test_filtered_chain_three_way_bijection(seed):
+    """The eps-filtered composition applied twice ((A o B) o D on eps DAGs) has exactly one path per
+    matched path triple, score s_a + s_b + s_d (Eq. (1) applied twice, eps-free label strings)."""
+    from types import SimpleNamespace
+
+    def paths(g):
+        out = []
+        for p in pins.accepting_paths(g):
+            il = tuple(int(g.ilabel[e]) for e in p if g.ilabel[e] != EPS)
+            ol = tuple(int(g.olabel[e]) for e in p if g.olabel[e] != EPS)
+            out.append((il, ol, sum(float(g.weight[e]) for e in p)))
+        return out
+
+    gs = [fstgen.random_dag(6, 3, 3, 0.25, 104729 * seed + k) for k in (5, 6, 7)]
+    c1 = oracle.compose_filtered(gs[0], gs[1])
+    c1n = SimpleNamespace(num_states=int(c1["num_states"]), num_arcs=int(c1["num_arcs"]),
+                          **{k: c1[k] for k in ("row_ptr", "ilabel", "olabel", "dst", "weight", "is_start", "is_accept")})
+    got = pins.composed_path_table(oracle.compose_filtered(c1n, gs[2]))
+    pb, pd = collections.defaultdict(list), collections.defaultdict(list)
+    for y, z, sb in paths(gs[1]):
+        pb[y].append((z, sb))
+    for z, w, sd in paths(gs[2]):
+        pd[z].append((w, sd))
+    exp = collections.defaultdict(collections.Counter)
+    for x, y, sa in paths(gs[0]):
+        for z, sb in pb.get(y, ()):
+            for w, sd in pd.get(z, ()):
+                exp[(x, w)][sa + sb + sd] += 1
+    assert got == exp
