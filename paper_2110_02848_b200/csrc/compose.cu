@@ -1116,6 +1116,7 @@ __device__ __forceinline__ void level_pull(const Ctx& cx, TaskSmem& s, uint32_t*
       }
     }
     __syncthreads();
+    const bool fastp = staged && s.small;
     auto in_r = [&](const Cand& c) -> bool {
       const uint32_t bit = 1u << (c.col & 31);
       if (staged && c.slot >= 0) return RS[c.slot * wpr + (c.col >> 5)] & bit;
@@ -1159,14 +1160,35 @@ __device__ __forceinline__ void level_pull(const Ctx& cx, TaskSmem& s, uint32_t*
         const int32_t ub = (w0 + lw) * 32 + pos;
         // forward moves of (u_a, ub): the sentinel item (M2) then its B arcs (M1, M3), early exit
         // (the sentinel carries only M2 moves: skipped when the A row has no eps outputs)
-        const int32_t i0 = __ldg(&Bv.off[ub]) + ub + (s.aeps == 0 ? 1 : 0), i1 = __ldg(&Bv.off[ub + 1]) + ub + 1;
         bool hit = false;
-        int2 kn = i0 < i1 ? __ldg(&Bv.ikd[i0]) : make_int2(0, 0);
-        for (int32_t it = i0; it < i1 && !hit; ++it) {
-          const int2 kd = kn;
-          if (it + 1 < i1) kn = __ldg(&Bv.ikd[it + 1]);  // next item in flight while this one is tested
-          const Item x = make_item(s, Av, it, ub, kd, true);
-          for (int m = 0; m < x.n && !hit; ++m) hit = in_r(item_move(s, Av, ch.ua, x, m));
+        if (fastp) {  // label-mask rows with staged destination rows: direct bit tests
+          const uint32_t ubit = 1u << (ub & 31);
+          for (int a = 0; a < s.aeps && !hit; ++a) hit = RS[s.a_slot[a] * wpr + (ub >> 5)] & ubit;  // M2
+          const int32_t i0 = __ldg(&Bv.off[ub]) + ub + 1, i1 = __ldg(&Bv.off[ub + 1]) + ub + 1;
+          int2 kn = i0 < i1 ? __ldg(&Bv.ikd[i0]) : make_int2(0, 0);
+          for (int32_t it = i0; it < i1 && !hit; ++it) {
+            const int2 kd = kn;
+            if (it + 1 < i1) kn = __ldg(&Bv.ikd[it + 1]);  // next item in flight while this one is tested
+            const int cw = kd.y >> 5;
+            const uint32_t cbit = 1u << (kd.y & 31);
+            unsigned long long m = (unsigned)(kd.x + 1) < 64u ? s.labmask[kd.x + 1] : 0ull;
+            while (m && !hit) {  // M1
+              const int a = __ffsll((long long)m) - 1;
+              m &= m - 1;
+              hit = RS[s.a_slot[a] * wpr + cw] & cbit;
+            }
+            if (kd.x == FST_EPS && !hit) hit = RS[cw] & cbit;  // M3: slot 0 = u_a
+          }
+        } else {
+          // (the sentinel carries only M2 moves: skipped when the A row has no eps outputs)
+          const int32_t i0 = __ldg(&Bv.off[ub]) + ub + (s.aeps == 0 ? 1 : 0), i1 = __ldg(&Bv.off[ub + 1]) + ub + 1;
+          int2 kn = i0 < i1 ? __ldg(&Bv.ikd[i0]) : make_int2(0, 0);
+          for (int32_t it = i0; it < i1 && !hit; ++it) {
+            const int2 kd = kn;
+            if (it + 1 < i1) kn = __ldg(&Bv.ikd[it + 1]);
+            const Item x = make_item(s, Av, it, ub, kd, true);
+            for (int m = 0; m < x.n && !hit; ++m) hit = in_r(item_move(s, Av, ch.ua, x, m));
+          }
         }
         if (hit) atomicOr(&NEWW[lw], 1u << pos);
       }
