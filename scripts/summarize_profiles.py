@@ -19,7 +19,12 @@ METRICS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.
            "smsp__average_warps_issue_stalled_long_scoreboard_per_issue_active.ratio",
            "smsp__average_warps_issue_stalled_barrier_per_issue_active.ratio",
            "smsp__average_warps_issue_stalled_short_scoreboard_per_issue_active.ratio",
-           "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum"]
+           "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum",
+           # atomic throughput: claims are shared-memory atomics, merged into the global bitmaps word-wise
+           "l1tex__data_pipe_lsu_wavefronts_mem_shared_op_atom.sum",
+           "l1tex__data_pipe_lsu_wavefronts_mem_shared_op_atom.sum.pct_of_peak_sustained_elapsed",
+           "l1tex__t_requests_pipe_lsu_mem_global_op_atom.sum", "l1tex__t_requests_pipe_lsu_mem_global_op_red.sum",
+           "lts__t_requests_srcunit_tex_op_atom_dot_alu.sum"]
 
 
 def launches(path):
