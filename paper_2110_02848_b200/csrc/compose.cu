@@ -961,12 +961,18 @@ __device__ __forceinline__ void bfs_chunk_fast(TaskSmem& s, const ViewDev& Bv, i
       kept = 0;
       // arc slot -> owner lane: a per-warp byte table when the batch is small enough, else a
       // binary search over the lanes' start offsets
+      // (uniform power-of-two degree over the batch's states, e.g. random graphs: owner = c >> log2 d)
+      const unsigned dmax = __reduce_max_sync(0xffffffffu, (unsigned)deg);
+      const unsigned dmin = __reduce_min_sync(0xffffffffu, k < stot ? (unsigned)deg : dmax);
+      const bool uni = dmax == dmin && (dmax & (dmax - 1u)) == 0u;
+      const int ush = __ffs((int)dmax) - 1;
       uint8_t* own = dynsm + (kDynSmem - kOwnerBytes) + (threadIdx.x >> 5) * kOwnerCap;
-      const bool tbl = total <= kOwnerCap;
+      const bool tbl = !uni && total <= kOwnerCap;
       if (tbl)
         for (int p = start; p < incl; ++p) own[p] = (uint8_t)lane;
       __syncwarp();
       auto owner_of = [&](int c) -> int {
+        if (uni) return c < total ? c >> ush : 0;
         if (tbl) return c < total ? own[c] : 0;
         int jj = 0;
 #pragma unroll
