@@ -65,10 +65,18 @@ def c5_shard(rank: int, world: int):
     return As, B, mine
 
 
+# c4-paper: with one accept state and in-degree ~5 over 10 labels, the accept pair often has no
+# label-matched in-arc pair (R = {accept pair}, an empty composition: seed offsets 0, 1, 3); offset 2
+# gives the nonempty instance (|R| = 6.0e7) the bench times.
+SEED_OFFSET = {"c4-paper": 2}
+REF_SEED_OFFSET = {"c4-paper": 2, "c4-d4": 1}  # the oracle samples: offset 0 of c4-d4's V=2048 sample is empty too
+
+
 def make_inputs(workload: str, rank: int):
     _, V, D, T = WORKLOADS[workload]
-    A = fstgen.random_graph(V, D, T, 1000 + V + D + 100003 * rank)
-    B = fstgen.random_graph(V, D, T, 2000 + V + D + 100003 * rank)
+    o = SEED_OFFSET.get(workload, 0)
+    A = fstgen.random_graph(V, D, T, 1000 + V + D + o + 100003 * rank)
+    B = fstgen.random_graph(V, D, T, 2000 + V + D + o + 100003 * rank)
     return A, B
 
 
@@ -169,8 +177,9 @@ def reference_sample(workload: str):
         return As[0], B, f"utterance 0 of the c5 batch (T={As[0].num_states - 1}) o closure(10k-word lexicon)"
     V = REF_SAMPLE_V[workload]
     _, _, D, T = WORKLOADS[workload]
-    A = fstgen.random_graph(V, D, T, 1000 + V + D)
-    B = fstgen.random_graph(V, D, T, 2000 + V + D)
+    o = REF_SEED_OFFSET.get(workload, 0)
+    A = fstgen.random_graph(V, D, T, 1000 + V + D + o)
+    B = fstgen.random_graph(V, D, T, 2000 + V + D + o)
     return A, B, f"random acceptors V={V} D={D} {T} tokens (same generator as the workload, scaled down)"
 
 
@@ -373,9 +382,7 @@ def run_sharded(args, fstc, stream, dev, pg, rank, local_rank, world):
     strong scaling; value = composed arcs of the whole composition / max over ranks of the time."""
     import torch
     from paper_2110_02848_b200 import parallel
-    _, V, D, T = WORKLOADS[args.workload]
-    A = fstgen.random_graph(V, D, T, 1000 + V + D)
-    B = fstgen.random_graph(V, D, T, 2000 + V + D)
+    A, B = make_inputs(args.workload, 0)
     uid = [fstc.Comm.unique_id() if rank == 0 else None]
     if pg:
         pg.broadcast_object_list(uid, src=0)

@@ -848,6 +848,10 @@ __device__ __forceinline__ int emit_block_fast(TaskSmem& s, const ViewDev& Bv, c
 }
 
 
+// ceil(2^32 / d) for 2 <= d < 64: floor(c / d) = __umulhi(c, kRecip32[d]) exactly for every batch
+// slot c < 32 d + 32 (checked exhaustively for d <= 62)
+__constant__ unsigned kRecip32[64] = {0u, 0u, 2147483648u, 1431655766u, 1073741824u, 858993460u, 715827883u, 613566757u, 536870912u, 477218589u, 429496730u, 390451573u, 357913942u, 330382100u, 306783379u, 286331154u, 268435456u, 252645136u, 238609295u, 226050911u, 214748365u, 204522253u, 195225787u, 186737709u, 178956971u, 171798692u, 165191050u, 159072863u, 153391690u, 148102321u, 143165577u, 138547333u, 134217728u, 130150525u, 126322568u, 122713352u, 119304648u, 116080198u, 113025456u, 110127367u, 107374183u, 104755300u, 102261127u, 99882961u, 97612894u, 95443718u, 93368855u, 91382283u, 89478486u, 87652394u, 85899346u, 84215046u, 82595525u, 81037119u, 79536432u, 78090315u, 76695845u, 75350304u, 74051161u, 72796056u, 71582789u, 70409300u, 69273667u, 68174085u};
+
 // Whole-chunk BFS walk (fast path): one thread per source state of the chunk, no per-block barriers.
 // kStaged: candidates claimed in the staged NEW bits; else test-and-set on the global bitmaps.
 // Per-block kept counts (stage 2) are accumulated warp-aggregated in s.keptc[].
@@ -961,18 +965,19 @@ __device__ __forceinline__ void bfs_chunk_fast(TaskSmem& s, const ViewDev& Bv, i
       kept = 0;
       // arc slot -> owner lane: a per-warp byte table when the batch is small enough, else a
       // binary search over the lanes' start offsets
-      // (uniform power-of-two degree over the batch's states, e.g. random graphs: owner = c >> log2 d)
+      // (uniform degree d <= 62 over the batch's states, e.g. random graphs: owner = floor(c / d) as
+      // the high word of c * ceil(2^32 / d), exact for the slots c < 32 d + 32 <= 2016 of a batch)
       const unsigned dmax = __reduce_max_sync(0xffffffffu, (unsigned)deg);
       const unsigned dmin = __reduce_min_sync(0xffffffffu, k < stot ? (unsigned)deg : dmax);
-      const bool uni = dmax == dmin && (dmax & (dmax - 1u)) == 0u;
-      const int ush = __ffs((int)dmax) - 1;
+      const bool uni = dmax == dmin && dmax <= 62u;
+      const unsigned uinv = uni ? kRecip32[dmax] : 0u;
       uint8_t* own = dynsm + (kDynSmem - kOwnerBytes) + (threadIdx.x >> 5) * kOwnerCap;
       const bool tbl = !uni && total <= kOwnerCap;
       if (tbl)
         for (int p = start; p < incl; ++p) own[p] = (uint8_t)lane;
       __syncwarp();
       auto owner_of = [&](int c) -> int {
-        if (uni) return c < total ? c >> ush : 0;
+        if (uni) return c < total ? (int)__umulhi((unsigned)c, uinv) : 0;
         if (tbl) return c < total ? own[c] : 0;
         int jj = 0;
 #pragma unroll
