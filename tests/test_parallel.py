@@ -91,3 +91,16 @@ def test_gloo_world2_nccl_uid_bootstrap():
         p.join(timeout=60)
         assert p.exitcode == 0
     assert len(res[0][1]) == 128 and res[0][1] == res[1][1]
+
+
+def test_bench_reference_samples_are_nonempty():
+    """Every random-graph bench workload's oracle sample composes to a nonempty graph (a degenerate
+    seed -- the single accept pair with no label-matched in-arcs -- would time an empty composition)."""
+    import os
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import bench
+    import oracle
+    for w in ("c4", "c4-d4", "c4-paper", "fig3b-d16"):
+        A, B, _ = bench.reference_sample(w)
+        assert oracle.compose(A, B)["num_arcs"] > 0, w
