@@ -111,6 +111,8 @@ typedef struct {
   int64_t emit_launches;  /* of which emit kernels */
   int64_t expand_launches;/* of which BFS level kernels */
   int64_t staged_tasks;   /* chunk tasks of the BFS levels that used shared-memory staging */
+  int32_t tile_path;      /* 1: the call ran the tile kernels (bottom-up levels, count, emit) */
+  int32_t pull_levels;    /* BFS levels (both stages) that ran bottom-up on the tile kernels */
 } fst_compose_stats;
 
 /* Upload + validate + build label-sorted adjacency views.  On success *out is a
@@ -255,6 +257,13 @@ fst_status fst_shard_info(fst_handle c, fst_shard_desc* out);
 /* Profiling: when on, fst_compose* records CUDA events per phase (fst_compose_stats) and
  * computes |R|.  Off by default. */
 void fst_set_profiling(int32_t on);
+
+/* Tile path selection for single compositions: 0 = never, 1 = automatic (pair space
+ * >= 2^23 pairs and the inputs fit: degrees <= 31, labels <= 252, V_B small enough for the staged
+ * tables), 2 = whenever the inputs fit, 3 = as 2 with every BFS level bottom-up (tests).  The
+ * environment variable FSTC_TILE sets the initial mode.  Both paths return the same graph (state
+ * numbering by ascending key; arc order within a state may differ). */
+void fst_set_tile_mode(int32_t mode);
 
 /* Total kernels launched by this process through the library (monotone counter). */
 int64_t fst_launch_count(void);

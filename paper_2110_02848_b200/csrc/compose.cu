@@ -27,6 +27,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <atomic>
 #include <vector>
 
 #include "fstc_handle.h"
@@ -74,6 +75,8 @@ struct Ctx {
   unsigned long long* hist;  // per-level frontier sizes
   unsigned long long* misc;  // [0] nonempty levels, [1] |R|, [2] emit consistency errors, [3] staged tasks
   uint8_t* cnt8;             // per pair: out-degree in C recorded by the stage-2 fast path (255 = recount)
+  uint32_t* warc;            // tile path: per word, arcs of its states (k_tile_count), then the exclusive
+                             // prefix inside the word's block (k_block_counts); aliases cnt8's memory
   uint32_t* OUT;             // sharded mode: claims for pairs in rows owned by other shards
   const CompDev* comps;
   const int64_t* seedbase;
@@ -1518,6 +1521,11 @@ __global__ void k_block_counts(Ctx cx) {
     int inc = warp_incl_scan(pc);
     if (lane < nw) cx.wpre[w0 + lane] = (uint16_t)(inc - pc);
     if (lane == 31) cx.vcount[blk] = inc;
+    if (cx.warc) {  // tile path: arc offset of each word inside its block
+      const uint32_t a = lane < nw ? cx.warc[w0 + lane] : 0u;
+      const uint32_t ai = warp_incl_scan(a);
+      if (lane < nw) cx.warc[w0 + lane] = ai - a;
+    }
   }
 }
 
@@ -1852,6 +1860,8 @@ __global__ void __launch_bounds__(kThreads, 2) k_emit(Ctx cx, const int64_t* __r
   }
 }
 
+#include "tile.cuh"
+
 inline unsigned nblk(int64_t n, int t) { return (unsigned)std::max<int64_t>(1, (n + t - 1) / t); }
 
 int g_grid = 0;
@@ -2045,7 +2055,272 @@ unsigned long long* pinned_scratch() {
   return p;
 }
 
+// ------------------------------------------------------------------------------ tile path (host)
+std::atomic<int>& tile_mode_ref() {
+  static std::atomic<int> m{[] {
+    const char* e = getenv("FSTC_TILE");
+    const int v = e ? atoi(e) : 1;
+    return (v >= 0 && v <= 3) ? v : 1;
+  }()};
+  return m;
+}
+
+constexpr int64_t kTileMinPairs = 1ll << 23;
+
+// FSTC_TILE_PULL_K=k: a level runs bottom-up when frontier * k >= the stage's pair set (stage 1: the
+// pair space, stage 2: R).  A bottom-up level costs about one sweep whatever its frontier, a push level
+// grows with its frontier (default 256).
+int64_t tile_pull_k() {
+  static const int64_t v = [] {
+    const char* e = getenv("FSTC_TILE_PULL_K");
+    const long long k = e ? atoll(e) : 256;
+    return (int64_t)(k > 0 ? k : 256);
+  }();
+  return v;
+}
+
+int smem_optin() {
+  static int v = 0;
+  if (!v) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    if (v <= 0) v = 227 * 1024;
+  }
+  return v;
+}
+
+// B role: ELL of view `which` (0 = out-by-ilabel, with (carry, weight); 1 = in-by-ilabel), cached in
+// the handle.
+fst_status ensure_tile_ell(fst* B, int which, cudaStream_t s) {
+  fst::TileEll& T = B->tile_ell[which];
+  if (T.ok) return FST_OK;
+  const View& v = B->views[which == 0 ? kOutByIlabel : kInByIlabel];
+  const int32_t V = B->V;
+  const int wd = v.max_deg + 1;
+  const int wpr = (V + 31) / 32;
+  size_t off = 0;
+  auto take = [&](size_t bytes) { size_t o = off; off += (bytes + 255) & ~size_t(255); return o; };
+  const size_t o_ell = take(4ull * wd * V), o_cw = which == 0 ? take(8ull * wd * V) : 0;
+  const size_t o_wmax = take(wpr), o_flag = take(4);
+  BufferPtr buf;
+  fst_status st = alloc_buffer(off, s, &buf);
+  if (st) return st;
+  char* base = (char*)buf->ptr;
+  T.ell = (uint32_t*)(base + o_ell);
+  T.cw = which == 0 ? (int2*)(base + o_cw) : nullptr;
+  T.wmax = (uint8_t*)(base + o_wmax);
+  int32_t* d_flag = (int32_t*)(base + o_flag);
+  FSTC_CUDA_TRY(cudaMemsetAsync(d_flag, 0, 4, s));
+  k_build_ell<<<nblk(V, 256), 256, 0, s>>>(V, v.off, v.key, v.other, which == 0 ? v.cw : nullptr, wd, T.ell, T.cw,
+                                            T.wmax, d_flag);
+  FSTC_LAUNCH_CHECK();
+  int32_t flag = 0;
+  FSTC_CUDA_TRY(cudaMemcpyAsync(&flag, d_flag, 4, cudaMemcpyDeviceToHost, s));
+  FSTC_CUDA_TRY(cudaStreamSynchronize(s));
+  T.has_eps = flag != 0;
+  T.wd = wd;
+  T.buf = buf;
+  T.ok = true;
+  return FST_OK;
+}
+
+// A role: tile row starts for view `which` (0 = out-by-olabel, 1 = in-by-olabel): consecutive rows,
+// at most kTRows rows and `slot_cap` slots (arcs + self slot; 8 per row in byte mode) per tile, and
+// (slots + rows) <= vr_cap when vr_cap > 0 (the emit's staged rank rows).  Greedy; cached.
+fst_status tile_rows(fst* A, int which, int self, int slot_cap, int vr_cap, int bytemode, cudaStream_t s,
+                     const int32_t** d, int32_t* ntiles) {
+  const int64_t key = (int64_t)which | ((int64_t)self << 1) | ((int64_t)bytemode << 2) | ((int64_t)slot_cap << 3) |
+                      ((int64_t)vr_cap << 16);
+  for (const auto& tr : A->tile_rows)
+    if (tr.key == key) {
+      *d = tr.d;
+      *ntiles = tr.n;
+      return FST_OK;
+    }
+  std::vector<int32_t>& hoff = A->tile_hoff[which];
+  const int32_t V = A->V;
+  if ((int32_t)hoff.size() != V + 1) {
+    hoff.resize(V + 1);
+    const View& v = A->views[which == 0 ? kOutByOlabel : kInByOlabel];
+    FSTC_CUDA_TRY(cudaMemcpyAsync(hoff.data(), v.off, sizeof(int32_t) * (V + 1), cudaMemcpyDeviceToHost, s));
+    FSTC_CUDA_TRY(cudaStreamSynchronize(s));
+  }
+  std::vector<int32_t> tr{0};
+  int slots = 0, rows = 0;
+  for (int32_t r = 0; r < V; ++r) {
+    const int n = bytemode ? 8 : hoff[r + 1] - hoff[r] + self;
+    if (rows > 0 && (slots + n > slot_cap || rows + 1 > kTRows || (vr_cap > 0 && slots + n + rows + 1 > vr_cap))) {
+      tr.push_back(r);
+      slots = rows = 0;
+    }
+    slots += n;
+    ++rows;
+  }
+  tr.push_back(V);
+  fst::TileRows out;
+  out.key = key;
+  out.n = (int32_t)tr.size() - 1;
+  fst_status st = alloc_buffer(sizeof(int32_t) * tr.size(), s, &out.buf);
+  if (st) return st;
+  out.d = (int32_t*)out.buf->ptr;
+  FSTC_CUDA_TRY(cudaMemcpyAsync(out.d, tr.data(), sizeof(int32_t) * tr.size(), cudaMemcpyHostToDevice, s));
+  FSTC_CUDA_TRY(cudaStreamSynchronize(s));
+  A->tile_rows.push_back(out);
+  *d = out.d;
+  *ntiles = out.n;
+  return FST_OK;
+}
+
+size_t tile_emit_smem(int vr_rows, int wpr, int wd) {
+  const size_t vr = (size_t)vr_rows * wpr;
+  return 4 * vr + 4 * ((vr + 1) / 2) + (size_t)kEWarps * (2 * wd * 32 + kECap / 2) * 4;
+}
+
+// Everything the tile kernels need for one composition; ok = false if the inputs do not fit.
+struct TilePlan {
+  bool ok = false;
+  TileArgs s1, s2, cnt, emit;
+  int vr_rows = 0;
+  size_t smem_pull = 0, smem_count = 0, smem_emit = 0;
+  int grid_pull1 = 0, grid_pull2 = 0, grid_count = 0, grid_emit = 0;
+};
+
+fst_status tile_plan(fst* A, fst* B, int64_t pairs, bool want_prov, cudaStream_t s, TilePlan* P) {
+  P->ok = false;
+  const int mode = tile_mode_ref().load();
+  if (mode == 0 || want_prov) return FST_OK;
+  if (mode == 1 && pairs < kTileMinPairs) return FST_OK;
+  if (A->V < 1 || B->V < 1 || B->V > 65535) return FST_OK;
+  if (A->max_olabel > 252 || B->max_ilabel > 252) return FST_OK;
+  if (B->views[kOutByIlabel].max_deg + 1 > 32 || B->views[kInByIlabel].max_deg + 1 > 32) return FST_OK;
+  const int degA_out = A->views[kOutByOlabel].max_deg, degA_in = A->views[kInByOlabel].max_deg;
+  if (degA_out + 1 > kESlots || degA_in + 1 > kPSlots) return FST_OK;
+  const int wpr = (B->V + 31) / 32, bpr = (wpr + kWordsPerBlock - 1) / kWordsPerBlock;
+  const int smem_cap = smem_optin() - 4096;  // static shared memory of the kernels stays below 4 KB
+  const size_t smem_pull = (size_t)wpr * 256, smem_count = smem_pull + 8ull * kTRows * bpr;
+  if (smem_count > (size_t)smem_cap) return FST_OK;
+  const int wd_out = B->views[kOutByIlabel].max_deg + 1;
+  // emit: staged rank rows fill what the per-warp buffers leave
+  const size_t per_warp = (size_t)kEWarps * (2 * wd_out * 32 + kECap / 2) * 4;
+  if ((size_t)smem_cap <= per_warp) return FST_OK;
+  int vr_rows = (int)std::min<size_t>(kESlots + kTRows, ((size_t)smem_cap - per_warp) / ((size_t)wpr * 6 + 2));
+  while (vr_rows > 0 && tile_emit_smem(vr_rows, wpr, wd_out) > (size_t)smem_cap) --vr_rows;
+  if (vr_rows < degA_out + 2) return FST_OK;  // one row with its self slot must fit
+  fst_status st = ensure_tile_ell(B, 0, s);
+  if (!st) st = ensure_tile_ell(B, 1, s);
+  if (st) return st;
+  const int self = B->tile_ell[0].has_eps ? 1 : 0;  // same flag for both views (B ilabels)
+  auto side = [&](int which_a, int which_b) {
+    const View& v = A->views[which_a == 0 ? kOutByOlabel : kInByOlabel];
+    const fst::TileEll& T = B->tile_ell[which_b];
+    return TileSide{v.off, v.key, v.other, v.carry, v.w, T.ell, T.cw, T.wmax, T.wd};
+  };
+  const int byte1 = degA_out + self <= 8 ? 1 : 0, byte2 = degA_in + self <= 8 ? 1 : 0;
+  const int32_t* d;
+  int32_t nt;
+  st = tile_rows(A, 0, self, kPSlots, 0, byte1, s, &d, &nt);
+  if (st) return st;
+  P->s1 = TileArgs{side(0, 0), d, nt, self, byte1, 8};
+  P->cnt = P->s1;
+  st = tile_rows(A, 1, self, kPSlots, 0, byte2, s, &d, &nt);
+  if (st) return st;
+  P->s2 = TileArgs{side(1, 1), d, nt, self, byte2, 8};
+  st = tile_rows(A, 0, self, kESlots, vr_rows, 0, s, &d, &nt);
+  if (st) return st;
+  P->emit = TileArgs{side(0, 0), d, nt, self, 0, 8};
+  P->vr_rows = vr_rows;
+  P->smem_pull = smem_pull;
+  P->smem_count = smem_count;
+  P->smem_emit = tile_emit_smem(vr_rows, wpr, wd_out);
+  static bool attrs = false;
+  if (!attrs) {
+    const void* fs[] = {(const void*)k_tile_pull<false, 8>, (const void*)k_tile_pull<false, 16>,
+                        (const void*)k_tile_pull<true, 8>,  (const void*)k_tile_pull<true, 16>,
+                        (const void*)k_tile_count<false, 8>, (const void*)k_tile_count<false, 16>,
+                        (const void*)k_tile_count<true, 8>,  (const void*)k_tile_count<true, 16>,
+                        (const void*)k_tile_emit<8>,        (const void*)k_tile_emit<16>};
+    for (const void* f : fs) FSTC_CUDA_TRY(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_cap));
+    attrs = true;
+  }
+  P->s1.kj = B->tile_ell[0].wd - 1 <= 8 ? 8 : 16;
+  P->cnt.kj = P->s1.kj;
+  P->emit.kj = P->s1.kj;
+  P->s2.kj = B->tile_ell[1].wd - 1 <= 8 ? 8 : 16;
+  // one CTA per SM (the staged tables take the shared memory), never more CTAs than tiles
+  P->grid_pull1 = std::max(1, std::min(P->s1.ntiles, sm_count()));
+  P->grid_pull2 = std::max(1, std::min(P->s2.ntiles, sm_count()));
+  P->grid_count = std::max(1, std::min(P->cnt.ntiles, sm_count()));
+  P->grid_emit = std::max(1, std::min(P->emit.ntiles, sm_count()));
+  P->ok = true;
+  return FST_OK;
+}
+
+template <bool kStage2>
+void launch_tile_pull(const TileArgs& ta, int grid, size_t smem, cudaStream_t s, const Ctx& cx, int level) {
+  if (ta.kj == 8) k_tile_pull<kStage2, 8><<<grid, kTThreads, smem, s>>>(cx, ta, level);
+  else k_tile_pull<kStage2, 16><<<grid, kTThreads, smem, s>>>(cx, ta, level);
+}
+void launch_tile_count(const TileArgs& ta, int grid, size_t smem, cudaStream_t s, const Ctx& cx) {
+  if (ta.bytemode) {
+    if (ta.kj == 8) k_tile_count<true, 8><<<grid, kTThreads, smem, s>>>(cx, ta);
+    else k_tile_count<true, 16><<<grid, kTThreads, smem, s>>>(cx, ta);
+  } else {
+    if (ta.kj == 8) k_tile_count<false, 8><<<grid, kTThreads, smem, s>>>(cx, ta);
+    else k_tile_count<false, 16><<<grid, kTThreads, smem, s>>>(cx, ta);
+  }
+}
+void launch_tile_emit(const TileArgs& ta, int grid, size_t smem, cudaStream_t s, const Ctx& cx, const int64_t* tot,
+                      int vr_rows) {
+  if (ta.kj == 8) k_tile_emit<8><<<grid, kEThreads, smem, s>>>(cx, ta, tot, vr_rows);
+  else k_tile_emit<16><<<grid, kEThreads, smem, s>>>(cx, ta, tot, vr_rows);
+}
+
+// One BFS stage with per-level direction choice: push levels are k_level; a level whose frontier is a
+// sizable share of the stage's pairs (frontier * k >= total) runs bottom-up on the tile kernels.
+template <bool kStage2>
+fst_status run_stage_tile(const Ctx& cx, const TileArgs& ta, int grid_pull, size_t smem_pull, int64_t total,
+                          cudaStream_t s, unsigned long long* hp, int64_t* level_launches, std::vector<int64_t>* sizes,
+                          int* npull) {
+  const int64_t K = tile_pull_k();
+  const bool all_pull = tile_mode_ref().load() == 3;  // test mode: every level bottom-up
+  int level = 0;
+  for (;;) {
+    FSTC_CUDA_TRY(cudaMemcpyAsync(hp, &cx.ctrl[level % 3], sizeof(LevelCtrl), cudaMemcpyDeviceToHost, s));
+    FSTC_CUDA_TRY(cudaStreamSynchronize(s));
+    const unsigned long long cnt = hp[0], nf = hp[1], pad0 = hp[2];
+    if (cnt == 0) break;
+    const int64_t visited = (int64_t)(pad0 + nf);
+    const int64_t unvisited = total > visited ? total - visited : 0;
+    (void)unvisited;
+    if (all_pull || (int64_t)nf * K >= total) {
+      launch_tile_pull<kStage2>(ta, grid_pull, smem_pull, s, cx, level);
+      FSTC_LAUNCH_CHECK();
+      k_tile_merge<kStage2><<<sm_count() * 8, 256, 0, s>>>(cx, level);
+      FSTC_LAUNCH_CHECK();
+      ++*npull;
+    } else {
+      k_level<kStage2><<<g_grid, kThreads, kDynSmem, s>>>(cx, level);
+      FSTC_LAUNCH_CHECK();
+    }
+    ++*level_launches;
+    ++level;
+  }
+  FSTC_CUDA_TRY(cudaMemcpyAsync(hp, cx.misc, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+  FSTC_CUDA_TRY(cudaStreamSynchronize(s));
+  const int n = (int)std::min<unsigned long long>(hp[0], kMaxLevelStats);
+  std::vector<unsigned long long> tmp(n);
+  if (n) {
+    FSTC_CUDA_TRY(cudaMemcpyAsync(tmp.data(), cx.hist, sizeof(unsigned long long) * n, cudaMemcpyDeviceToHost, s));
+    FSTC_CUDA_TRY(cudaStreamSynchronize(s));
+  }
+  sizes->assign(tmp.begin(), tmp.end());
+  return FST_OK;
+}
+
 }  // namespace
+
+void tile_mode_set(int mode) { tile_mode_ref().store((mode >= 0 && mode <= 3) ? mode : 1); }
 
 std::vector<int64_t>& level_sizes_slot(fst* h, int stage);
 
@@ -2113,6 +2388,11 @@ fst_status compose_impl(int32_t n, const fst_handle* a, const fst_handle* b, cud
     seed2[i + 1] = seed2[i] + (int64_t)C.nStartA * C.nStartB;
   }
   const int64_t nwords = W, nblocks = K, nchunks = Q;
+  TilePlan tp;
+  if (n == 1) {  // single large compositions: bottom-up levels, count and emit on the tile kernels
+    st = tile_plan(a[0], b[0], pairs, want_prov, s, &tp);
+    if (st) return st;
+  }
   if (nblocks >= INT32_MAX || nchunks >= INT32_MAX) {
     set_error(FST_E_CAPACITY, "pair space too large (%lld blocks)", (long long)nblocks);
     return FST_E_CAPACITY;
@@ -2156,12 +2436,13 @@ fst_status compose_impl(int32_t n, const fst_handle* a, const fst_handle* b, cud
   cx.hist = (unsigned long long*)(base + ohist);
   cx.misc = (unsigned long long*)(base + omisc);
   cx.cnt8 = (uint8_t*)(base + ocnt8);
+  cx.warc = nullptr;  // set after stage 2 when the tile path runs (the push levels use cnt8 until then)
   CompDev* d_comps = (CompDev*)(base + ocomps);
   cx.comps = d_comps;
   cx.ncomp = n;
   for (int i = 0; i < n && i < kCompQ; ++i) cx.compQ[i] = comps[i].Q;
   cx.ptotal = pairs;
-  cx.pull_ok = (pull_enabled() && n == 1) ? 1 : 0;  // batches are many narrow problems (trellises)
+  cx.pull_ok = (pull_enabled() && n == 1 && !tp.ok) ? 1 : 0;  // batches are many narrow problems (trellises)
   cx.pull_num = pull_num();
   cx.nwords = nwords;
   cx.nblocks = nblocks;
@@ -2199,7 +2480,9 @@ fst_status compose_impl(int32_t n, const fst_handle* a, const fst_handle* b, cud
     if (seed1[n] > 0) {
       k_seed<false><<<nblk(seed1[n], 256), 256, 0, s>>>(cx);
       FSTC_LAUNCH_CHECK();
-      st = run_stage<false>(cx, s, hp, &level_launches, &sizes1);
+      st = tp.ok ? run_stage_tile<false>(cx, tp.s1, tp.grid_pull1, tp.smem_pull, pairs, s, hp, &level_launches,
+                                         &sizes1, &stats.pull_levels)
+                 : run_stage<false>(cx, s, hp, &level_launches, &sizes1);
       if (st) return st;
     }
     stats.levels_stage1 = (int32_t)sizes1.size();
@@ -2214,8 +2497,23 @@ fst_status compose_impl(int32_t n, const fst_handle* a, const fst_handle* b, cud
     if (seed2[n] > 0 && seed1[n] > 0) {
       k_seed<true><<<nblk(seed2[n], 256), 256, 0, s>>>(cx);
       FSTC_LAUNCH_CHECK();
-      st = run_stage<true>(cx, s, hp, &level_launches, &sizes2);
+      if (tp.ok) {
+        k_popcount<<<sm_count() * 4, 256, 0, s>>>(cx.R, nwords, cx.misc + 1);  // |R|: stage 2's unvisited set
+        FSTC_LAUNCH_CHECK();
+        FSTC_CUDA_TRY(cudaMemcpyAsync(hp + 8, cx.misc + 1, 8, cudaMemcpyDeviceToHost, s));
+        FSTC_CUDA_TRY(cudaStreamSynchronize(s));
+        stats.num_coaccessible = (int64_t)hp[8];
+        st = run_stage_tile<true>(cx, tp.s2, tp.grid_pull2, tp.smem_pull, (int64_t)hp[8], s, hp, &level_launches,
+                                  &sizes2, &stats.pull_levels);
+      } else {
+        st = run_stage<true>(cx, s, hp, &level_launches, &sizes2);
+      }
       if (st) return st;
+    }
+    if (tp.ok) {  // pass-1 counts of every block (the bottom-up levels do not count)
+      cx.warc = (uint32_t*)cx.cnt8;
+      launch_tile_count(tp.cnt, tp.grid_count, tp.smem_count, s, cx);
+      FSTC_LAUNCH_CHECK();
     }
     stats.levels_stage2 = (int32_t)sizes2.size();
     stats.ms_stage2 = t.stop();
@@ -2239,14 +2537,14 @@ fst_status compose_impl(int32_t n, const fst_handle* a, const fst_handle* b, cud
     if (st) return st;
     k_comp_bases<<<nblk(n + 1, 128), 128, 0, s>>>(cx, d_tot);
     FSTC_LAUNCH_CHECK();
-    if (prof) {
+    if (prof && !tp.ok) {
       k_popcount<<<sm_count() * 4, 256, 0, s>>>(cx.R, nwords, cx.misc + 1);
       FSTC_LAUNCH_CHECK();
     }
     FSTC_CUDA_TRY(cudaMemcpyAsync(tot.data(), d_tot, 8 * 2 * (n + 1), cudaMemcpyDeviceToHost, s));
     FSTC_CUDA_TRY(cudaMemcpyAsync(hp + 1, cx.misc + 1, 8, cudaMemcpyDeviceToHost, s));
     FSTC_CUDA_TRY(cudaStreamSynchronize(s));
-    if (prof) stats.num_coaccessible = (int64_t)hp[1];
+    if (prof || tp.ok) stats.num_coaccessible = (int64_t)hp[1];
     stats.ms_number = t.stop();
   }
   // ---- output allocation (one buffer per composition)
@@ -2312,7 +2610,8 @@ fst_status compose_impl(int32_t n, const fst_handle* a, const fst_handle* b, cud
   // ---- emit
   {
     EventTimer te(prof, s);
-    k_emit<<<g_grid, kThreads, kDynSmem, s>>>(cx, d_tot);
+    if (tp.ok) launch_tile_emit(tp.emit, tp.grid_emit, tp.smem_emit, s, cx, d_tot, tp.vr_rows);
+    else k_emit<<<g_grid, kThreads, kDynSmem, s>>>(cx, d_tot);
     FSTC_LAUNCH_CHECK();
     stats.ms_emit = te.stop();
     k_finish_rowptr<<<nblk(n, 128), 128, 0, s>>>(cx, d_tot);
@@ -2336,6 +2635,7 @@ fst_status compose_impl(int32_t n, const fst_handle* a, const fst_handle* b, cud
   stats.launches = fst_launch_count() - launches0;
   stats.expand_launches = level_launches;
   stats.emit_launches = 1;
+  stats.tile_path = tp.ok ? 1 : 0;
   for (int i = 0; i < n; ++i) {
     outs[i]->stats = stats;
     level_sizes_slot(outs[i], 1) = sizes1;

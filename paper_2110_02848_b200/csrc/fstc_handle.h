@@ -87,4 +87,22 @@ struct fst {
   int64_t shard_state_offset = 0, shard_arc_offset = 0, shard_total_states = 0, shard_total_arcs = 0;
   std::vector<int64_t> level_sizes[2];  // frontier size per BFS level, stage 1 / stage 2
   std::vector<fstc::BufferPtr> buffers;  // owned (or shared with a batch) device memory
+  // tile path caches (compose.cu / tile.cuh), built on first use; a handle is immutable
+  struct TileEll {  // B role: ELL of a view ([0] out-by-ilabel with (carry, weight), [1] in-by-ilabel)
+    bool ok = false;
+    fstc::BufferPtr buf;
+    uint32_t* ell = nullptr;
+    int2* cw = nullptr;
+    uint8_t* wmax = nullptr;
+    int32_t wd = 0;
+    bool has_eps = false;
+  } tile_ell[2];
+  struct TileRows {  // A role: tile row starts for (view, self slot, caps)
+    int64_t key = 0;
+    fstc::BufferPtr buf;
+    int32_t* d = nullptr;
+    int32_t n = 0;
+  };
+  std::vector<TileRows> tile_rows;
+  std::vector<int32_t> tile_hoff[2];  // host copy of the A-role view offsets ([0] out, [1] in by olabel)
 };

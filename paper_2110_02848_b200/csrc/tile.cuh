@@ -1,0 +1,701 @@
+// tile.cuh -- the "tile" kernels of a single large composition.  Included by
+// compose.cu inside its anonymous namespace (uses Ctx, CompDev, LevelCtrl, chunk_of).
+//
+// A TILE is a run of consecutive pair-space rows (A states) a_0..a_{X-1} (X <= 8) whose A arcs in one
+// A-role view fit in the SLOTS of a mask word M (64 for the bottom-up levels and the counts, 32 for the
+// emit; slot = one A arc, plus one "self" slot per row when B's view has eps items).  For every column
+// b (B state) the tile looks at the pairs (a_x, b) of all its rows at once:
+//   * lm[li]  (M): the slots whose A arc matches a B item of label index li
+//                  (li = 0: B's sentinel item "B stays" -> A arcs with olabel eps (M2);
+//                   li = 1: eps items -> A eps arcs (M1 eps:eps) and self slots (M3);
+//                   li = l + 2: label l; 255 = padding)
+//   * RT[b']  (M): the slot-transposed bitmap -- bit s = vis(row of slot s, b')
+//   * B items of b in an ELL [j][b] (column 0 = the sentinel "b itself"), packed (li << 24 | b')
+// so ONE shared load per (b, item) and an AND give the candidate moves of all X pairs into vis:
+//   hits = lm[li] & RT[b'];  pair (a_x, b) has a move into vis  <=>  hits & rowmask[x] != 0.
+// This is the frontier-parallel arc-pair exploration of PAPER.md:237-248 (§3.3) organised so that the
+// arc-pair test is word-parallel over the A side (64 slots per AND) instead of one thread per pair.
+// BYTE mode (every row of the view has <= 8 slots): row x owns slots [8x, 8x + 8), so per-row counts
+// are the byte popcounts of the hit word (SWAR).
+//
+// Kernels:
+//   k_tile_pull<false>  stage 1 bottom-up level (PAPER.md:108-111 backward BFS): unvisited pair
+//                       (~R) joins the next frontier iff one forward move lands in R.
+//   k_tile_pull<true>   stage 2 bottom-up level (Alg. 1 l.12-31, restricted to R): unvisited pair in
+//                       R \ V joins iff one predecessor (reversed move, in-views) is in V.
+//   k_tile_merge        vis |= next frontier; consumed frontier cleared; chunk lists for push levels.
+//   k_tile_count        pass-1 arc counts: kept moves per 1024-pair block.
+//   k_tile_emit         pass 2: writes the composed CSR at scan-derived slots.
+// Checking against V (R) instead of "the current frontier" is exact for unvisited pairs: a pair
+// with a predecessor (successor) visited at an earlier level would have been claimed then.
+
+constexpr int kTThreads = 1024;          // pull / count CTAs (1 per SM: the 64-bit RT takes the smem)
+constexpr int kTWarps = kTThreads / 32;
+constexpr int kEThreads = 1024;          // emit CTAs (1 per SM: the rank tables take the shared memory)
+constexpr int kEWarps = kEThreads / 32;
+constexpr int kPSlots = 64;              // slots of the pull / count tiles
+constexpr int kESlots = 32;              // slots of the emit tiles
+constexpr int kTRows = 8;
+constexpr int kTLab = 256;
+constexpr uint32_t kLiSent = 0u, kLiEps = 1u, kLiPad = 255u;
+constexpr int kECap = 256;               // per-warp arc-code buffer of the emit (arcs per flush)
+constexpr int kTileSmemMax = 200 * 1024;
+constexpr int kJReg = 16;                // ELL columns held in registers per word (more: a tail loop)
+
+struct TileSide {
+  // A-role view (slots): arcs of row a are [off[a], off[a+1])
+  const int32_t* off;
+  const int32_t* key;
+  const int32_t* other;
+  const int32_t* carry;
+  const float* w;
+  // B-role ELL
+  const uint32_t* ell;  // [wd][VB]
+  const int2* ellcw;    // [wd][VB] (carry, weight bits) of the arc behind ELL entry (emit)
+  const uint8_t* wmax;  // [wpr] ELL columns used by the 32 states of each word
+  int32_t wd;
+};
+
+struct TileArgs {
+  TileSide sd;
+  const int32_t* trow;  // [ntiles + 1]
+  int32_t ntiles;
+  int32_t self;         // one self slot per row (B view has eps items)
+  int32_t bytemode;     // row x owns slots [8x, 8x + 8)
+  int32_t kj;           // ELL columns held in registers (template instance: 8 or 16)
+};
+
+template <typename M>
+struct TileSmem {
+  M lm[kTLab];
+  int32_t srow[8 * sizeof(M)];
+  int32_t scarry[8 * sizeof(M)];
+  float sw[8 * sizeof(M)];
+  M rmask[kTRows];
+  M selfm;
+  int32_t r0, nr, ns;
+};
+
+__device__ __forceinline__ int popc_m(uint32_t x) { return __popc(x); }
+__device__ __forceinline__ int popc_m(unsigned long long x) { return __popcll(x); }
+__device__ __forceinline__ int ffs_m(uint32_t x) { return __ffs(x); }
+__device__ __forceinline__ int ffs_m(unsigned long long x) { return __ffsll((long long)x); }
+
+// lane i holds row i (bit j = element (i, j)); returns column `lane` (bit i = element (i, lane)).
+__device__ __forceinline__ uint32_t transpose32(uint32_t x, int lane) {
+#pragma unroll
+  for (int k = 16; k >= 1; k >>= 1) {
+    const uint32_t m = k == 16 ? 0x0000FFFFu : k == 8 ? 0x00FF00FFu : k == 4 ? 0x0F0F0F0Fu : k == 2 ? 0x33333333u : 0x55555555u;
+    const uint32_t y = __shfl_xor_sync(0xffffffffu, x, k);
+    x = (lane & k) ? ((x & ~m) | ((y >> k) & m)) : ((x & m) | ((y << k) & ~m));
+  }
+  return x;
+}
+
+// Slots and label masks of tile `tile` (all threads; ends with a barrier).
+template <typename M>
+__device__ void tile_slots(TileSmem<M>& t, const TileArgs& ta, int tile) {
+  constexpr int kS = 8 * sizeof(M);
+  for (int i = threadIdx.x; i < kTLab; i += blockDim.x) t.lm[i] = M(0);
+  if (threadIdx.x == 0) t.selfm = M(0);
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    const int32_t r0 = __ldg(&ta.trow[tile]), r1 = __ldg(&ta.trow[tile + 1]);
+    const int nr = r1 - r0;
+    int32_t e0 = 0, d = 0;
+    if (lane < nr) {
+      e0 = __ldg(&ta.sd.off[r0 + lane]);
+      d = __ldg(&ta.sd.off[r0 + lane + 1]) - e0;
+    }
+    const int n = lane < nr ? d + ta.self : 0;
+    int s0, ns;
+    if (ta.bytemode) {
+      s0 = 8 * lane;
+      ns = 8 * nr;
+      for (int s = lane; s < ns; s += 32) t.srow[s] = r0;  // unused slots: any valid row (never in lm)
+      __syncwarp();
+    } else {
+      const int inc = warp_incl_scan(n);
+      s0 = inc - n;
+      ns = __shfl_sync(0xffffffffu, inc, 31);
+    }
+    if (lane < nr) {
+      t.rmask[lane] = n >= kS ? ~M(0) : (((M(1) << n) - M(1)) << s0);
+      int s = s0;
+      if (ta.self) {
+        t.srow[s] = r0 + lane;
+        t.scarry[s] = FST_EPS;
+        t.sw[s] = 0.f;
+        atomicOr(&t.lm[kLiEps], M(1) << s);  // M3: B eps item, A stays
+        atomicOr(&t.selfm, M(1) << s);
+        ++s;
+      }
+      for (int k = 0; k < d; ++k, ++s) {
+        const int32_t e = e0 + k;
+        const int32_t l = __ldg(&ta.sd.key[e]);
+        t.srow[s] = __ldg(&ta.sd.other[e]);
+        t.scarry[s] = __ldg(&ta.sd.carry[e]);
+        t.sw[s] = __ldg(&ta.sd.w[e]);
+        atomicOr(&t.lm[l + 2], M(1) << s);                       // M1 (eps:eps included: l = -1 -> 1)
+        if (l == FST_EPS) atomicOr(&t.lm[kLiSent], M(1) << s);  // M2: A eps arc, B stays (sentinel)
+      }
+    }
+    if (lane == 0) {
+      t.r0 = r0;
+      t.nr = nr;
+      t.ns = ns;
+    }
+  }
+  __syncthreads();
+}
+
+// RT[b'] = bits over slots s of vis(srow[s], b'), for all columns (all threads; no barrier).  Each
+// warp issues the loads of 4 words before transposing them.
+__device__ __forceinline__ void tile_rt(uint32_t* RT, const TileSmem<uint32_t>& t, const uint32_t* __restrict__ vis,
+                                        int64_t W, int wpr, int nwarps) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint32_t* rowp = lane < t.ns ? vis + W + (int64_t)t.srow[lane] * wpr : nullptr;
+  for (int w0 = warp; w0 < wpr; w0 += 4 * nwarps) {
+    uint32_t x[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int w = w0 + u * nwarps;
+      x[u] = (rowp && w < wpr) ? __ldg(rowp + w) : 0u;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int w = w0 + u * nwarps;
+      const uint32_t c = transpose32(x[u], lane);
+      if (w < wpr) RT[w * 32 + lane] = c;
+    }
+  }
+}
+__device__ __forceinline__ void tile_rt(unsigned long long* RT, const TileSmem<unsigned long long>& t,
+                                        const uint32_t* __restrict__ vis, int64_t W, int wpr, int nwarps) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint32_t* rp0 = lane < t.ns ? vis + W + (int64_t)t.srow[lane] * wpr : nullptr;
+  const uint32_t* rp1 = lane + 32 < t.ns ? vis + W + (int64_t)t.srow[lane + 32] * wpr : nullptr;
+  for (int w0 = warp; w0 < wpr; w0 += 2 * nwarps) {
+    uint32_t x[4];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int w = w0 + u * nwarps;
+      x[2 * u] = (rp0 && w < wpr) ? __ldg(rp0 + w) : 0u;
+      x[2 * u + 1] = (rp1 && w < wpr) ? __ldg(rp1 + w) : 0u;
+    }
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int w = w0 + u * nwarps;
+      const uint32_t lo = transpose32(x[2 * u], lane), hi = transpose32(x[2 * u + 1], lane);
+      if (w < wpr) RT[w * 32 + lane] = ((unsigned long long)hi << 32) | lo;
+    }
+  }
+}
+
+// Ring bookkeeping of a level that runs on tile kernels (the same as k_level's block-0 prologue).
+__device__ __forceinline__ void tile_level_prologue(const Ctx& cx, int level) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    LevelCtrl* ctrl_cur = &cx.ctrl[level % 3];
+    LevelCtrl* ctrl_nxt = &cx.ctrl[(level + 1) % 3];
+    LevelCtrl* z = &cx.ctrl[(level + 2) % 3];
+    z->count = 0;
+    z->nnew = 0;
+    cx.misc[0] += 1;
+    if (level < kMaxLevelStats) cx.hist[level] = ctrl_cur->nnew;
+    ctrl_nxt->pad[0] = ctrl_cur->pad[0] + ctrl_cur->nnew;
+  }
+}
+
+// Fields of the (single) composition the tile kernels use, hoisted into registers (the kernels store
+// to global memory, so reads through cx.comps would be repeated after every store).
+struct TC {
+  int64_t W, K;
+  int32_t wpr, VB, bpr, VA;
+};
+__device__ __forceinline__ TC tc_of(const Ctx& cx) {
+  const CompDev& C = cx.comps[0];
+  return TC{C.W, C.K, C.wpr, C.VB, C.bpr, C.VA};
+}
+
+// Items of column b (ELL columns 1..jn-1; column 0, the sentinel, when j0 == 0): the first kJ
+// columns are loaded together into registers, the rest (rare) in a tail loop.  f(x) per item.
+template <int kJ, typename F>
+__device__ __forceinline__ void for_items(const uint32_t* __restrict__ ell, int VB, int b, int j0, int jn, F&& f) {
+  if (j0 == 0) f(__ldg(ell + b));
+  const uint32_t* p = ell + VB + b;
+  uint32_t it[kJ];
+#pragma unroll
+  for (int k = 0; k < kJ; ++k) {
+    it[k] = (k + 1 < jn) ? __ldg(p) : (kLiPad << 24);
+    p += VB;
+  }
+#pragma unroll
+  for (int k = 0; k < kJ; ++k) f(it[k]);
+  for (int j = kJ + 1; j < jn; ++j, p += VB) f(__ldg(p));
+}
+
+// ------------------------------------------------------------------------------ bottom-up level
+template <bool kStage2, int kJ>
+__global__ void __launch_bounds__(kTThreads, 1) k_tile_pull(Ctx cx, TileArgs ta, int level) {
+  using M = unsigned long long;
+  __shared__ TileSmem<M> t;
+  extern __shared__ __align__(16) unsigned long long tdyn64[];
+  M* RT = tdyn64;
+  tile_level_prologue(cx, level);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const TC c = tc_of(cx);
+  const uint32_t* __restrict__ vis = kStage2 ? cx.V : cx.R;
+  const uint32_t* __restrict__ Rb = cx.R;
+  uint32_t* Fn = (level & 1) ? cx.F0 : cx.F1;
+  const uint32_t* __restrict__ ell = ta.sd.ell;
+  const uint8_t* __restrict__ wmax = ta.sd.wmax;
+  const int wpr = c.wpr, VB = c.VB;
+  const uint32_t lastmask = (VB & 31) ? (1u << (VB & 31)) - 1u : ~0u;
+  auto unvisited = [&](int32_t row, int w) -> uint32_t {
+    const int64_t gw = c.W + (int64_t)row * wpr + w;
+    uint32_t u = kStage2 ? (__ldg(&Rb[gw]) & ~__ldg(&vis[gw])) : ~__ldg(&vis[gw]);
+    return w == wpr - 1 ? (u & lastmask) : u;
+  };
+  unsigned nnew = 0;
+  for (int tile = blockIdx.x; tile < ta.ntiles; tile += gridDim.x) {
+    tile_slots(t, ta, tile);
+    const int nr = t.nr;
+    const int32_t r0 = t.r0;
+    bool any = false;  // skip tiles whose rows are fully visited
+    for (int i = threadIdx.x; i < nr * wpr && !any; i += kTThreads) {
+      const int x = i / wpr;
+      any = unvisited(r0 + x, i - x * wpr) != 0u;
+    }
+    if (!__syncthreads_or(any)) continue;
+    tile_rt(RT, t, vis, c.W, wpr, kTWarps);
+    __syncthreads();
+    const int j0 = t.lm[kLiSent] ? 0 : 1;  // the sentinel column only matters with A eps arcs
+    M rm[kTRows];
+#pragma unroll
+    for (int x = 0; x < kTRows; ++x) rm[x] = x < nr ? t.rmask[x] : M(0);
+    const M* lm = t.lm;
+    uint32_t u = (warp < wpr && lane < nr) ? unvisited(r0 + lane, warp) : 0u;
+    for (int w = warp; w < wpr; w += kTWarps) {
+      const int wn = w + kTWarps;
+      const uint32_t un = (wn < wpr && lane < nr) ? unvisited(r0 + lane, wn) : 0u;  // next word, in flight
+      if (__any_sync(0xffffffffu, u != 0u)) {
+        const int b = w * 32 + lane;
+        M acc = M(0);
+        if (b < VB)
+          for_items<kJ>(ell, VB, b, j0, wmax[w], [&](uint32_t x) { acc |= lm[x >> 24] & RT[x & 0xFFFFFFu]; });
+        uint32_t mine = 0u;
+#pragma unroll
+        for (int x = 0; x < kTRows; ++x) {
+          if (x >= nr) break;
+          const uint32_t ux = __shfl_sync(0xffffffffu, u, x);
+          const uint32_t nb = __ballot_sync(0xffffffffu, (acc & rm[x]) != M(0)) & ux;
+          if (lane == x) mine = nb;
+        }
+        if (mine) {
+          Fn[c.W + (int64_t)(r0 + lane) * wpr + w] = mine;
+          nnew += __popc(mine);
+        }
+      }
+      u = un;
+    }
+    __syncthreads();
+  }
+  nnew = warp_sum(nnew);
+  if (lane == 0 && nnew) atomicAdd(&cx.ctrl[(level + 1) % 3].nnew, (unsigned long long)nnew);
+}
+
+// After a bottom-up level (one warp per chunk): vis |= next frontier; the consumed frontier and the
+// chunk flags are cleared; chunks with next-frontier bits are listed for a following push level.
+template <bool kStage2>
+__global__ void k_tile_merge(Ctx cx, int level) {
+  const int p = level & 1;
+  uint32_t* Fc = p ? cx.F1 : cx.F0;
+  const uint32_t* Fn = p ? cx.F0 : cx.F1;
+  uint32_t* flagc = p ? cx.flag1 : cx.flag0;
+  uint32_t* flagn = p ? cx.flag0 : cx.flag1;
+  int32_t* listn = p ? cx.list0 : cx.list1;
+  LevelCtrl* ctrl_nxt = &cx.ctrl[(level + 1) % 3];
+  uint32_t* vis = kStage2 ? cx.V : cx.R;
+  const int lane = threadIdx.x & 31;
+  const TC c = tc_of(cx);
+  const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const int32_t cpr = cx.comps[0].cpr, CB = cx.comps[0].CB;
+  for (int64_t q = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); q < cx.nchunks; q += nw) {
+    const int32_t row = (int32_t)(q / cpr), j = (int32_t)(q - (int64_t)row * cpr);
+    const int w0 = j * CB * 32, w1 = min(w0 + CB * 32, c.wpr);
+    const int64_t rw = c.W + (int64_t)row * c.wpr;
+    bool any = false;
+    for (int w = w0 + lane; w < w1; w += 32) {
+      const int64_t gw = rw + w;
+      if (Fc[gw]) Fc[gw] = 0u;
+      const uint32_t f = Fn[gw];
+      if (f) {
+        vis[gw] |= f;
+        any = true;
+      }
+    }
+    if (lane == 0) {
+      if (flagc[q]) flagc[q] = 0u;
+    }
+    if (__any_sync(0xffffffffu, any) && lane == 0) {
+      flagn[q] = 1u;
+      const unsigned long long pos = atomicAdd(&ctrl_nxt->count, 1ull);
+      listn[pos] = (int32_t)q;
+    }
+  }
+}
+
+// ------------------------------------------------------------------------------ pass 1: counts
+// kept[block] = number of moves out of the block's states of C (their out-degrees), OVERWRITTEN
+// for every block of the composition, and warc[word] = the same per word (the emit's offsets).
+// Tested against V (for a state of C, dst in R <=> dst in V).  Byte mode: per-row counts are SWAR
+// byte popcounts of the hit words (kByte).
+template <bool kByte, int kJ>
+__global__ void __launch_bounds__(kTThreads, 1) k_tile_count(Ctx cx, TileArgs ta) {
+  using M = unsigned long long;
+  __shared__ TileSmem<M> t;
+  extern __shared__ __align__(16) unsigned long long tdyn64[];
+  const TC c = tc_of(cx);
+  const int wpr = c.wpr, VB = c.VB, bpr = c.bpr;
+  M* RT = tdyn64;
+  unsigned long long* kacc = tdyn64 + (size_t)wpr * 32;  // [kTRows][bpr]
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint32_t* __restrict__ V = cx.V;
+  const uint32_t* __restrict__ ell = ta.sd.ell;
+  const uint8_t* __restrict__ wmax = ta.sd.wmax;
+  uint32_t* warc = cx.warc;
+  for (int tile = blockIdx.x; tile < ta.ntiles; tile += gridDim.x) {
+    tile_slots(t, ta, tile);
+    const int nr = t.nr;
+    const int32_t r0 = t.r0;
+    for (int i = threadIdx.x; i < kTRows * bpr; i += kTThreads) kacc[i] = 0ull;
+    tile_rt(RT, t, V, c.W, wpr, kTWarps);
+    __syncthreads();
+    const int j0 = t.lm[kLiSent] ? 0 : 1;
+    M rm[kTRows];
+#pragma unroll
+    for (int x = 0; x < kTRows; ++x) rm[x] = x < nr ? t.rmask[x] : M(0);
+    const M* lm = t.lm;
+    // warp task: a quarter of one block (8 words)
+    for (int task = warp; task < bpr * 4; task += kTWarps) {
+      const int jb = task >> 2;
+      const int w0 = jb * 32 + (task & 3) * 8, w1 = min(w0 + 8, wpr);
+      uint32_t sums[kTRows];
+#pragma unroll
+      for (int x = 0; x < kTRows; ++x) sums[x] = 0u;
+      uint32_t sv = (w0 < w1 && lane < nr) ? __ldg(&V[c.W + (int64_t)(r0 + lane) * wpr + w0]) : 0u;
+      for (int w = w0; w < w1; ++w) {
+        const uint32_t svn = (w + 1 < w1 && lane < nr) ? __ldg(&V[c.W + (int64_t)(r0 + lane) * wpr + w + 1]) : 0u;
+        uint32_t wc = 0u;  // lane x < nr: arcs of the states (row x, word w)
+        if (__any_sync(0xffffffffu, sv != 0u)) {
+          const int b = w * 32 + lane;
+          uint32_t cr[kTRows];
+#pragma unroll
+          for (int x = 0; x < kTRows; ++x) cr[x] = 0u;
+          if (b < VB) {
+            if (kByte) {
+              M bc = 0ull;  // 8 byte counters (row x = byte x); <= 31 items x 8 slots < 256
+              for_items<kJ>(ell, VB, b, j0, wmax[w], [&](uint32_t x) {
+                const M h = lm[x >> 24] & RT[x & 0xFFFFFFu];
+                M v = h - ((h >> 1) & 0x5555555555555555ull);
+                v = (v & 0x3333333333333333ull) + ((v >> 2) & 0x3333333333333333ull);
+                bc += (v + (v >> 4)) & 0x0F0F0F0F0F0F0F0Full;
+              });
+#pragma unroll
+              for (int x = 0; x < kTRows; ++x) cr[x] = (uint32_t)(bc >> (8 * x)) & 0xFFu;
+            } else {
+              for_items<kJ>(ell, VB, b, j0, wmax[w], [&](uint32_t x) {
+                const M h = lm[x >> 24] & RT[x & 0xFFFFFFu];
+#pragma unroll
+                for (int r = 0; r < kTRows; ++r) cr[r] += __popcll(h & rm[r]);
+              });
+            }
+          }
+#pragma unroll
+          for (int x = 0; x < kTRows; ++x) {
+            if (x >= nr) break;
+            const uint32_t sx = __shfl_sync(0xffffffffu, sv, x);
+            const uint32_t cx_ = ((sx >> lane) & 1u) ? cr[x] : 0u;
+            const uint32_t ws = warp_sum(cx_);
+            sums[x] += ws;
+            if (lane == x) wc = ws;
+          }
+        }
+        if (lane < nr) warc[c.W + (int64_t)(r0 + lane) * wpr + w] = wc;
+        sv = svn;
+      }
+#pragma unroll
+      for (int x = 0; x < kTRows; ++x) {
+        if (x >= nr) break;
+        if (lane == 0 && sums[x]) atomicAdd(&kacc[x * bpr + jb], (unsigned long long)sums[x]);
+      }
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < nr * bpr; i += kTThreads) {
+      const int x = i / bpr, jb = i - x * bpr;
+      cx.kept[c.K + (int64_t)(r0 + x) * bpr + jb] = kacc[x * bpr + jb];
+    }
+    __syncthreads();
+  }
+}
+
+// ------------------------------------------------------------------------------ pass 2: emit
+// Shared memory: for the tile's slots [0, ns) and source rows [ns, ns + nr): V words (u32) and
+// the rank of each word's first pair inside its row (u16), + per-row base ids; per warp: the word's
+// ELL items, the hit masks of its items and a buffer of arc codes (lane << 10 | item << 5 | slot).
+// One warp task = one word w (32 columns) for ALL rows of the tile: the word's items are loaded once
+// (registers + the warp's smem copy) and serve every row.  Row x's arcs of word w start at
+// arcbase[block] + warc[word] (k_tile_count / k_block_counts).  Per (row, word): walk 1 tests every
+// candidate against the staged V words and stores the per-item hit masks; a warp scan of the per-state
+// counts gives each state's first arc slot; walk 2 writes the arc codes in (state, item, slot) order;
+// then lanes take CONSECUTIVE arcs (coalesced streaming stores of dst / ilabel / olabel / weight).
+template <int kJ>
+__global__ void __launch_bounds__(kEThreads, 1) k_tile_emit(Ctx cx, TileArgs ta, const int64_t* __restrict__ tot,
+                                                             int vr_rows) {
+  __shared__ TileSmem<uint32_t> t;
+  __shared__ int32_t rbase[kESlots + kTRows];
+  extern __shared__ __align__(16) uint32_t tdyn[];
+  const TC c = tc_of(cx);
+  const CompDev& C = cx.comps[0];
+  int64_t* const row_ptr = C.row_ptr;
+  int32_t* const o_dst = C.dst;
+  int32_t* const o_il = C.ilabel;
+  int32_t* const o_ol = C.olabel;
+  float* const o_w = C.weight;
+  int32_t* const o_pa = C.pair_a;
+  int32_t* const o_pb = C.pair_b;
+  uint8_t* const o_st = C.is_start;
+  uint8_t* const o_ac = C.is_accept;
+  const uint8_t* __restrict__ startA = C.startA;
+  const uint8_t* __restrict__ accA = C.accA;
+  const uint8_t* __restrict__ startB = C.startB;
+  const uint8_t* __restrict__ accB = C.accB;
+  const int wpr = c.wpr, VB = c.VB, bpr = c.bpr, wd = ta.sd.wd;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t* Vw = tdyn;                                                 // [vr_rows * wpr]
+  uint16_t* Pw = (uint16_t*)(tdyn + (size_t)vr_rows * wpr);             // [vr_rows * wpr]
+  uint32_t* wbuf = tdyn + (size_t)vr_rows * wpr + ((size_t)vr_rows * wpr + 1) / 2;
+  uint32_t* its = wbuf + (size_t)warp * (2 * wd * 32 + kECap / 2);    // [wd][32] items of the word
+  uint32_t* hm = its + wd * 32;                                        // [wd][32] hit masks
+  uint16_t* code = (uint16_t*)(hm + wd * 32);                          // [kECap]
+  const int64_t id_comp = tot[0], arc_comp = tot[1];
+  const uint32_t* __restrict__ V = cx.V;
+  const uint32_t* __restrict__ ell = ta.sd.ell;
+  const int2* __restrict__ ellcw = ta.sd.ellcw;
+  const uint8_t* __restrict__ wmax = ta.sd.wmax;
+  const uint32_t* __restrict__ warc = cx.warc;
+  const int64_t* __restrict__ arcbase = cx.arcbase;
+  for (int tile = blockIdx.x; tile < ta.ntiles; tile += gridDim.x) {
+    tile_slots(t, ta, tile);
+    const int nr = t.nr, ns = t.ns;
+    const int32_t r0 = t.r0;
+    const int nk = ns + nr;
+    for (int i0 = threadIdx.x; i0 < nk * wpr; i0 += 4 * kEThreads) {
+      uint32_t v[4], pr[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int i = i0 + u * kEThreads;
+        v[u] = pr[u] = 0u;
+        if (i < nk * wpr) {
+          const int k = i / wpr, w = i - k * wpr;
+          const int32_t row = k < ns ? t.srow[k] : r0 + (k - ns);
+          const int64_t gw = c.W + (int64_t)row * wpr + w;
+          const int64_t kb = c.K + (int64_t)row * bpr;
+          v[u] = __ldg(&V[gw]);
+          pr[u] = (uint32_t)(__ldg(&cx.idbase[kb + (w >> 5)]) - __ldg(&cx.idbase[kb]) + __ldg(&cx.wpre[gw]));
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int i = i0 + u * kEThreads;
+        if (i < nk * wpr) {
+          Vw[i] = v[u];
+          Pw[i] = (uint16_t)pr[u];
+        }
+      }
+    }
+    for (int k = threadIdx.x; k < nk; k += kEThreads) {
+      const int32_t row = k < ns ? t.srow[k] : r0 + (k - ns);
+      rbase[k] = (int32_t)(__ldg(&cx.idbase[c.K + (int64_t)row * bpr]) - id_comp);
+    }
+    __syncthreads();
+    const int j0 = t.lm[kLiSent] ? 0 : 1;
+    const uint32_t selfm = t.selfm;
+    // per-lane constants of row `lane` (lanes < nr), broadcast per row
+    const uint8_t stA_l = lane < nr ? __ldg(&startA[r0 + lane]) : 0, acA_l = lane < nr ? __ldg(&accA[r0 + lane]) : 0;
+    const uint32_t rm_l = lane < nr ? t.rmask[lane] : 0u;
+    for (int w = warp; w < wpr; w += kEWarps) {
+      // lane x < nr: V word of (row x, w) and the arc base of its states
+      uint32_t vw_l = 0u;
+      int64_t base_l = 0;
+      int32_t exp_l = 0;  // arcs of (row lane, word w) by the counts (consistency check)
+      if (lane < nr) {
+        const int64_t gw = c.W + (int64_t)(r0 + lane) * wpr + w;
+        const int64_t blk = c.K + (int64_t)(r0 + lane) * bpr + (w >> 5);
+        vw_l = Vw[(size_t)(ns + lane) * wpr + w];
+        const uint32_t pre = __ldg(&warc[gw]);
+        base_l = __ldg(&arcbase[blk]) - arc_comp + pre;
+        const bool last = (w & 31) == 31 || w == wpr - 1;
+        exp_l = (int32_t)((last ? (uint32_t)__ldg(&cx.kept[blk]) : __ldg(&warc[gw + 1])) - pre);
+      }
+      if (!__any_sync(0xffffffffu, vw_l != 0u)) continue;
+      const int b = w * 32 + lane;
+      const bool inb = b < VB;
+      const int jn = wmax[w];
+      // the word's items: registers + the warp's smem copy (phase 3 reads other lanes' items)
+      uint32_t it[kJ + 1];
+      {
+        it[0] = (j0 == 0 && inb) ? __ldg(ell + b) : (kLiPad << 24);
+        const uint32_t* p = ell + VB + b;
+#pragma unroll
+        for (int k = 0; k < kJ; ++k) {
+          it[k + 1] = (inb && k + 1 < jn) ? __ldg(p) : (kLiPad << 24);
+          p += VB;
+        }
+#pragma unroll
+        for (int k = 0; k <= kJ; ++k)
+          if (k < jn) its[k * 32 + lane] = it[k];
+        for (int j = kJ + 1; j < jn; ++j) its[j * 32 + lane] = inb ? __ldg(ell + (size_t)j * VB + b) : (kLiPad << 24);
+      }
+      for (int x = 0; x < nr; ++x) {
+        const uint32_t vw = __shfl_sync(0xffffffffu, vw_l, x);
+        if (!vw) continue;
+        const int64_t run = __shfl_sync(0xffffffffu, base_l, x);
+        const uint32_t rmx = __shfl_sync(0xffffffffu, rm_l, x);
+        const bool act = (vw >> lane) & 1u;
+        // walk 1: per-item hit masks and the state's arc count
+        int cnt = 0;
+        auto walk1 = [&](int j, uint32_t xi) {
+          uint32_t m = act ? (t.lm[xi >> 24] & rmx) : 0u, h = 0u;
+          const uint32_t o = xi & 0xFFFFFFu;
+          const int ow = o >> 5;
+          const uint32_t ob = 1u << (o & 31);
+          while (m) {
+            const int s = __ffs(m) - 1;
+            m &= m - 1u;
+            if (Vw[s * wpr + ow] & ob) h |= 1u << s;
+          }
+          hm[j * 32 + lane] = h;
+          cnt += __popc(h);
+        };
+#pragma unroll
+        for (int k = 0; k <= kJ; ++k)
+          if (k < jn && k >= j0) walk1(k, it[k]);
+        for (int j = kJ + 1; j < jn; ++j) walk1(j, its[j * 32 + lane]);
+        const int inc = warp_incl_scan(cnt);
+        const int ex = inc - cnt;
+        const int T = __shfl_sync(0xffffffffu, inc, 31);
+        if (lane == x && T != exp_l) atomicAdd(&cx.misc[2], 1ull);
+        const int32_t row = r0 + x;
+        if (act) {  // the state's own outputs
+          const int32_t id = rbase[ns + x] + Pw[(size_t)(ns + x) * wpr + w] + __popc(vw & ((1u << lane) - 1u));
+          __stcs((long long*)&row_ptr[id], (long long)(run + ex));
+          __stcs(&o_pa[id], row);
+          __stcs(&o_pb[id], b);
+          o_st[id] = (uint8_t)(__shfl_sync(0xffffffffu, stA_l, x) & __ldg(&startB[b]));
+          o_ac[id] = (uint8_t)(__shfl_sync(0xffffffffu, acA_l, x) & __ldg(&accB[b]));
+        } else {
+          __shfl_sync(0xffffffffu, stA_l, x);
+          __shfl_sync(0xffffffffu, acA_l, x);
+        }
+        for (int p = 0; p < T; p += kECap) {
+          // walk 2: arc codes of positions [p, p + kECap)
+          if (cnt && ex < p + kECap && ex + cnt > p) {
+            int pos = ex;
+            for (int j = j0; j < jn && pos < p + kECap; ++j) {
+              uint32_t h = hm[j * 32 + lane];
+              const int nh = __popc(h);
+              if (pos + nh <= p) {
+                pos += nh;
+                continue;
+              }
+              while (h && pos < p + kECap) {
+                const int s = __ffs(h) - 1;
+                h &= h - 1u;
+                if (pos >= p) code[pos - p] = (uint16_t)((lane << 10) | (j << 5) | s);
+                ++pos;
+              }
+            }
+          }
+          __syncwarp();
+          const int n = min(kECap, T - p);
+          for (int i0 = lane; i0 < n; i0 += 64) {  // two arcs per lane in flight
+            int2 cw[2];
+            uint32_t cd[2];
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+              const int i = i0 + 32 * u;
+              cd[u] = i < n ? code[i] : 0u;
+              const int L = cd[u] >> 10, j = (cd[u] >> 5) & 31;
+              cw[u] = (i < n && j != 0) ? __ldg(ellcw + (size_t)j * VB + w * 32 + L) : make_int2(0, 0);
+            }
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+              const int i = i0 + 32 * u;
+              if (i >= n) break;
+              const int L = cd[u] >> 10, j = (cd[u] >> 5) & 31, s = cd[u] & 31;
+              const uint32_t o = its[j * 32 + L] & 0xFFFFFFu;
+              const uint32_t vword = Vw[s * wpr + (o >> 5)];
+              const int32_t did = rbase[s] + Pw[s * wpr + (o >> 5)] + __popc(vword & ((1u << (o & 31)) - 1u));
+              int32_t il, ol;
+              float wt;
+              if (j == 0) {  // M2: A eps arc, B stays (bit copy)
+                il = t.scarry[s];
+                ol = FST_EPS;
+                wt = t.sw[s];
+              } else if ((selfm >> s) & 1u) {  // M3: B eps arc, A stays (bit copy)
+                il = FST_EPS;
+                ol = cw[u].x;
+                wt = __int_as_float(cw[u].y);
+              } else {                         // M1: one binary32 add, RN-even
+                il = t.scarry[s];
+                ol = cw[u].x;
+                wt = __fadd_rn(t.sw[s], __int_as_float(cw[u].y));
+              }
+              const int64_t q = run + p + i;
+              __stcs(&o_dst[q], did);
+              __stcs(&o_il[q], il);
+              __stcs(&o_ol[q], ol);
+              __stcs(&o_w[q], wt);
+            }
+          }
+          __syncwarp();
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// B-role ELL of a view: column 0 = the sentinel item (b itself), columns 1.. = the node's arcs in
+// view order, padded; wmax[word] = columns used by the word's 32 nodes; *has_eps |= any eps key.
+__global__ void k_build_ell(int32_t V, const int32_t* __restrict__ off, const int32_t* __restrict__ key,
+                            const int32_t* __restrict__ other, const int2* __restrict__ cw, int wd, uint32_t* ell,
+                            int2* ellcw, uint8_t* wmax, int32_t* has_eps) {
+  const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  int d = 0;
+  bool eps = false;
+  if (b < V) {
+    const int32_t e0 = off[b];
+    d = off[b + 1] - e0;
+    ell[b] = (kLiSent << 24) | (uint32_t)b;
+    if (ellcw) ellcw[b] = make_int2(0, 0);
+    for (int j = 1; j < wd; ++j) {
+      const int k = j - 1;
+      if (k < d) {
+        const int32_t l = key[e0 + k];
+        eps |= l == FST_EPS;
+        ell[(size_t)j * V + b] = ((uint32_t)(l + 2) << 24) | (uint32_t)other[e0 + k];
+        if (ellcw) ellcw[(size_t)j * V + b] = cw[e0 + k];
+      } else {
+        ell[(size_t)j * V + b] = kLiPad << 24;
+        if (ellcw) ellcw[(size_t)j * V + b] = make_int2(0, 0);
+      }
+    }
+  }
+  const unsigned m = __reduce_max_sync(0xffffffffu, (unsigned)(b < V ? d + 1 : 0));
+  if (lane == 0 && b < V) wmax[b >> 5] = (uint8_t)m;
+  if (__any_sync(0xffffffffu, eps) && lane == 0) atomicOr(has_eps, 1);
+}
