@@ -2173,8 +2173,9 @@ fst_status tile_rows(fst* A, int which, int self, int slot_cap, int vr_cap, int 
 }
 
 size_t tile_emit_smem(int vr_rows, int wpr, int wd) {
+  (void)wd;
   const size_t vr = (size_t)vr_rows * wpr;
-  return 4 * vr + 4 * ((vr + 1) / 2) + (size_t)kEWarps * (2 * wd * 32 + kECap / 2) * 4;
+  return (size_t)wpr * 128 + 4 * vr + 4 * ((vr + 1) / 2) + (size_t)kEWarps * kECap * 4;
 }
 
 // Everything the tile kernels need for one composition; ok = false if the inputs do not fit.
@@ -2201,9 +2202,9 @@ fst_status tile_plan(fst* A, fst* B, int64_t pairs, bool want_prov, cudaStream_t
   const size_t smem_pull = (size_t)wpr * 256, smem_count = smem_pull + 8ull * kTRows * bpr;
   if (smem_count > (size_t)smem_cap) return FST_OK;
   const int wd_out = B->views[kOutByIlabel].max_deg + 1;
-  // emit: staged rank rows fill what the per-warp buffers leave
-  const size_t per_warp = (size_t)kEWarps * (2 * wd_out * 32 + kECap / 2) * 4;
-  if ((size_t)smem_cap <= per_warp) return FST_OK;
+  // emit: staged rank rows fill what RT and the per-warp code buffers leave
+  const size_t per_warp = (size_t)kEWarps * kECap * 4 + (size_t)wpr * 128;
+  if ((size_t)smem_cap <= per_warp || B->V > 65535) return FST_OK;
   int vr_rows = (int)std::min<size_t>(kESlots + kTRows, ((size_t)smem_cap - per_warp) / ((size_t)wpr * 6 + 2));
   while (vr_rows > 0 && tile_emit_smem(vr_rows, wpr, wd_out) > (size_t)smem_cap) --vr_rows;
   if (vr_rows < degA_out + 2) return FST_OK;  // one row with its self slot must fit
@@ -2270,10 +2271,12 @@ void launch_tile_count(const TileArgs& ta, int grid, size_t smem, cudaStream_t s
     else k_tile_count<false, 16><<<grid, kTThreads, smem, s>>>(cx, ta);
   }
 }
-void launch_tile_emit(const TileArgs& ta, int grid, size_t smem, cudaStream_t s, const Ctx& cx, const int64_t* tot,
-                      int vr_rows) {
-  if (ta.kj == 8) k_tile_emit<8><<<grid, kEThreads, smem, s>>>(cx, ta, tot, vr_rows);
-  else k_tile_emit<16><<<grid, kEThreads, smem, s>>>(cx, ta, tot, vr_rows);
+void launch_tile_emit(const TileArgs& ta, int grid, size_t smem, cudaStream_t s, const Ctx& cx, const CompDev& C,
+                      const int64_t* tot, int vr_rows) {
+  const EmitIO io{C.row_ptr, C.dst,    C.ilabel, C.olabel, C.weight, C.pair_a, C.pair_b,
+                  C.is_start, C.is_accept, C.startA, C.accA,  C.startB, C.accB};
+  if (ta.kj == 8) k_tile_emit<8><<<grid, kEThreads, smem, s>>>(cx, ta, io, tot, vr_rows);
+  else k_tile_emit<16><<<grid, kEThreads, smem, s>>>(cx, ta, io, tot, vr_rows);
 }
 
 // One BFS stage with per-level direction choice: push levels are k_level; a level whose frontier is a
@@ -2610,7 +2613,7 @@ fst_status compose_impl(int32_t n, const fst_handle* a, const fst_handle* b, cud
   // ---- emit
   {
     EventTimer te(prof, s);
-    if (tp.ok) launch_tile_emit(tp.emit, tp.grid_emit, tp.smem_emit, s, cx, d_tot, tp.vr_rows);
+    if (tp.ok) launch_tile_emit(tp.emit, tp.grid_emit, tp.smem_emit, s, cx, comps[0], d_tot, tp.vr_rows);
     else k_emit<<<g_grid, kThreads, kDynSmem, s>>>(cx, d_tot);
     FSTC_LAUNCH_CHECK();
     stats.ms_emit = te.stop();

@@ -38,7 +38,7 @@ constexpr int kESlots = 32;              // slots of the emit tiles
 constexpr int kTRows = 8;
 constexpr int kTLab = 256;
 constexpr uint32_t kLiSent = 0u, kLiEps = 1u, kLiPad = 255u;
-constexpr int kECap = 256;               // per-warp arc-code buffer of the emit (arcs per flush)
+constexpr int kECap = 192;               // per-warp arc-code buffer of the emit (arcs per flush)
 constexpr int kTileSmemMax = 200 * 1024;
 constexpr int kJReg = 16;                // ELL columns held in registers per word (more: a tail loop)
 
@@ -441,51 +441,48 @@ __global__ void __launch_bounds__(kTThreads, 1) k_tile_count(Ctx cx, TileArgs ta
 }
 
 // ------------------------------------------------------------------------------ pass 2: emit
-// Shared memory: for the tile's slots [0, ns) and source rows [ns, ns + nr): V words (u32) and
-// the rank of each word's first pair inside its row (u16), + per-row base ids; per warp: the word's
-// ELL items, the hit masks of its items and a buffer of arc codes (lane << 10 | item << 5 | slot).
-// One warp task = one word w (32 columns) for ALL rows of the tile: the word's items are loaded once
-// (registers + the warp's smem copy) and serve every row.  Row x's arcs of word w start at
-// arcbase[block] + warc[word] (k_tile_count / k_block_counts).  Per (row, word): walk 1 tests every
-// candidate against the staged V words and stores the per-item hit masks; a warp scan of the per-state
-// counts gives each state's first arc slot; walk 2 writes the arc codes in (state, item, slot) order;
-// then lanes take CONSECUTIVE arcs (coalesced streaming stores of dst / ilabel / olabel / weight).
+// Output / flag arrays of the composition, passed by value (constant bank, no registers).
+struct EmitIO {
+  int64_t* row_ptr;
+  int32_t* dst;
+  int32_t* ilabel;
+  int32_t* olabel;
+  float* weight;
+  int32_t* pair_a;
+  int32_t* pair_b;
+  uint8_t* is_start;
+  uint8_t* is_accept;
+  const uint8_t* startA;
+  const uint8_t* accA;
+  const uint8_t* startB;
+  const uint8_t* accB;
+};
+
+// Shared memory: RT (32-bit slot-transposed V of the tile's slot rows, for the hit tests), and for
+// the slot rows [0, ns) and source rows [ns, ns + nr) the V words (u32) and the rank of each word's
+// first pair inside its row (u16), + per-row base ids; per warp a buffer of kECap arc codes
+// (dst column << 15 | lane << 10 | item << 5 | slot).
+// One warp task = one word w (32 columns) for ALL rows of the tile: the word's ELL items are loaded
+// once into registers and serve every row.  Row x's arcs of word w start at arcbase[block] +
+// warc[word] (k_tile_count, k_block_counts).  Per (row, word): walk 1 -- one AND per item gives the
+// item's hit slots (lm[li] & RT[b'] & rowmask), kept in registers, a warp scan of the per-state counts
+// gives each state's first arc slot; walk 2 writes the arc codes in (state, item, slot) order; then
+// lanes take CONSECUTIVE arcs (coalesced streaming stores of dst / ilabel / olabel / weight).
 template <int kJ>
-__global__ void __launch_bounds__(kEThreads, 1) k_tile_emit(Ctx cx, TileArgs ta, const int64_t* __restrict__ tot,
-                                                             int vr_rows) {
+__global__ void __launch_bounds__(kEThreads, 1) k_tile_emit(Ctx cx, TileArgs ta, EmitIO io,
+                                                             const int64_t* __restrict__ tot, int vr_rows) {
   __shared__ TileSmem<uint32_t> t;
   __shared__ int32_t rbase[kESlots + kTRows];
   extern __shared__ __align__(16) uint32_t tdyn[];
   const TC c = tc_of(cx);
-  const CompDev& C = cx.comps[0];
-  int64_t* const row_ptr = C.row_ptr;
-  int32_t* const o_dst = C.dst;
-  int32_t* const o_il = C.ilabel;
-  int32_t* const o_ol = C.olabel;
-  float* const o_w = C.weight;
-  int32_t* const o_pa = C.pair_a;
-  int32_t* const o_pb = C.pair_b;
-  uint8_t* const o_st = C.is_start;
-  uint8_t* const o_ac = C.is_accept;
-  const uint8_t* __restrict__ startA = C.startA;
-  const uint8_t* __restrict__ accA = C.accA;
-  const uint8_t* __restrict__ startB = C.startB;
-  const uint8_t* __restrict__ accB = C.accB;
-  const int wpr = c.wpr, VB = c.VB, bpr = c.bpr, wd = ta.sd.wd;
+  const int wpr = c.wpr, VB = c.VB, bpr = c.bpr;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  uint32_t* Vw = tdyn;                                                 // [vr_rows * wpr]
-  uint16_t* Pw = (uint16_t*)(tdyn + (size_t)vr_rows * wpr);             // [vr_rows * wpr]
-  uint32_t* wbuf = tdyn + (size_t)vr_rows * wpr + ((size_t)vr_rows * wpr + 1) / 2;
-  uint32_t* its = wbuf + (size_t)warp * (2 * wd * 32 + kECap / 2);    // [wd][32] items of the word
-  uint32_t* hm = its + wd * 32;                                        // [wd][32] hit masks
-  uint16_t* code = (uint16_t*)(hm + wd * 32);                          // [kECap]
+  uint32_t* RT = tdyn;                                                  // [wpr * 32]
+  uint32_t* Vw = RT + (size_t)wpr * 32;                                 // [vr_rows * wpr]
+  uint16_t* Pw = (uint16_t*)(Vw + (size_t)vr_rows * wpr);                // [vr_rows * wpr]
+  uint32_t* code = Vw + (size_t)vr_rows * wpr + ((size_t)vr_rows * wpr + 1) / 2 + (size_t)warp * kECap;
   const int64_t id_comp = tot[0], arc_comp = tot[1];
   const uint32_t* __restrict__ V = cx.V;
-  const uint32_t* __restrict__ ell = ta.sd.ell;
-  const int2* __restrict__ ellcw = ta.sd.ellcw;
-  const uint8_t* __restrict__ wmax = ta.sd.wmax;
-  const uint32_t* __restrict__ warc = cx.warc;
-  const int64_t* __restrict__ arcbase = cx.arcbase;
   for (int tile = blockIdx.x; tile < ta.ntiles; tile += gridDim.x) {
     tile_slots(t, ta, tile);
     const int nr = t.nr, ns = t.ns;
@@ -520,102 +517,95 @@ __global__ void __launch_bounds__(kEThreads, 1) k_tile_emit(Ctx cx, TileArgs ta,
       rbase[k] = (int32_t)(__ldg(&cx.idbase[c.K + (int64_t)row * bpr]) - id_comp);
     }
     __syncthreads();
+    // RT from the staged slot rows (lane s reads row s: bank (s * wpr + w) % 32, conflict-free for odd wpr)
+    for (int w = warp; w < wpr; w += kEWarps) {
+      const uint32_t x = lane < ns ? Vw[lane * wpr + w] : 0u;
+      RT[w * 32 + lane] = transpose32(x, lane);
+    }
+    __syncthreads();
     const int j0 = t.lm[kLiSent] ? 0 : 1;
     const uint32_t selfm = t.selfm;
-    // per-lane constants of row `lane` (lanes < nr), broadcast per row
-    const uint8_t stA_l = lane < nr ? __ldg(&startA[r0 + lane]) : 0, acA_l = lane < nr ? __ldg(&accA[r0 + lane]) : 0;
+    const uint32_t* lm = t.lm;
+    const uint8_t stA_l = lane < nr ? __ldg(&io.startA[r0 + lane]) : 0, acA_l = lane < nr ? __ldg(&io.accA[r0 + lane]) : 0;
     const uint32_t rm_l = lane < nr ? t.rmask[lane] : 0u;
     for (int w = warp; w < wpr; w += kEWarps) {
-      // lane x < nr: V word of (row x, w) and the arc base of its states
+      // lane x < nr: V word of (row x, w), the arc base of its states and their arc count
       uint32_t vw_l = 0u;
       int64_t base_l = 0;
-      int32_t exp_l = 0;  // arcs of (row lane, word w) by the counts (consistency check)
+      int32_t exp_l = 0;
       if (lane < nr) {
         const int64_t gw = c.W + (int64_t)(r0 + lane) * wpr + w;
         const int64_t blk = c.K + (int64_t)(r0 + lane) * bpr + (w >> 5);
         vw_l = Vw[(size_t)(ns + lane) * wpr + w];
-        const uint32_t pre = __ldg(&warc[gw]);
-        base_l = __ldg(&arcbase[blk]) - arc_comp + pre;
+        const uint32_t pre = __ldg(&cx.warc[gw]);
+        base_l = __ldg(&cx.arcbase[blk]) - arc_comp + pre;
         const bool last = (w & 31) == 31 || w == wpr - 1;
-        exp_l = (int32_t)((last ? (uint32_t)__ldg(&cx.kept[blk]) : __ldg(&warc[gw + 1])) - pre);
+        exp_l = (int32_t)((last ? (uint32_t)__ldg(&cx.kept[blk]) : __ldg(&cx.warc[gw + 1])) - pre);
       }
       if (!__any_sync(0xffffffffu, vw_l != 0u)) continue;
       const int b = w * 32 + lane;
       const bool inb = b < VB;
-      const int jn = wmax[w];
-      // the word's items: registers + the warp's smem copy (phase 3 reads other lanes' items)
+      const int jn = ta.sd.wmax[w];
       uint32_t it[kJ + 1];
       {
-        it[0] = (j0 == 0 && inb) ? __ldg(ell + b) : (kLiPad << 24);
-        const uint32_t* p = ell + VB + b;
+        it[0] = (j0 == 0 && inb) ? __ldg(ta.sd.ell + b) : (kLiPad << 24);
+        const uint32_t* p = ta.sd.ell + VB + b;
 #pragma unroll
         for (int k = 0; k < kJ; ++k) {
           it[k + 1] = (inb && k + 1 < jn) ? __ldg(p) : (kLiPad << 24);
           p += VB;
         }
-#pragma unroll
-        for (int k = 0; k <= kJ; ++k)
-          if (k < jn) its[k * 32 + lane] = it[k];
-        for (int j = kJ + 1; j < jn; ++j) its[j * 32 + lane] = inb ? __ldg(ell + (size_t)j * VB + b) : (kLiPad << 24);
       }
       for (int x = 0; x < nr; ++x) {
         const uint32_t vw = __shfl_sync(0xffffffffu, vw_l, x);
-        if (!vw) continue;
         const int64_t run = __shfl_sync(0xffffffffu, base_l, x);
         const uint32_t rmx = __shfl_sync(0xffffffffu, rm_l, x);
-        const bool act = (vw >> lane) & 1u;
-        // walk 1: per-item hit masks and the state's arc count
+        const uint8_t stA = __shfl_sync(0xffffffffu, stA_l, x), acA = __shfl_sync(0xffffffffu, acA_l, x);
+        if (!vw) continue;
+        const uint32_t rmv = ((vw >> lane) & 1u) ? rmx : 0u;
+        // walk 1: hit slots of every item (registers) and the state's arc count
+        uint32_t h[kJ + 1];
         int cnt = 0;
-        auto walk1 = [&](int j, uint32_t xi) {
-          uint32_t m = act ? (t.lm[xi >> 24] & rmx) : 0u, h = 0u;
-          const uint32_t o = xi & 0xFFFFFFu;
-          const int ow = o >> 5;
-          const uint32_t ob = 1u << (o & 31);
-          while (m) {
-            const int s = __ffs(m) - 1;
-            m &= m - 1u;
-            if (Vw[s * wpr + ow] & ob) h |= 1u << s;
-          }
-          hm[j * 32 + lane] = h;
-          cnt += __popc(h);
-        };
 #pragma unroll
-        for (int k = 0; k <= kJ; ++k)
-          if (k < jn && k >= j0) walk1(k, it[k]);
-        for (int j = kJ + 1; j < jn; ++j) walk1(j, its[j * 32 + lane]);
+        for (int k = 0; k <= kJ; ++k) {
+          h[k] = lm[it[k] >> 24] & RT[it[k] & 0xFFFFFFu] & rmv;
+          cnt += __popc(h[k]);
+        }
+        for (int j = kJ + 1; j < jn; ++j) {  // (wide B rows: items beyond the registers)
+          const uint32_t xi = inb ? __ldg(ta.sd.ell + (size_t)j * VB + b) : (kLiPad << 24);
+          cnt += __popc(lm[xi >> 24] & RT[xi & 0xFFFFFFu] & rmv);
+        }
         const int inc = warp_incl_scan(cnt);
         const int ex = inc - cnt;
         const int T = __shfl_sync(0xffffffffu, inc, 31);
         if (lane == x && T != exp_l) atomicAdd(&cx.misc[2], 1ull);
         const int32_t row = r0 + x;
-        if (act) {  // the state's own outputs
+        if (rmv) {  // the state's own outputs
           const int32_t id = rbase[ns + x] + Pw[(size_t)(ns + x) * wpr + w] + __popc(vw & ((1u << lane) - 1u));
-          __stcs((long long*)&row_ptr[id], (long long)(run + ex));
-          __stcs(&o_pa[id], row);
-          __stcs(&o_pb[id], b);
-          o_st[id] = (uint8_t)(__shfl_sync(0xffffffffu, stA_l, x) & __ldg(&startB[b]));
-          o_ac[id] = (uint8_t)(__shfl_sync(0xffffffffu, acA_l, x) & __ldg(&accB[b]));
-        } else {
-          __shfl_sync(0xffffffffu, stA_l, x);
-          __shfl_sync(0xffffffffu, acA_l, x);
+          __stcs((long long*)&io.row_ptr[id], (long long)(run + ex));
+          __stcs(&io.pair_a[id], row);
+          __stcs(&io.pair_b[id], b);
+          io.is_start[id] = (uint8_t)(stA & __ldg(&io.startB[b]));
+          io.is_accept[id] = (uint8_t)(acA & __ldg(&io.accB[b]));
         }
         for (int p = 0; p < T; p += kECap) {
           // walk 2: arc codes of positions [p, p + kECap)
           if (cnt && ex < p + kECap && ex + cnt > p) {
             int pos = ex;
-            for (int j = j0; j < jn && pos < p + kECap; ++j) {
-              uint32_t h = hm[j * 32 + lane];
-              const int nh = __popc(h);
-              if (pos + nh <= p) {
-                pos += nh;
-                continue;
-              }
-              while (h && pos < p + kECap) {
-                const int s = __ffs(h) - 1;
-                h &= h - 1u;
-                if (pos >= p) code[pos - p] = (uint16_t)((lane << 10) | (j << 5) | s);
+            auto put = [&](int j, uint32_t hj, uint32_t xi) {
+              const uint32_t hi = ((xi & 0xFFFFu) << 15) | (lane << 10) | (j << 5);
+              while (hj) {
+                const int s = __ffs(hj) - 1;
+                hj &= hj - 1u;
+                if (pos >= p && pos < p + kECap) code[pos - p] = hi | s;
                 ++pos;
               }
+            };
+#pragma unroll
+            for (int k = 0; k <= kJ; ++k) put(k, h[k], it[k]);
+            for (int j = kJ + 1; j < jn; ++j) {
+              const uint32_t xi = inb ? __ldg(ta.sd.ell + (size_t)j * VB + b) : (kLiPad << 24);
+              put(j, lm[xi >> 24] & RT[xi & 0xFFFFFFu] & rmv, xi);
             }
           }
           __syncwarp();
@@ -627,15 +617,15 @@ __global__ void __launch_bounds__(kEThreads, 1) k_tile_emit(Ctx cx, TileArgs ta,
             for (int u = 0; u < 2; ++u) {
               const int i = i0 + 32 * u;
               cd[u] = i < n ? code[i] : 0u;
-              const int L = cd[u] >> 10, j = (cd[u] >> 5) & 31;
-              cw[u] = (i < n && j != 0) ? __ldg(ellcw + (size_t)j * VB + w * 32 + L) : make_int2(0, 0);
+              const int L = (cd[u] >> 10) & 31, j = (cd[u] >> 5) & 31;
+              cw[u] = (i < n && j != 0) ? __ldg(ta.sd.ellcw + (size_t)j * VB + w * 32 + L) : make_int2(0, 0);
             }
 #pragma unroll
             for (int u = 0; u < 2; ++u) {
               const int i = i0 + 32 * u;
               if (i >= n) break;
-              const int L = cd[u] >> 10, j = (cd[u] >> 5) & 31, s = cd[u] & 31;
-              const uint32_t o = its[j * 32 + L] & 0xFFFFFFu;
+              const uint32_t o = cd[u] >> 15;
+              const int j = (cd[u] >> 5) & 31, s = cd[u] & 31;
               const uint32_t vword = Vw[s * wpr + (o >> 5)];
               const int32_t did = rbase[s] + Pw[s * wpr + (o >> 5)] + __popc(vword & ((1u << (o & 31)) - 1u));
               int32_t il, ol;
@@ -654,10 +644,10 @@ __global__ void __launch_bounds__(kEThreads, 1) k_tile_emit(Ctx cx, TileArgs ta,
                 wt = __fadd_rn(t.sw[s], __int_as_float(cw[u].y));
               }
               const int64_t q = run + p + i;
-              __stcs(&o_dst[q], did);
-              __stcs(&o_il[q], il);
-              __stcs(&o_ol[q], ol);
-              __stcs(&o_w[q], wt);
+              __stcs(&io.dst[q], did);
+              __stcs(&io.ilabel[q], il);
+              __stcs(&io.olabel[q], ol);
+              __stcs(&io.weight[q], wt);
             }
           }
           __syncwarp();
