@@ -2201,6 +2201,7 @@ fst_status tile_plan(fst* A, fst* B, int64_t pairs, bool want_prov, cudaStream_t
   const int smem_cap = smem_optin() - 4096;  // static shared memory of the kernels stays below 4 KB
   const size_t smem_pull = (size_t)wpr * 256, smem_count = smem_pull + 8ull * kTRows * bpr;
   if (smem_count > (size_t)smem_cap) return FST_OK;
+  if ((bpr + 0) > 64) return FST_OK;  // the bottom-up rounds track <= 64 chunks per row
   const int wd_out = B->views[kOutByIlabel].max_deg + 1;
   // emit: staged rank rows fill what RT and the per-warp code buffers leave
   const size_t per_warp = (size_t)kEWarps * kECap * 4 + (size_t)wpr * 128;
@@ -2298,8 +2299,6 @@ fst_status run_stage_tile(const Ctx& cx, const TileArgs& ta, int grid_pull, size
     (void)unvisited;
     if (all_pull || (int64_t)nf * K >= total) {
       launch_tile_pull<kStage2>(ta, grid_pull, smem_pull, s, cx, level);
-      FSTC_LAUNCH_CHECK();
-      k_tile_merge<kStage2><<<sm_count() * 8, 256, 0, s>>>(cx, level);
       FSTC_LAUNCH_CHECK();
       ++*npull;
     } else {

@@ -19,15 +19,12 @@
 // are the byte popcounts of the hit word (SWAR).
 //
 // Kernels:
-//   k_tile_pull<false>  stage 1 bottom-up level (PAPER.md:108-111 backward BFS): unvisited pair
-//                       (~R) joins the next frontier iff one forward move lands in R.
-//   k_tile_pull<true>   stage 2 bottom-up level (Alg. 1 l.12-31, restricted to R): unvisited pair in
-//                       R \ V joins iff one predecessor (reversed move, in-views) is in V.
-//   k_tile_merge        vis |= next frontier; consumed frontier cleared; chunk lists for push levels.
-//   k_tile_count        pass-1 arc counts: kept moves per 1024-pair block.
+//   k_tile_pull<false>  stage 1 bottom-up round (PAPER.md:108-111 backward BFS): an unvisited pair
+//                       (~R) is claimed iff one forward move lands in R.
+//   k_tile_pull<true>   stage 2 bottom-up round (Alg. 1 l.12-31, restricted to R): an unvisited pair
+//                       in R \ V is claimed iff one predecessor (reversed move, in-views) is in V.
+//   k_tile_count        pass-1 arc counts: kept moves per 1024-pair block / word.
 //   k_tile_emit         pass 2: writes the composed CSR at scan-derived slots.
-// Checking against V (R) instead of "the current frontier" is exact for unvisited pairs: a pair
-// with a predecessor (successor) visited at an earlier level would have been claimed then.
 
 constexpr int kTThreads = 1024;          // pull / count CTAs (1 per SM: the 64-bit RT takes the smem)
 constexpr int kTWarps = kTThreads / 32;
@@ -172,7 +169,7 @@ __device__ __forceinline__ void tile_rt(uint32_t* RT, const TileSmem<uint32_t>& 
   }
 }
 __device__ __forceinline__ void tile_rt(unsigned long long* RT, const TileSmem<unsigned long long>& t,
-                                        const uint32_t* __restrict__ vis, int64_t W, int wpr, int nwarps) {
+                                        const uint32_t* vis, int64_t W, int wpr, int nwarps) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint32_t* rp0 = lane < t.ns ? vis + W + (int64_t)t.srow[lane] * wpr : nullptr;
   const uint32_t* rp1 = lane + 32 < t.ns ? vis + W + (int64_t)t.srow[lane + 32] * wpr : nullptr;
@@ -181,8 +178,8 @@ __device__ __forceinline__ void tile_rt(unsigned long long* RT, const TileSmem<u
 #pragma unroll
     for (int u = 0; u < 2; ++u) {
       const int w = w0 + u * nwarps;
-      x[2 * u] = (rp0 && w < wpr) ? __ldg(rp0 + w) : 0u;
-      x[2 * u + 1] = (rp1 && w < wpr) ? __ldg(rp1 + w) : 0u;
+      x[2 * u] = (rp0 && w < wpr) ? __ldca(rp0 + w) : 0u;  // (L1-cached; a stale word only delays a claim)
+      x[2 * u + 1] = (rp1 && w < wpr) ? __ldca(rp1 + w) : 0u;
     }
 #pragma unroll
     for (int u = 0; u < 2; ++u) {
@@ -210,12 +207,12 @@ __device__ __forceinline__ void tile_level_prologue(const Ctx& cx, int level) {
 // Fields of the (single) composition the tile kernels use, hoisted into registers (the kernels store
 // to global memory, so reads through cx.comps would be repeated after every store).
 struct TC {
-  int64_t W, K;
-  int32_t wpr, VB, bpr, VA;
+  int64_t W, K, Q;
+  int32_t wpr, VB, bpr, VA, cpr, CB;
 };
 __device__ __forceinline__ TC tc_of(const Ctx& cx) {
   const CompDev& C = cx.comps[0];
-  return TC{C.W, C.K, C.wpr, C.VB, C.bpr, C.VA};
+  return TC{C.W, C.K, C.Q, C.wpr, C.VB, C.bpr, C.VA, C.cpr, C.CB};
 }
 
 // Items of column b (ELL columns 1..jn-1; column 0, the sentinel, when j0 == 0): the first kJ
@@ -235,26 +232,43 @@ __device__ __forceinline__ void for_items(const uint32_t* __restrict__ ell, int 
   for (int j = kJ + 1; j < jn; ++j, p += VB) f(__ldg(p));
 }
 
-// ------------------------------------------------------------------------------ bottom-up level
+// ------------------------------------------------------------------------------ bottom-up round
+// One bottom-up round, IN PLACE: an unvisited pair of the tile's rows whose move set hits vis is
+// claimed (vis |= new, next frontier |= new) right away, so tiles staged later in the same round see it
+// and a round can claim pairs several BFS distances deep.  R and V are sets (Alg. 1 line 3; the
+// forward closure restricted to R): claiming a pair as soon as one move reaches the set is sound, and
+// the stage loop runs until a round claims nothing (the fixed point), so the sets are exact.  Only the
+// per-round sizes differ from per-BFS-distance counts.  Each tile also consumes the current frontier
+// words and chunk flags of its rows and lists the chunks that gained next-frontier bits (for a
+// following push level), so no separate merge pass is needed.
 template <bool kStage2, int kJ>
 __global__ void __launch_bounds__(kTThreads, 1) k_tile_pull(Ctx cx, TileArgs ta, int level) {
   using M = unsigned long long;
   __shared__ TileSmem<M> t;
+  __shared__ uint32_t chit[kTRows][2];  // per tile row: chunks (<= 64) that gained next-frontier bits
+  __shared__ int s_any;
   extern __shared__ __align__(16) unsigned long long tdyn64[];
   M* RT = tdyn64;
   tile_level_prologue(cx, level);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const TC c = tc_of(cx);
-  const uint32_t* __restrict__ vis = kStage2 ? cx.V : cx.R;
-  const uint32_t* __restrict__ Rb = cx.R;
-  uint32_t* Fn = (level & 1) ? cx.F0 : cx.F1;
+  uint32_t* vis = kStage2 ? cx.V : cx.R;   // read and written in place (plain loads: other CTAs write it)
+  const uint32_t* __restrict__ Rb = cx.R;  // stage 2: R is fixed
+  const int p = level & 1;
+  uint32_t* Fc = p ? cx.F1 : cx.F0;
+  uint32_t* Fn = p ? cx.F0 : cx.F1;
+  uint32_t* flagc = p ? cx.flag1 : cx.flag0;
+  uint32_t* flagn = p ? cx.flag0 : cx.flag1;
+  int32_t* listn = p ? cx.list0 : cx.list1;
+  LevelCtrl* ctrl_nxt = &cx.ctrl[(level + 1) % 3];
   const uint32_t* __restrict__ ell = ta.sd.ell;
   const uint8_t* __restrict__ wmax = ta.sd.wmax;
   const int wpr = c.wpr, VB = c.VB;
   const uint32_t lastmask = (VB & 31) ? (1u << (VB & 31)) - 1u : ~0u;
   auto unvisited = [&](int32_t row, int w) -> uint32_t {
     const int64_t gw = c.W + (int64_t)row * wpr + w;
-    uint32_t u = kStage2 ? (__ldg(&Rb[gw]) & ~__ldg(&vis[gw])) : ~__ldg(&vis[gw]);
+    const uint32_t v = __ldca(&vis[gw]);
+    uint32_t u = kStage2 ? (__ldg(&Rb[gw]) & ~v) : ~v;
     return w == wpr - 1 ? (u & lastmask) : u;
   };
   unsigned nnew = 0;
@@ -262,88 +276,72 @@ __global__ void __launch_bounds__(kTThreads, 1) k_tile_pull(Ctx cx, TileArgs ta,
     tile_slots(t, ta, tile);
     const int nr = t.nr;
     const int32_t r0 = t.r0;
-    bool any = false;  // skip tiles whose rows are fully visited
-    for (int i = threadIdx.x; i < nr * wpr && !any; i += kTThreads) {
-      const int x = i / wpr;
-      any = unvisited(r0 + x, i - x * wpr) != 0u;
-    }
-    if (!__syncthreads_or(any)) continue;
-    tile_rt(RT, t, vis, c.W, wpr, kTWarps);
+    if (threadIdx.x < 2 * kTRows) chit[threadIdx.x >> 1][threadIdx.x & 1] = 0u;
+    if (threadIdx.x == 0) s_any = 0;
     __syncthreads();
-    const int j0 = t.lm[kLiSent] ? 0 : 1;  // the sentinel column only matters with A eps arcs
-    M rm[kTRows];
+    // consume the rows' frontier words; any unvisited pair left?
+    bool any = false;
+    for (int i = threadIdx.x; i < nr * wpr; i += kTThreads) {
+      const int x = i / wpr, w = i - x * wpr;
+      const int64_t gw = c.W + (int64_t)(r0 + x) * wpr + w;
+      if (Fc[gw]) Fc[gw] = 0u;
+      any |= unvisited(r0 + x, w) != 0u;
+    }
+    if (any) s_any = 1;
+    __syncthreads();
+    if (s_any) {
+      tile_rt(RT, t, vis, c.W, wpr, kTWarps);
+      __syncthreads();
+      const int j0 = t.lm[kLiSent] ? 0 : 1;  // the sentinel column only matters with A eps arcs
+      M rm[kTRows];
 #pragma unroll
-    for (int x = 0; x < kTRows; ++x) rm[x] = x < nr ? t.rmask[x] : M(0);
-    const M* lm = t.lm;
-    uint32_t u = (warp < wpr && lane < nr) ? unvisited(r0 + lane, warp) : 0u;
-    for (int w = warp; w < wpr; w += kTWarps) {
-      const int wn = w + kTWarps;
-      const uint32_t un = (wn < wpr && lane < nr) ? unvisited(r0 + lane, wn) : 0u;  // next word, in flight
-      if (__any_sync(0xffffffffu, u != 0u)) {
-        const int b = w * 32 + lane;
-        M acc = M(0);
-        if (b < VB)
-          for_items<kJ>(ell, VB, b, j0, wmax[w], [&](uint32_t x) { acc |= lm[x >> 24] & RT[x & 0xFFFFFFu]; });
-        uint32_t mine = 0u;
+      for (int x = 0; x < kTRows; ++x) rm[x] = x < nr ? t.rmask[x] : M(0);
+      const M* lm = t.lm;
+      uint32_t u = (warp < wpr && lane < nr) ? unvisited(r0 + lane, warp) : 0u;
+      for (int w = warp; w < wpr; w += kTWarps) {
+        const int wn = w + kTWarps;
+        const uint32_t un = (wn < wpr && lane < nr) ? unvisited(r0 + lane, wn) : 0u;  // next word, in flight
+        if (__any_sync(0xffffffffu, u != 0u)) {
+          const int b = w * 32 + lane;
+          M acc = M(0);
+          if (b < VB)
+            for_items<kJ>(ell, VB, b, j0, wmax[w], [&](uint32_t x) { acc |= lm[x >> 24] & RT[x & 0xFFFFFFu]; });
+          uint32_t mine = 0u;
 #pragma unroll
-        for (int x = 0; x < kTRows; ++x) {
-          if (x >= nr) break;
-          const uint32_t ux = __shfl_sync(0xffffffffu, u, x);
-          const uint32_t nb = __ballot_sync(0xffffffffu, (acc & rm[x]) != M(0)) & ux;
-          if (lane == x) mine = nb;
+          for (int x = 0; x < kTRows; ++x) {
+            if (x >= nr) break;
+            const uint32_t ux = __shfl_sync(0xffffffffu, u, x);
+            const uint32_t nb = __ballot_sync(0xffffffffu, (acc & rm[x]) != M(0)) & ux;
+            if (lane == x) mine = nb;
+          }
+          if (mine) {  // lane x: claim the new pairs of (row x, w) in place
+            const int64_t gw = c.W + (int64_t)(r0 + lane) * wpr + w;
+            vis[gw] = __ldca(&vis[gw]) | mine;  // only this tile writes its rows
+            Fn[gw] = mine;
+            nnew += __popc(mine);
+            const int qj = (w >> 5) / c.CB;
+            atomicOr(&chit[lane][qj >> 5], 1u << (qj & 31));
+          }
         }
-        if (mine) {
-          Fn[c.W + (int64_t)(r0 + lane) * wpr + w] = mine;
-          nnew += __popc(mine);
-        }
+        u = un;
       }
-      u = un;
+    }
+    __syncthreads();
+    // chunk flags of the tile's rows: consumed ones cleared, chunks with new bits listed
+    for (int i = threadIdx.x; i < nr * c.cpr; i += kTThreads) {
+      const int x = i / c.cpr, j = i - x * c.cpr;
+      const int64_t q = c.Q + (int64_t)(r0 + x) * c.cpr + j;
+      if (flagc[q]) flagc[q] = 0u;
+      if ((chit[x][j >> 5] >> (j & 31)) & 1u) {
+        flagn[q] = 1u;
+        const unsigned long long pos = atomicAdd(&ctrl_nxt->count, 1ull);
+        listn[pos] = (int32_t)q;
+      }
     }
     __syncthreads();
   }
   nnew = warp_sum(nnew);
-  if (lane == 0 && nnew) atomicAdd(&cx.ctrl[(level + 1) % 3].nnew, (unsigned long long)nnew);
-}
-
-// After a bottom-up level (one warp per chunk): vis |= next frontier; the consumed frontier and the
-// chunk flags are cleared; chunks with next-frontier bits are listed for a following push level.
-template <bool kStage2>
-__global__ void k_tile_merge(Ctx cx, int level) {
-  const int p = level & 1;
-  uint32_t* Fc = p ? cx.F1 : cx.F0;
-  const uint32_t* Fn = p ? cx.F0 : cx.F1;
-  uint32_t* flagc = p ? cx.flag1 : cx.flag0;
-  uint32_t* flagn = p ? cx.flag0 : cx.flag1;
-  int32_t* listn = p ? cx.list0 : cx.list1;
-  LevelCtrl* ctrl_nxt = &cx.ctrl[(level + 1) % 3];
-  uint32_t* vis = kStage2 ? cx.V : cx.R;
-  const int lane = threadIdx.x & 31;
-  const TC c = tc_of(cx);
-  const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
-  const int32_t cpr = cx.comps[0].cpr, CB = cx.comps[0].CB;
-  for (int64_t q = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); q < cx.nchunks; q += nw) {
-    const int32_t row = (int32_t)(q / cpr), j = (int32_t)(q - (int64_t)row * cpr);
-    const int w0 = j * CB * 32, w1 = min(w0 + CB * 32, c.wpr);
-    const int64_t rw = c.W + (int64_t)row * c.wpr;
-    bool any = false;
-    for (int w = w0 + lane; w < w1; w += 32) {
-      const int64_t gw = rw + w;
-      if (Fc[gw]) Fc[gw] = 0u;
-      const uint32_t f = Fn[gw];
-      if (f) {
-        vis[gw] |= f;
-        any = true;
-      }
-    }
-    if (lane == 0) {
-      if (flagc[q]) flagc[q] = 0u;
-    }
-    if (__any_sync(0xffffffffu, any) && lane == 0) {
-      flagn[q] = 1u;
-      const unsigned long long pos = atomicAdd(&ctrl_nxt->count, 1ull);
-      listn[pos] = (int32_t)q;
-    }
-  }
+  if (lane == 0 && nnew) atomicAdd(&ctrl_nxt->nnew, (unsigned long long)nnew);
 }
 
 // ------------------------------------------------------------------------------ pass 1: counts
