@@ -41,7 +41,8 @@ WORKLOADS = {
     "c5": ("configs[4] batched lexicon x emissions: closure(10k-word letter lexicon) composed with "
            "32 emissions graphs per GPU (T_i = 100 + rand(401), 28 tokens), fst_compose_batch", 0, 0, 28),
 }
-REF_SAMPLE_V = {"c4": 1024, "c4-d4": 2048, "c4-paper": 1024, "fig3b-d16": 256, "fig3b-d64": 256}  # oracle sample sizes (~2-8 s per step)
+# oracle sample sizes: one composition of the same generator at this V takes a few seconds on one core
+REF_SAMPLE_V = {"c4": 3072, "c4-d4": 4096, "c4-paper": 2048, "fig3b-d16": 256, "fig3b-d64": 256}
 UTTS_PER_GPU = 32
 L2_FLUSH_BYTES = 512 << 20
 
@@ -72,12 +73,37 @@ SEED_OFFSET = {"c4-paper": 2}
 REF_SEED_OFFSET = {"c4-paper": 2, "c4-d4": 1}  # the oracle samples: offset 0 of c4-d4's V=2048 sample is empty too
 
 
-def make_inputs(workload: str, rank: int):
+def host_info():
+    """CPU model and the cores this process may run on (the oracle baselines say which they used)."""
+    model = "unknown"
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                model = ln.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"cpu_model": model, "affinity_cores": len(os.sched_getaffinity(0))}
+
+
+def input_seeds(workload: str, rank: int, bump: int = 0):
+    _, V, D, _ = WORKLOADS[workload]
+    o = SEED_OFFSET.get(workload, 0) + bump
+    return 1000 + V + D + o + 100003 * rank, 2000 + V + D + o + 100003 * rank
+
+
+def workload_config(workload: str, As, B):
+    """The `config` of both arms' JSON lines (inputs only, no results: the arms must agree)."""
+    return {"workload": WORKLOADS[workload][0], "compositions_per_gpu": len(As),
+            "V_A": sum(A.num_states for A in As), "V_B": B.num_states,
+            "E_A": sum(A.num_arcs for A in As), "E_B": B.num_arcs,
+            "pair_space": sum(A.num_states * B.num_states for A in As)}
+
+
+def make_inputs(workload: str, rank: int, bump: int = 0):
     _, V, D, T = WORKLOADS[workload]
-    o = SEED_OFFSET.get(workload, 0)
-    A = fstgen.random_graph(V, D, T, 1000 + V + D + o + 100003 * rank)
-    B = fstgen.random_graph(V, D, T, 2000 + V + D + o + 100003 * rank)
-    return A, B
+    sa, sb = input_seeds(workload, rank, bump)
+    return fstgen.random_graph(V, D, T, sa), fstgen.random_graph(V, D, T, sb)
 
 
 class ClockSampler:
@@ -144,6 +170,12 @@ def run_reference(args):
         return 0
     import oracle
     oracle.build()
+    if args.workload == "c5":
+        As_w, B_w, _ = c5_shard(0, world)
+    else:
+        A_w, B_w = make_inputs(args.workload, 0)
+        As_w = [A_w]
+    config = workload_config(args.workload, As_w, B_w)
     A, B, sample = reference_sample(args.workload)
     for _ in range(args.warmup):
         oracle.compose(A, B)
@@ -160,10 +192,12 @@ def run_reference(args):
         "impl": "reference", "metric": "composed arcs/sec", "value": value, "unit": "arcs/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": WORKLOADS[args.workload][0], "sample": f"{sample}: {arcs} composed arcs per step",
-                   "parallelism": "single host thread"},
-        "cpu_baseline": {"value": value, "unit": "arcs/s", "cores": cores, "kind": "oracle",
-                         "sample": f"Algorithm 1 C oracle on {sample}, {arcs} arcs/step, single-threaded"},
+        "config": config,
+        "parallelism": "single host thread",
+        "cpu_baseline": {"value": value, "unit": "arcs/s", "cores": cores, "kind": "oracle", **host_info(),
+                         "sample": f"each step: the Algorithm 1 C oracle on {sample}, {arcs} composed arcs, "
+                                   f"single-threaded (a bounded sample of the workload: the full configuration "
+                                   f"takes minutes per composition on one core, see DESIGN.md section 9)"},
         "e2e": {"value": value, "unit": "arcs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -184,9 +218,39 @@ def reference_sample(workload: str):
 
 
 # ------------------------------------------------------------------------------------ our arm
+def _oracle_arcs(pair):
+    import oracle
+    A, B = pair
+    t0 = time.perf_counter()
+    C = oracle.compose(A, B)
+    return int(C["num_arcs"]), time.perf_counter() - t0
+
+
+def cpu_baseline_pool(budget_utts: int = 32):
+    """configs[4]: independent utterances over ALL host cores (process pool), SURVEY 8(d) d.6."""
+    import multiprocessing as mp
+    import oracle
+    oracle.build()
+    As, B, _ = c5_shard(0, 1)
+    As = As[:budget_utts]
+    cores = len(os.sched_getaffinity(0))
+    t0 = time.perf_counter()
+    with mp.get_context("fork").Pool(cores) as pool:
+        res = pool.map(_oracle_arcs, [(A, B) for A in As])
+    wall = time.perf_counter() - t0
+    arcs = sum(r[0] for r in res)
+    single = sum(r[1] for r in res) / len(res)
+    return {"value": arcs / wall, "unit": "arcs/s", "cores": cores, "kind": "oracle", **host_info(),
+            "sample": f"{len(As)} utterances of the configs[4] batch o closure(10k-word lexicon), one Algorithm 1 "
+                      f"C oracle composition per utterance in a process pool over {cores} cores "
+                      f"({wall:.1f} s wall; {single:.2f} s per utterance on one core)"}
+
+
 def cpu_baseline(workload: str, budget_s: float = 12.0):
     import oracle
     oracle.build()
+    if workload == "c5":
+        return cpu_baseline_pool()
     A, B, sample = reference_sample(workload)
     t_end = time.perf_counter() + budget_s
     n, tot, arcs = 0, 0.0, 0
@@ -198,7 +262,7 @@ def cpu_baseline(workload: str, budget_s: float = 12.0):
         n += 1
         if n >= 20:
             break
-    return {"value": arcs * n / tot, "unit": "arcs/s", "cores": 1, "kind": "oracle",
+    return {"value": arcs * n / tot, "unit": "arcs/s", "cores": 1, "kind": "oracle", **host_info(),
             "sample": f"{n} runs of the Algorithm 1 C oracle on {sample}, {arcs} composed arcs each, "
                       f"single host thread"}
 
@@ -229,7 +293,18 @@ def run_ours(args):
         parallelism = (f"{world} rank(s); the {UTTS_PER_GPU * world}-utterance batch LPT-sharded by frames "
                        f"(this rank: {len(As)} utterances, one fst_compose_batch call)")
     else:
-        A, B = make_inputs(args.workload, rank)
+        # every rank times a NONEMPTY instance: the first seed offset (0, 1, ...) whose composition has arcs
+        # (random instances can have no co-accessible start pair, see SEED_OFFSET)
+        bump = 0
+        while True:
+            A, B = make_inputs(args.workload, rank, bump)
+            with torch.cuda.stream(stream):
+                c0 = fstc.fst_compose(fstc.fst_create(A, stream), fstc.fst_create(B, stream), stream)
+            ne = c0.num_arcs
+            c0.free()
+            if ne > 0 or bump >= 7:
+                break
+            bump += 1
         As = [A]
         parallelism = f"{world} independent replica(s), one composition per GPU (seeds offset by rank)"
     P = sum(A.num_states * B.num_states for A in As)
@@ -237,7 +312,7 @@ def run_ours(args):
         ha = [fstc.fst_create(A, stream) for A in As]
         hb = fstc.fst_create(B, stream)
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.int32, device=dev)
-    fstc.fst_set_profiling(True)
+    fstc.fst_set_profiling(False)  # the timed steps run without per-phase events (phases: separate pass)
 
     def compose_all():
         if len(ha) == 1:
@@ -302,40 +377,53 @@ def run_ours(args):
     max_ms, arcs_all = parallel.reduce_timing(tot_ms, float(E_C), pg, dev)
     value = arcs_all * args.steps / (max_ms / 1e3)
 
-    # ---------------- roofline of the dominant kernel (emit) and of the whole step
+    # ---------------- phases: a separate UNTIMED pass with per-phase CUDA events on the library stream
+    fstc.fst_set_profiling(True)
+    pstats = []
+    for _ in range(2):
+        _, st, _ = step()
+        pstats.append(st)
+    fstc.fst_set_profiling(False)
+    ms_step = tot_ms / args.steps
     hbm, peak_src = peaks()
-    R = stats[-1]["num_coaccessible"]
+    R = pstats[-1]["num_coaccessible"]
     k = 4 if P < 2 ** 32 else 8
-    emit_ms = statistics.mean(s["ms_emit"] for s in stats)
-    s1 = statistics.mean(s["ms_stage1"] for s in stats)
-    s2 = statistics.mean(s["ms_stage2"] for s in stats)
-    num = statistics.mean(s["ms_number"] for s in stats)
+    emit_ms = statistics.mean(s["ms_emit"] for s in pstats)
+    s1 = statistics.mean(s["ms_stage1"] for s in pstats)
+    s2 = statistics.mean(s["ms_stage2"] for s in pstats)
+    cnt_ms = statistics.mean(s["ms_count"] for s in pstats)
+    num = statistics.mean(s["ms_number"] for s in pstats)
+    tile = bool(pstats[-1]["tile_path"])
     ab = 24 if args.provenance else 16  # + arc_a / arc_b per arc with provenance
     emit_bytes = ab * E_C + 18 * V_C + P / 8
     step_bytes = ab * E_C + 18 * V_C + 2 * k * (R + V_C) + P / 4
+    emit_name = "k_tile_emit" if tile else "k_emit"
     traffic = None
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tp):
         try:
-            traffic = json.load(open(tp)).get(args.workload, {}).get("k_emit")
+            traffic = json.load(open(tp)).get(args.workload, {}).get(emit_name)
         except Exception:
             traffic = None
+    # roofline: the dominant KERNEL of the step (by device time in the phases pass).  The emit is one
+    # launch; the BFS stages are many launches of the level kernels (k_tile_pull rounds + k_level push
+    # levels), reported as roofline_bfs with their share.
     achieved = emit_bytes / (emit_ms / 1e3) / 1e9
-    roof = {"kernel": "k_emit", "bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+    roof = {"kernel": emit_name, "bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
             "frac": achieved / hbm, "traffic": traffic, "peak_source": peak_src,
-            "algorithmic_bytes_per_launch": emit_bytes,
-            "bytes_formula": f"{ab}*E_C + 18*V_C + P/8 (arc SoA + row_ptr/pairs/flags written, V bitmap read)"}
-    ms_step = tot_ms / args.steps
-    # the BFS level kernels (k_level: the larger share of the step) against the same HBM peak: their
-    # algorithmic bytes are the frontier keys in and out of every level (2k per state per stage) plus
-    # the R / V bitmaps (P/4) -- they are issue-bound graph traversal, far from HBM-bound (ncu:
-    # profiles/<round>_summary.md, issue-active ~60%, DRAM < 5%)
+            "share_of_step": emit_ms / ms_step, "algorithmic_bytes_per_launch": emit_bytes,
+            "bytes_formula": f"{ab}*E_C + 18*V_C + P/8 (arc SoA + row_ptr/pairs/flags written, V bitmap read)",
+            "timing": "CUDA events around the launch on the library stream, phases pass (profiling on)"}
+    # the BFS level kernels against the same HBM peak: their algorithmic bytes are the frontier keys in
+    # and out of every level (2k per state per stage) plus the R / V bitmaps (P/4) -- graph traversal
+    # bound by instruction issue and shared-memory bandwidth, far from HBM-bound (profiles/r02_summary.md)
     bfs_bytes = 2 * k * (R + V_C) + P / 4
-    bfs_ms = s1 + s2
-    bfs_roof = {"kernel": "k_level", "bound": "hbm", "achieved": bfs_bytes / (bfs_ms / 1e3) / 1e9, "peak": hbm,
-                "unit": "GB/s", "frac": bfs_bytes / (bfs_ms / 1e3) / 1e9 / hbm, "share_of_step": bfs_ms / (tot_ms / args.steps),
+    bfs_ms = s1 + s2 - cnt_ms
+    bfs_roof = {"kernel": "k_tile_pull+k_level" if tile else "k_level", "bound": "hbm",
+                "achieved": bfs_bytes / (bfs_ms / 1e3) / 1e9, "peak": hbm, "unit": "GB/s",
+                "frac": bfs_bytes / (bfs_ms / 1e3) / 1e9 / hbm, "share_of_step": bfs_ms / ms_step,
                 "algorithmic_bytes_per_step": bfs_bytes, "bytes_formula": "2k(|R|+V_C) + P/4 over both BFS stages",
-                "note": "issue-bound (see profiles/*_summary.md k_level captures), not HBM-bound"}
+                "note": "issue / shared-memory bound (profiles/r02_summary.md), not HBM-bound"}
     step_roof = {"algorithmic_bytes": step_bytes, "frac_of_hbm": step_bytes / (ms_step / 1e3) / 1e9 / hbm,
                  "formula": f"{ab}*E_C + 18*V_C + 2k(|R|+V_C) + P/4 (SURVEY 8(d) d.4)"}
 
@@ -348,16 +436,20 @@ def run_ours(args):
         "metric": "composed arcs/sec", "value": value, "unit": "arcs/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": max_ms / args.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": WORKLOADS[args.workload][0], "compositions_per_gpu": len(As),
-                   "V_A": sum(A.num_states for A in As), "V_B": B.num_states,
-                   "E_A": sum(A.num_arcs for A in As), "E_B": B.num_arcs, "pair_space": P, "V_C": V_C, "E_C": E_C,
-                   "coaccessible": R, "levels": [stats[-1]["levels_stage1"], stats[-1]["levels_stage2"]],
-                   "parallelism": parallelism, "provenance": bool(args.provenance),
-                   **({"eps_filter": "three-state eps filter (A~ o F, then o B~); phases_ms / roofline are "
-                                     "the second pass's, ms_per_step covers both"} if args.eps_filter else {}),
-                   "l2": "flushed before every step (512 MiB write), outside the timed events; the working set "
-                         "(pair-space bitmaps + composed graph) exceeds L2"},
-        "phases_ms": {"stage1_backward_bfs": s1, "stage2_forward_bfs": s2, "numbering": num, "emit": emit_ms},
+        "config": workload_config(args.workload, As, B),
+        "result": {"V_C": V_C, "E_C": E_C, "coaccessible": R,
+                   "levels": [pstats[-1]["levels_stage1"], pstats[-1]["levels_stage2"]],
+                   "bottom_up_rounds": pstats[-1]["pull_levels"], "tile_path": tile},
+        "setup": {"parallelism": parallelism, "provenance": bool(args.provenance),
+                  **({"seeds": list(input_seeds(args.workload, rank, bump))} if args.workload != "c5" else
+                     {"utterances": [int(i) for i in mine]}),
+                  **({"eps_filter": "three-state eps filter (A~ o F, then o B~); phases_ms / roofline are "
+                                    "the second pass's, ms_per_step covers both"} if args.eps_filter else {}),
+                  "l2": "flushed before every step (512 MiB write), outside the timed events; the working set "
+                        "(pair-space bitmaps + composed graph) exceeds L2",
+                  "timing": "timed steps without per-phase events; phases_ms from 2 extra untimed steps"},
+        "phases_ms": {"stage1_backward_bfs": s1, "stage2_forward_bfs": s2 - cnt_ms, "count": cnt_ms,
+                      "numbering": num, "emit": emit_ms},
         "roofline": roof,
         **({"forward_score": fwd} if fwd else {}),
         "roofline_bfs": bfs_roof,

@@ -2513,9 +2513,11 @@ fst_status compose_impl(int32_t n, const fst_handle* a, const fst_handle* b, cud
       if (st) return st;
     }
     if (tp.ok) {  // pass-1 counts of every block (the bottom-up levels do not count)
+      EventTimer tc(prof, s);
       cx.warc = (uint32_t*)cx.cnt8;
       launch_tile_count(tp.cnt, tp.grid_count, tp.smem_count, s, cx);
       FSTC_LAUNCH_CHECK();
+      stats.ms_count = tc.stop();
     }
     stats.levels_stage2 = (int32_t)sizes2.size();
     stats.ms_stage2 = t.stop();

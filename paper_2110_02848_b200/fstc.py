@@ -60,7 +60,7 @@ class fst_compose_stats(C.Structure):
                 ("ms_number", C.c_float), ("ms_alloc", C.c_float), ("ms_emit", C.c_float),
                 ("ms_total", C.c_float), ("launches", C.c_int64), ("emit_launches", C.c_int64),
                 ("expand_launches", C.c_int64), ("staged_tasks", C.c_int64), ("tile_path", C.c_int32),
-                ("pull_levels", C.c_int32)]
+                ("pull_levels", C.c_int32), ("ms_count", C.c_float)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
