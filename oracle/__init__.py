@@ -14,6 +14,8 @@ Functions:
                           states (pair_a, pair_b, pair_f)
   compose_chain(gs)    -> N-way composition as a left fold of compose
   coaccessible(A, B)   -> uint8 [V_A * V_B] co-accessible set R (Alg. 1 line 3)
+  digest(A, B)         -> {num_states, num_arcs, d0, d1}: Alg. 1 with the arcs streamed into the
+                          order-independent digest (full-size parity)
   in_adjacency(g)      -> (inArcOffset, inArcs) per §3.2
 """
 from __future__ import annotations
@@ -65,6 +67,7 @@ def _load():
             lib.orc_compose_filtered.argtypes = [C.POINTER(_Fst), C.POINTER(_Fst), C.POINTER(_Graph)]
             lib.orc_canonicalize.argtypes = [C.POINTER(_Graph), C.c_int32]
             lib.orc_coaccessible.argtypes = [C.POINTER(_Fst), C.POINTER(_Fst), C.c_void_p]
+            lib.orc_digest.argtypes = [C.POINTER(_Fst), C.POINTER(_Fst), C.c_void_p]
             lib.orc_in_adjacency.argtypes = [C.POINTER(_Fst), C.c_void_p, C.c_void_p]
             lib.orc_free.argtypes = [C.POINTER(_Graph)]
             _lib = lib
@@ -158,6 +161,20 @@ def coaccessible(A, B) -> np.ndarray:
         raise MemoryError
     del ka, kb
     return R[: A.num_states * B.num_states]
+
+
+def digest(A, B) -> dict:
+    """Algorithm 1 with the arcs streamed into the order-independent digest (the
+    definition is in compose.c): {num_states, num_arcs, d0, d1}.  Nothing is stored per arc, so the
+    full-size configurations fit in host memory."""
+    lib = _load()
+    da, ka = _desc(A)
+    db, kb = _desc(B)
+    out = np.zeros(4, np.uint64)
+    if lib.orc_digest(C.byref(da), C.byref(db), out.ctypes.data) != 0:
+        raise MemoryError
+    del ka, kb
+    return {"num_states": int(out[0]), "num_arcs": int(out[1]), "d0": int(out[2]), "d1": int(out[3])}
 
 
 def in_adjacency(g):

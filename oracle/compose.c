@@ -174,9 +174,39 @@ typedef struct {
   int64_t n, cap;
   int32_t *il, *ol, *dst, *aa, *ab;
   float* w;
+  uint64_t* dig;  /* digest mode (orc_digest): arcs are hashed into dig[0..1] instead of stored */
 } arcbuf;
 
-static int arc_push(arcbuf* b, int32_t il, int32_t ol, int32_t d, float w, int32_t aa, int32_t ab) {
+/* ---------------------------------------------------------------- order-independent digest
+ * SURVEY 8(d) d.7, for parity at sizes where the composed graph is too large to compare array by
+ * array: D_f = sum over states s of hS_f(key(s), start, accept, out-degree) + sum over arcs of
+ * hA_f(key(src), key(dst), ilabel, olabel, weight bits), mod 2^64, f = 0, 1 (two seeds).  Sums of
+ * per-state / per-arc hashes are invariant under state renumbering and arc order, so equal canonical
+ * graphs (reading 24) have equal digests.  fin = the splitmix64 finalizer. */
+static uint64_t fin(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+static const uint64_t kDigestSeed[2] = {0x9E3779B97F4A7C15ull, 0xD1B54A32D192ED03ull};
+static uint64_t hash_state(int f, uint64_t key, int st, int ac, uint64_t deg) {
+  return fin(fin(fin(key ^ kDigestSeed[f]) ^ (uint64_t)(st | (ac << 1) | 4)) ^ deg);
+}
+static uint64_t hash_arc(int f, uint64_t ksrc, uint64_t kdst, int32_t il, int32_t ol, float w) {
+  uint32_t wb;
+  memcpy(&wb, &w, 4);
+  return fin(fin(fin(fin(ksrc ^ kDigestSeed[f] ^ 0x5555555555555555ull) ^ kdst) ^
+                 (((uint64_t)(uint32_t)il << 32) | (uint32_t)ol)) ^ wb);
+}
+
+static int arc_push(arcbuf* b, int32_t il, int32_t ol, int32_t d, float w, int32_t aa, int32_t ab,
+                    uint64_t ksrc, uint64_t kdst) {
+  if (b->dig) {
+    b->dig[0] += hash_arc(0, ksrc, kdst, il, ol, w);
+    b->dig[1] += hash_arc(1, ksrc, kdst, il, ol, w);
+    b->n++;
+    return 0;
+  }
   if (b->n == b->cap) {
     int64_t nc = b->cap ? 2 * b->cap : 1024;
     int32_t* a1 = (int32_t*)realloc(b->il, sizeof(int32_t) * (size_t)nc);
@@ -221,7 +251,7 @@ void orc_free(orc_graph* g) {
   memset(g, 0, sizeof(*g));
 }
 
-int orc_compose(const orc_fst* A, const orc_fst* B, orc_graph* C) {
+static int compose_impl(const orc_fst* A, const orc_fst* B, orc_graph* C, uint64_t* dig) {
   int64_t VB = B->V, P = (int64_t)A->V * B->V;
   orc_adj aA, aB;
   uint8_t* R;
@@ -234,6 +264,7 @@ int orc_compose(const orc_fst* A, const orc_fst* B, orc_graph* C) {
   int32_t sa, sb;
   memset(C, 0, sizeof(*C));
   memset(&arcs, 0, sizeof(arcs));
+  arcs.dig = dig;
   if (adj_build(A, &aA) || adj_build(B, &aB)) return -1;
   /* line 2-3 */
   R = (uint8_t*)malloc((size_t)(P ? P : 1));
@@ -287,7 +318,8 @@ int orc_compose(const orc_fst* A, const orc_fst* B, orc_graph* C) {
         if (!R[v]) continue;                       /* lines 20-22 */
         if (id[v] < 0) NEW_STATE(va, vb, lv[u] + 1); /* lines 23-28 */
         w = A->weight[ea] + B->weight[eb];         /* line 29-30: one binary32 add */
-        if (arc_push(&arcs, A->ilabel[ea], B->olabel[eb], id[v], w, (int32_t)ea, (int32_t)eb)) return -1;
+        if (arc_push(&arcs, A->ilabel[ea], B->olabel[eb], id[v], w, (int32_t)ea, (int32_t)eb,
+                     (uint64_t)ua * VB + ub, (uint64_t)v)) return -1;
       }
     }
     /* (ii) M2: e_a with o_a = eps, B stays */
@@ -299,7 +331,8 @@ int orc_compose(const orc_fst* A, const orc_fst* B, orc_graph* C) {
       v = (int64_t)va * VB + ub;
       if (!R[v]) continue;
       if (id[v] < 0) NEW_STATE(va, ub, lv[u] + 1);
-      if (arc_push(&arcs, A->ilabel[ea], ORC_EPS, id[v], A->weight[ea], (int32_t)ea, -1)) return -1;
+      if (arc_push(&arcs, A->ilabel[ea], ORC_EPS, id[v], A->weight[ea], (int32_t)ea, -1, (uint64_t)ua * VB + ub,
+                   (uint64_t)v)) return -1;
     }
     /* (iii) M3: e_b with i_b = eps, A stays */
     for (eb = B->row_ptr[ub]; eb < B->row_ptr[ub + 1]; ++eb) {
@@ -310,7 +343,13 @@ int orc_compose(const orc_fst* A, const orc_fst* B, orc_graph* C) {
       v = (int64_t)ua * VB + vb;
       if (!R[v]) continue;
       if (id[v] < 0) NEW_STATE(ua, vb, lv[u] + 1);
-      if (arc_push(&arcs, ORC_EPS, B->olabel[eb], id[v], B->weight[eb], -1, (int32_t)eb)) return -1;
+      if (arc_push(&arcs, ORC_EPS, B->olabel[eb], id[v], B->weight[eb], -1, (int32_t)eb, (uint64_t)ua * VB + ub,
+                   (uint64_t)v)) return -1;
+    }
+    if (dig) {  /* the state's own term: its key, flags and out-degree (its arcs were just pushed) */
+      const uint64_t deg = (uint64_t)(arcs.n - rp[u]);
+      dig[0] += hash_state(0, (uint64_t)ua * VB + ub, st[u], ac[u], deg);
+      dig[1] += hash_state(1, (uint64_t)ua * VB + ub, st[u], ac[u], deg);
     }
   }
 #undef NEW_STATE
@@ -334,6 +373,23 @@ int orc_compose(const orc_fst* A, const orc_fst* B, orc_graph* C) {
   free(id);
   adj_free(&aA);
   adj_free(&aB);
+  return 0;
+}
+
+int orc_compose(const orc_fst* A, const orc_fst* B, orc_graph* C) { return compose_impl(A, B, C, NULL); }
+
+/* Algorithm 1 with the composed arcs streamed into the digest (nothing stored per arc): out[0] = V_C,
+ * out[1] = E_C, out[2..3] = D_0, D_1.  Memory is the pair tables only, so configs[3] at full size fits. */
+int orc_digest(const orc_fst* A, const orc_fst* B, uint64_t* out) {
+  orc_graph C;
+  uint64_t dig[2] = {0, 0};
+  int rc = compose_impl(A, B, &C, dig);
+  if (rc) return rc;
+  out[0] = (uint64_t)C.V;
+  out[1] = (uint64_t)C.E;
+  out[2] = dig[0];
+  out[3] = dig[1];
+  orc_free(&C);
   return 0;
 }
 
@@ -448,7 +504,7 @@ int orc_compose_filtered(const orc_fst* A, const orc_fst* B, orc_graph* C) {
     int64_t v_ = FK(va_, vb_, vf_);                                                       \
     if (R[v_]) {                                                                          \
       if (id[v_] < 0) NEW_STATE3(va_, vb_, vf_, lv[u] + 1);                               \
-      if (arc_push(&arcs, il_, ol_, id[v_], w_, xa_, xb_)) return -1;                     \
+      if (arc_push(&arcs, il_, ol_, id[v_], w_, xa_, xb_, 0, 0)) return -1;               \
     }                                                                                     \
   } while (0)
 

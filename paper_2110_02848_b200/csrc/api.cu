@@ -61,6 +61,20 @@ fst_status device_ready() {
     set_error(FST_E_CUDA, "no usable CUDA device (%s); libfstc has no CPU fallback", cudaGetErrorString(e));
     return FST_E_CUDA;
   }
+  // One device per process (the multi-GPU design is one process per GPU): the library's buffer
+  // cache, level scratch, capture stream, grid sizes and kernel attributes are per-process state set
+  // up on the first device used, so calls made while another device is current are rejected.
+  {
+    static int first_dev = -1;
+    int cur = 0;
+    cudaGetDevice(&cur);
+    if (first_dev < 0) first_dev = cur;
+    if (cur != first_dev) {  // NOLINT
+      set_error(FST_E_INVALID_ARG, "libfstc is bound to CUDA device %d (first use); device %d is current -- "
+                "use one process per GPU", first_dev, cur);
+      return FST_E_INVALID_ARG;
+    }
+  }
   static bool pool_done = false;
   if (!pool_done) {  // keep freed stream-ordered memory in the pool (repeat compositions reuse it)
     int dev = 0;
@@ -189,7 +203,17 @@ fst_status fst_forward_score(fst_handle h, void* stream, double* total, double* 
   return forward_score_impl(h, (cudaStream_t)stream, total, alpha);
 }
 
-void fst_free(fst_handle h) { delete h; }
+void fst_free(fst_handle h) {
+  if (!h) return;
+  // stream-ordered release: every buffer's stream first waits for the asynchronous work other streams
+  // still run on this handle (fst_grad_scatter on a caller stream)
+  for (cudaEvent_t ev : h->use_events) {
+    for (auto& b : h->buffers)
+      if (b) cudaStreamWaitEvent(b->stream, ev, 0);
+    cudaEventDestroy(ev);
+  }
+  delete h;
+}
 
 fst_status fst_info(fst_handle h, fst_view* v) {
   if (!h || !v) {

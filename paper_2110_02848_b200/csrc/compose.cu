@@ -972,7 +972,9 @@ __device__ __forceinline__ void bfs_chunk_fast(TaskSmem& s, const ViewDev& Bv, i
       // the high word of c * ceil(2^32 / d), exact for the slots c < 32 d + 32 <= 2016 of a batch)
       const unsigned dmax = __reduce_max_sync(0xffffffffu, (unsigned)deg);
       const unsigned dmin = __reduce_min_sync(0xffffffffu, k < stot ? (unsigned)deg : dmax);
-      const bool uni = dmax == dmin && dmax <= 62u;
+      // (dmax >= 2: kRecip32[d] = ceil(2^32 / d) does not fit 32 bits for d = 1; batches with d <= 2
+      // take the low-degree branch above anyway, this keeps the lookup valid on its own)
+      const bool uni = dmax == dmin && dmax >= 2u && dmax <= 62u;
       const unsigned uinv = uni ? kRecip32[dmax] : 0u;
       uint8_t* own = dynsm + (kDynSmem - kOwnerBytes) + (threadIdx.x >> 5) * kOwnerCap;
       const bool tbl = !uni && total <= kOwnerCap;
@@ -2679,6 +2681,14 @@ fst_status grad_scatter_impl(fst* c, const float* grad_c, float* grad_a, int64_t
   const unsigned grid = (unsigned)std::min<int64_t>((c->E + 255) / 256, 148 * 16);
   k_grad_scatter<<<grid, 256, 0, s>>>(c->E, c->arc_a, c->arc_b, grad_c, grad_a, grad_b);
   FSTC_LAUNCH_CHECK();
+  // the scatter reads c's arc_a / arc_b asynchronously on s: fst_free(c) makes the release of c's
+  // buffers wait for it (the buffers are released stream-ordered on the stream that allocated them)
+  if (s != c->stream) {
+    cudaEvent_t ev;
+    FSTC_CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    FSTC_CUDA_TRY(cudaEventRecord(ev, s));
+    c->use_events.push_back(ev);
+  }
   return FST_OK;
 }
 }  // namespace fstc

@@ -87,6 +87,7 @@ struct fst {
   int64_t shard_state_offset = 0, shard_arc_offset = 0, shard_total_states = 0, shard_total_arcs = 0;
   std::vector<int64_t> level_sizes[2];  // frontier size per BFS level, stage 1 / stage 2
   std::vector<fstc::BufferPtr> buffers;  // owned (or shared with a batch) device memory
+  std::vector<cudaEvent_t> use_events;   // async work on other streams that reads the buffers (fst_free waits)
   // tile path caches (compose.cu / tile.cuh), built on first use; a handle is immutable
   struct TileEll {  // B role: ELL of a view ([0] out-by-ilabel with (carry, weight), [1] in-by-ilabel)
     bool ok = false;

@@ -51,3 +51,63 @@ def test_c4_fullsize_against_oracle_R(fst):
         exp_rows = sorted((d[0] * VB + d[1], il, ol, pins.wbits(w)) for d, il, ol, w in pins.n1_moves(A, B, a, b)
                           if R[d[0] * VB + d[1]])
         assert got_rows == exp_rows, (sid, a, b)
+
+
+# ------------------------------------------------------------------ digest parity at the stated sizes
+# V_C, E_C and two 64-bit order-independent digests (tests/digest.py; the oracle
+# streams the same definition through Algorithm 1, oracle/compose.c orc_digest) -- equality means the
+# canonical graphs are equal (w.h.p.), at sizes the array-by-array comparison cannot reach.
+import digest  # noqa: E402
+
+
+def test_digest_device_matches_host(fst):
+    """The device-side digest (torch) equals the host numpy one on a graph both can handle."""
+    A, B = fstgen.config_c4(V=3000, D=8)
+    c = fst.fst_compose(fst.fst_create(A), fst.fst_create(B))
+    assert digest.digest_device(c.device_tensors(), B.num_states) == digest.digest_graph(c.to_host(), B.num_states)
+    assert digest.digest_graph(c.to_host(), B.num_states) == oracle.digest(A, B)
+
+
+def test_c4_fullsize_digest(fst):
+    """configs[3] at the bench size (20k x 20k, D = 8, 16 tokens; E_C = 1.44e9): the whole composed graph
+    equals the oracle's (digest), in the launch configuration bench.py times."""
+    A, B = fstgen.config_c4(V=20000, D=8)
+    c = fst.fst_compose(fst.fst_create(A), fst.fst_create(B))
+    got = digest.digest_device(c.device_tensors(), B.num_states)
+    exp = oracle.digest(A, B)
+    assert got == exp
+    assert exp["num_arcs"] > 1.4e9
+
+
+def test_c4_int64_arc_slots(fst):
+    """20k x 20k, D = 8, 8 tokens: E_C ~ 3.2e9 > 2^31 composed arcs (int64 row_ptr / arc slots), against
+    the oracle's digest."""
+    A, B = fstgen.config_c4(V=20000, D=8, tokens=8)
+    c = fst.fst_compose(fst.fst_create(A), fst.fst_create(B))
+    assert c.num_arcs > 2 ** 31
+    got = digest.digest_device(c.device_tensors(), B.num_states)
+    assert got == oracle.digest(A, B)
+
+
+def _oracle_digest_pair(pair):
+    A, B = pair
+    return oracle.digest(A, B)
+
+
+def test_c5_batch_digests(fst):
+    """configs[4] as bench.py times it: the 32-utterance batch (T_i = 100..500) o closure(10k-word lexicon)
+    in one fst_compose_batch; every utterance's composition equals the oracle's (digest; the oracle runs
+    one utterance per host core)."""
+    import multiprocessing as mp
+    import os
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import bench
+    As, B, _ = bench.c5_shard(0, 1)
+    hb = fst.fst_create(B)
+    cs = fst.fst_compose_batch([fst.fst_create(A) for A in As], [hb] * len(As))
+    got = [digest.digest_device(c.device_tensors(), B.num_states) for c in cs]
+    with mp.get_context("fork").Pool(min(len(As), len(os.sched_getaffinity(0)))) as pool:
+        exp = pool.map(_oracle_digest_pair, [(A, B) for A in As])
+    assert got == exp
+    assert sum(e["num_arcs"] for e in exp) > 5e8
