@@ -2103,7 +2103,7 @@ fst_status ensure_tile_ell(fst* B, int which, cudaStream_t s) {
   const int wpr = (V + 31) / 32;
   size_t off = 0;
   auto take = [&](size_t bytes) { size_t o = off; off += (bytes + 255) & ~size_t(255); return o; };
-  const size_t o_ell = take(4ull * wd * V), o_cw = which == 0 ? take(8ull * wd * V) : 0;
+  const size_t o_ell = take(4ull * wd * wpr * 32), o_cw = which == 0 ? take(8ull * wd * wpr * 32) : 0;
   const size_t o_wmax = take(wpr), o_flag = take(4);
   BufferPtr buf;
   fst_status st = alloc_buffer(off, s, &buf);
@@ -2114,8 +2114,8 @@ fst_status ensure_tile_ell(fst* B, int which, cudaStream_t s) {
   T.wmax = (uint8_t*)(base + o_wmax);
   int32_t* d_flag = (int32_t*)(base + o_flag);
   FSTC_CUDA_TRY(cudaMemsetAsync(d_flag, 0, 4, s));
-  k_build_ell<<<nblk(V, 256), 256, 0, s>>>(V, v.off, v.key, v.other, which == 0 ? v.cw : nullptr, wd, T.ell, T.cw,
-                                            T.wmax, d_flag);
+  k_build_ell<<<nblk((int64_t)wpr * 32, 256), 256, 0, s>>>(V, v.off, v.key, v.other, which == 0 ? v.cw : nullptr, wd,
+                                                           T.ell, T.cw, T.wmax, d_flag);
   FSTC_LAUNCH_CHECK();
   int32_t flag = 0;
   FSTC_CUDA_TRY(cudaMemcpyAsync(&flag, d_flag, 4, cudaMemcpyDeviceToHost, s));

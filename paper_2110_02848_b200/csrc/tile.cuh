@@ -10,7 +10,8 @@
 //                   li = 1: eps items -> A eps arcs (M1 eps:eps) and self slots (M3);
 //                   li = l + 2: label l; 255 = padding)
 //   * RT[b']  (M): the slot-transposed bitmap -- bit s = vis(row of slot s, b')
-//   * B items of b in an ELL [j][b] (column 0 = the sentinel "b itself"), packed (li << 24 | b')
+//   * B items of b in an ELL tiled by words: item j of column b at [(b / 32) * wd + j][b % 32] (column
+//     0 = the sentinel "b itself"), packed (li << 24 | b'); a word's items are one contiguous block
 // so ONE shared load per (b, item) and an AND give the candidate moves of all X pairs into vis:
 //   hits = lm[li] & RT[b'];  pair (a_x, b) has a move into vis  <=>  hits & rowmask[x] != 0.
 // This is the frontier-parallel arc-pair exploration of PAPER.md:237-248 (§3.3) organised so that the
@@ -47,8 +48,8 @@ struct TileSide {
   const int32_t* carry;
   const float* w;
   // B-role ELL
-  const uint32_t* ell;  // [wd][VB]
-  const int2* ellcw;    // [wd][VB] (carry, weight bits) of the arc behind ELL entry (emit)
+  const uint32_t* ell;  // [wpr][wd][32] (word-tiled ELL)
+  const int2* ellcw;    // [wpr][wd][32] (carry, weight bits) of the arc behind each ELL entry (emit)
   const uint8_t* wmax;  // [wpr] ELL columns used by the 32 states of each word
   int32_t wd;
 };
@@ -215,21 +216,20 @@ __device__ __forceinline__ TC tc_of(const Ctx& cx) {
   return TC{C.W, C.K, C.Q, C.wpr, C.VB, C.bpr, C.VA, C.cpr, C.CB};
 }
 
-// Items of column b (ELL columns 1..jn-1; column 0, the sentinel, when j0 == 0): the first kJ
-// columns are loaded together into registers, the rest (rare) in a tail loop.  f(x) per item.
+// Items of column b = 32 w + lane (ELL columns 1..jn-1; column 0, the sentinel, when j0 == 0): the
+// first kJ columns are loaded together into registers (immediate offsets inside the word's block),
+// the rest (rare) in a tail loop.  f(x) per item.
 template <int kJ, typename F>
-__device__ __forceinline__ void for_items(const uint32_t* __restrict__ ell, int VB, int b, int j0, int jn, F&& f) {
-  if (j0 == 0) f(__ldg(ell + b));
-  const uint32_t* p = ell + VB + b;
+__device__ __forceinline__ void for_items(const uint32_t* __restrict__ ell, int wd, int w, int lane, int j0, int jn,
+                                          F&& f) {
+  const uint32_t* p = ell + (size_t)w * wd * 32 + lane;
+  if (j0 == 0) f(__ldg(p));
   uint32_t it[kJ];
 #pragma unroll
-  for (int k = 0; k < kJ; ++k) {
-    it[k] = (k + 1 < jn) ? __ldg(p) : (kLiPad << 24);
-    p += VB;
-  }
+  for (int k = 0; k < kJ; ++k) it[k] = (k + 1 < jn) ? __ldg(p + (k + 1) * 32) : (kLiPad << 24);
 #pragma unroll
   for (int k = 0; k < kJ; ++k) f(it[k]);
-  for (int j = kJ + 1; j < jn; ++j, p += VB) f(__ldg(p));
+  for (int j = kJ + 1; j < jn; ++j) f(__ldg(p + j * 32));
 }
 
 // ------------------------------------------------------------------------------ bottom-up round
@@ -305,7 +305,7 @@ __global__ void __launch_bounds__(kTThreads, 1) k_tile_pull(Ctx cx, TileArgs ta,
           const int b = w * 32 + lane;
           M acc = M(0);
           if (b < VB)
-            for_items<kJ>(ell, VB, b, j0, wmax[w], [&](uint32_t x) { acc |= lm[x >> 24] & RT[x & 0xFFFFFFu]; });
+            for_items<kJ>(ell, ta.sd.wd, w, lane, j0, wmax[w], [&](uint32_t x) { acc |= lm[x >> 24] & RT[x & 0xFFFFFFu]; });
           uint32_t mine = 0u;
 #pragma unroll
           for (int x = 0; x < kTRows; ++x) {
@@ -394,7 +394,7 @@ __global__ void __launch_bounds__(kTThreads, 1) k_tile_count(Ctx cx, TileArgs ta
           if (b < VB) {
             if (kByte) {
               M bc = 0ull;  // 8 byte counters (row x = byte x); <= 31 items x 8 slots < 256
-              for_items<kJ>(ell, VB, b, j0, wmax[w], [&](uint32_t x) {
+              for_items<kJ>(ell, ta.sd.wd, w, lane, j0, wmax[w], [&](uint32_t x) {
                 const M h = lm[x >> 24] & RT[x & 0xFFFFFFu];
                 M v = h - ((h >> 1) & 0x5555555555555555ull);
                 v = (v & 0x3333333333333333ull) + ((v >> 2) & 0x3333333333333333ull);
@@ -403,7 +403,7 @@ __global__ void __launch_bounds__(kTThreads, 1) k_tile_count(Ctx cx, TileArgs ta
 #pragma unroll
               for (int x = 0; x < kTRows; ++x) cr[x] = (uint32_t)(bc >> (8 * x)) & 0xFFu;
             } else {
-              for_items<kJ>(ell, VB, b, j0, wmax[w], [&](uint32_t x) {
+              for_items<kJ>(ell, ta.sd.wd, w, lane, j0, wmax[w], [&](uint32_t x) {
                 const M h = lm[x >> 24] & RT[x & 0xFFFFFFu];
 #pragma unroll
                 for (int r = 0; r < kTRows; ++r) cr[r] += __popcll(h & rm[r]);
@@ -473,7 +473,7 @@ __global__ void __launch_bounds__(kEThreads, 1) k_tile_emit(Ctx cx, TileArgs ta,
   __shared__ int32_t rbase[kESlots + kTRows];
   extern __shared__ __align__(16) uint32_t tdyn[];
   const TC c = tc_of(cx);
-  const int wpr = c.wpr, VB = c.VB, bpr = c.bpr;
+  const int wpr = c.wpr, VB = c.VB, bpr = c.bpr, wd = ta.sd.wd;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   uint32_t* RT = tdyn;                                                  // [wpr * 32]
   uint32_t* Vw = RT + (size_t)wpr * 32;                                 // [vr_rows * wpr]
@@ -546,13 +546,10 @@ __global__ void __launch_bounds__(kEThreads, 1) k_tile_emit(Ctx cx, TileArgs ta,
       const int jn = ta.sd.wmax[w];
       uint32_t it[kJ + 1];
       {
-        it[0] = (j0 == 0 && inb) ? __ldg(ta.sd.ell + b) : (kLiPad << 24);
-        const uint32_t* p = ta.sd.ell + VB + b;
+        const uint32_t* p = ta.sd.ell + (size_t)w * wd * 32 + lane;
+        it[0] = (j0 == 0 && inb) ? __ldg(p) : (kLiPad << 24);
 #pragma unroll
-        for (int k = 0; k < kJ; ++k) {
-          it[k + 1] = (inb && k + 1 < jn) ? __ldg(p) : (kLiPad << 24);
-          p += VB;
-        }
+        for (int k = 0; k < kJ; ++k) it[k + 1] = (inb && k + 1 < jn) ? __ldg(p + (k + 1) * 32) : (kLiPad << 24);
       }
       for (int x = 0; x < nr; ++x) {
         const uint32_t vw = __shfl_sync(0xffffffffu, vw_l, x);
@@ -570,7 +567,7 @@ __global__ void __launch_bounds__(kEThreads, 1) k_tile_emit(Ctx cx, TileArgs ta,
           cnt += __popc(h[k]);
         }
         for (int j = kJ + 1; j < jn; ++j) {  // (wide B rows: items beyond the registers)
-          const uint32_t xi = inb ? __ldg(ta.sd.ell + (size_t)j * VB + b) : (kLiPad << 24);
+          const uint32_t xi = inb ? __ldg(ta.sd.ell + ((size_t)w * wd + j) * 32 + lane) : (kLiPad << 24);
           cnt += __popc(lm[xi >> 24] & RT[xi & 0xFFFFFFu] & rmv);
         }
         const int inc = warp_incl_scan(cnt);
@@ -602,7 +599,7 @@ __global__ void __launch_bounds__(kEThreads, 1) k_tile_emit(Ctx cx, TileArgs ta,
 #pragma unroll
             for (int k = 0; k <= kJ; ++k) put(k, h[k], it[k]);
             for (int j = kJ + 1; j < jn; ++j) {
-              const uint32_t xi = inb ? __ldg(ta.sd.ell + (size_t)j * VB + b) : (kLiPad << 24);
+              const uint32_t xi = inb ? __ldg(ta.sd.ell + ((size_t)w * wd + j) * 32 + lane) : (kLiPad << 24);
               put(j, lm[xi >> 24] & RT[xi & 0xFFFFFFu] & rmv, xi);
             }
           }
@@ -616,7 +613,7 @@ __global__ void __launch_bounds__(kEThreads, 1) k_tile_emit(Ctx cx, TileArgs ta,
               const int i = i0 + 32 * u;
               cd[u] = i < n ? code[i] : 0u;
               const int L = (cd[u] >> 10) & 31, j = (cd[u] >> 5) & 31;
-              cw[u] = (i < n && j != 0) ? __ldg(ta.sd.ellcw + (size_t)j * VB + w * 32 + L) : make_int2(0, 0);
+              cw[u] = (i < n && j != 0) ? __ldg(ta.sd.ellcw + ((size_t)w * wd + j) * 32 + L) : make_int2(0, 0);
             }
 #pragma unroll
             for (int u = 0; u < 2; ++u) {
@@ -656,8 +653,9 @@ __global__ void __launch_bounds__(kEThreads, 1) k_tile_emit(Ctx cx, TileArgs ta,
   }
 }
 
-// B-role ELL of a view: column 0 = the sentinel item (b itself), columns 1.. = the node's arcs in
-// view order, padded; wmax[word] = columns used by the word's 32 nodes; *has_eps |= any eps key.
+// B-role ELL of a view, word-tiled: item j of node b at [(b / 32) * wd + j][b % 32]; column 0 = the
+// sentinel item (b itself), columns 1.. = the node's arcs in view order, padded; wmax[word] = columns
+// used by the word's 32 nodes; *has_eps |= any eps key.
 __global__ void k_build_ell(int32_t V, const int32_t* __restrict__ off, const int32_t* __restrict__ key,
                             const int32_t* __restrict__ other, const int2* __restrict__ cw, int wd, uint32_t* ell,
                             int2* ellcw, uint8_t* wmax, int32_t* has_eps) {
@@ -665,22 +663,28 @@ __global__ void k_build_ell(int32_t V, const int32_t* __restrict__ off, const in
   const int lane = threadIdx.x & 31;
   int d = 0;
   bool eps = false;
+  const size_t base = (size_t)(b >> 5) * wd * 32 + lane;
   if (b < V) {
     const int32_t e0 = off[b];
     d = off[b + 1] - e0;
-    ell[b] = (kLiSent << 24) | (uint32_t)b;
-    if (ellcw) ellcw[b] = make_int2(0, 0);
+    ell[base] = (kLiSent << 24) | (uint32_t)b;
+    if (ellcw) ellcw[base] = make_int2(0, 0);
     for (int j = 1; j < wd; ++j) {
       const int k = j - 1;
       if (k < d) {
         const int32_t l = key[e0 + k];
         eps |= l == FST_EPS;
-        ell[(size_t)j * V + b] = ((uint32_t)(l + 2) << 24) | (uint32_t)other[e0 + k];
-        if (ellcw) ellcw[(size_t)j * V + b] = cw[e0 + k];
+        ell[base + (size_t)j * 32] = ((uint32_t)(l + 2) << 24) | (uint32_t)other[e0 + k];
+        if (ellcw) ellcw[base + (size_t)j * 32] = cw[e0 + k];
       } else {
-        ell[(size_t)j * V + b] = kLiPad << 24;
-        if (ellcw) ellcw[(size_t)j * V + b] = make_int2(0, 0);
+        ell[base + (size_t)j * 32] = kLiPad << 24;
+        if (ellcw) ellcw[base + (size_t)j * 32] = make_int2(0, 0);
       }
+    }
+  } else if ((b >> 5) * 32 < V) {  // padding lanes of the last word
+    for (int j = 0; j < wd; ++j) {
+      ell[base + (size_t)j * 32] = kLiPad << 24;
+      if (ellcw) ellcw[base + (size_t)j * 32] = make_int2(0, 0);
     }
   }
   const unsigned m = __reduce_max_sync(0xffffffffu, (unsigned)(b < V ? d + 1 : 0));
