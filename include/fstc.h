@@ -224,12 +224,17 @@ fst_status fst_adjacency(fst_handle h, int32_t role, int32_t match_on_olabel, in
 int32_t fst_level_sizes(fst_handle c, int32_t stage, int64_t* sizes, int32_t cap);
 
 /* ---- Sharded single composition over several GPUs ----------------------------
- * The pair-space rows (states of A) are split into `world` contiguous ranges; rank r owns rows
- * [V_A*r/world, V_A*(r+1)/world).  Each BFS level every rank expands its rows; pairs found in other
- * ranks' rows are delivered to their owners (NCCL send/recv of bitmap row slices) and claimed there;
- * R and V are replicated after each stage (NCCL all-reduce, sum of disjoint bits).  Rank r's result
- * handle holds the states of its rows (a contiguous id range) with GLOBAL state ids in dst; row_ptr
- * is local to the shard.  Concatenating the shards in rank order gives fst_compose's result. */
+ * Ownership by state-pair block: the pair space is cut into 1024-pair blocks (32 columns of one A
+ * state's row), block id = a * ceil(V_B/1024) + (b / 1024), and rank r owns the blocks with
+ * id % world == r -- every row (every BFS level of a trellis-shaped composition) is spread over all
+ * ranks.  Each BFS level every rank expands its own frontier pairs; pairs found in other ranks'
+ * blocks are delivered to their owners (the OUT bitmap words of each peer's blocks packed into one
+ * slice per peer, exchanged with grouped NCCL send/recv = all-to-all) and claimed there; R and V are
+ * replicated after each stage (NCCL all-reduce, sum of disjoint bits).  States are numbered
+ * OWNER-MAJOR (rank 0's states by ascending key, then rank 1's, ...): rank r's result handle holds
+ * one contiguous id range (shard_info.state_offset) with GLOBAL state ids in dst; row_ptr is local
+ * to the shard.  Concatenating the shards in rank order gives a valid CSR of the whole composition,
+ * equal to fst_compose's after canonicalisation (identical arrays for world = 1). */
 typedef struct fst_comm* fst_comm_handle;
 
 /* 128-byte NCCL unique id, generated on one rank and broadcast by the caller (e.g. with
@@ -241,8 +246,9 @@ void fst_comm_destroy(fst_comm_handle comm); /* NULL-safe */
 /* Collective: every rank calls it with the same inputs; *c_shard receives this rank's shard. */
 fst_status fst_compose_sharded(fst_handle a, fst_handle b, fst_comm_handle comm, void* stream,
                                fst_handle* c_shard);
-/* The same algorithm with all `world` shards hosted by this process on the current device (the
- * row-slice exchange is a device copy): c_shards[world].  Used to verify the sharding on one GPU. */
+/* The same algorithm with all `world` (<= 16) shards hosted by this process on the current device
+ * (the packed per-peer slices are handed over in device memory instead of NCCL): c_shards[world].
+ * Used to verify the sharding on one GPU. */
 fst_status fst_compose_sharded_local(fst_handle a, fst_handle b, int32_t world, void* stream,
                                      fst_handle* c_shards);
 

@@ -1065,7 +1065,7 @@ __global__ void k_seed(Ctx cx) {
     int32_t nb = kStage2 ? C.nStartB : C.nAccB;
     int32_t va = kStage2 ? C.startListA[i / nb] : C.accListA[i / nb];
     int32_t vb = kStage2 ? C.startListB[i % nb] : C.accListB[i % nb];
-    if (va < C.own_r0 || va >= C.own_r1) continue;  // sharded: another shard seeds it
+    if (!owned(C, va, vb)) continue;  // sharded: another shard seeds it
     const int64_t gw = C.W + (int64_t)va * C.wpr + (vb >> 5);
     const uint32_t bit = 1u << (vb & 31);
     if (kStage2 && !(cx.R[gw] & bit)) continue;
@@ -1341,7 +1341,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_level(Ctx cx, int level) {
           if (!(__ldg(&cx.R[gw]) & bit)) return;
           ++kept;
         }
-        if (c.row < C.own_r0 || c.row >= C.own_r1) {  // sharded: the owner claims it after the exchange
+        if (!owned(C, c.row, c.col)) {  // sharded: the owner claims it after the exchange
           atomicOr(&cx.OUT[gw], bit);
           return;
         }
@@ -1363,7 +1363,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_level(Ctx cx, int level) {
           if (!(__ldg(&cx.R[gw]) & bit)) return 0u;
           k = 1;
         }
-        if (row < C.own_r0 || row >= C.own_r1) {  // sharded: the owner claims it after the exchange
+        if (!owned(C, row, col)) {  // sharded: the owner claims it after the exchange
           atomicOr(&cx.OUT[gw], bit);
           return k;
         }
@@ -1449,7 +1449,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_level(Ctx cx, int level) {
         const int r = i / wpr, w = i - r * wpr;
         const int32_t row = s.slot_row[r];
         const int64_t gw = C.W + (int64_t)row * wpr + w;
-        if (row < C.own_r0 || row >= C.own_r1) {  // sharded: the owner claims it after the exchange
+        if (!owned(C, row, w * 32)) {  // sharded: the owner claims it after the exchange
           atomicOr(&cx.OUT[gw], nb);
           continue;
         }
@@ -1468,11 +1468,12 @@ __global__ void __launch_bounds__(kThreads, 2) k_level(Ctx cx, int level) {
 }
 
 // ------------------------------------------------------------------------------ sharded exchange
-// Owner-side claim of the pairs other shards found in this shard's rows during level `level`
-// (the OR of their OUT words over [own_r0, own_r1), received in `in`): new bits become visited and
-// join the next frontier exactly like local claims.  Single composition (ncomp == 1).
+// Owner-side claim of the pairs other shards found in this shard's blocks during level `level` (their
+// OUT bits): new bits become visited and join the next frontier exactly like local claims.  `in` is
+// either the sender's whole OUT bitmap (in-process shards) or a PACKED slice: this rank's blocks in
+// order (block id rank, rank + world, ...), 32 words each.  Single composition (ncomp == 1).
 template <bool kStage2>
-__global__ void k_apply_remote(Ctx cx, const uint32_t* __restrict__ in, int level) {
+__global__ void k_apply_remote(Ctx cx, const uint32_t* __restrict__ in, int packed, int level) {
   const int p = level & 1;
   LevelCtrl* ctrl_nxt = &cx.ctrl[(level + 1) % 3];
   uint32_t* Fn = p ? cx.F0 : cx.F1;
@@ -1480,25 +1481,79 @@ __global__ void k_apply_remote(Ctx cx, const uint32_t* __restrict__ in, int leve
   int32_t* listn = p ? cx.list0 : cx.list1;
   uint32_t* vis = kStage2 ? cx.V : cx.R;
   const CompDev& C = cx.comps[0];
-  const int64_t w0 = C.W + (int64_t)C.own_r0 * C.wpr, w1 = C.W + (int64_t)C.own_r1 * C.wpr;
+  const int G = C.sh_world, me = C.sh_rank;
+  const int64_t nb = (int64_t)C.VA * C.bpr, mine = nb > me ? (nb - me + G - 1) / G : 0;
   unsigned nnew = 0;
-  for (int64_t gw = w0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; gw < w1;
-       gw += (int64_t)gridDim.x * blockDim.x) {
-    const uint32_t nb = in[gw - w0];
-    if (!nb) continue;
-    const uint32_t win = nb & ~atomicOr(&vis[gw], nb);
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < mine * 32; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t blk = (t >> 5) * G + me;
+    const int32_t row = (int32_t)(blk / C.bpr), j = (int32_t)(blk - (int64_t)row * C.bpr);
+    const int w = j * 32 + (int)(t & 31);
+    if (w >= C.wpr) continue;
+    const int64_t gw = C.W + (int64_t)row * C.wpr + w;
+    const uint32_t nbits = packed ? in[t] : in[gw];
+    if (!nbits) continue;
+    const uint32_t win = nbits & ~atomicOr(&vis[gw], nbits);
     if (!win) continue;
     nnew += __popc(win);
-    const int64_t local = gw - C.W;
-    const int32_t row = (int32_t)(local / C.wpr);
-    const int32_t col = (int32_t)(local - (int64_t)row * C.wpr) * 32;
-    push_bits(C, row, col, gw, win, Fn, flagn, listn, ctrl_nxt);
+    push_bits(C, row, w * 32, gw, win, Fn, flagn, listn, ctrl_nxt);
   }
   nnew = warp_sum(nnew);
   if ((threadIdx.x & 31) == 0 && nnew) atomicAdd(&ctrl_nxt->nnew, (unsigned long long)nnew);
 }
 
-// dst[i] |= src[i] (merging bitmap / count slices of other shards)
+// Packs rank q's blocks of a bitmap (block id q, q + world, ...; 32 words each, zero-padded) into dst.
+__global__ void k_pack_owner(const CompDev* __restrict__ comp, const uint32_t* __restrict__ bits, int q,
+                             uint32_t* __restrict__ dst) {
+  const CompDev& C = comp[0];
+  const int G = C.sh_world;
+  const int64_t nb = (int64_t)C.VA * C.bpr, n = nb > q ? (nb - q + G - 1) / G : 0;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n * 32; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t blk = (t >> 5) * G + q;
+    const int32_t row = (int32_t)(blk / C.bpr), j = (int32_t)(blk - (int64_t)row * C.bpr);
+    const int w = j * 32 + (int)(t & 31);
+    dst[t] = w < C.wpr ? bits[C.W + (int64_t)row * C.wpr + w] : 0u;
+  }
+}
+
+// In-process shards: dst gets, for every word, the copy of its block's owner (replication of R / V).
+struct ShardPtrs {
+  const uint32_t* p[16];
+};
+__global__ void k_gather_owned(const CompDev* __restrict__ comp, ShardPtrs src, uint32_t* __restrict__ dst) {
+  const CompDev& C = comp[0];
+  const int64_t n = (int64_t)C.VA * C.wpr;
+  for (int64_t gw = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; gw < n; gw += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t row = (int32_t)(gw / C.wpr), w = (int32_t)(gw - (int64_t)row * C.wpr);
+    const int q = (int)((((int64_t)row * C.bpr) + (w >> 5)) % C.sh_world);
+    if (src.p[q] != dst) dst[gw] = src.p[q][gw];
+  }
+}
+struct ShardPtrs64 {
+  const unsigned long long* p[16];
+};
+__global__ void k_gather_owned_blocks(int64_t nblocks, int G, ShardPtrs64 src, unsigned long long* __restrict__ dst) {
+  for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < nblocks; b += (int64_t)gridDim.x * blockDim.x) {
+    const int q = (int)(b % G);
+    if (src.p[q] != dst) dst[b] = src.p[q][b];
+  }
+}
+
+// Owner-major numbering of a sharded composition: per-block values in the order (owner, block id)
+// -- rank q's blocks q, q + G, ... are positions [start_q, start_q + n_q) -- so every shard's states
+// and arcs are one contiguous range of ids / slots (the shards concatenate into the whole CSR).
+__device__ __forceinline__ int64_t om_pos(int64_t blk, int64_t nb, int G) {
+  const int64_t q = blk % G, base = nb / G, rem = nb % G;
+  return q * base + min(q, rem) + blk / G;
+}
+template <typename T>
+__global__ void k_om_gather(const T* __restrict__ in, int64_t nb, int G, T* __restrict__ out) {
+  for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < nb; b += (int64_t)gridDim.x * blockDim.x)
+    out[om_pos(b, nb, G)] = in[b];
+}
+__global__ void k_om_scatter(const int64_t* __restrict__ scanned, int64_t nb, int G, int64_t* __restrict__ out) {
+  for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b <= nb; b += (int64_t)gridDim.x * blockDim.x)
+    out[b] = b < nb ? scanned[om_pos(b, nb, G)] : scanned[nb];
+}
 
 __global__ void k_shift_i64(int64_t* __restrict__ a, int64_t n, int64_t d) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
@@ -1571,8 +1626,9 @@ __global__ void __launch_bounds__(kThreads, 2) k_emit(Ctx cx, const int64_t* __r
     const Chunk ch = decode_chunk(cx, q);
     const CompDev& C = cx.comps[ch.comp];
     const int64_t kb0 = C.K + (int64_t)ch.ua * C.bpr;  // global block index of (ua, block 0)
-    if (ch.ua < C.own_r0 || ch.ua >= C.own_r1) continue;            // sharded: another shard emits it
-    if (cx.idbase[kb0 + ch.b1] == cx.idbase[kb0 + ch.b0]) continue;  // no states in the chunk
+    if (!owned(C, ch.ua, ch.b0 * kPairsPerBlock)) continue;  // sharded (one block per chunk): another shard emits it
+    if (C.sh_world > 1 ? cx.vcount[kb0 + ch.b0] == 0 : cx.idbase[kb0 + ch.b1] == cx.idbase[kb0 + ch.b0])
+      continue;  // no states in the chunk
     const ViewDev& Av = C.Af;
     const ViewDev& Bv = C.Bf;
     const int64_t id_comp = tot[2 * ch.comp];
@@ -2379,8 +2435,8 @@ fst_status compose_impl(int32_t n, const fst_handle* a, const fst_handle* b, cud
     C.CB = std::max<int32_t>(1, (C.bpr + cpr - 1) / cpr);
     C.cpr = std::max<int32_t>(1, (C.bpr + C.CB - 1) / C.CB);
     C.smallA = A->max_olabel < 63;
-    C.own_r0 = 0;
-    C.own_r1 = C.VA;
+    C.sh_world = 1;
+    C.sh_rank = 0;
     C.W = W;
     C.K = K;
     C.Q = Q;
@@ -2750,13 +2806,14 @@ namespace {
 
 struct Shard {
   int rank = 0;
-  int32_t r0 = 0, r1 = 0;
   BufferPtr wb;
   Ctx cx{};
   CompDev comp{};
   CompDev* d_comp = nullptr;
   int64_t *d_seed1 = nullptr, *d_seed2 = nullptr, *d_tot = nullptr, *d_tmp = nullptr;
-  uint32_t* recv = nullptr;  // NCCL: one slice per peer
+  uint32_t* recv = nullptr;  // NCCL: one packed slice per peer (received claims in this rank's blocks)
+  uint32_t* send = nullptr;  // NCCL: one packed slice per peer (claims in the peer's blocks)
+  int64_t *om_vals = nullptr, *om_ids = nullptr, *om_arcs = nullptr;  // owner-major numbering scratch
   unsigned long long* d_cnt = nullptr;
   char* base = nullptr;
   size_t zero_lo = 0, zero_hi = 0, o_ctrl = 0, o_kept = 0, o_misc = 0;
@@ -2806,14 +2863,10 @@ fst_status compose_sharded_impl(fst* A, fst* B, int world, fst_comm* comm, cudaS
   C0.VB = B->V;
   C0.wpr = (B->V + 31) / 32;
   C0.bpr = (C0.wpr + kWordsPerBlock - 1) / kWordsPerBlock;
-  {
-    const int64_t rows = std::max<int64_t>(1, C0.VA / world);
-    int64_t want = (8ll * g_grid + rows - 1) / rows;
-    int32_t cpr = (int32_t)std::max<int64_t>(1, std::min<int64_t>(want, C0.bpr));
-    cpr = std::max<int32_t>(cpr, (C0.bpr + kChunkMaxBlocks - 1) / kChunkMaxBlocks);
-    C0.CB = std::max<int32_t>(1, (C0.bpr + cpr - 1) / cpr);
-    C0.cpr = std::max<int32_t>(1, (C0.bpr + C0.CB - 1) / C0.CB);
-  }
+  // one block per chunk: a chunk then has a single owner (blocks are dealt to the ranks round-robin)
+  C0.CB = 1;
+  C0.cpr = C0.bpr;
+  C0.sh_world = world;
   C0.smallA = A->max_olabel < 63;
   const int64_t nwords = (int64_t)C0.VA * C0.wpr, nblocks = (int64_t)C0.VA * C0.bpr,
                 nchunks = (int64_t)C0.VA * C0.cpr;
@@ -2822,9 +2875,14 @@ fst_status compose_sharded_impl(fst* A, fst* B, int world, fst_comm* comm, cudaS
     return FST_E_CAPACITY;
   }
   const int64_t seed1 = (int64_t)C0.nAccA * C0.nAccB, seed2 = (int64_t)C0.nStartA * C0.nStartB;
-  auto row0 = [&](int q) { return (int32_t)((int64_t)C0.VA * q / world); };
-  int32_t maxrows = 0;
-  for (int q = 0; q < world; ++q) maxrows = std::max(maxrows, row0(q + 1) - row0(q));
+  if (world > 16) {
+    set_error(FST_E_INVALID_ARG, "sharded compose: at most 16 shards");
+    return FST_E_INVALID_ARG;
+  }
+  // blocks of rank q: ids q, q + world, ...; owner-major positions [om_start(q), om_start(q) + om_n(q))
+  auto om_n = [&](int q) { return nblocks > q ? (nblocks - q + world - 1) / world : (int64_t)0; };
+  auto om_start = [&](int q) { return (int64_t)q * (nblocks / world) + std::min<int64_t>(q, nblocks % world); };
+  const int64_t slot = om_n(0) * 32;  // packed words per peer (rank 0 owns the most blocks)
   unsigned long long* hp = pinned_scratch();
   if (!hp) {
     set_error(FST_E_CUDA, "cudaMallocHost failed");
@@ -2835,8 +2893,6 @@ fst_status compose_sharded_impl(fst* A, fst* B, int world, fst_comm* comm, cudaS
   for (size_t i = 0; i < sh.size(); ++i) {
     Shard& S = sh[i];
     S.rank = local ? (int)i : comm->rank;
-    S.r0 = row0(S.rank);
-    S.r1 = row0(S.rank + 1);
     size_t off = 0;
     auto take = [&](size_t bytes) { size_t o = off; off += (bytes + 255) & ~size_t(255); return o; };
     const size_t oR = take(4 * nwords), oV = take(4 * nwords), oF0 = take(4 * nwords), oF1 = take(4 * nwords);
@@ -2850,7 +2906,8 @@ fst_status compose_sharded_impl(fst* A, fst* B, int world, fst_comm* comm, cudaS
     const size_t ohist = take(8 * kMaxLevelStats), omisc = take(8 * 8);
     const size_t ocomps = take(sizeof(CompDev)), oseed1 = take(16), oseed2 = take(16), otot = take(8 * 4);
     const size_t ocnt8 = take(32 * nwords), ocnt = take(8);
-    const size_t orecv = take(local ? 4 : 4 * (size_t)world * maxrows * C0.wpr);
+    const size_t orecv = take(local ? 4 : 4 * (size_t)world * slot), osend = take(local ? 4 * (size_t)slot : 4 * (size_t)world * slot);
+    const size_t oomv = take(8 * (nblocks + 1)), oomi = take(8 * (nblocks + 1)), oomk = take(8 * (nblocks + 1));
     st = alloc_buffer(off, s, &S.wb);
     if (st) return st == FST_E_OOM ? FST_E_CAPACITY : st;
     char* base = (char*)S.wb->ptr;
@@ -2886,14 +2943,17 @@ fst_status compose_sharded_impl(fst* A, fst* B, int world, fst_comm* comm, cudaS
     S.d_tmp = (int64_t*)(base + otmp);
     S.d_cnt = (unsigned long long*)(base + ocnt);
     S.recv = (uint32_t*)(base + orecv);
+    S.send = (uint32_t*)(base + osend);
+    S.om_vals = (int64_t*)(base + oomv);
+    S.om_ids = (int64_t*)(base + oomi);
+    S.om_arcs = (int64_t*)(base + oomk);
     S.zero_lo = oR;
     S.zero_hi = ol0;
     S.o_ctrl = octrl;
     S.o_kept = okept;
     S.o_misc = omisc;
     S.comp = C0;
-    S.comp.own_r0 = S.r0;
-    S.comp.own_r1 = S.r1;
+    S.comp.sh_rank = S.rank;
     FSTC_CUDA_TRY(cudaMemsetAsync(base + oR, 0, ol0 - oR, s));  // bitmaps, flags, OUT
     FSTC_CUDA_TRY(cudaMemsetAsync(base + octrl, 0, sizeof(LevelCtrl) * 3, s));
     FSTC_CUDA_TRY(cudaMemsetAsync(base + okept, 0, 8 * nblocks, s));
@@ -2903,23 +2963,20 @@ fst_status compose_sharded_impl(fst* A, fst* B, int world, fst_comm* comm, cudaS
     FSTC_CUDA_TRY(cudaMemcpyAsync(S.d_seed1, sd1, 16, cudaMemcpyHostToDevice, s));
     FSTC_CUDA_TRY(cudaMemcpyAsync(S.d_seed2, sd2, 16, cudaMemcpyHostToDevice, s));
   }
-  const int64_t wlo = 0;
-  (void)wlo;
-  // words of rank q's rows
-  auto wbeg = [&](int q) { return (int64_t)row0(q) * C0.wpr; };
-  auto wcnt = [&](int q) { return (int64_t)(row0(q + 1) - row0(q)) * C0.wpr; };
-  // replicate a bitmap (uint32 words over the whole pair space): every shard gets the owners' rows
+  const unsigned agrid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(nblk(slot, 256), 8 * sm_count()));
+  // replicate a bitmap (uint32 words over the whole pair space): every shard gets the owners' blocks
   auto replicate_bits = [&](uint32_t* Shard::*dummy, bool isR) -> fst_status {
     (void)dummy;
     if (local) {
-      for (auto& Sr : sh)
-        for (auto& Sq : sh)
-          if (&Sr != &Sq && wcnt(Sq.rank) > 0) {
-            uint32_t* dst = isR ? Sr.cx.R : Sr.cx.V;
-            const uint32_t* src = isR ? Sq.cx.R : Sq.cx.V;
-            FSTC_CUDA_TRY(cudaMemcpyAsync(dst + wbeg(Sq.rank), src + wbeg(Sq.rank), 4 * wcnt(Sq.rank),
-                                          cudaMemcpyDeviceToDevice, s));
-          }
+      if (world > 1) {
+        ShardPtrs src{};
+        for (auto& Sq : sh) src.p[Sq.rank] = isR ? Sq.cx.R : Sq.cx.V;
+        for (auto& Sr : sh) {
+          k_gather_owned<<<nblk(nwords, 256) < 8u * sm_count() ? nblk(nwords, 256) : 8u * sm_count(), 256, 0, s>>>(
+              Sr.d_comp, src, isR ? Sr.cx.R : Sr.cx.V);
+          FSTC_LAUNCH_CHECK();
+        }
+      }
     } else {
       uint32_t* p = isR ? sh[0].cx.R : sh[0].cx.V;
       FSTC_NCCL_TRY(nc->AllReduce(p, p, (size_t)nwords, kNcclUint32, kNcclSum, comm->comm, s));
@@ -2951,33 +3008,37 @@ fst_status compose_sharded_impl(fst* A, fst* B, int world, fst_comm* comm, cudaS
         FSTC_LAUNCH_CHECK();
         ++level_launches;
       }
-      // deliver the claims in other shards' rows to their owners, who claim them
-      if (local) {
+      // deliver the claims in other shards' blocks to their owners, who claim them: in-process shards
+      // read each other's OUT bitmaps; NCCL ranks pack the OUT words of every peer's blocks into one
+      // slice per peer and exchange them (grouped send / recv = all-to-all)
+      if (local) {  // the same packed slices as the NCCL path; the "transport" is the shared device
         for (auto& Sr : sh)
           for (auto& Sq : sh) {
-            if (&Sr == &Sq || wcnt(Sr.rank) == 0) continue;
-            const uint32_t* in = Sq.cx.OUT + wbeg(Sr.rank);
-            const unsigned grid = (unsigned)std::min<int64_t>(nblk(wcnt(Sr.rank), 256), 8 * sm_count());
-            if (stage2) k_apply_remote<true><<<grid, 256, 0, s>>>(Sr.cx, in, level);
-            else k_apply_remote<false><<<grid, 256, 0, s>>>(Sr.cx, in, level);
+            if (&Sr == &Sq) continue;
+            k_pack_owner<<<agrid, 256, 0, s>>>(Sq.d_comp, Sq.cx.OUT, Sr.rank, Sq.send);
+            FSTC_LAUNCH_CHECK();
+            if (stage2) k_apply_remote<true><<<agrid, 256, 0, s>>>(Sr.cx, Sq.send, 1, level);
+            else k_apply_remote<false><<<agrid, 256, 0, s>>>(Sr.cx, Sq.send, 1, level);
             FSTC_LAUNCH_CHECK();
           }
       } else if (world > 1) {
         Shard& S = sh[0];
-        const int64_t mine = wcnt(S.rank);
+        for (int q = 0; q < world; ++q) {
+          if (q == S.rank) continue;
+          k_pack_owner<<<agrid, 256, 0, s>>>(S.d_comp, S.cx.OUT, q, S.send + (size_t)q * slot);
+          FSTC_LAUNCH_CHECK();
+        }
         FSTC_NCCL_TRY(nc->GroupStart());
         for (int q = 0; q < world; ++q) {
           if (q == S.rank) continue;
-          FSTC_NCCL_TRY(nc->Send(S.cx.OUT + wbeg(q), (size_t)wcnt(q), kNcclUint32, q, comm->comm, s));
-          FSTC_NCCL_TRY(nc->Recv(S.recv + (size_t)q * maxrows * C0.wpr, (size_t)mine, kNcclUint32, q, comm->comm, s));
+          FSTC_NCCL_TRY(nc->Send(S.send + (size_t)q * slot, (size_t)(om_n(q) * 32), kNcclUint32, q, comm->comm, s));
+          FSTC_NCCL_TRY(nc->Recv(S.recv + (size_t)q * slot, (size_t)(om_n(S.rank) * 32), kNcclUint32, q, comm->comm, s));
         }
         FSTC_NCCL_TRY(nc->GroupEnd());
         for (int q = 0; q < world; ++q) {
-          if (q == S.rank || mine == 0) continue;
-          const unsigned grid = (unsigned)std::min<int64_t>(nblk(mine, 256), 8 * sm_count());
-          const uint32_t* in = S.recv + (size_t)q * maxrows * C0.wpr;
-          if (stage2) k_apply_remote<true><<<grid, 256, 0, s>>>(S.cx, in, level);
-          else k_apply_remote<false><<<grid, 256, 0, s>>>(S.cx, in, level);
+          if (q == S.rank) continue;
+          if (stage2) k_apply_remote<true><<<agrid, 256, 0, s>>>(S.cx, S.recv + (size_t)q * slot, 1, level);
+          else k_apply_remote<false><<<agrid, 256, 0, s>>>(S.cx, S.recv + (size_t)q * slot, 1, level);
           FSTC_LAUNCH_CHECK();
         }
       }
@@ -3029,14 +3090,16 @@ fst_status compose_sharded_impl(fst* A, fst* B, int world, fst_comm* comm, cudaS
     if (st) return st;
     st = replicate_bits(nullptr, false);
     if (st) return st;
-    // per-block arc counts of the owners' rows
+    // per-block arc counts of the owners' blocks
     if (local) {
-      for (auto& Sr : sh)
-        for (auto& Sq : sh)
-          if (&Sr != &Sq && wcnt(Sq.rank) > 0) {
-            const int64_t b0 = (int64_t)Sq.r0 * C0.bpr, nb = (int64_t)(Sq.r1 - Sq.r0) * C0.bpr;
-            FSTC_CUDA_TRY(cudaMemcpyAsync(Sr.cx.kept + b0, Sq.cx.kept + b0, 8 * nb, cudaMemcpyDeviceToDevice, s));
-          }
+      if (world > 1) {
+        ShardPtrs64 src{};
+        for (auto& Sq : sh) src.p[Sq.rank] = Sq.cx.kept;
+        for (auto& Sr : sh) {
+          k_gather_owned_blocks<<<nblk(nblocks, 256), 256, 0, s>>>(nblocks, world, src, Sr.cx.kept);
+          FSTC_LAUNCH_CHECK();
+        }
+      }
     } else {
       FSTC_NCCL_TRY(nc->AllReduce(sh[0].cx.kept, sh[0].cx.kept, (size_t)nblocks, kNcclUint64, kNcclSum, comm->comm, s));
     }
@@ -3057,18 +3120,29 @@ fst_status compose_sharded_impl(fst* A, fst* B, int world, fst_comm* comm, cudaS
     Shard& S = sh[i];
     k_block_counts<<<nblk(nblocks * 32, 256), 256, 0, s>>>(S.cx);
     FSTC_LAUNCH_CHECK();
-    st = exclusive_scan_i32(S.cx.vcount, nblocks, S.cx.idbase, S.d_tmp, s);
+    // owner-major numbering: scan the per-block counts in (owner, block id) order, then give every
+    // block its base (rank q's states / arcs are then the contiguous ranges starting at om_start(q))
+    const unsigned gb = nblk(nblocks + 1, 256);
+    k_om_gather<int32_t><<<gb, 256, 0, s>>>(S.cx.vcount, nblocks, world, (int32_t*)S.om_vals);
+    FSTC_LAUNCH_CHECK();
+    st = exclusive_scan_i32((const int32_t*)S.om_vals, nblocks, S.om_ids, S.d_tmp, s);
     if (st) return st;
-    st = exclusive_scan_u64(S.cx.kept, nblocks, S.cx.arcbase, S.d_tmp, s);
+    k_om_scatter<<<gb, 256, 0, s>>>(S.om_ids, nblocks, world, S.cx.idbase);
+    FSTC_LAUNCH_CHECK();
+    k_om_gather<unsigned long long><<<gb, 256, 0, s>>>(S.cx.kept, nblocks, world, (unsigned long long*)S.om_vals);
+    FSTC_LAUNCH_CHECK();
+    st = exclusive_scan_u64((const unsigned long long*)S.om_vals, nblocks, S.om_arcs, S.d_tmp, s);
     if (st) return st;
+    k_om_scatter<<<gb, 256, 0, s>>>(S.om_arcs, nblocks, world, S.cx.arcbase);
+    FSTC_LAUNCH_CHECK();
     int64_t hb[6];
-    const int64_t b0 = (int64_t)S.r0 * C0.bpr, b1 = (int64_t)S.r1 * C0.bpr;
-    FSTC_CUDA_TRY(cudaMemcpyAsync(&hb[0], S.cx.idbase + b0, 8, cudaMemcpyDeviceToHost, s));
-    FSTC_CUDA_TRY(cudaMemcpyAsync(&hb[1], S.cx.idbase + b1, 8, cudaMemcpyDeviceToHost, s));
-    FSTC_CUDA_TRY(cudaMemcpyAsync(&hb[2], S.cx.arcbase + b0, 8, cudaMemcpyDeviceToHost, s));
-    FSTC_CUDA_TRY(cudaMemcpyAsync(&hb[3], S.cx.arcbase + b1, 8, cudaMemcpyDeviceToHost, s));
-    FSTC_CUDA_TRY(cudaMemcpyAsync(&hb[4], S.cx.idbase + nblocks, 8, cudaMemcpyDeviceToHost, s));
-    FSTC_CUDA_TRY(cudaMemcpyAsync(&hb[5], S.cx.arcbase + nblocks, 8, cudaMemcpyDeviceToHost, s));
+    const int64_t p0 = om_start(S.rank), p1 = p0 + om_n(S.rank);
+    FSTC_CUDA_TRY(cudaMemcpyAsync(&hb[0], S.om_ids + p0, 8, cudaMemcpyDeviceToHost, s));
+    FSTC_CUDA_TRY(cudaMemcpyAsync(&hb[1], S.om_ids + p1, 8, cudaMemcpyDeviceToHost, s));
+    FSTC_CUDA_TRY(cudaMemcpyAsync(&hb[2], S.om_arcs + p0, 8, cudaMemcpyDeviceToHost, s));
+    FSTC_CUDA_TRY(cudaMemcpyAsync(&hb[3], S.om_arcs + p1, 8, cudaMemcpyDeviceToHost, s));
+    FSTC_CUDA_TRY(cudaMemcpyAsync(&hb[4], S.om_ids + nblocks, 8, cudaMemcpyDeviceToHost, s));
+    FSTC_CUDA_TRY(cudaMemcpyAsync(&hb[5], S.om_arcs + nblocks, 8, cudaMemcpyDeviceToHost, s));
     FSTC_CUDA_TRY(cudaStreamSynchronize(s));
     total_states = hb[4];
     total_arcs = hb[5];

@@ -65,7 +65,7 @@ struct CompDev {
   int64_t W;         // first word of this composition's pair space
   int64_t K;         // first block
   int64_t Q;         // first chunk
-  int32_t own_r0, own_r1;  // rows (A states) owned by this shard: [own_r0, own_r1) (all rows if unsharded)
+  int32_t sh_world, sh_rank;  // sharded composition: block (row * bpr + j) is owned by rank (block % sh_world)
   // outputs (filled before the emit kernel; for a shard they are biased so that a global state id /
   // arc slot indexes the shard's own buffers)
   int64_t* row_ptr;
@@ -89,6 +89,12 @@ struct LevelCtrl {
 };
 
 constexpr int kMaxLevelStats = 1 << 16;
+
+// Ownership of pair-space blocks in a sharded composition: the 1024-pair block j of row a
+// has linear id a * bpr + j and belongs to rank (id mod world) -- every row is spread over all ranks.
+__device__ __forceinline__ bool owned(const CompDev& C, int32_t row, int32_t col) {
+  return C.sh_world <= 1 || (((int64_t)row * C.bpr + (col >> 10)) % C.sh_world) == C.sh_rank;
+}
 
 __device__ __forceinline__ int find_comp(const CompDev* __restrict__ comps, int ncomp, int64_t blk) {
   // largest i with comps[i].K <= blk

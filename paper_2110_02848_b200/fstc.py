@@ -302,18 +302,6 @@ def fst_compose_sharded(a: "Fst", b: "Fst", comm: Comm, stream=None) -> "Fst":
     return Fst(h)
 
 
-def merge_shards(parts: Sequence[Dict[str, np.ndarray]], arc_offsets: Sequence[int]) -> Dict[str, np.ndarray]:
-    """Concatenate shard host copies (rank order) into the unsharded graph (numpy; host helper)."""
-    out = {k: np.concatenate([p[k] for p in parts]) for k in ("ilabel", "olabel", "dst", "weight", "is_start",
-                                                              "is_accept", "pair_a", "pair_b")}
-    rps = [p["row_ptr"][:-1] + off for p, off in zip(parts, arc_offsets)]
-    total = sum(int(p["num_arcs"]) for p in parts)
-    out["row_ptr"] = np.concatenate(rps + [np.array([total], np.int64)])
-    out["num_states"] = sum(int(p["num_states"]) for p in parts)
-    out["num_arcs"] = total
-    return out
-
-
 def fst_set_profiling(on: bool):
     load_library().fst_set_profiling(1 if on else 0)
 

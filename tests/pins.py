@@ -489,3 +489,16 @@ def trellis_compose(A, B):
                 arcs.append(((t, b), (t + 1, d), int(A.ilabel[ea]), int(B.olabel[eb]),
                              f32add(A.weight[ea], B.weight[eb])))
     return build_canonical(VB, states, arcs)
+
+
+def merge_shards(parts, arc_offsets):
+    """Concatenates the host copies of a sharded composition's shards (rank order) into one CSR: the
+    shards hold contiguous state-id ranges with global dst ids and shard-local row_ptr (test helper)."""
+    out = {k: np.concatenate([p[k] for p in parts]) for k in ("ilabel", "olabel", "dst", "weight", "is_start",
+                                                              "is_accept", "pair_a", "pair_b")}
+    rps = [p["row_ptr"][:-1] + off for p, off in zip(parts, arc_offsets)]
+    total = sum(int(p["num_arcs"]) for p in parts)
+    out["row_ptr"] = np.concatenate(rps + [np.array([total], np.int64)])
+    out["num_states"] = sum(int(p["num_states"]) for p in parts)
+    out["num_arcs"] = total
+    return out
