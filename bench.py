@@ -481,7 +481,7 @@ def run_sharded(args, fstc, stream, dev, pg, rank, local_rank, world):
     comm = fstc.Comm(world, rank, uid[0])
     a, b = fstc.fst_create(A, stream), fstc.fst_create(B, stream)
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.int32, device=dev)
-    fstc.fst_set_profiling(True)
+    fstc.fst_set_profiling(False)
 
     def step():
         with torch.cuda.stream(stream):
@@ -510,16 +510,26 @@ def run_sharded(args, fstc, stream, dev, pg, rank, local_rank, world):
         ms, info, st = step()
         times.append(ms)
     launches = fstc.fst_launch_count() - l0
+    torch.cuda.synchronize()
+    if pg:
+        pg.barrier()
     clocks = sampler.stop()
     max_ms, _ = parallel.reduce_timing(sum(times), 0.0, pg, dev)
+    fstc.fst_set_profiling(True)  # phases: one extra untimed step
+    _, _, st = step()
+    fstc.fst_set_profiling(False)
     E_C = info["total_arcs"]
     value = E_C * args.steps / (max_ms / 1e3)
     line = {"metric": "composed arcs/sec", "value": value, "unit": "arcs/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": max_ms / args.steps, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": WORKLOADS[args.workload][0], "E_C": E_C, "V_C": info["total_states"],
-                       "parallelism": f"one composition sharded by pair-space rows over {world} rank(s); "
-                                      f"per-level NCCL send/recv of claimed row slices, R/V all-reduce"},
+            "config": workload_config(args.workload, [A], B),
+            "result": {"E_C": E_C, "V_C": info["total_states"]},
+            "setup": {"parallelism": f"one composition sharded over {world} rank(s) by state-pair block (block id "
+                                     f"mod {world}); per-level all-to-all of packed claim slices (NCCL grouped "
+                                     f"send/recv), R / V all-reduce after each stage",
+                      "seeds": list(input_seeds(args.workload, 0)),
+                      "timing": "timed steps without per-phase events; phases_ms from 1 extra untimed step"},
             "phases_ms": {"stage1_backward_bfs": st["ms_stage1"], "stage2_forward_bfs": st["ms_stage2"],
                           "emit": st["ms_emit"]},
             "gpu_launches": launches, "clocks": clocks}
@@ -606,8 +616,10 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default=os.environ.get("FSTC_BENCH_WORKLOAD", "c4"), choices=sorted(WORKLOADS))
     ap.add_argument("--e2e-steps", type=int, default=3)
-    ap.add_argument("--mode", default=os.environ.get("FSTC_BENCH_MODE", "replicas"), choices=["replicas", "sharded"],
-                    help="replicas: independent compositions per GPU (weak); sharded: one composition over all GPUs")
+    ap.add_argument("--mode", default=os.environ.get("FSTC_BENCH_MODE", "auto"), choices=["auto", "replicas", "sharded"],
+                    help="replicas: independent compositions per GPU (weak); sharded: one composition over all GPUs "
+                         "(strong); auto: sharded for configs[3] at N > 1 (BASELINE: 'sharded by state-pair owner'), "
+                         "the LPT-split batch for configs[4], replicas otherwise")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--forward", action="store_true",
                     help="also time fst_forward_score over the composed graphs (c5: lexicon o emissions DAGs)")
@@ -619,6 +631,9 @@ def main():
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3
+    if args.mode == "auto":
+        world = int(os.environ.get("WORLD_SIZE", 1))
+        args.mode = "sharded" if (world > 1 and args.workload.startswith("c4")) else "replicas"
     if args.impl == "reference":
         return run_reference(args)
     return run_ours(args)
