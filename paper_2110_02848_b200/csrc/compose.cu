@@ -1481,11 +1481,11 @@ __global__ void k_apply_remote(Ctx cx, const uint32_t* __restrict__ in, int pack
   int32_t* listn = p ? cx.list0 : cx.list1;
   uint32_t* vis = kStage2 ? cx.V : cx.R;
   const CompDev& C = cx.comps[0];
-  const int G = C.sh_world, me = C.sh_rank;
-  const int64_t nb = (int64_t)C.VA * C.bpr, mine = nb > me ? (nb - me + G - 1) / G : 0;
+  const int me = C.sh_rank;
+  const int64_t mine = owner_nblocks(C, me);
   unsigned nnew = 0;
   for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < mine * 32; t += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t blk = (t >> 5) * G + me;
+    const int64_t blk = owner_block(C, me, t >> 5);
     const int32_t row = (int32_t)(blk / C.bpr), j = (int32_t)(blk - (int64_t)row * C.bpr);
     const int w = j * 32 + (int)(t & 31);
     if (w >= C.wpr) continue;
@@ -1505,10 +1505,9 @@ __global__ void k_apply_remote(Ctx cx, const uint32_t* __restrict__ in, int pack
 __global__ void k_pack_owner(const CompDev* __restrict__ comp, const uint32_t* __restrict__ bits, int q,
                              uint32_t* __restrict__ dst) {
   const CompDev& C = comp[0];
-  const int G = C.sh_world;
-  const int64_t nb = (int64_t)C.VA * C.bpr, n = nb > q ? (nb - q + G - 1) / G : 0;
+  const int64_t n = owner_nblocks(C, q);
   for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n * 32; t += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t blk = (t >> 5) * G + q;
+    const int64_t blk = owner_block(C, q, t >> 5);
     const int32_t row = (int32_t)(blk / C.bpr), j = (int32_t)(blk - (int64_t)row * C.bpr);
     const int w = j * 32 + (int)(t & 31);
     dst[t] = w < C.wpr ? bits[C.W + (int64_t)row * C.wpr + w] : 0u;
@@ -1524,24 +1523,39 @@ __global__ void k_gather_owned(const CompDev* __restrict__ comp, ShardPtrs src, 
   const int64_t n = (int64_t)C.VA * C.wpr;
   for (int64_t gw = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; gw < n; gw += (int64_t)gridDim.x * blockDim.x) {
     const int32_t row = (int32_t)(gw / C.wpr), w = (int32_t)(gw - (int64_t)row * C.wpr);
-    const int q = (int)((((int64_t)row * C.bpr) + (w >> 5)) % C.sh_world);
+    const int q = blk_owner(C, (int64_t)row * C.bpr + (w >> 5));
     if (src.p[q] != dst) dst[gw] = src.p[q][gw];
   }
 }
 struct ShardPtrs64 {
   const unsigned long long* p[16];
 };
-__global__ void k_gather_owned_blocks(int64_t nblocks, int G, ShardPtrs64 src, unsigned long long* __restrict__ dst) {
+__global__ void k_gather_owned_blocks(const CompDev* __restrict__ comp, ShardPtrs64 src,
+                                      unsigned long long* __restrict__ dst) {
+  const CompDev& C = comp[0];
+  const int64_t nblocks = (int64_t)C.VA * C.bpr;
   for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < nblocks; b += (int64_t)gridDim.x * blockDim.x) {
-    const int q = (int)(b % G);
+    const int q = blk_owner(C, b);
     if (src.p[q] != dst) dst[b] = src.p[q][b];
+  }
+}
+
+// NCCL replication of a bitmap: every rank keeps only the words of its own blocks, then an all-reduce
+// (sum of disjoint bits = OR) gives every rank the whole bitmap.
+__global__ void k_mask_unowned(const CompDev* __restrict__ comp, uint32_t* __restrict__ bits) {
+  const CompDev& C = comp[0];
+  const int64_t n = (int64_t)C.VA * C.wpr;
+  for (int64_t gw = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; gw < n; gw += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t row = (int32_t)(gw / C.wpr), w = (int32_t)(gw - (int64_t)row * C.wpr);
+    if (!owned(C, row, w * 32) && bits[gw]) bits[gw] = 0u;
   }
 }
 
 // Owner-major numbering of a sharded composition: per-block values in the order (owner, block id)
 // -- rank q's blocks q, q + G, ... are positions [start_q, start_q + n_q) -- so every shard's states
 // and arcs are one contiguous range of ids / slots (the shards concatenate into the whole CSR).
-__device__ __forceinline__ int64_t om_pos(int64_t blk, int64_t nb, int G) {
+__device__ __forceinline__ int64_t om_pos(int64_t blk, int64_t nb, int G) {  // block-interleaved mode
+  if (G <= 1) return blk;  // (rows mode passes G = 1: owner-major order is block order)
   const int64_t q = blk % G, base = nb / G, rem = nb % G;
   return q * base + min(q, rem) + blk / G;
 }
@@ -2219,6 +2233,7 @@ fst_status tile_rows(fst* A, int which, int self, int slot_cap, int vr_cap, int 
   fst::TileRows out;
   out.key = key;
   out.n = (int32_t)tr.size() - 1;
+  out.h = tr;
   fst_status st = alloc_buffer(sizeof(int32_t) * tr.size(), s, &out.buf);
   if (st) return st;
   out.d = (int32_t*)out.buf->ptr;
@@ -2281,14 +2296,14 @@ fst_status tile_plan(fst* A, fst* B, int64_t pairs, bool want_prov, cudaStream_t
   int32_t nt;
   st = tile_rows(A, 0, self, kPSlots, 0, byte1, s, &d, &nt);
   if (st) return st;
-  P->s1 = TileArgs{side(0, 0), d, nt, self, byte1, 8};
+  P->s1 = TileArgs{side(0, 0), d, nt, self, byte1, 8, 0, nt};
   P->cnt = P->s1;
   st = tile_rows(A, 1, self, kPSlots, 0, byte2, s, &d, &nt);
   if (st) return st;
-  P->s2 = TileArgs{side(1, 1), d, nt, self, byte2, 8};
+  P->s2 = TileArgs{side(1, 1), d, nt, self, byte2, 8, 0, nt};
   st = tile_rows(A, 0, self, kESlots, vr_rows, 0, s, &d, &nt);
   if (st) return st;
-  P->emit = TileArgs{side(0, 0), d, nt, self, 0, 8};
+  P->emit = TileArgs{side(0, 0), d, nt, self, 0, 8, 0, nt};
   P->vr_rows = vr_rows;
   P->smem_pull = smem_pull;
   P->smem_count = smem_count;
@@ -2863,10 +2878,16 @@ fst_status compose_sharded_impl(fst* A, fst* B, int world, fst_comm* comm, cudaS
   C0.VB = B->V;
   C0.wpr = (B->V + 31) / 32;
   C0.bpr = (C0.wpr + kWordsPerBlock - 1) / kWordsPerBlock;
-  // one block per chunk: a chunk then has a single owner (blocks are dealt to the ranks round-robin)
+  // one block per chunk: a chunk then has a single owner
   C0.CB = 1;
   C0.cpr = C0.bpr;
   C0.sh_world = world;
+  // compositions that fit the tile path are sharded by contiguous row ranges (each rank's tiles are its
+  // own; ids stay in key order); the others by interleaved blocks (trellis rows spread over all ranks)
+  TilePlan tp;
+  st = tile_plan(A, B, (int64_t)A->V * B->V, false, s, &tp);
+  if (st) return st;
+  C0.sh_rows = tp.ok ? 1 : 0;
   C0.smallA = A->max_olabel < 63;
   const int64_t nwords = (int64_t)C0.VA * C0.wpr, nblocks = (int64_t)C0.VA * C0.bpr,
                 nchunks = (int64_t)C0.VA * C0.cpr;
@@ -2879,10 +2900,16 @@ fst_status compose_sharded_impl(fst* A, fst* B, int world, fst_comm* comm, cudaS
     set_error(FST_E_INVALID_ARG, "sharded compose: at most 16 shards");
     return FST_E_INVALID_ARG;
   }
-  // blocks of rank q: ids q, q + world, ...; owner-major positions [om_start(q), om_start(q) + om_n(q))
-  auto om_n = [&](int q) { return nblocks > q ? (nblocks - q + world - 1) / world : (int64_t)0; };
-  auto om_start = [&](int q) { return (int64_t)q * (nblocks / world) + std::min<int64_t>(q, nblocks % world); };
-  const int64_t slot = om_n(0) * 32;  // packed words per peer (rank 0 owns the most blocks)
+  // blocks of rank q (owner_block / owner_nblocks); owner-major positions [om_start(q), +om_n(q))
+  auto om_n = [&](int q) { return owner_nblocks(C0, q); };
+  auto om_start = [&](int q) {
+    int64_t st0 = 0;
+    for (int r = 0; r < q; ++r) st0 += om_n(r);
+    return st0;
+  };
+  const int omG = C0.sh_rows ? 1 : world;  // owner-major order == block order in rows mode
+  int64_t slot = 0;  // packed words per peer
+  for (int q = 0; q < world; ++q) slot = std::max<int64_t>(slot, om_n(q) * 32);
   unsigned long long* hp = pinned_scratch();
   if (!hp) {
     set_error(FST_E_CUDA, "cudaMallocHost failed");
@@ -2954,6 +2981,8 @@ fst_status compose_sharded_impl(fst* A, fst* B, int world, fst_comm* comm, cudaS
     S.o_misc = omisc;
     S.comp = C0;
     S.comp.sh_rank = S.rank;
+    S.comp.sh_r0 = sh_row0(C0, S.rank);
+    S.comp.sh_r1 = sh_row0(C0, S.rank + 1);
     FSTC_CUDA_TRY(cudaMemsetAsync(base + oR, 0, ol0 - oR, s));  // bitmaps, flags, OUT
     FSTC_CUDA_TRY(cudaMemsetAsync(base + octrl, 0, sizeof(LevelCtrl) * 3, s));
     FSTC_CUDA_TRY(cudaMemsetAsync(base + okept, 0, 8 * nblocks, s));
@@ -2977,12 +3006,34 @@ fst_status compose_sharded_impl(fst* A, fst* B, int world, fst_comm* comm, cudaS
           FSTC_LAUNCH_CHECK();
         }
       }
-    } else {
+    } else if (world > 1) {
       uint32_t* p = isR ? sh[0].cx.R : sh[0].cx.V;
+      k_mask_unowned<<<8 * sm_count(), 256, 0, s>>>(sh[0].d_comp, p);  // others' (stale) copies out
+      FSTC_LAUNCH_CHECK();
       FSTC_NCCL_TRY(nc->AllReduce(p, p, (size_t)nwords, kNcclUint32, kNcclSum, comm->comm, s));
     }
     return FST_OK;
   };
+  // tile ranges of every shard: the tiles over its rows
+  auto tile_range = [&](const TileArgs& ta0, const fst* Ah, int which, const Shard& S) {
+    TileArgs ta = ta0;
+    if (world > 1) {
+      const std::vector<int32_t>* tr = nullptr;
+      for (const auto& r : Ah->tile_rows)
+        if (r.d == ta0.trow) tr = &r.h;
+      const int32_t lo = sh_row0(C0, S.rank), hi = sh_row0(C0, S.rank + 1);
+      int t0 = 0, t1 = 0;
+      if (tr && hi > lo) {
+        t0 = (int)(std::upper_bound(tr->begin(), tr->end(), lo) - tr->begin()) - 1;
+        t1 = (int)(std::lower_bound(tr->begin(), tr->end(), hi) - tr->begin());
+      }
+      ta.t0 = std::max(0, t0);
+      ta.t1 = std::min(ta0.ntiles, std::max(ta.t0, t1));
+    }
+    (void)which;
+    return ta;
+  };
+  const int64_t K_pull = tile_pull_k();
   fst_compose_stats stats{};
   stats.pair_space = (int64_t)C0.VA * C0.VB;
   stats.num_coaccessible = -1;
@@ -3001,13 +3052,45 @@ fst_status compose_sharded_impl(fst* A, fst* B, int world, fst_comm* comm, cudaS
       }
     }
     if ((stage2 ? seed2 : seed1) == 0 || (stage2 && seed1 == 0)) return FST_OK;
+    // pairs of the stage (direction choice on the tile path): the pair space, then |R|
+    int64_t stage_total = (int64_t)C0.VA * C0.VB;
+    if (stage2 && tp.ok) {
+      FSTC_CUDA_TRY(cudaMemsetAsync(sh[0].cx.misc + 1, 0, 8, s));
+      k_popcount<<<sm_count() * 4, 256, 0, s>>>(sh[0].cx.R, nwords, sh[0].cx.misc + 1);  // R is replicated
+      FSTC_LAUNCH_CHECK();
+      FSTC_CUDA_TRY(cudaMemcpyAsync(hp + 8, sh[0].cx.misc + 1, 8, cudaMemcpyDeviceToHost, s));
+      FSTC_CUDA_TRY(cudaStreamSynchronize(s));
+      stage_total = (int64_t)hp[8];
+    }
+    unsigned long long nf_global = stage2 ? seed2 : seed1;  // (an upper bound for level 0)
+    bool replicated = false;  // vis complete on every shard (after a bottom-up round)
     for (int level = 0;; ++level) {
+      const bool pull = tp.ok && (int64_t)nf_global * K_pull >= stage_total;
+      if (pull) {
+        if (!replicated) {  // a round tests against the whole visited set
+          st = replicate_bits(nullptr, !stage2);
+          if (st) return st;
+        }
+        for (auto& S : sh) {
+          const TileArgs ta = tile_range(stage2 ? tp.s2 : tp.s1, A, stage2 ? 1 : 0, S);
+          if (stage2) launch_tile_pull<true>(ta, tp.grid_pull2, tp.smem_pull, s, S.cx, level);
+          else launch_tile_pull<false>(ta, tp.grid_pull1, tp.smem_pull, s, S.cx, level);
+          FSTC_LAUNCH_CHECK();
+          ++level_launches;
+          ++stats.pull_levels;
+        }
+        // the round's claims (own rows only) -> every shard
+        st = replicate_bits(nullptr, !stage2);
+        if (st) return st;
+        replicated = true;
+      } else {
       for (auto& S : sh) {
         if (stage2) k_level<true><<<g_grid, kThreads, kDynSmem, s>>>(S.cx, level);
         else k_level<false><<<g_grid, kThreads, kDynSmem, s>>>(S.cx, level);
         FSTC_LAUNCH_CHECK();
         ++level_launches;
       }
+      replicated = false;
       // deliver the claims in other shards' blocks to their owners, who claim them: in-process shards
       // read each other's OUT bitmaps; NCCL ranks pack the OUT words of every peer's blocks into one
       // slice per peer and exchange them (grouped send / recv = all-to-all)
@@ -3043,22 +3126,26 @@ fst_status compose_sharded_impl(fst* A, fst* B, int world, fst_comm* comm, cudaS
         }
       }
       for (auto& S : sh) FSTC_CUDA_TRY(cudaMemsetAsync(S.cx.OUT, 0, 4 * nwords, s));
-      // global size of the next frontier
-      unsigned long long total = 0;
+      }  // push level
+      // global size of the next frontier: (active chunks, pairs), summed over the ranks
+      unsigned long long total = 0, nfn = 0;
       if (local) {
         for (auto& S : sh) {
-          FSTC_CUDA_TRY(cudaMemcpyAsync(hp, &S.cx.ctrl[(level + 1) % 3].count, 8, cudaMemcpyDeviceToHost, s));
+          FSTC_CUDA_TRY(cudaMemcpyAsync(hp, &S.cx.ctrl[(level + 1) % 3].count, 16, cudaMemcpyDeviceToHost, s));
           FSTC_CUDA_TRY(cudaStreamSynchronize(s));
-          total += *hp;
+          total += hp[0];
+          nfn += hp[1];
         }
       } else {
         Shard& S = sh[0];
-        FSTC_CUDA_TRY(cudaMemcpyAsync(S.d_cnt, &S.cx.ctrl[(level + 1) % 3].count, 8, cudaMemcpyDeviceToDevice, s));
-        FSTC_NCCL_TRY(nc->AllReduce(S.d_cnt, S.d_cnt, 1, kNcclUint64, kNcclSum, comm->comm, s));
-        FSTC_CUDA_TRY(cudaMemcpyAsync(hp, S.d_cnt, 8, cudaMemcpyDeviceToHost, s));
+        FSTC_CUDA_TRY(cudaMemcpyAsync(S.d_cnt, &S.cx.ctrl[(level + 1) % 3].count, 16, cudaMemcpyDeviceToDevice, s));
+        FSTC_NCCL_TRY(nc->AllReduce(S.d_cnt, S.d_cnt, 2, kNcclUint64, kNcclSum, comm->comm, s));
+        FSTC_CUDA_TRY(cudaMemcpyAsync(hp, S.d_cnt, 16, cudaMemcpyDeviceToHost, s));
         FSTC_CUDA_TRY(cudaStreamSynchronize(s));
-        total = *hp;
+        total = hp[0];
+        nfn = hp[1];
       }
+      nf_global = nfn;
       if (total == 0) {
         for (auto& S : sh) {  // per-level frontier sizes of this shard
           FSTC_CUDA_TRY(cudaMemcpyAsync(hp, S.cx.misc, 8, cudaMemcpyDeviceToHost, s));
@@ -3090,13 +3177,20 @@ fst_status compose_sharded_impl(fst* A, fst* B, int world, fst_comm* comm, cudaS
     if (st) return st;
     st = replicate_bits(nullptr, false);
     if (st) return st;
+    if (tp.ok) {  // pass-1 counts of the own rows (the bottom-up rounds do not count)
+      for (auto& S : sh) {
+        S.cx.warc = (uint32_t*)S.cx.cnt8;
+        launch_tile_count(tile_range(tp.cnt, A, 0, S), tp.grid_count, tp.smem_count, s, S.cx);
+        FSTC_LAUNCH_CHECK();
+      }
+    }
     // per-block arc counts of the owners' blocks
     if (local) {
       if (world > 1) {
         ShardPtrs64 src{};
         for (auto& Sq : sh) src.p[Sq.rank] = Sq.cx.kept;
         for (auto& Sr : sh) {
-          k_gather_owned_blocks<<<nblk(nblocks, 256), 256, 0, s>>>(nblocks, world, src, Sr.cx.kept);
+          k_gather_owned_blocks<<<nblk(nblocks, 256), 256, 0, s>>>(Sr.d_comp, src, Sr.cx.kept);
           FSTC_LAUNCH_CHECK();
         }
       }
@@ -3123,17 +3217,17 @@ fst_status compose_sharded_impl(fst* A, fst* B, int world, fst_comm* comm, cudaS
     // owner-major numbering: scan the per-block counts in (owner, block id) order, then give every
     // block its base (rank q's states / arcs are then the contiguous ranges starting at om_start(q))
     const unsigned gb = nblk(nblocks + 1, 256);
-    k_om_gather<int32_t><<<gb, 256, 0, s>>>(S.cx.vcount, nblocks, world, (int32_t*)S.om_vals);
+    k_om_gather<int32_t><<<gb, 256, 0, s>>>(S.cx.vcount, nblocks, omG, (int32_t*)S.om_vals);
     FSTC_LAUNCH_CHECK();
     st = exclusive_scan_i32((const int32_t*)S.om_vals, nblocks, S.om_ids, S.d_tmp, s);
     if (st) return st;
-    k_om_scatter<<<gb, 256, 0, s>>>(S.om_ids, nblocks, world, S.cx.idbase);
+    k_om_scatter<<<gb, 256, 0, s>>>(S.om_ids, nblocks, omG, S.cx.idbase);
     FSTC_LAUNCH_CHECK();
-    k_om_gather<unsigned long long><<<gb, 256, 0, s>>>(S.cx.kept, nblocks, world, (unsigned long long*)S.om_vals);
+    k_om_gather<unsigned long long><<<gb, 256, 0, s>>>(S.cx.kept, nblocks, omG, (unsigned long long*)S.om_vals);
     FSTC_LAUNCH_CHECK();
     st = exclusive_scan_u64((const unsigned long long*)S.om_vals, nblocks, S.om_arcs, S.d_tmp, s);
     if (st) return st;
-    k_om_scatter<<<gb, 256, 0, s>>>(S.om_arcs, nblocks, world, S.cx.arcbase);
+    k_om_scatter<<<gb, 256, 0, s>>>(S.om_arcs, nblocks, omG, S.cx.arcbase);
     FSTC_LAUNCH_CHECK();
     int64_t hb[6];
     const int64_t p0 = om_start(S.rank), p1 = p0 + om_n(S.rank);
@@ -3199,7 +3293,9 @@ fst_status compose_sharded_impl(fst* A, fst* B, int world, fst_comm* comm, cudaS
     FSTC_CUDA_TRY(cudaMemcpyAsync(S.d_tot, tot, sizeof(tot), cudaMemcpyHostToDevice, s));
     {
       EventTimer te(prof, s);
-      k_emit<<<g_grid, kThreads, kDynSmem, s>>>(S.cx, S.d_tot);
+      if (tp.ok) launch_tile_emit(tile_range(tp.emit, A, 0, S), tp.grid_emit, tp.smem_emit, s, S.cx, S.comp, S.d_tot,
+                                  tp.vr_rows);
+      else k_emit<<<g_grid, kThreads, kDynSmem, s>>>(S.cx, S.d_tot);
       FSTC_LAUNCH_CHECK();
       stats.ms_emit += te.stop();
     }
@@ -3221,6 +3317,7 @@ fst_status compose_sharded_impl(fst* A, fst* B, int world, fst_comm* comm, cudaS
   stats.launches = fst_launch_count() - launches0;
   stats.expand_launches = level_launches;
   stats.emit_launches = (int64_t)sh.size();
+  stats.tile_path = tp.ok ? 1 : 0;
   for (size_t i = 0; i < sh.size(); ++i) {
     outs[i]->stats = stats;
     outs[i]->shard_total_states = total_states;

@@ -103,6 +103,7 @@ struct fst {
     fstc::BufferPtr buf;
     int32_t* d = nullptr;
     int32_t n = 0;
+    std::vector<int32_t> h;  // host copy (the sharded path picks each rank's tiles)
   };
   std::vector<TileRows> tile_rows;
   std::vector<int32_t> tile_hoff[2];  // host copy of the A-role view offsets ([0] out, [1] in by olabel)

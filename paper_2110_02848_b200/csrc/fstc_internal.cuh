@@ -65,7 +65,9 @@ struct CompDev {
   int64_t W;         // first word of this composition's pair space
   int64_t K;         // first block
   int64_t Q;         // first chunk
-  int32_t sh_world, sh_rank;  // sharded composition: block (row * bpr + j) is owned by rank (block % sh_world)
+  int32_t sh_world, sh_rank;  // sharded composition (world > 1): see owned() / blk_owner()
+  int32_t sh_rows;            // 1: rank q owns the rows [V_A*q/world, V_A*(q+1)/world); 0: block-interleaved
+  int32_t sh_r0, sh_r1;       // rows mode: this rank's rows
   // outputs (filled before the emit kernel; for a shard they are biased so that a global state id /
   // arc slot indexes the shard's own buffers)
   int64_t* row_ptr;
@@ -90,10 +92,38 @@ struct LevelCtrl {
 
 constexpr int kMaxLevelStats = 1 << 16;
 
-// Ownership of pair-space blocks in a sharded composition: the 1024-pair block j of row a
-// has linear id a * bpr + j and belongs to rank (id mod world) -- every row is spread over all ranks.
+// Ownership of pair-space blocks in a sharded composition.  Block-interleaved mode: the
+// 1024-pair block j of row a has linear id a * bpr + j and belongs to rank (id mod world) -- every row
+// is spread over all ranks (trellis-shaped compositions).  Rows mode (compositions on the tile path):
+// rank q owns the contiguous rows [V_A*q/world, V_A*(q+1)/world), so its tiles are its own.
+__device__ __host__ __forceinline__ int32_t sh_row0(const CompDev& C, int q) {
+  return (int32_t)(((int64_t)C.VA * q) / C.sh_world);
+}
+__device__ __forceinline__ int blk_owner(const CompDev& C, int64_t blk) {
+  if (C.sh_world <= 1) return 0;
+  if (!C.sh_rows) return (int)(blk % C.sh_world);
+  const int32_t row = (int32_t)(blk / C.bpr);
+  int q = (int)(((int64_t)row * C.sh_world) / (C.VA > 0 ? C.VA : 1));
+  while (q + 1 < C.sh_world && sh_row0(C, q + 1) <= row) ++q;
+  while (q > 0 && sh_row0(C, q) > row) --q;
+  return q;
+}
 __device__ __forceinline__ bool owned(const CompDev& C, int32_t row, int32_t col) {
-  return C.sh_world <= 1 || (((int64_t)row * C.bpr + (col >> 10)) % C.sh_world) == C.sh_rank;
+  if (C.sh_world <= 1) return true;
+  if (C.sh_rows) return row >= C.sh_r0 && row < C.sh_r1;
+  return (((int64_t)row * C.bpr + (col >> 10)) % C.sh_world) == C.sh_rank;
+}
+// Blocks of rank q in block-id order: the p-th is owner_block(C, q, p); owner_nblocks(C, q) of them.
+__device__ __host__ __forceinline__ int64_t owner_nblocks(const CompDev& C, int q) {
+  const int64_t nb = (int64_t)C.VA * C.bpr;
+  if (C.sh_world <= 1) return nb;
+  if (C.sh_rows) return (int64_t)(sh_row0(C, q + 1) - sh_row0(C, q)) * C.bpr;
+  return nb > q ? (nb - q + C.sh_world - 1) / C.sh_world : 0;
+}
+__device__ __host__ __forceinline__ int64_t owner_block(const CompDev& C, int q, int64_t p) {
+  if (C.sh_world <= 1) return p;
+  if (C.sh_rows) return (int64_t)sh_row0(C, q) * C.bpr + p;
+  return p * C.sh_world + q;
 }
 
 __device__ __forceinline__ int find_comp(const CompDev* __restrict__ comps, int ncomp, int64_t blk) {

@@ -61,6 +61,7 @@ struct TileArgs {
   int32_t self;         // one self slot per row (B view has eps items)
   int32_t bytemode;     // row x owns slots [8x, 8x + 8)
   int32_t kj;           // ELL columns held in registers (template instance: 8 or 16)
+  int32_t t0, t1;       // tiles [t0, t1) this launch processes (a shard: the tiles over its rows)
 };
 
 template <typename M>
@@ -210,10 +211,13 @@ __device__ __forceinline__ void tile_level_prologue(const Ctx& cx, int level) {
 struct TC {
   int64_t W, K, Q;
   int32_t wpr, VB, bpr, VA, cpr, CB;
+  int32_t r0, r1;  // rows this rank owns (all rows unless sharded; the tile path shards by row ranges)
+  __device__ __forceinline__ bool own(int32_t row) const { return row >= r0 && row < r1; }
 };
 __device__ __forceinline__ TC tc_of(const Ctx& cx) {
   const CompDev& C = cx.comps[0];
-  return TC{C.W, C.K, C.Q, C.wpr, C.VB, C.bpr, C.VA, C.cpr, C.CB};
+  const bool sh = C.sh_world > 1;
+  return TC{C.W, C.K, C.Q, C.wpr, C.VB, C.bpr, C.VA, C.cpr, C.CB, sh ? C.sh_r0 : 0, sh ? C.sh_r1 : C.VA};
 }
 
 // Items of column b = 32 w + lane (ELL columns 1..jn-1; column 0, the sentinel, when j0 == 0): the
@@ -265,14 +269,15 @@ __global__ void __launch_bounds__(kTThreads, 1) k_tile_pull(Ctx cx, TileArgs ta,
   const uint8_t* __restrict__ wmax = ta.sd.wmax;
   const int wpr = c.wpr, VB = c.VB;
   const uint32_t lastmask = (VB & 31) ? (1u << (VB & 31)) - 1u : ~0u;
-  auto unvisited = [&](int32_t row, int w) -> uint32_t {
+  auto unvisited = [&](int32_t row, int w) -> uint32_t {  // (0 for rows of other shards)
+    if (!c.own(row)) return 0u;
     const int64_t gw = c.W + (int64_t)row * wpr + w;
     const uint32_t v = __ldca(&vis[gw]);
     uint32_t u = kStage2 ? (__ldg(&Rb[gw]) & ~v) : ~v;
     return w == wpr - 1 ? (u & lastmask) : u;
   };
   unsigned nnew = 0;
-  for (int tile = blockIdx.x; tile < ta.ntiles; tile += gridDim.x) {
+  for (int tile = ta.t0 + blockIdx.x; tile < ta.t1; tile += gridDim.x) {
     tile_slots(t, ta, tile);
     const int nr = t.nr;
     const int32_t r0 = t.r0;
@@ -330,6 +335,7 @@ __global__ void __launch_bounds__(kTThreads, 1) k_tile_pull(Ctx cx, TileArgs ta,
     // chunk flags of the tile's rows: consumed ones cleared, chunks with new bits listed
     for (int i = threadIdx.x; i < nr * c.cpr; i += kTThreads) {
       const int x = i / c.cpr, j = i - x * c.cpr;
+      if (!c.own(r0 + x)) continue;
       const int64_t q = c.Q + (int64_t)(r0 + x) * c.cpr + j;
       if (flagc[q]) flagc[q] = 0u;
       if ((chit[x][j >> 5] >> (j & 31)) & 1u) {
@@ -363,7 +369,7 @@ __global__ void __launch_bounds__(kTThreads, 1) k_tile_count(Ctx cx, TileArgs ta
   const uint32_t* __restrict__ ell = ta.sd.ell;
   const uint8_t* __restrict__ wmax = ta.sd.wmax;
   uint32_t* warc = cx.warc;
-  for (int tile = blockIdx.x; tile < ta.ntiles; tile += gridDim.x) {
+  for (int tile = ta.t0 + blockIdx.x; tile < ta.t1; tile += gridDim.x) {
     tile_slots(t, ta, tile);
     const int nr = t.nr;
     const int32_t r0 = t.r0;
@@ -382,9 +388,10 @@ __global__ void __launch_bounds__(kTThreads, 1) k_tile_count(Ctx cx, TileArgs ta
       uint32_t sums[kTRows];
 #pragma unroll
       for (int x = 0; x < kTRows; ++x) sums[x] = 0u;
-      uint32_t sv = (w0 < w1 && lane < nr) ? __ldg(&V[c.W + (int64_t)(r0 + lane) * wpr + w0]) : 0u;
+      const bool ownl = lane < nr && c.own(r0 + lane);  // (other shards' rows count 0 here)
+      uint32_t sv = (w0 < w1 && ownl) ? __ldg(&V[c.W + (int64_t)(r0 + lane) * wpr + w0]) : 0u;
       for (int w = w0; w < w1; ++w) {
-        const uint32_t svn = (w + 1 < w1 && lane < nr) ? __ldg(&V[c.W + (int64_t)(r0 + lane) * wpr + w + 1]) : 0u;
+        const uint32_t svn = (w + 1 < w1 && ownl) ? __ldg(&V[c.W + (int64_t)(r0 + lane) * wpr + w + 1]) : 0u;
         uint32_t wc = 0u;  // lane x < nr: arcs of the states (row x, word w)
         if (__any_sync(0xffffffffu, sv != 0u)) {
           const int b = w * 32 + lane;
@@ -420,7 +427,7 @@ __global__ void __launch_bounds__(kTThreads, 1) k_tile_count(Ctx cx, TileArgs ta
             if (lane == x) wc = ws;
           }
         }
-        if (lane < nr) warc[c.W + (int64_t)(r0 + lane) * wpr + w] = wc;
+        if (ownl) warc[c.W + (int64_t)(r0 + lane) * wpr + w] = wc;
         sv = svn;
       }
 #pragma unroll
@@ -432,7 +439,7 @@ __global__ void __launch_bounds__(kTThreads, 1) k_tile_count(Ctx cx, TileArgs ta
     __syncthreads();
     for (int i = threadIdx.x; i < nr * bpr; i += kTThreads) {
       const int x = i / bpr, jb = i - x * bpr;
-      cx.kept[c.K + (int64_t)(r0 + x) * bpr + jb] = kacc[x * bpr + jb];
+      if (c.own(r0 + x)) cx.kept[c.K + (int64_t)(r0 + x) * bpr + jb] = kacc[x * bpr + jb];
     }
     __syncthreads();
   }
@@ -481,7 +488,7 @@ __global__ void __launch_bounds__(kEThreads, 1) k_tile_emit(Ctx cx, TileArgs ta,
   uint32_t* code = Vw + (size_t)vr_rows * wpr + ((size_t)vr_rows * wpr + 1) / 2 + (size_t)warp * kECap;
   const int64_t id_comp = tot[0], arc_comp = tot[1];
   const uint32_t* __restrict__ V = cx.V;
-  for (int tile = blockIdx.x; tile < ta.ntiles; tile += gridDim.x) {
+  for (int tile = ta.t0 + blockIdx.x; tile < ta.t1; tile += gridDim.x) {
     tile_slots(t, ta, tile);
     const int nr = t.nr, ns = t.ns;
     const int32_t r0 = t.r0;
@@ -531,7 +538,7 @@ __global__ void __launch_bounds__(kEThreads, 1) k_tile_emit(Ctx cx, TileArgs ta,
       uint32_t vw_l = 0u;
       int64_t base_l = 0;
       int32_t exp_l = 0;
-      if (lane < nr) {
+      if (lane < nr && c.own(r0 + lane)) {  // (rows of other shards are emitted there)
         const int64_t gw = c.W + (int64_t)(r0 + lane) * wpr + w;
         const int64_t blk = c.K + (int64_t)(r0 + lane) * bpr + (w >> 5);
         vw_l = Vw[(size_t)(ns + lane) * wpr + w];

@@ -74,6 +74,37 @@ def test_sharded_local_equals_unsharded(fst, name, make, world):
         pins.assert_canonical_equal(pins.canonicalize_any(got, B.num_states), oracle.canonical(A, B), name)
 
 
+TILE_CASES = [("c4-2000", lambda: fstgen.config_c4(V=2000, D=8)), ("c4-1500-D6", lambda: fstgen.config_c4(V=1500, D=6)),
+              ("c2-0", lambda: fstgen.config_c2(0)), ("c1-3", lambda: fstgen.config_c1(3))]
+
+
+@pytest.mark.parametrize("name,make", TILE_CASES, ids=[c[0] for c in TILE_CASES])
+@pytest.mark.parametrize("world", [1, 2, 3, 8])
+@pytest.mark.parametrize("mode", [2, 3])
+def test_sharded_tile_path(fst, name, make, world, mode):
+    """Compositions on the tile path are sharded by contiguous row ranges: bottom-up rounds over each
+    rank's tiles (claims replicated after every round), counts and emit of the own rows; ids stay in
+    key order, so the concatenated shards equal the unsharded arrays (mode 3: every level bottom-up)."""
+    A, B = make()
+    a, b = fst.fst_create(A), fst.fst_create(B)
+    fst.fst_set_tile_mode(mode)
+    try:
+        shards = fst.fst_compose_sharded_local(a, b, world)
+        st = shards[0].stats()
+        got = _merged(shards)
+        fst.fst_set_tile_mode(0)
+        ref = fst.fst_compose(a, b).to_host()
+    finally:
+        fst.fst_set_tile_mode(1)
+    assert st["tile_path"] == 1
+    if mode == 3 and ref["num_states"]:
+        assert st["pull_levels"] > 0
+    for k in ("row_ptr", "is_start", "is_accept", "pair_a", "pair_b"):
+        assert np.array_equal(np.asarray(got[k]), np.asarray(ref[k])), (name, world, k)
+    pins.assert_canonical_equal(pins.canonicalize_rows(got, B.num_states), pins.canonicalize_rows(ref, B.num_states),
+                                f"{name} world {world} mode {mode}")
+
+
 def test_sharded_trellis_spreads_levels(fst):
     """A trellis (lexicon o emissions): every BFS level is one A row; with block ownership every rank
     owns part of each level's row, so all shards hold states of (almost) every frame."""
