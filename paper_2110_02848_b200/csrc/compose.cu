@@ -2878,9 +2878,6 @@ fst_status compose_sharded_impl(fst* A, fst* B, int world, fst_comm* comm, cudaS
   C0.VB = B->V;
   C0.wpr = (B->V + 31) / 32;
   C0.bpr = (C0.wpr + kWordsPerBlock - 1) / kWordsPerBlock;
-  // one block per chunk: a chunk then has a single owner
-  C0.CB = 1;
-  C0.cpr = C0.bpr;
   C0.sh_world = world;
   // compositions that fit the tile path are sharded by contiguous row ranges (each rank's tiles are its
   // own; ids stay in key order); the others by interleaved blocks (trellis rows spread over all ranks)
@@ -2888,6 +2885,17 @@ fst_status compose_sharded_impl(fst* A, fst* B, int world, fst_comm* comm, cudaS
   st = tile_plan(A, B, (int64_t)A->V * B->V, false, s, &tp);
   if (st) return st;
   C0.sh_rows = tp.ok ? 1 : 0;
+  if (C0.sh_rows) {  // chunks as in the unsharded call, for the rows of one rank
+    const int64_t rows = std::max<int64_t>(1, C0.VA / world);
+    int64_t want = (8ll * g_grid + rows - 1) / rows;
+    int32_t cpr = (int32_t)std::max<int64_t>(1, std::min<int64_t>(want, C0.bpr));
+    cpr = std::max<int32_t>(cpr, (C0.bpr + kChunkMaxBlocks - 1) / kChunkMaxBlocks);
+    C0.CB = std::max<int32_t>(1, (C0.bpr + cpr - 1) / cpr);
+    C0.cpr = std::max<int32_t>(1, (C0.bpr + C0.CB - 1) / C0.CB);
+  } else {  // one block per chunk: a chunk then has a single owner
+    C0.CB = 1;
+    C0.cpr = C0.bpr;
+  }
   C0.smallA = A->max_olabel < 63;
   const int64_t nwords = (int64_t)C0.VA * C0.wpr, nblocks = (int64_t)C0.VA * C0.bpr,
                 nchunks = (int64_t)C0.VA * C0.cpr;
