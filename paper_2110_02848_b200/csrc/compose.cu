@@ -2139,6 +2139,17 @@ std::atomic<int>& tile_mode_ref() {
 
 constexpr int64_t kTileMinPairs = 1ll << 23;
 
+// FSTC_TILE_PUSH=1: the tile path's push levels run on k_tile_push instead of k_level (opt-in: measured
+// 13.0 ms vs 9.9 ms over the 34 push levels of configs[3] -- the per-tile RT builds cost more than the
+// word-parallel tests save at these frontier sizes).
+bool tile_push_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("FSTC_TILE_PUSH");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+
 // FSTC_TILE_PULL_K=k: a level runs bottom-up when frontier * k >= the stage's pair set (stage 1: the
 // pair space, stage 2: R).  A bottom-up level costs about one sweep whatever its frontier, a push level
 // grows with its frontier (default 256).
@@ -2256,7 +2267,7 @@ struct TilePlan {
   bool ok = false;
   TileArgs s1, s2, cnt, emit;
   int vr_rows = 0;
-  size_t smem_pull = 0, smem_count = 0, smem_emit = 0;
+  size_t smem_pull = 0, smem_count = 0, smem_emit = 0, smem_push = 0;
   int grid_pull1 = 0, grid_pull2 = 0, grid_count = 0, grid_emit = 0;
 };
 
@@ -2273,6 +2284,8 @@ fst_status tile_plan(fst* A, fst* B, int64_t pairs, bool want_prov, cudaStream_t
   const int wpr = (B->V + 31) / 32, bpr = (wpr + kWordsPerBlock - 1) / kWordsPerBlock;
   const int smem_cap = smem_optin() - 4096;  // static shared memory of the kernels stays below 4 KB
   const size_t smem_pull = (size_t)wpr * 256, smem_count = smem_pull + 8ull * kTRows * bpr;
+  const size_t smem_push = smem_pull + 4ull * kTRows * wpr;
+  if (smem_push > (size_t)(smem_optin() - 4096)) return FST_OK;
   if (smem_count > (size_t)smem_cap) return FST_OK;
   if ((bpr + 0) > 64) return FST_OK;  // the bottom-up rounds track <= 64 chunks per row
   const int wd_out = B->views[kOutByIlabel].max_deg + 1;
@@ -2306,11 +2319,14 @@ fst_status tile_plan(fst* A, fst* B, int64_t pairs, bool want_prov, cudaStream_t
   P->emit = TileArgs{side(0, 0), d, nt, self, 0, 8, 0, nt};
   P->vr_rows = vr_rows;
   P->smem_pull = smem_pull;
+  P->smem_push = smem_push;
   P->smem_count = smem_count;
   P->smem_emit = tile_emit_smem(vr_rows, wpr, wd_out);
   static bool attrs = false;
   if (!attrs) {
-    const void* fs[] = {(const void*)k_tile_pull<false, 8>, (const void*)k_tile_pull<false, 16>,
+    const void* fs[] = {(const void*)k_tile_push<false, 8>, (const void*)k_tile_push<false, 16>,
+                        (const void*)k_tile_push<true, 8>,  (const void*)k_tile_push<true, 16>,
+                        (const void*)k_tile_pull<false, 8>, (const void*)k_tile_pull<false, 16>,
                         (const void*)k_tile_pull<true, 8>,  (const void*)k_tile_pull<true, 16>,
                         (const void*)k_tile_count<false, 8>, (const void*)k_tile_count<false, 16>,
                         (const void*)k_tile_count<true, 8>,  (const void*)k_tile_count<true, 16>,
@@ -2336,6 +2352,13 @@ void launch_tile_pull(const TileArgs& ta, int grid, size_t smem, cudaStream_t s,
   if (ta.kj == 8) k_tile_pull<kStage2, 8><<<grid, kTThreads, smem, s>>>(cx, ta, level);
   else k_tile_pull<kStage2, 16><<<grid, kTThreads, smem, s>>>(cx, ta, level);
 }
+// push level in tile form: stage 1 walks the reversed moves (in-view tiles: TilePlan::s2), stage 2 the
+// forward moves (out-view tiles: TilePlan::s1)
+template <bool kStage2>
+void launch_tile_push(const TileArgs& ta, int grid, size_t smem, cudaStream_t s, const Ctx& cx, int level) {
+  if (ta.kj == 8) k_tile_push<kStage2, 8><<<grid, kTThreads, smem, s>>>(cx, ta, level);
+  else k_tile_push<kStage2, 16><<<grid, kTThreads, smem, s>>>(cx, ta, level);
+}
 void launch_tile_count(const TileArgs& ta, int grid, size_t smem, cudaStream_t s, const Ctx& cx) {
   if (ta.bytemode) {
     if (ta.kj == 8) k_tile_count<true, 8><<<grid, kTThreads, smem, s>>>(cx, ta);
@@ -2356,11 +2379,14 @@ void launch_tile_emit(const TileArgs& ta, int grid, size_t smem, cudaStream_t s,
 // One BFS stage with per-level direction choice: push levels are k_level; a level whose frontier is a
 // sizable share of the stage's pairs (frontier * k >= total) runs bottom-up on the tile kernels.
 template <bool kStage2>
-fst_status run_stage_tile(const Ctx& cx, const TileArgs& ta, int grid_pull, size_t smem_pull, int64_t total,
-                          cudaStream_t s, unsigned long long* hp, int64_t* level_launches, std::vector<int64_t>* sizes,
-                          int* npull) {
+fst_status run_stage_tile(const Ctx& cx, const TilePlan& tp, int64_t total, cudaStream_t s, unsigned long long* hp,
+                          int64_t* level_launches, std::vector<int64_t>* sizes, int* npull) {
   const int64_t K = tile_pull_k();
   const bool all_pull = tile_mode_ref().load() == 3;  // test mode: every level bottom-up
+  const TileArgs& ta = kStage2 ? tp.s2 : tp.s1;       // bottom-up rounds: in-view tiles for stage 2
+  const TileArgs& tb = kStage2 ? tp.s1 : tp.s2;       // push levels: the opposite direction
+  const int grid_pull = kStage2 ? tp.grid_pull2 : tp.grid_pull1, grid_push = kStage2 ? tp.grid_pull1 : tp.grid_pull2;
+  const bool tile_push = tile_push_enabled();
   int level = 0;
   for (;;) {
     FSTC_CUDA_TRY(cudaMemcpyAsync(hp, &cx.ctrl[level % 3], sizeof(LevelCtrl), cudaMemcpyDeviceToHost, s));
@@ -2371,9 +2397,14 @@ fst_status run_stage_tile(const Ctx& cx, const TileArgs& ta, int grid_pull, size
     const int64_t unvisited = total > visited ? total - visited : 0;
     (void)unvisited;
     if (all_pull || (int64_t)nf * K >= total) {
-      launch_tile_pull<kStage2>(ta, grid_pull, smem_pull, s, cx, level);
+      launch_tile_pull<kStage2>(ta, grid_pull, tp.smem_pull, s, cx, level);
       FSTC_LAUNCH_CHECK();
       ++*npull;
+    } else if (tile_push) {
+      launch_tile_push<kStage2>(tb, grid_push, tp.smem_push, s, cx, level);
+      FSTC_LAUNCH_CHECK();
+      k_push_finish<<<sm_count() * 8, 256, 0, s>>>(cx, level);
+      FSTC_LAUNCH_CHECK();
     } else {
       k_level<kStage2><<<g_grid, kThreads, kDynSmem, s>>>(cx, level);
       FSTC_LAUNCH_CHECK();
@@ -2555,8 +2586,7 @@ fst_status compose_impl(int32_t n, const fst_handle* a, const fst_handle* b, cud
     if (seed1[n] > 0) {
       k_seed<false><<<nblk(seed1[n], 256), 256, 0, s>>>(cx);
       FSTC_LAUNCH_CHECK();
-      st = tp.ok ? run_stage_tile<false>(cx, tp.s1, tp.grid_pull1, tp.smem_pull, pairs, s, hp, &level_launches,
-                                         &sizes1, &stats.pull_levels)
+      st = tp.ok ? run_stage_tile<false>(cx, tp, pairs, s, hp, &level_launches, &sizes1, &stats.pull_levels)
                  : run_stage<false>(cx, s, hp, &level_launches, &sizes1);
       if (st) return st;
     }
@@ -2578,8 +2608,7 @@ fst_status compose_impl(int32_t n, const fst_handle* a, const fst_handle* b, cud
         FSTC_CUDA_TRY(cudaMemcpyAsync(hp + 8, cx.misc + 1, 8, cudaMemcpyDeviceToHost, s));
         FSTC_CUDA_TRY(cudaStreamSynchronize(s));
         stats.num_coaccessible = (int64_t)hp[8];
-        st = run_stage_tile<true>(cx, tp.s2, tp.grid_pull2, tp.smem_pull, (int64_t)hp[8], s, hp, &level_launches,
-                                  &sizes2, &stats.pull_levels);
+        st = run_stage_tile<true>(cx, tp, (int64_t)hp[8], s, hp, &level_launches, &sizes2, &stats.pull_levels);
       } else {
         st = run_stage<true>(cx, s, hp, &level_launches, &sizes2);
       }

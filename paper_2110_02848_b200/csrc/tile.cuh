@@ -350,6 +350,160 @@ __global__ void __launch_bounds__(kTThreads, 1) k_tile_pull(Ctx cx, TileArgs ta,
   if (lane == 0 && nnew) atomicAdd(&ctrl_nxt->nnew, (unsigned long long)nnew);
 }
 
+// ------------------------------------------------------------------------------ push level (tile form)
+// A frontier-synchronous level (Alg. 1's rounds) over the tiles that hold frontier
+// pairs: for a frontier pair (a_x, b) the moves out of it are lm[li] & rowmask[x] over b's items, and
+// the claimable targets are the bits of RT_C = (stage 1: ~R | stage 2: R & ~V) of the slot rows; each
+// target is claimed by a global test-and-set and joins the next frontier (chunk flags / lists as in
+// k_level).  Stage 1 walks the reversed moves (tiles over A's in-view, B's in-item ELL), stage 2 the
+// forward moves (A's out-view, B's out-items).  Tiles without frontier pairs are skipped before any
+// staging, so sparse levels cost about one read of the frontier bitmap.
+template <bool kStage2, int kJ>
+__global__ void __launch_bounds__(kTThreads, 1) k_tile_push(Ctx cx, TileArgs ta, int level) {
+  using M = unsigned long long;
+  __shared__ TileSmem<M> t;
+  __shared__ int s_any;
+  extern __shared__ __align__(16) unsigned long long tdyn64[];
+  M* RT = tdyn64;
+  const TC c = tc_of(cx);
+  const int wpr = c.wpr, VB = c.VB;
+  uint32_t* FW = (uint32_t*)(tdyn64 + (size_t)wpr * 32);  // [kTRows][wpr] the tile's frontier words
+  tile_level_prologue(cx, level);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t* vis = kStage2 ? cx.V : cx.R;
+  const uint32_t* __restrict__ Rb = cx.R;
+  const int p = level & 1;
+  uint32_t* Fc = p ? cx.F1 : cx.F0;
+  uint32_t* Fn = p ? cx.F0 : cx.F1;
+  uint32_t* flagc = p ? cx.flag1 : cx.flag0;
+  uint32_t* flagn = p ? cx.flag0 : cx.flag1;
+  int32_t* listn = p ? cx.list0 : cx.list1;
+  LevelCtrl* ctrl_nxt = &cx.ctrl[(level + 1) % 3];
+  const CompDev& C = cx.comps[0];
+  const uint32_t* __restrict__ ell = ta.sd.ell;
+  const uint8_t* __restrict__ wmax = ta.sd.wmax;
+  const uint32_t lastmask = (VB & 31) ? (1u << (VB & 31)) - 1u : ~0u;
+  unsigned nnew = 0;
+  for (int tile = ta.t0 + blockIdx.x; tile < ta.t1; tile += gridDim.x) {
+    // the rows' frontier words (consumed) -> FW; skip tiles without frontier pairs
+    const int32_t r0 = __ldg(&ta.trow[tile]), nr = __ldg(&ta.trow[tile + 1]) - r0;
+    if (threadIdx.x == 0) s_any = 0;
+    __syncthreads();
+    bool any = false;
+    for (int i = threadIdx.x; i < nr * wpr; i += kTThreads) {
+      const int x = i / wpr, w = i - x * wpr;
+      uint32_t f = 0u;
+      if (c.own(r0 + x)) {
+        const int64_t gw = c.W + (int64_t)(r0 + x) * wpr + w;
+        f = Fc[gw];
+        if (f) Fc[gw] = 0u;
+      }
+      FW[x * wpr + w] = f;
+      any |= f != 0u;
+    }
+    for (int i = threadIdx.x; i < nr * c.cpr; i += kTThreads) {  // consumed chunk flags
+      const int x = i / c.cpr;
+      if (!c.own(r0 + x)) continue;
+      const int64_t q = c.Q + (int64_t)(r0 + x) * c.cpr + (i - x * c.cpr);
+      if (flagc[q]) flagc[q] = 0u;
+    }
+    if (any) s_any = 1;
+    __syncthreads();
+    if (!s_any) continue;
+    tile_slots(t, ta, tile);
+    // RT_C: claimable bits of the slot rows
+    {
+      const uint32_t* rp0 = lane < t.ns ? vis + c.W + (int64_t)t.srow[lane] * wpr : nullptr;
+      const uint32_t* rq0 = lane < t.ns ? Rb + c.W + (int64_t)t.srow[lane] * wpr : nullptr;
+      const uint32_t* rp1 = lane + 32 < t.ns ? vis + c.W + (int64_t)t.srow[lane + 32] * wpr : nullptr;
+      const uint32_t* rq1 = lane + 32 < t.ns ? Rb + c.W + (int64_t)t.srow[lane + 32] * wpr : nullptr;
+      for (int w = warp; w < wpr; w += kTWarps) {
+        const uint32_t mk = w == wpr - 1 ? lastmask : ~0u;
+        uint32_t x0 = 0u, x1 = 0u;
+        if (rp0) x0 = (kStage2 ? (__ldg(rq0 + w) & ~__ldca(rp0 + w)) : ~__ldca(rp0 + w)) & mk;
+        if (rp1) x1 = (kStage2 ? (__ldg(rq1 + w) & ~__ldca(rp1 + w)) : ~__ldca(rp1 + w)) & mk;
+        const uint32_t lo = transpose32(x0, lane), hi = transpose32(x1, lane);
+        RT[w * 32 + lane] = ((unsigned long long)hi << 32) | lo;
+      }
+    }
+    __syncthreads();
+    const int j0 = t.lm[kLiSent] ? 0 : 1;
+    const M* lm = t.lm;
+    for (int w = warp; w < wpr; w += kTWarps) {
+      const uint32_t fl = lane < nr ? FW[lane * wpr + w] : 0u;
+      if (!__any_sync(0xffffffffu, fl != 0u)) continue;
+      const int b = w * 32 + lane;
+      const int jn = wmax[w];
+      // rows x whose pair (x, b) is in the frontier, as a per-lane bit set (usually 0 or 1 rows)
+      unsigned rows = 0u;
+#pragma unroll
+      for (int x = 0; x < kTRows; ++x) {
+        const uint32_t fx = __shfl_sync(0xffffffffu, fl, x);
+        if (x < nr && ((fx >> lane) & 1u) && b < VB) rows |= 1u << x;
+      }
+#pragma unroll 1
+      while (rows) {  // (not unrolled: one copy of the item loop)
+        const int x = __ffs(rows) - 1;
+        rows &= rows - 1u;
+        const M rmx = t.rmask[x];
+        for_items<kJ>(ell, ta.sd.wd, w, lane, j0, jn, [&](uint32_t it) {
+          M h = lm[it >> 24] & rmx;
+          if (!h) return;
+          const uint32_t o = it & 0xFFFFFFu;
+          h &= RT[o];
+          while (h) {  // fire-and-forget claims (RT_C excludes every pair of an earlier level)
+            const int s = __ffsll((long long)h) - 1;
+            h &= h - 1ull;
+            const int32_t row = t.srow[s];
+            const int64_t gw = c.W + (int64_t)row * wpr + (o >> 5);
+            const uint32_t bit = 1u << (o & 31);
+            if (!owned(C, row, (int32_t)o)) {  // sharded: the owner claims it after the exchange
+              atomicOr(&cx.OUT[gw], bit);
+              continue;
+            }
+            atomicOr(&vis[gw], bit);
+            atomicOr(&Fn[gw], bit);
+          }
+        });
+      }
+    }
+    __syncthreads();
+  }
+  (void)nnew;
+  (void)flagn;
+  (void)listn;
+  (void)ctrl_nxt;
+}
+
+// After a tile push level: the next frontier's size and its chunk list (one warp per chunk; the
+// push kernel's claims are plain reductions, so the exact count comes from the bitmap).
+__global__ void k_push_finish(Ctx cx, int level) {
+  const int p = level & 1;
+  const uint32_t* Fn = p ? cx.F0 : cx.F1;
+  uint32_t* flagn = p ? cx.flag0 : cx.flag1;
+  int32_t* listn = p ? cx.list0 : cx.list1;
+  LevelCtrl* ctrl_nxt = &cx.ctrl[(level + 1) % 3];
+  const int lane = threadIdx.x & 31;
+  const TC c = tc_of(cx);
+  const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+  unsigned nnew = 0;
+  for (int64_t q = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); q < cx.nchunks; q += nw) {
+    const int32_t row = (int32_t)(q / c.cpr), j = (int32_t)(q - (int64_t)row * c.cpr);
+    const int w0 = j * c.CB * 32, w1 = min(w0 + c.CB * 32, c.wpr);
+    const int64_t rw = c.W + (int64_t)row * c.wpr;
+    unsigned cnt = 0;
+    for (int w = w0 + lane; w < w1; w += 32) cnt += __popc(Fn[rw + w]);
+    if (__any_sync(0xffffffffu, cnt != 0u) && lane == 0) {
+      flagn[q] = 1u;
+      const unsigned long long pos = atomicAdd(&ctrl_nxt->count, 1ull);
+      listn[pos] = (int32_t)q;
+    }
+    nnew += cnt;
+  }
+  nnew = warp_sum(nnew);
+  if (lane == 0 && nnew) atomicAdd(&ctrl_nxt->nnew, (unsigned long long)nnew);
+}
+
 // ------------------------------------------------------------------------------ pass 1: counts
 // kept[block] = number of moves out of the block's states of C (their out-degrees), OVERWRITTEN
 // for every block of the composition, and warc[word] = the same per word (the emit's offsets).
