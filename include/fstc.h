@@ -267,7 +267,8 @@ void fst_set_profiling(int32_t on);
 
 /* Tile path selection for single compositions: 0 = never, 1 = automatic (pair space
  * >= 2^23 pairs and the inputs fit: degrees <= 31, labels <= 252, V_B small enough for the staged
- * tables), 2 = whenever the inputs fit, 3 = as 2 with every BFS level bottom-up (tests).  The
+ * tables), 2 = whenever the inputs fit, 3 = as 2 with every BFS level bottom-up, 4 = as 2 with the
+ * push levels on the tile-form push kernel (tests / A-B; FSTC_TILE_PUSH=1 does the same).  The
  * environment variable FSTC_TILE sets the initial mode.  Both paths return the same graph (state
  * numbering by ascending key; arc order within a state may differ). */
 void fst_set_tile_mode(int32_t mode);

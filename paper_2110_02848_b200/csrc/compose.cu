@@ -2132,7 +2132,7 @@ std::atomic<int>& tile_mode_ref() {
   static std::atomic<int> m{[] {
     const char* e = getenv("FSTC_TILE");
     const int v = e ? atoi(e) : 1;
-    return (v >= 0 && v <= 3) ? v : 1;
+    return (v >= 0 && v <= 4) ? v : 1;
   }()};
   return m;
 }
@@ -2386,7 +2386,7 @@ fst_status run_stage_tile(const Ctx& cx, const TilePlan& tp, int64_t total, cuda
   const TileArgs& ta = kStage2 ? tp.s2 : tp.s1;       // bottom-up rounds: in-view tiles for stage 2
   const TileArgs& tb = kStage2 ? tp.s1 : tp.s2;       // push levels: the opposite direction
   const int grid_pull = kStage2 ? tp.grid_pull2 : tp.grid_pull1, grid_push = kStage2 ? tp.grid_pull1 : tp.grid_pull2;
-  const bool tile_push = tile_push_enabled();
+  const bool tile_push = tile_push_enabled() || tile_mode_ref().load() == 4;
   int level = 0;
   for (;;) {
     FSTC_CUDA_TRY(cudaMemcpyAsync(hp, &cx.ctrl[level % 3], sizeof(LevelCtrl), cudaMemcpyDeviceToHost, s));
@@ -2426,7 +2426,7 @@ fst_status run_stage_tile(const Ctx& cx, const TilePlan& tp, int64_t total, cuda
 
 }  // namespace
 
-void tile_mode_set(int mode) { tile_mode_ref().store((mode >= 0 && mode <= 3) ? mode : 1); }
+void tile_mode_set(int mode) { tile_mode_ref().store((mode >= 0 && mode <= 4) ? mode : 1); }
 
 std::vector<int64_t>& level_sizes_slot(fst* h, int stage);
 

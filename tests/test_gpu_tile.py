@@ -129,6 +129,20 @@ def test_tile_all_levels_bottom_up(fst, V, D):
     check_rounds(c, st, A, B)
 
 
+@pytest.mark.parametrize("make", [lambda: fstgen.config_c4(V=1500, D=8), lambda: fstgen.config_c2(0),
+                                  lambda: fstgen.config_c2(3), lambda: fstgen.config_c1(7)])
+def test_tile_push_levels(fst, make):
+    """Mode 4: the push levels run on k_tile_push (claims as reductions, counts from the bitmap):
+    exact graph and, for the push levels, the exact BFS level sizes."""
+    A, B = make()
+    fst.fst_set_tile_mode(4)
+    try:
+        c, st, got = check_tile(fst, A, B, "tile push")
+    finally:
+        fst.fst_set_tile_mode(2)
+    check_rounds(c, st, A, B)
+
+
 @pytest.mark.parametrize("seed", [0, 3, 8])
 def test_tile_all_levels_bottom_up_eps(fst, seed):
     A, B = fstgen.config_c2(seed)
