@@ -2151,13 +2151,14 @@ bool tile_push_enabled() {
 }
 
 // FSTC_TILE_PULL_K=k: a level runs bottom-up when frontier * k >= the stage's pair set (stage 1: the
-// pair space, stage 2: R).  A bottom-up level costs about one sweep whatever its frontier, a push level
-// grows with its frontier (default 256).
+// pair space, stage 2: R).  A bottom-up round costs about one sweep whatever its frontier, a push level
+// grows with its frontier.  Default 1024 (configs[3]: K = 64 / 256 / 1024 / 4096 -> 45.2 / 42.1 /
+// 41.1 / 41.4 ms per composition).
 int64_t tile_pull_k() {
   static const int64_t v = [] {
     const char* e = getenv("FSTC_TILE_PULL_K");
-    const long long k = e ? atoll(e) : 256;
-    return (int64_t)(k > 0 ? k : 256);
+    const long long k = e ? atoll(e) : 1024;
+    return (int64_t)(k > 0 ? k : 1024);
   }();
   return v;
 }
