@@ -2085,7 +2085,15 @@ bool graph_loop_enabled() {
 // Runs one BFS stage (level loop); fills the per-level frontier sizes.  The first levels run as
 // host-driven speculative batches; a BFS still going after kHostLevels levels continues in one
 // graph launch (run_levels_graph).
-constexpr int kHostLevels = 64;
+// FSTC_HOST_LEVELS=n: levels run host-driven before the graph loop takes over (default 64).
+int host_levels() {
+  static const int v = [] {
+    const char* e = getenv("FSTC_HOST_LEVELS");
+    const int k = e ? atoi(e) : 64;
+    return k >= 0 ? k : 64;
+  }();
+  return v;
+}
 template <bool kStage2>
 fst_status run_stage(const Ctx& cx, cudaStream_t s, unsigned long long* h_pinned, int64_t* level_launches,
                      std::vector<int64_t>* sizes) {
@@ -2101,7 +2109,7 @@ fst_status run_stage(const Ctx& cx, cudaStream_t s, unsigned long long* h_pinned
                                   cudaMemcpyDeviceToHost, s));
     FSTC_CUDA_TRY(cudaStreamSynchronize(s));
     if (*h_pinned == 0) break;
-    if (level >= kHostLevels && graph_loop_enabled()) {  // deep BFS: the rest in one graph launch
+    if (level >= host_levels() && graph_loop_enabled()) {  // deep BFS: the rest in one graph launch
       fst_status st = run_levels_graph<kStage2>(cx, s, &level, level_launches);
       if (st) return st;
       break;
