@@ -235,7 +235,7 @@ def cpu_baseline_pool(budget_utts: int = 32):
     As = As[:budget_utts]
     cores = len(os.sched_getaffinity(0))
     t0 = time.perf_counter()
-    with mp.get_context("fork").Pool(cores) as pool:
+    with mp.get_context("spawn").Pool(cores) as pool:
         res = pool.map(_oracle_arcs, [(A, B) for A in As])
     wall = time.perf_counter() - t0
     arcs = sum(r[0] for r in res)

@@ -121,7 +121,7 @@ def test_c5_batch_digests(fst):
     hb = fst.fst_create(B)
     cs = fst.fst_compose_batch([fst.fst_create(A) for A in As], [hb] * len(As))
     got = [digest.digest_device(c.device_tensors(), B.num_states) for c in cs]
-    with mp.get_context("fork").Pool(min(len(As), len(os.sched_getaffinity(0)))) as pool:
+    with mp.get_context("spawn").Pool(min(len(As), len(os.sched_getaffinity(0)))) as pool:
         exp = pool.map(_oracle_digest_pair, [(A, B) for A in As])
     assert got == exp
     assert sum(e["num_arcs"] for e in exp) > 5e8
