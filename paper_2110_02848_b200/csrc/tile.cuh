@@ -91,13 +91,13 @@ __device__ __forceinline__ uint32_t transpose32(uint32_t x, int lane) {
   return x;
 }
 
-// Slots and label masks of tile `tile` (all threads; ends with a barrier).
+// Slots and label masks of tile `tile` (all threads; two barriers).  Warp 0 lays out the rows' slot
+// ranges; then one thread per slot loads its arc (one round of independent loads, not a chain).
 template <typename M>
 __device__ void tile_slots(TileSmem<M>& t, const TileArgs& ta, int tile) {
   constexpr int kS = 8 * sizeof(M);
+  __shared__ int32_t s_e0[kTRows], s_s0[kTRows], s_d[kTRows];
   for (int i = threadIdx.x; i < kTLab; i += blockDim.x) t.lm[i] = M(0);
-  if (threadIdx.x == 0) t.selfm = M(0);
-  __syncthreads();
   if (threadIdx.x < 32) {
     const int lane = threadIdx.x;
     const int32_t r0 = __ldg(&ta.trow[tile]), r1 = __ldg(&ta.trow[tile + 1]);
@@ -112,38 +112,58 @@ __device__ void tile_slots(TileSmem<M>& t, const TileArgs& ta, int tile) {
     if (ta.bytemode) {
       s0 = 8 * lane;
       ns = 8 * nr;
-      for (int s = lane; s < ns; s += 32) t.srow[s] = r0;  // unused slots: any valid row (never in lm)
-      __syncwarp();
     } else {
       const int inc = warp_incl_scan(n);
       s0 = inc - n;
       ns = __shfl_sync(0xffffffffu, inc, 31);
     }
+    M self = M(0);
     if (lane < nr) {
       t.rmask[lane] = n >= kS ? ~M(0) : (((M(1) << n) - M(1)) << s0);
-      int s = s0;
+      s_e0[lane] = e0;
+      s_s0[lane] = s0;
+      s_d[lane] = d;
       if (ta.self) {
-        t.srow[s] = r0 + lane;
-        t.scarry[s] = FST_EPS;
-        t.sw[s] = 0.f;
-        atomicOr(&t.lm[kLiEps], M(1) << s);  // M3: B eps item, A stays
-        atomicOr(&t.selfm, M(1) << s);
-        ++s;
-      }
-      for (int k = 0; k < d; ++k, ++s) {
-        const int32_t e = e0 + k;
-        const int32_t l = __ldg(&ta.sd.key[e]);
-        t.srow[s] = __ldg(&ta.sd.other[e]);
-        t.scarry[s] = __ldg(&ta.sd.carry[e]);
-        t.sw[s] = __ldg(&ta.sd.w[e]);
-        atomicOr(&t.lm[l + 2], M(1) << s);                       // M1 (eps:eps included: l = -1 -> 1)
-        if (l == FST_EPS) atomicOr(&t.lm[kLiSent], M(1) << s);  // M2: A eps arc, B stays (sentinel)
+        t.srow[s0] = r0 + lane;
+        t.scarry[s0] = FST_EPS;
+        t.sw[s0] = 0.f;
+        self = M(1) << s0;
       }
     }
+    // OR of the self-slot bits over the rows (warp reduction)
+    unsigned long long sm64 = (unsigned long long)self;
+#pragma unroll
+    for (int k = 16; k > 0; k >>= 1) sm64 |= __shfl_xor_sync(0xffffffffu, sm64, k);
     if (lane == 0) {
       t.r0 = r0;
       t.nr = nr;
       t.ns = ns;
+      t.selfm = (M)sm64;
+    }
+  }
+  __syncthreads();
+  const int nr = t.nr;
+  // label-mask bits via 32-bit shared atomics (a 64-bit shared atomicOr is a CAS loop)
+  auto lm_or = [&](int li, int s) { atomicOr((uint32_t*)&t.lm[li] + (s >> 5), 1u << (s & 31)); };
+  if (ta.self && threadIdx.x < 32 && threadIdx.x < nr) lm_or(kLiEps, s_s0[threadIdx.x]);  // M3: B eps item, A stays
+  // one thread per (row, arc): slot s0_x + self + k
+  for (int i = threadIdx.x; i < nr * kS; i += blockDim.x) {
+    const int x = i / kS, k = i - x * kS;
+    if (k >= s_d[x]) continue;
+    const int32_t e = s_e0[x] + k;
+    const int s = s_s0[x] + ta.self + k;
+    const int32_t l = __ldg(&ta.sd.key[e]);
+    t.srow[s] = __ldg(&ta.sd.other[e]);
+    t.scarry[s] = __ldg(&ta.sd.carry[e]);
+    t.sw[s] = __ldg(&ta.sd.w[e]);
+    lm_or(l + 2, s);                     // M1 (eps:eps included: l = -1 -> 1)
+    if (l == FST_EPS) lm_or(kLiSent, s);  // M2: A eps arc, B stays (sentinel)
+  }
+  if (ta.bytemode) {  // unused slots of byte mode: any valid row (they are in no label mask)
+    for (int s = threadIdx.x; s < t.ns; s += blockDim.x) {
+      const int x = s >> 3, k = (s & 7) - ta.self;
+      if ((s & 7) >= s_d[x] + ta.self) t.srow[s] = t.r0;
+      (void)k;
     }
   }
   __syncthreads();
@@ -302,33 +322,57 @@ __global__ void __launch_bounds__(kTThreads, 1) k_tile_pull(Ctx cx, TileArgs ta,
 #pragma unroll
       for (int x = 0; x < kTRows; ++x) rm[x] = x < nr ? t.rmask[x] : M(0);
       const M* lm = t.lm;
-      uint32_t u = (warp < wpr && lane < nr) ? unvisited(r0 + lane, warp) : 0u;
-      for (int w = warp; w < wpr; w += kTWarps) {
-        const int wn = w + kTWarps;
-        const uint32_t un = (wn < wpr && lane < nr) ? unvisited(r0 + lane, wn) : 0u;  // next word, in flight
-        if (__any_sync(0xffffffffu, u != 0u)) {
-          const int b = w * 32 + lane;
-          M acc = M(0);
-          if (b < VB)
-            for_items<kJ>(ell, ta.sd.wd, w, lane, j0, wmax[w], [&](uint32_t x) { acc |= lm[x >> 24] & RT[x & 0xFFFFFFu]; });
-          uint32_t mine = 0u;
+      // two words per warp iteration: both words' item loads are in flight together
+      auto claim = [&](int w, uint32_t u, M acc) {
+        uint32_t mine = 0u;
 #pragma unroll
-          for (int x = 0; x < kTRows; ++x) {
-            if (x >= nr) break;
-            const uint32_t ux = __shfl_sync(0xffffffffu, u, x);
-            const uint32_t nb = __ballot_sync(0xffffffffu, (acc & rm[x]) != M(0)) & ux;
-            if (lane == x) mine = nb;
-          }
-          if (mine) {  // lane x: claim the new pairs of (row x, w) in place
-            const int64_t gw = c.W + (int64_t)(r0 + lane) * wpr + w;
-            vis[gw] = __ldca(&vis[gw]) | mine;  // only this tile writes its rows
-            Fn[gw] = mine;
-            nnew += __popc(mine);
-            const int qj = (w >> 5) / c.CB;
-            atomicOr(&chit[lane][qj >> 5], 1u << (qj & 31));
-          }
+        for (int x = 0; x < kTRows; ++x) {
+          if (x >= nr) break;
+          const uint32_t ux = __shfl_sync(0xffffffffu, u, x);
+          const uint32_t nb = __ballot_sync(0xffffffffu, (acc & rm[x]) != M(0)) & ux;
+          if (lane == x) mine = nb;
         }
-        u = un;
+        if (mine) {  // lane x: claim the new pairs of (row x, w) in place
+          const int64_t gw = c.W + (int64_t)(r0 + lane) * wpr + w;
+          vis[gw] = __ldca(&vis[gw]) | mine;  // only this tile writes its rows
+          Fn[gw] = mine;
+          nnew += __popc(mine);
+          const int qj = (w >> 5) / c.CB;
+          atomicOr(&chit[lane][qj >> 5], 1u << (qj & 31));
+        }
+      };
+      const int wd = ta.sd.wd;
+      for (int w = warp; w < wpr; w += 2 * kTWarps) {
+        const int w2 = w + kTWarps;
+        const uint32_t u1 = lane < nr ? unvisited(r0 + lane, w) : 0u;
+        const uint32_t u2 = (w2 < wpr && lane < nr) ? unvisited(r0 + lane, w2) : 0u;
+        const bool a1 = __any_sync(0xffffffffu, u1 != 0u), a2 = __any_sync(0xffffffffu, u2 != 0u);
+        if (!a1 && !a2) continue;
+        const int b1 = w * 32 + lane, b2 = w2 * 32 + lane;
+        const bool v1 = a1 && b1 < VB, v2 = a2 && b2 < VB;
+        const int jn1 = v1 ? wmax[w] : 0, jn2 = v2 ? wmax[w2] : 0;
+        const uint32_t* p1 = ell + (size_t)w * wd * 32 + lane;
+        const uint32_t* p2 = ell + (size_t)w2 * wd * 32 + lane;
+        uint32_t i1[kJ], i2[kJ];
+#pragma unroll
+        for (int k = 0; k < kJ; ++k) {
+          i1[k] = (k + 1 < jn1) ? __ldg(p1 + (k + 1) * 32) : (kLiPad << 24);
+          i2[k] = (k + 1 < jn2) ? __ldg(p2 + (k + 1) * 32) : (kLiPad << 24);
+        }
+        M acc1 = M(0), acc2 = M(0);
+        if (j0 == 0) {
+          if (v1) { const uint32_t x = __ldg(p1); acc1 |= lm[x >> 24] & RT[x & 0xFFFFFFu]; }
+          if (v2) { const uint32_t x = __ldg(p2); acc2 |= lm[x >> 24] & RT[x & 0xFFFFFFu]; }
+        }
+#pragma unroll
+        for (int k = 0; k < kJ; ++k) {
+          acc1 |= lm[i1[k] >> 24] & RT[i1[k] & 0xFFFFFFu];
+          acc2 |= lm[i2[k] >> 24] & RT[i2[k] & 0xFFFFFFu];
+        }
+        for (int j = kJ + 1; j < jn1; ++j) { const uint32_t x = __ldg(p1 + j * 32); acc1 |= lm[x >> 24] & RT[x & 0xFFFFFFu]; }
+        for (int j = kJ + 1; j < jn2; ++j) { const uint32_t x = __ldg(p2 + j * 32); acc2 |= lm[x >> 24] & RT[x & 0xFFFFFFu]; }
+        if (a1) claim(w, u1, acc1);
+        if (a2) claim(w2, u2, acc2);
       }
     }
     __syncthreads();
