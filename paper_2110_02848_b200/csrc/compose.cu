@@ -2147,6 +2147,15 @@ std::atomic<int>& tile_mode_ref() {
 
 constexpr int64_t kTileMinPairs = 1ll << 23;
 
+// FSTC_SPARSE_PUSH=0: the tile path's push levels run on k_level instead of k_sparse_push (A/B).
+bool sparse_push_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("FSTC_SPARSE_PUSH");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 // FSTC_TILE_PUSH=1: the tile path's push levels run on k_tile_push instead of k_level (opt-in: measured
 // 13.0 ms vs 9.9 ms over the 34 push levels of configs[3] -- the per-tile RT builds cost more than the
 // word-parallel tests save at these frontier sizes).
@@ -2277,6 +2286,7 @@ struct TilePlan {
   TileArgs s1, s2, cnt, emit;
   int vr_rows = 0;
   size_t smem_pull = 0, smem_count = 0, smem_emit = 0, smem_push = 0;
+  int max_li = 255;  // largest label index (label + 2) of the matched tapes
   int grid_pull1 = 0, grid_pull2 = 0, grid_count = 0, grid_emit = 0;
 };
 
@@ -2327,6 +2337,7 @@ fst_status tile_plan(fst* A, fst* B, int64_t pairs, bool want_prov, cudaStream_t
   if (st) return st;
   P->emit = TileArgs{side(0, 0), d, nt, self, 0, 8, 0, nt};
   P->vr_rows = vr_rows;
+  P->max_li = std::max(A->max_olabel, B->max_ilabel) + 2;
   P->smem_pull = smem_pull;
   P->smem_push = smem_push;
   P->smem_count = smem_count;
@@ -2396,6 +2407,7 @@ fst_status run_stage_tile(const Ctx& cx, const TilePlan& tp, int64_t total, cuda
   const TileArgs& tb = kStage2 ? tp.s1 : tp.s2;       // push levels: the opposite direction
   const int grid_pull = kStage2 ? tp.grid_pull2 : tp.grid_pull1, grid_push = kStage2 ? tp.grid_pull1 : tp.grid_pull2;
   const bool tile_push = tile_push_enabled() || tile_mode_ref().load() == 4;
+  const bool sparse_push_ok = sparse_push_enabled() && tp.max_li < kSPLab;
   int level = 0;
   for (;;) {
     FSTC_CUDA_TRY(cudaMemcpyAsync(hp, &cx.ctrl[level % 3], sizeof(LevelCtrl), cudaMemcpyDeviceToHost, s));
@@ -2411,6 +2423,11 @@ fst_status run_stage_tile(const Ctx& cx, const TilePlan& tp, int64_t total, cuda
       ++*npull;
     } else if (tile_push) {
       launch_tile_push<kStage2>(tb, grid_push, tp.smem_push, s, cx, level);
+      FSTC_LAUNCH_CHECK();
+      k_push_finish<<<sm_count() * 8, 256, 0, s>>>(cx, level);
+      FSTC_LAUNCH_CHECK();
+    } else if (sparse_push_ok) {
+      k_sparse_push<kStage2><<<sm_count() * 8, 256, 0, s>>>(cx, tb, level);
       FSTC_LAUNCH_CHECK();
       k_push_finish<<<sm_count() * 8, 256, 0, s>>>(cx, level);
       FSTC_LAUNCH_CHECK();

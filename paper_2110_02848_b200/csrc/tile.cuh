@@ -519,6 +519,98 @@ __global__ void __launch_bounds__(kTThreads, 1) k_tile_push(Ctx cx, TileArgs ta,
   (void)ctrl_nxt;
 }
 
+// ------------------------------------------------------------------------------ sparse push level
+// A push level for small frontiers (the levels before and after the bottom-up rounds): one warp per
+// active chunk (row a, <= 1024 words) from the level's list.  The warp stages the row's A arcs of the
+// level's direction (stage 1: in-arcs = reversed moves, stage 2: out-arcs) as label masks over <= 64
+// slots; each lane takes frontier words of the chunk and, per frontier pair (a, b), walks b's items in
+// B's word-tiled ELL: a target (row of slot s, b') is claimed when its vis bit is clear -- a plain
+// load, then fire-and-forget reductions on vis and the next frontier (every pair of an earlier level
+// has its bit set, so the next frontier gets exactly this level's new pairs; duplicates are ORs).
+// k_push_finish then counts the next frontier and lists its chunks.
+constexpr int kSPLab = 64;  // label-mask entries staged per warp (label index < 64; else the tile rounds' k_level)
+template <bool kStage2>
+__global__ void __launch_bounds__(256) k_sparse_push(Ctx cx, TileArgs ta, int level) {
+  __shared__ unsigned long long lmw[8][kSPLab];
+  __shared__ int32_t sroww[8][64];
+  tile_level_prologue(cx, level);
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int p = level & 1;
+  uint32_t* Fc = p ? cx.F1 : cx.F0;
+  uint32_t* Fn = p ? cx.F0 : cx.F1;
+  uint32_t* flagc = p ? cx.flag1 : cx.flag0;
+  const int32_t* listc = p ? cx.list1 : cx.list0;
+  uint32_t* vis = kStage2 ? cx.V : cx.R;
+  const uint32_t* __restrict__ Rb = cx.R;
+  const CompDev& C = cx.comps[0];
+  const TC c = tc_of(cx);
+  const int wpr = c.wpr, VB = c.VB, wd = ta.sd.wd;
+  const unsigned long long nlist = *((volatile unsigned long long*)&cx.ctrl[level % 3].count);
+  unsigned long long* lm = lmw[wib];
+  int32_t* srow = sroww[wib];
+  const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t e = (int64_t)blockIdx.x * (blockDim.x >> 5) + wib; e < (int64_t)nlist; e += nwarps) {
+    const int64_t q = listc[e];
+    const int32_t row = (int32_t)((q - c.Q) / c.cpr), jc = (int32_t)(q - c.Q - (int64_t)row * c.cpr);
+    if (lane == 0) flagc[q] = 0u;
+    // the row's slots: self slot (when B has eps items) then its arcs
+    const int32_t e0 = __ldg(&ta.sd.off[row]), d = __ldg(&ta.sd.off[row + 1]) - e0;
+    for (int i = lane; i < kSPLab; i += 32) lm[i] = 0ull;
+    __syncwarp();
+    const int self = ta.self;
+    if (self && lane == 0) {
+      srow[0] = row;
+      atomicOr((uint32_t*)&lm[kLiEps], 1u);  // M3
+    }
+    for (int k = lane; k < d; k += 32) {
+      const int s = self + k;
+      const int32_t l = __ldg(&ta.sd.key[e0 + k]);
+      srow[s] = __ldg(&ta.sd.other[e0 + k]);
+      atomicOr((uint32_t*)&lm[l + 2] + (s >> 5), 1u << (s & 31));
+      if (l == FST_EPS) atomicOr((uint32_t*)&lm[kLiSent] + (s >> 5), 1u << (s & 31));
+    }
+    __syncwarp();
+    const bool sent = lm[kLiSent] != 0ull;
+    const int w0 = jc * c.CB * 32, w1 = min(w0 + c.CB * 32, wpr);
+    const int64_t rw = c.W + (int64_t)row * wpr;
+    for (int w = w0 + lane; w < w1; w += 32) {
+      uint32_t f = Fc[rw + w];
+      if (!f) continue;
+      Fc[rw + w] = 0u;
+      const int jn = ta.sd.wmax[w];
+      const uint32_t* pb = ta.sd.ell + (size_t)w * wd * 32;
+      while (f) {
+        const int bb = __ffs(f) - 1;
+        f &= f - 1u;
+        if (w * 32 + bb >= VB) continue;
+        for (int j = sent ? 0 : 1; j < jn; ++j) {
+          const uint32_t it = __ldg(pb + j * 32 + bb);
+          const uint32_t li = it >> 24;
+          if (li >= (uint32_t)kSPLab) continue;
+          unsigned long long m = lm[li];
+          const uint32_t o = it & 0xFFFFFFu;
+          while (m) {
+            const int s = __ffsll((long long)m) - 1;
+            m &= m - 1ull;
+            const int32_t tr = srow[s];
+            const int64_t gw = c.W + (int64_t)tr * wpr + (o >> 5);
+            const uint32_t bit = 1u << (o & 31);
+            if (kStage2 && !(__ldg(&Rb[gw]) & bit)) continue;  // stage 2: only pairs of R
+            if (!owned(C, tr, (int32_t)o)) {                    // sharded: the owner claims it
+              atomicOr(&cx.OUT[gw], bit);
+              continue;
+            }
+            if (__ldca(&vis[gw]) & bit) continue;
+            atomicOr(&vis[gw], bit);
+            atomicOr(&Fn[gw], bit);
+          }
+        }
+      }
+    }
+    __syncwarp();
+  }
+}
+
 // After a tile push level: the next frontier's size and its chunk list (one warp per chunk; the
 // push kernel's claims are plain reductions, so the exact count comes from the bitmap).
 __global__ void k_push_finish(Ctx cx, int level) {
