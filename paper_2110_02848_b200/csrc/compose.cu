@@ -2169,13 +2169,23 @@ bool tile_push_enabled() {
 
 // FSTC_TILE_PULL_K=k: a level runs bottom-up when frontier * k >= the stage's pair set (stage 1: the
 // pair space, stage 2: R).  A bottom-up round costs about one sweep whatever its frontier, a push level
-// grows with its frontier.  Default 1024 (configs[3]: K = 64 / 256 / 1024 / 4096 -> 45.2 / 42.1 /
-// 41.1 / 41.4 ms per composition).
+// grows with its frontier.  Default 512 (configs[3] with the sparse push levels: K = 128 / 256 / 512 /
+// 1024 -> 38.8 / 37.7 / 36.9 / 37.5 ms per composition).
 int64_t tile_pull_k() {
   static const int64_t v = [] {
     const char* e = getenv("FSTC_TILE_PULL_K");
-    const long long k = e ? atoll(e) : 1024;
-    return (int64_t)(k > 0 ? k : 1024);
+    const long long k = e ? atoll(e) : 512;
+    return (int64_t)(k > 0 ? k : 512);
+  }();
+  return v;
+}
+// FSTC_TILE_PULL_KEXIT=k: after a bottom-up round, the next level stays bottom-up only while the
+// round's claims * k >= the stage's pairs (default = FSTC_TILE_PULL_K).
+int64_t tile_pull_kexit() {
+  static const int64_t v = [] {
+    const char* e = getenv("FSTC_TILE_PULL_KEXIT");
+    const long long k = e ? atoll(e) : 0;
+    return (int64_t)(k > 0 ? k : tile_pull_k());
   }();
   return v;
 }
@@ -2401,8 +2411,9 @@ void launch_tile_emit(const TileArgs& ta, int grid, size_t smem, cudaStream_t s,
 template <bool kStage2>
 fst_status run_stage_tile(const Ctx& cx, const TilePlan& tp, int64_t total, cudaStream_t s, unsigned long long* hp,
                           int64_t* level_launches, std::vector<int64_t>* sizes, int* npull) {
-  const int64_t K = tile_pull_k();
+  const int64_t K = tile_pull_k(), Kexit = tile_pull_kexit();
   const bool all_pull = tile_mode_ref().load() == 3;  // test mode: every level bottom-up
+  bool pulled = false;                                 // the previous level was a bottom-up round
   const TileArgs& ta = kStage2 ? tp.s2 : tp.s1;       // bottom-up rounds: in-view tiles for stage 2
   const TileArgs& tb = kStage2 ? tp.s1 : tp.s2;       // push levels: the opposite direction
   const int grid_pull = kStage2 ? tp.grid_pull2 : tp.grid_pull1, grid_push = kStage2 ? tp.grid_pull1 : tp.grid_pull2;
@@ -2417,7 +2428,9 @@ fst_status run_stage_tile(const Ctx& cx, const TilePlan& tp, int64_t total, cuda
     const int64_t visited = (int64_t)(pad0 + nf);
     const int64_t unvisited = total > visited ? total - visited : 0;
     (void)unvisited;
-    if (all_pull || (int64_t)nf * K >= total) {
+    const bool pull = all_pull || (int64_t)nf * (pulled ? Kexit : K) >= total;
+    pulled = pull;
+    if (pull) {
       launch_tile_pull<kStage2>(ta, grid_pull, tp.smem_pull, s, cx, level);
       FSTC_LAUNCH_CHECK();
       ++*npull;
