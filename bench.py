@@ -419,7 +419,7 @@ def run_ours(args):
     # bound by instruction issue and shared-memory bandwidth, far from HBM-bound (profiles/r02_summary.md)
     bfs_bytes = 2 * k * (R + V_C) + P / 4
     bfs_ms = s1 + s2 - cnt_ms
-    bfs_roof = {"kernel": "k_tile_pull+k_level" if tile else "k_level", "bound": "hbm", "traffic": None,
+    bfs_roof = {"kernel": "k_tile_pull+k_sparse_push" if tile else "k_level", "bound": "hbm", "traffic": None,
                 "achieved": bfs_bytes / (bfs_ms / 1e3) / 1e9, "peak": hbm, "unit": "GB/s",
                 "frac": bfs_bytes / (bfs_ms / 1e3) / 1e9 / hbm, "share_of_step": bfs_ms / ms_step,
                 "algorithmic_bytes_per_step": bfs_bytes, "bytes_formula": "2k(|R|+V_C) + P/4 over both BFS stages",
