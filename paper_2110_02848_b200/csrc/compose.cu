@@ -2261,7 +2261,7 @@ fst_status tile_rows(fst* A, int which, int self, int slot_cap, int vr_cap, int 
   int slots = 0, rows = 0;
   for (int32_t r = 0; r < V; ++r) {
     const int n = bytemode ? 8 : hoff[r + 1] - hoff[r] + self;
-    if (rows > 0 && (slots + n > slot_cap || rows + 1 > kTRows || (vr_cap > 0 && slots + n + rows + 1 > vr_cap))) {
+    if (rows > 0 && (slots + n > slot_cap || rows + 1 > kTRows || (vr_cap > 0 && slots + n > vr_cap))) {
       tr.push_back(r);
       slots = rows = 0;
     }
@@ -2321,9 +2321,9 @@ fst_status tile_plan(fst* A, fst* B, int64_t pairs, bool want_prov, cudaStream_t
   // emit: staged rank rows fill what RT and the per-warp code buffers leave
   const size_t per_warp = (size_t)kEWarps * kECap * 4 + (size_t)wpr * 128;
   if ((size_t)smem_cap <= per_warp || B->V > 65535) return FST_OK;
-  int vr_rows = (int)std::min<size_t>(kESlots + kTRows, ((size_t)smem_cap - per_warp) / ((size_t)wpr * 6 + 2));
+  int vr_rows = (int)std::min<size_t>(kESlots, ((size_t)smem_cap - per_warp) / ((size_t)wpr * 6 + 2));  // slot rows
   while (vr_rows > 0 && tile_emit_smem(vr_rows, wpr, wd_out) > (size_t)smem_cap) --vr_rows;
-  if (vr_rows < degA_out + 2) return FST_OK;  // one row with its self slot must fit
+  if (vr_rows < degA_out + 1) return FST_OK;  // one row with its self slot must fit
   fst_status st = ensure_tile_ell(B, 0, s);
   if (!st) st = ensure_tile_ell(B, 1, s);
   if (st) return st;

@@ -29,7 +29,10 @@
 
 constexpr int kTThreads = 1024;          // pull / count CTAs (1 per SM: the 64-bit RT takes the smem)
 constexpr int kTWarps = kTThreads / 32;
-constexpr int kEThreads = 1024;          // emit CTAs (1 per SM: the rank tables take the shared memory)
+#ifndef FSTC_E_THREADS
+#define FSTC_E_THREADS 1024
+#endif
+constexpr int kEThreads = FSTC_E_THREADS; // emit CTAs (1 per SM: the rank tables take the shared memory)
 constexpr int kEWarps = kEThreads / 32;
 constexpr int kPSlots = 64;              // slots of the pull / count tiles
 constexpr int kESlots = 32;              // slots of the emit tiles
@@ -754,20 +757,22 @@ struct EmitIO {
 };
 
 // Shared memory: RT (32-bit slot-transposed V of the tile's slot rows, for the hit tests), and for
-// the slot rows [0, ns) and source rows [ns, ns + nr) the V words (u32) and the rank of each word's
-// first pair inside its row (u16), + per-row base ids; per warp a buffer of kECap arc codes
-// (dst column << 15 | lane << 10 | item << 5 | slot).
+// the slot rows (the A-arc destinations, ns <= vr_rows) the V words (u32) and the rank of each word's
+// first pair inside its row (u16), + per-slot-row base ids; per warp a buffer of kECap arc codes
+// (dst column << 15 | item << 10 | lane << 5 | slot).  The source rows' words come from global memory
+// (one load per lane and word), so the staged rows are slot rows only.
 // One warp task = one word w (32 columns) for ALL rows of the tile: the word's ELL items are loaded
-// once into registers and serve every row.  Row x's arcs of word w start at arcbase[block] +
-// warc[word] (k_tile_count, k_block_counts).  Per (row, word): walk 1 -- one AND per item gives the
-// item's hit slots (lm[li] & RT[b'] & rowmask), kept in registers, a warp scan of the per-state counts
-// gives each state's first arc slot; walk 2 writes the arc codes in (state, item, slot) order; then
-// lanes take CONSECUTIVE arcs (coalesced streaming stores of dst / ilabel / olabel / weight).
+// once into registers and their hit masks lm[li] & RT[b'] (row-independent) computed once; row x's
+// hits of item k are that mask & the row's slot mask.  Row x's arcs of word w start at arcbase[block] +
+// warc[word] (k_tile_count, k_block_counts).  Per (row, word): walk 1 -- the per-state arc counts and
+// a warp scan give each state's first arc slot; walk 2 writes the arc codes in (state, item, slot)
+// order; then lanes take CONSECUTIVE arcs (coalesced streaming stores of dst / ilabel / olabel /
+// weight).
 template <int kJ>
 __global__ void __launch_bounds__(kEThreads, 1) k_tile_emit(Ctx cx, TileArgs ta, EmitIO io,
                                                              const int64_t* __restrict__ tot, int vr_rows) {
   __shared__ TileSmem<uint32_t> t;
-  __shared__ int32_t rbase[kESlots + kTRows];
+  __shared__ int32_t rbase[kESlots];
   extern __shared__ __align__(16) uint32_t tdyn[];
   const TC c = tc_of(cx);
   const int wpr = c.wpr, VB = c.VB, bpr = c.bpr, wd = ta.sd.wd;
@@ -782,34 +787,31 @@ __global__ void __launch_bounds__(kEThreads, 1) k_tile_emit(Ctx cx, TileArgs ta,
     tile_slots(t, ta, tile);
     const int nr = t.nr, ns = t.ns;
     const int32_t r0 = t.r0;
-    const int nk = ns + nr;
-    for (int i0 = threadIdx.x; i0 < nk * wpr; i0 += 4 * kEThreads) {
-      uint32_t v[4], pr[4];
+    for (int k = warp; k < ns; k += kEWarps) {  // stage the slot rows: a warp per row, coalesced
+      const int32_t row = t.srow[k];
+      const int64_t gw0 = c.W + (int64_t)row * wpr, kb = c.K + (int64_t)row * bpr;
+      const int64_t ib = __ldg(&cx.idbase[kb]);
+      if (lane == 0) rbase[k] = (int32_t)(ib - id_comp);
+      for (int w0 = lane; w0 < wpr; w0 += 4 * 32) {
+        uint32_t v[4], pr[4];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int i = i0 + u * kEThreads;
-        v[u] = pr[u] = 0u;
-        if (i < nk * wpr) {
-          const int k = i / wpr, w = i - k * wpr;
-          const int32_t row = k < ns ? t.srow[k] : r0 + (k - ns);
-          const int64_t gw = c.W + (int64_t)row * wpr + w;
-          const int64_t kb = c.K + (int64_t)row * bpr;
-          v[u] = __ldg(&V[gw]);
-          pr[u] = (uint32_t)(__ldg(&cx.idbase[kb + (w >> 5)]) - __ldg(&cx.idbase[kb]) + __ldg(&cx.wpre[gw]));
+        for (int u = 0; u < 4; ++u) {
+          const int w = w0 + 32 * u;
+          v[u] = pr[u] = 0u;
+          if (w < wpr) {
+            v[u] = __ldg(&V[gw0 + w]);
+            pr[u] = (uint32_t)(__ldg(&cx.idbase[kb + (w >> 5)]) - ib + __ldg(&cx.wpre[gw0 + w]));
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int w = w0 + 32 * u;
+          if (w < wpr) {
+            Vw[(size_t)k * wpr + w] = v[u];
+            Pw[(size_t)k * wpr + w] = (uint16_t)pr[u];
+          }
         }
       }
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int i = i0 + u * kEThreads;
-        if (i < nk * wpr) {
-          Vw[i] = v[u];
-          Pw[i] = (uint16_t)pr[u];
-        }
-      }
-    }
-    for (int k = threadIdx.x; k < nk; k += kEThreads) {
-      const int32_t row = k < ns ? t.srow[k] : r0 + (k - ns);
-      rbase[k] = (int32_t)(__ldg(&cx.idbase[c.K + (int64_t)row * bpr]) - id_comp);
     }
     __syncthreads();
     // RT from the staged slot rows (lane s reads row s: bank (s * wpr + w) % 32, conflict-free for odd wpr)
@@ -821,17 +823,19 @@ __global__ void __launch_bounds__(kEThreads, 1) k_tile_emit(Ctx cx, TileArgs ta,
     const int j0 = t.lm[kLiSent] ? 0 : 1;
     const uint32_t selfm = t.selfm;
     const uint32_t* lm = t.lm;
-    const uint8_t stA_l = lane < nr ? __ldg(&io.startA[r0 + lane]) : 0, acA_l = lane < nr ? __ldg(&io.accA[r0 + lane]) : 0;
+    // lane x < nr: row x's slot mask and start / accept flags (bits 0 / 1)
     const uint32_t rm_l = lane < nr ? t.rmask[lane] : 0u;
+    const uint32_t fl_l = lane < nr ? (uint32_t)__ldg(&io.startA[r0 + lane]) | ((uint32_t)__ldg(&io.accA[r0 + lane]) << 1) : 0u;
     for (int w = warp; w < wpr; w += kEWarps) {
-      // lane x < nr: V word of (row x, w), the arc base of its states and their arc count
+      // lane x < nr: V word of (row x, w), the id of its first state, the arc base and arc count
       uint32_t vw_l = 0u;
+      int32_t id_l = 0, exp_l = 0;
       int64_t base_l = 0;
-      int32_t exp_l = 0;
       if (lane < nr && c.own(r0 + lane)) {  // (rows of other shards are emitted there)
         const int64_t gw = c.W + (int64_t)(r0 + lane) * wpr + w;
         const int64_t blk = c.K + (int64_t)(r0 + lane) * bpr + (w >> 5);
-        vw_l = Vw[(size_t)(ns + lane) * wpr + w];
+        vw_l = __ldg(&V[gw]);
+        id_l = (int32_t)(__ldg(&cx.idbase[blk]) - id_comp + __ldg(&cx.wpre[gw]));
         const uint32_t pre = __ldg(&cx.warc[gw]);
         base_l = __ldg(&cx.arcbase[blk]) - arc_comp + pre;
         const bool last = (w & 31) == 31 || w == wpr - 1;
@@ -841,67 +845,49 @@ __global__ void __launch_bounds__(kEThreads, 1) k_tile_emit(Ctx cx, TileArgs ta,
       const int b = w * 32 + lane;
       const bool inb = b < VB;
       const int jn = ta.sd.wmax[w];
-      uint32_t it[kJ + 1];
-      {
-        const uint32_t* p = ta.sd.ell + (size_t)w * wd * 32 + lane;
-        it[0] = (j0 == 0 && inb) ? __ldg(p) : (kLiPad << 24);
+      const uint32_t* __restrict__ ellw = ta.sd.ell + (size_t)w * wd * 32 + lane;
+      const int2* __restrict__ cww = ta.sd.ellcw + (size_t)w * wd * 32;
+      // per item: hit slots of all tile rows (g) and the code's item bits (cb)
+      uint32_t g[kJ + 1], cb[kJ + 1];
 #pragma unroll
-        for (int k = 0; k < kJ; ++k) it[k + 1] = (inb && k + 1 < jn) ? __ldg(p + (k + 1) * 32) : (kLiPad << 24);
+      for (int k = 0; k <= kJ; ++k) {
+        const uint32_t xi = (inb && (k == 0 ? j0 == 0 : k < jn)) ? __ldg(ellw + k * 32) : (kLiPad << 24);
+        g[k] = lm[xi >> 24] & RT[xi & 0xFFFFFFu];
+        cb[k] = ((xi & 0xFFFFu) << 15) | ((uint32_t)k << 10) | ((uint32_t)lane << 5);
       }
       for (int x = 0; x < nr; ++x) {
         const uint32_t vw = __shfl_sync(0xffffffffu, vw_l, x);
+        if (!vw) continue;
         const int64_t run = __shfl_sync(0xffffffffu, base_l, x);
         const uint32_t rmx = __shfl_sync(0xffffffffu, rm_l, x);
-        const uint8_t stA = __shfl_sync(0xffffffffu, stA_l, x), acA = __shfl_sync(0xffffffffu, acA_l, x);
-        if (!vw) continue;
         const uint32_t rmv = ((vw >> lane) & 1u) ? rmx : 0u;
-        // walk 1: hit slots of every item (registers) and the state's arc count
-        uint32_t h[kJ + 1];
+        // walk 1: the state's arc count
         int cnt = 0;
 #pragma unroll
-        for (int k = 0; k <= kJ; ++k) {
-          h[k] = lm[it[k] >> 24] & RT[it[k] & 0xFFFFFFu] & rmv;
-          cnt += __popc(h[k]);
-        }
+        for (int k = 0; k <= kJ; ++k) cnt += __popc(g[k] & rmv);
         for (int j = kJ + 1; j < jn; ++j) {  // (wide B rows: items beyond the registers)
-          const uint32_t xi = inb ? __ldg(ta.sd.ell + ((size_t)w * wd + j) * 32 + lane) : (kLiPad << 24);
+          const uint32_t xi = inb ? __ldg(ellw + j * 32) : (kLiPad << 24);
           cnt += __popc(lm[xi >> 24] & RT[xi & 0xFFFFFFu] & rmv);
         }
         const int inc = warp_incl_scan(cnt);
         const int ex = inc - cnt;
         const int T = __shfl_sync(0xffffffffu, inc, 31);
         if (lane == x && T != exp_l) atomicAdd(&cx.misc[2], 1ull);
-        const int32_t row = r0 + x;
-        if (rmv) {  // the state's own outputs
-          const int32_t id = rbase[ns + x] + Pw[(size_t)(ns + x) * wpr + w] + __popc(vw & ((1u << lane) - 1u));
-          __stcs((long long*)&io.row_ptr[id], (long long)(run + ex));
-          __stcs(&io.pair_a[id], row);
-          __stcs(&io.pair_b[id], b);
-          io.is_start[id] = (uint8_t)(stA & __ldg(&io.startB[b]));
-          io.is_accept[id] = (uint8_t)(acA & __ldg(&io.accB[b]));
-        }
-        for (int p = 0; p < T; p += kECap) {
-          // walk 2: arc codes of positions [p, p + kECap)
-          if (cnt && ex < p + kECap && ex + cnt > p) {
-            int pos = ex;
-            auto put = [&](int j, uint32_t hj, uint32_t xi) {
-              const uint32_t hi = ((xi & 0xFFFFu) << 15) | (lane << 10) | (j << 5);
-              while (hj) {
-                const int s = __ffs(hj) - 1;
-                hj &= hj - 1u;
-                if (pos >= p && pos < p + kECap) code[pos - p] = hi | s;
-                ++pos;
-              }
-            };
-#pragma unroll
-            for (int k = 0; k <= kJ; ++k) put(k, h[k], it[k]);
-            for (int j = kJ + 1; j < jn; ++j) {
-              const uint32_t xi = inb ? __ldg(ta.sd.ell + ((size_t)w * wd + j) * 32 + lane) : (kLiPad << 24);
-              put(j, lm[xi >> 24] & RT[xi & 0xFFFFFFu] & rmv, xi);
-            }
+        {
+          const int32_t idw = __shfl_sync(0xffffffffu, id_l, x);
+          const uint32_t fl = __shfl_sync(0xffffffffu, fl_l, x);
+          if (rmv) {  // the state's own outputs
+            const int32_t id = idw + __popc(vw & ((1u << lane) - 1u));
+            __stcs((long long*)&io.row_ptr[id], (long long)(run + ex));
+            __stcs(&io.pair_a[id], r0 + x);
+            __stcs(&io.pair_b[id], b);
+            io.is_start[id] = (uint8_t)((fl & 1u) & __ldg(&io.startB[b]));
+            io.is_accept[id] = (uint8_t)((fl >> 1) & __ldg(&io.accB[b]));
           }
+        }
+        // phase 3: arcs [p, p + n) of the (row, word) from the code buffer
+        auto flush = [&](int p, int n) {
           __syncwarp();
-          const int n = min(kECap, T - p);
           for (int i0 = lane; i0 < n; i0 += 64) {  // two arcs per lane in flight
             int2 cw[2];
             uint32_t cd[2];
@@ -909,20 +895,19 @@ __global__ void __launch_bounds__(kEThreads, 1) k_tile_emit(Ctx cx, TileArgs ta,
             for (int u = 0; u < 2; ++u) {
               const int i = i0 + 32 * u;
               cd[u] = i < n ? code[i] : 0u;
-              const int L = (cd[u] >> 10) & 31, j = (cd[u] >> 5) & 31;
-              cw[u] = (i < n && j != 0) ? __ldg(ta.sd.ellcw + ((size_t)w * wd + j) * 32 + L) : make_int2(0, 0);
+              cw[u] = (i < n && (cd[u] & (31u << 10))) ? __ldg(cww + ((cd[u] >> 5) & 1023u)) : make_int2(0, 0);
             }
 #pragma unroll
             for (int u = 0; u < 2; ++u) {
               const int i = i0 + 32 * u;
               if (i >= n) break;
               const uint32_t o = cd[u] >> 15;
-              const int j = (cd[u] >> 5) & 31, s = cd[u] & 31;
+              const int s = cd[u] & 31;
               const uint32_t vword = Vw[s * wpr + (o >> 5)];
               const int32_t did = rbase[s] + Pw[s * wpr + (o >> 5)] + __popc(vword & ((1u << (o & 31)) - 1u));
               int32_t il, ol;
               float wt;
-              if (j == 0) {  // M2: A eps arc, B stays (bit copy)
+              if (!(cd[u] & (31u << 10))) {  // item 0 = M2: A eps arc, B stays (bit copy)
                 il = t.scarry[s];
                 ol = FST_EPS;
                 wt = t.sw[s];
@@ -943,6 +928,49 @@ __global__ void __launch_bounds__(kEThreads, 1) k_tile_emit(Ctx cx, TileArgs ta,
             }
           }
           __syncwarp();
+        };
+        if (T <= kECap) {  // walk 2, one flush (the common case: no range tests)
+          uint32_t* cp = code + ex;
+#pragma unroll
+          for (int k = 0; k <= kJ; ++k) {
+            uint32_t hj = g[k] & rmv;
+            while (hj) {
+              *cp++ = cb[k] | (uint32_t)(__ffs(hj) - 1);
+              hj &= hj - 1u;
+            }
+          }
+          for (int j = kJ + 1; j < jn; ++j) {
+            const uint32_t xi = inb ? __ldg(ellw + j * 32) : (kLiPad << 24);
+            uint32_t hj = lm[xi >> 24] & RT[xi & 0xFFFFFFu] & rmv;
+            const uint32_t cj = ((xi & 0xFFFFu) << 15) | ((uint32_t)j << 10) | ((uint32_t)lane << 5);
+            while (hj) {
+              *cp++ = cj | (uint32_t)(__ffs(hj) - 1);
+              hj &= hj - 1u;
+            }
+          }
+          flush(0, T);
+          continue;
+        }
+        for (int p = 0; p < T; p += kECap) {
+          // walk 2: arc codes of positions [p, p + kECap)
+          if (cnt && ex < p + kECap && ex + cnt > p) {
+            int pos = ex;
+            auto put = [&](uint32_t hj, uint32_t hi) {
+              while (hj) {
+                const int s = __ffs(hj) - 1;
+                hj &= hj - 1u;
+                if (pos >= p && pos < p + kECap) code[pos - p] = hi | s;
+                ++pos;
+              }
+            };
+#pragma unroll
+            for (int k = 0; k <= kJ; ++k) put(g[k] & rmv, cb[k]);
+            for (int j = kJ + 1; j < jn; ++j) {
+              const uint32_t xi = inb ? __ldg(ellw + j * 32) : (kLiPad << 24);
+              put(lm[xi >> 24] & RT[xi & 0xFFFFFFu] & rmv, ((xi & 0xFFFFu) << 15) | ((uint32_t)j << 10) | ((uint32_t)lane << 5));
+            }
+          }
+          flush(p, min(kECap, T - p));
         }
       }
     }
