@@ -273,6 +273,16 @@ void fst_set_profiling(int32_t on);
  * numbering by ascending key; arc order within a state may differ). */
 void fst_set_tile_mode(int32_t mode);
 
+/* Wave path selection: compositions whose A is topologically numbered (every arc
+ * src < dst: lexicon o emissions trellises, DAGs) computed row by row (stage 1 rows descending, stage 2
+ * ascending, one thread-block cluster per composition) instead of by BFS levels.  0 = never,
+ * 1 = automatic (every A qualifies, rows <= 4096 per composition, A rows <= 64 arcs, B ilabels <= 252,
+ * V_B < 2^24), 2 = whenever the inputs qualify, whatever their row count.  A forced tile mode (>= 2)
+ * keeps single compositions on the tile path.  The environment variable FSTC_WAVE sets the initial
+ * mode.  Same graph as the level path; fst_compose_stats.tile_path = 2 and levels_stage1/2 = the row
+ * steps of the longest composition; no per-level sizes (fst_level_sizes returns 0 levels). */
+void fst_set_wave_mode(int32_t mode);
+
 /* Total kernels launched by this process through the library (monotone counter). */
 int64_t fst_launch_count(void);
 

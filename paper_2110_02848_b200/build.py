@@ -10,7 +10,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libfstc.so")
-SOURCES = ["api.cu", "create.cu", "compose.cu", "scan.cu", "memory.cu", "forward.cu", "filter.cu"]
+SOURCES = ["api.cu", "create.cu", "compose.cu", "scan.cu", "memory.cu", "forward.cu", "filter.cu", "wave.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xcompiler", "-O2", "--expt-relaxed-constexpr", "--extended-lambda",

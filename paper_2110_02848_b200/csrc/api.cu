@@ -52,6 +52,7 @@ fst_status compose_filtered_impl(int32_t n, const fst_handle* a, const fst_handl
                                  uint32_t flags);
 fst_status compose_chain_impl(int32_t n, const fst_handle* g, uint32_t flags, cudaStream_t s, fst_handle* out);
 void tile_mode_set(int mode);
+void wave_mode_set(int mode);
 
 fst_status device_ready() {
   int n = 0;
@@ -403,6 +404,8 @@ fst_status fst_shard_info(fst_handle c, fst_shard_desc* out) {
 void fst_set_profiling(int32_t on) { g_profiling.store(on ? 1 : 0); }
 
 void fst_set_tile_mode(int32_t mode) { fstc::tile_mode_set(mode); }
+
+void fst_set_wave_mode(int32_t mode) { fstc::wave_mode_set(mode); }
 
 int64_t fst_launch_count(void) { return g_launches.load(); }
 

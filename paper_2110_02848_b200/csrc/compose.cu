@@ -33,6 +33,7 @@
 #include "fstc_handle.h"
 #include "fstc_internal.cuh"
 #include "scan.cuh"
+#include "wave.h"
 
 namespace fstc {
 
@@ -2533,8 +2534,17 @@ fst_status compose_impl(int32_t n, const fst_handle* a, const fst_handle* b, cud
     seed2[i + 1] = seed2[i] + (int64_t)C.nStartA * C.nStartB;
   }
   const int64_t nwords = W, nblocks = K, nchunks = Q;
+  // compositions whose A is topologically numbered (trellises): row-by-row stages (wave.cu); a
+  // forced tile mode (>= 2) keeps single compositions on the tile path
+  WavePlan wp;
+  if (n > 1 || tile_mode_ref().load() < 2) {
+    std::vector<int64_t> Wv(n), Kv(n);
+    for (int i = 0; i < n; ++i) Wv[i] = comps[i].W, Kv[i] = comps[i].K;
+    st = wave_plan(n, a, b, Wv.data(), Kv.data(), s, &wp);
+    if (st) return st;
+  }
   TilePlan tp;
-  if (n == 1) {  // single large compositions: bottom-up levels, count and emit on the tile kernels
+  if (n == 1 && !wp.ok) {  // single large compositions: bottom-up levels, count and emit on the tile kernels
     st = tile_plan(a[0], b[0], pairs, want_prov, s, &tp);
     if (st) return st;
   }
@@ -2622,14 +2632,19 @@ fst_status compose_impl(int32_t n, const fst_handle* a, const fst_handle* b, cud
   {
     EventTimer t(prof, s);
     cx.seedbase = d_seed1;
-    if (seed1[n] > 0) {
+    if (wp.ok) {
+      if (seed1[n] > 0) {
+        st = wave_stage(wp, 1, cx.R, cx.V, s);
+        if (st) return st;
+      }
+    } else if (seed1[n] > 0) {
       k_seed<false><<<nblk(seed1[n], 256), 256, 0, s>>>(cx);
       FSTC_LAUNCH_CHECK();
       st = tp.ok ? run_stage_tile<false>(cx, tp, pairs, s, hp, &level_launches, &sizes1, &stats.pull_levels)
                  : run_stage<false>(cx, s, hp, &level_launches, &sizes1);
       if (st) return st;
     }
-    stats.levels_stage1 = (int32_t)sizes1.size();
+    stats.levels_stage1 = wp.ok ? wp.depth : (int32_t)sizes1.size();
     stats.ms_stage1 = t.stop();
   }
   // ---- stage 2: accessible states restricted to R (forward BFS from start pairs)
@@ -2638,7 +2653,16 @@ fst_status compose_impl(int32_t n, const fst_handle* a, const fst_handle* b, cud
   {
     EventTimer t(prof, s);
     cx.seedbase = d_seed2;
-    if (seed2[n] > 0 && seed1[n] > 0) {
+    if (wp.ok) {
+      if (seed2[n] > 0 && seed1[n] > 0) {
+        st = wave_stage(wp, 2, cx.R, cx.V, s);
+        if (st) return st;
+        EventTimer tc(prof, s);
+        st = wave_count(wp, cx.V, cx.cnt8, cx.kept, s);
+        if (st) return st;
+        stats.ms_count = tc.stop();
+      }
+    } else if (seed2[n] > 0 && seed1[n] > 0) {
       k_seed<true><<<nblk(seed2[n], 256), 256, 0, s>>>(cx);
       FSTC_LAUNCH_CHECK();
       if (tp.ok) {
@@ -2660,7 +2684,7 @@ fst_status compose_impl(int32_t n, const fst_handle* a, const fst_handle* b, cud
       FSTC_LAUNCH_CHECK();
       stats.ms_count = tc.stop();
     }
-    stats.levels_stage2 = (int32_t)sizes2.size();
+    stats.levels_stage2 = wp.ok ? wp.depth : (int32_t)sizes2.size();
     stats.ms_stage2 = t.stop();
   }
   // ---- numbering: per-block state counts, word prefixes, scans, per-composition totals
@@ -2780,7 +2804,7 @@ fst_status compose_impl(int32_t n, const fst_handle* a, const fst_handle* b, cud
   stats.launches = fst_launch_count() - launches0;
   stats.expand_launches = level_launches;
   stats.emit_launches = 1;
-  stats.tile_path = tp.ok ? 1 : 0;
+  stats.tile_path = tp.ok ? 1 : (wp.ok ? 2 : 0);
   for (int i = 0; i < n; ++i) {
     outs[i]->stats = stats;
     level_sizes_slot(outs[i], 1) = sizes1;

@@ -107,4 +107,18 @@ struct fst {
   };
   std::vector<TileRows> tile_rows;
   std::vector<int32_t> tile_hoff[2];  // host copy of the A-role view offsets ([0] out, [1] in by olabel)
+  // wave path caches (wave.cu), built on first use
+  int8_t a_topo = -1;  // A role: 1 if every arc has src < dst (rows in topological order), 0 if not
+  struct WaveEll {     // B role, [0] out-by-ilabel, [1] in-by-ilabel: ELL of the light columns by word
+    bool ok = false;
+    fstc::BufferPtr buf;
+    uint32_t* ell = nullptr;   // [(woff[w] + j) * 32 + lane] = (label + 2) << 24 | other; 255 << 24 = pad
+    uint32_t* woff = nullptr;  // [wpr + 1] first ELL row of each word
+    uint8_t* wmax = nullptr;   // [wpr] ELL rows of each word (max light degree in the word)
+    uint32_t* hmask = nullptr; // [wpr] lanes of heavy columns
+    int4* heavy = nullptr;     // (col, first item, first non-eps item, end) of heavy columns, by col
+    int32_t nheavy = 0;
+    int2* eps = nullptr;       // [0] only: B arcs with ilabel eps as (src, dst)
+    int32_t neps = 0;
+  } wave_ell[2];
 };

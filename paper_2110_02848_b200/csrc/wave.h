@@ -1,0 +1,34 @@
+// wave.h -- the wave path (wave.cu): row-by-row stages for compositions whose A is
+// topologically numbered.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/fstc.h"
+
+namespace fstc {
+
+struct WavePlan {
+  bool ok = false;
+  int32_t depth = 0;    // row steps of the longest composition (sequential per cluster)
+  int32_t cluster = 1;  // CTAs per cluster (one composition per cluster)
+  struct Impl;
+  Impl* impl;
+  WavePlan();
+  ~WavePlan();
+  WavePlan(const WavePlan&) = delete;
+  WavePlan& operator=(const WavePlan&) = delete;
+};
+
+// plan->ok when every composition qualifies (A topologically numbered, A rows <= 64 arcs, B ilabels
+// <= 252, V_B < 2^24; automatic mode: V_A <= 4096) and the wave mode allows it.  W / K: first word /
+// block of each composition's pair space.
+fst_status wave_plan(int32_t n, const fst_handle* a, const fst_handle* b, const int64_t* W, const int64_t* K,
+                     cudaStream_t s, WavePlan* plan);
+// stage 1 writes every word of R, stage 2 every word of V (reads R).
+fst_status wave_stage(const WavePlan& plan, int stage, uint32_t* R, uint32_t* V, cudaStream_t s);
+// pass-1 counts: cnt8 of every state of C and kept[] of every block (overwritten).
+fst_status wave_count(const WavePlan& plan, uint32_t* V, uint8_t* cnt8, unsigned long long* kept, cudaStream_t s);
+void wave_mode_set(int mode);
+
+}  // namespace fstc

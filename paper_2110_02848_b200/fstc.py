@@ -26,7 +26,7 @@ STATUS = {0: "FST_OK", 1: "FST_E_INVALID_ARG", 2: "FST_E_INVALID_GRAPH", 3: "FST
           5: "FST_E_CUDA", 6: "FST_E_NCCL", 7: "FST_E_INTERNAL"}
 
 EXPORTED = ["fst_create", "fst_compose", "fst_compose_batch", "fst_free", "fst_info", "fst_copy_to_host",
-            "fst_get_stats", "fst_level_sizes", "fst_adjacency", "fst_set_profiling", "fst_set_tile_mode", "fst_launch_count",
+            "fst_get_stats", "fst_level_sizes", "fst_adjacency", "fst_set_profiling", "fst_set_tile_mode", "fst_set_wave_mode", "fst_launch_count",
             "fst_last_error", "fst_version", "fst_comm_unique_id", "fst_comm_init", "fst_comm_destroy",
             "fst_compose_sharded", "fst_compose_sharded_local", "fst_shard_info", "fst_copy_arcs_to_host",
             "fst_compose_ex", "fst_compose_batch_ex", "fst_copy_provenance_to_host", "fst_grad_scatter",
@@ -115,6 +115,8 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
         lib.fst_set_profiling.restype = None
         lib.fst_set_tile_mode.argtypes = [C.c_int32]
         lib.fst_set_tile_mode.restype = None
+        lib.fst_set_wave_mode.argtypes = [C.c_int32]
+        lib.fst_set_wave_mode.restype = None
         lib.fst_launch_count.restype = C.c_int64
         lib.fst_last_error.restype = C.c_char_p
         lib.fst_version.restype = C.c_char_p
@@ -309,6 +311,12 @@ def fst_set_profiling(on: bool):
 def fst_set_tile_mode(mode: int):
     """0 = never use the tile kernels, 1 = automatic (default), 2 = whenever the inputs fit."""
     load_library().fst_set_tile_mode(int(mode))
+
+
+def fst_set_wave_mode(mode: int):
+    """Wave path (row-by-row stages for topologically numbered A): 0 = never, 1 = automatic (default),
+    2 = whenever the inputs qualify."""
+    load_library().fst_set_wave_mode(int(mode))
 
 
 def fst_launch_count() -> int:

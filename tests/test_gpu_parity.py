@@ -75,7 +75,11 @@ def test_golden_fixture_gpu(fst, name):
 def test_fig2_round_profile_gpu(fst):
     g = golden_io.load("f2_fig2.txt")
     a, b = fst.fst_create(g["A"]), fst.fst_create(g["B"])
-    c = fst.fst_compose(a, b)
+    fst.fst_set_wave_mode(0)  # BFS levels exist on the level path only
+    try:
+        c = fst.fst_compose(a, b)
+    finally:
+        fst.fst_set_wave_mode(1)
     assert c.level_sizes(2) == g["levels"]["frontier"]  # |Q| = 1, 2, 2
     assert sum(c.level_sizes(1)) == len(g["R"])
 
@@ -266,7 +270,11 @@ def test_deep_bfs_level_profile(fst, T):
     itself equals the oracle's."""
     A, B = fstgen.config_c3(num_words=300, T=T)
     a, b = fst.fst_create(A), fst.fst_create(B)
-    c = fst.fst_compose(a, b)
+    fst.fst_set_wave_mode(0)  # the level path (the wave path has no BFS levels; tests/test_gpu_wave.py)
+    try:
+        c = fst.fst_compose(a, b)
+    finally:
+        fst.fst_set_wave_mode(1)
     exp = oracle.compose(A, B)
     lv = np.bincount(exp["level"]) if exp["num_states"] else np.zeros(0, np.int64)
     assert c.level_sizes(2) == [int(x) for x in lv]
