@@ -2797,7 +2797,7 @@ fst_status compose_impl(int32_t n, const fst_handle* a, const fst_handle* b, cud
       set_error(FST_E_INTERNAL, "emit/count mismatch in %llu blocks", hp[2]);
       return FST_E_INTERNAL;
     }
-    stats.staged_tasks = (int64_t)hp[3];
+    stats.staged_tasks = wp.ok ? wp.cluster : (int64_t)hp[3];
   }
   wb.reset();
   stats.ms_total = t_total.stop();

@@ -112,13 +112,22 @@ struct fst {
   struct WaveEll {     // B role, [0] out-by-ilabel, [1] in-by-ilabel: ELL of the light columns by word
     bool ok = false;
     fstc::BufferPtr buf;
-    uint32_t* ell = nullptr;   // [(woff[w] + j) * 32 + lane] = (label + 2) << 24 | other; 255 << 24 = pad
+    uint32_t* ell = nullptr;   // non-eps items: [(woff[w] + j) * 32 + lane] = (label + 2) << 24 | other; 255 << 24 = pad
     uint32_t* woff = nullptr;  // [wpr + 1] first ELL row of each word
-    uint8_t* wmax = nullptr;   // [wpr] ELL rows of each word (max light degree in the word)
+    uint8_t* wmax = nullptr;   // [wpr] ELL rows of each word (max light non-eps degree in the word)
+    uint32_t* eell = nullptr;  // eps items of the light columns, same layout
+    uint32_t* ewoff = nullptr;
+    uint8_t* ewmax = nullptr;
+    uint32_t blab[8] = {};     // label indices (label + 2) of the light non-eps items
     uint32_t* hmask = nullptr; // [wpr] lanes of heavy columns
     int4* heavy = nullptr;     // (col, first item, first non-eps item, end) of heavy columns, by col
     int32_t nheavy = 0;
-    int2* eps = nullptr;       // [0] only: B arcs with ilabel eps as (src, dst)
+    int2* eps = nullptr;       // [0] only: B arcs with ilabel eps as (src, dst), dst not a hub
     int32_t neps = 0;
+    int32_t nhub = 0;          // [0] only: eps hub targets (many eps in-arcs)
+    int32_t* hub_col = nullptr;
+    uint32_t* hub_src = nullptr;  // [nhub][wpr] eps sources of each hub
+    uint32_t* hitems = nullptr;   // items of the heavy columns, packed like the ELL
+    uint32_t* rel = nullptr;      // [0] only: [4][wpr] relevance masks of the M3 passes (wave.cu)
   } wave_ell[2];
 };

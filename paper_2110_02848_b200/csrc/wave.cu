@@ -29,10 +29,12 @@
 // k_wave_count then writes pass-1 counts for the general emit: cnt8 (the kept-move
 // count of every state of C, saturated at 255 = recount) and kept[block] (exact), fully parallel.
 #include <cooperative_groups.h>
+#include <cuda_pipeline.h>
 #include <stdio.h>
 #include <stdlib.h>
 
 #include <algorithm>
+#include <functional>
 #include <atomic>
 #include <vector>
 
@@ -52,16 +54,21 @@ constexpr int kWHeavy = 32;    // B columns with more items (in a direction) are
 constexpr int kWSlots = 64;    // A arcs per row (label -> slot masks are 64-bit)
 constexpr int kWLab = 256;     // label index = label + 2 (eps = 1); 255 = ELL padding (never set)
 constexpr int kCThreads = 512; // count CTAs
+constexpr int kEpsHub = 64;    // eps in-arcs that make a column an M3 hub (source set kept as a bitmap)
+constexpr int kEpsHubMax = 16;
 
 struct WaveDir {  // B role, one direction (view by ilabel)
-  const uint32_t* ell;
+  const uint32_t* ell;   // light columns' non-eps items by word: [(woff[w] + j) * 32 + lane]
   const uint32_t* woff;
   const uint8_t* wmax;
+  const uint32_t* eell;  // light columns' eps items, same layout
+  const uint32_t* ewoff;
+  const uint8_t* ewmax;
   const uint32_t* hmask;
   const int4* heavy;
   int32_t nheavy;
-  const int32_t* key;    // the view's arrays (heavy columns are walked there)
-  const int32_t* other;
+  const uint32_t* hitems; // items of the heavy columns, packed like the ELL (heavy[h].y/.z/.w index them)
+  uint32_t blab[8];       // label indices of the light non-eps items
 };
 
 struct WaveComp {
@@ -76,8 +83,15 @@ struct WaveComp {
   const uint8_t* startB;
   const uint8_t* accB;
   WaveDir bd[2];     // B role: [0] out-by-ilabel (stage 1, counts), [1] in-by-ilabel (stage 2)
-  const int2* eps;   // B arcs with ilabel eps, (src, dst): the M3 moves
+  const int2* eps;   // B arcs with ilabel eps, (src, dst), whose dst is not a hub: the M3 moves
   int32_t neps;
+  int32_t nhub;      // hub targets: columns with >= kEpsHub eps in-arcs
+  const int32_t* hub_col;
+  const uint32_t* hub_src;  // [nhub][wpr] bitmap of each hub's eps sources
+  // relevance masks of the M3 passes ([wpr] each): [0] stage 1 arc phase (dsts of non-hub eps arcs),
+  // [1] stage 1 hub phase ([0] + hub columns), [2] stage 2 hub phase (eps sources of hubs), [3] stage 2
+  // arc phase ([2] + sources of non-hub eps arcs)
+  const uint32_t* rel[4];
 };
 
 struct WaveArgs {
@@ -90,6 +104,7 @@ struct WaveArgs {
   uint8_t* cnt8;
   unsigned long long* kept;
   int32_t* next;         // composition counter of the stage kernels
+  uint32_t cache_words;  // shared-memory words for the ELL cache of a stage CTA
   int64_t nrows;         // rows of all compositions (count tasks)
 };
 
@@ -103,11 +118,15 @@ __global__ void __launch_bounds__(kWThreads, 1) k_wave(WaveArgs wa) {
   extern __shared__ __align__(16) unsigned char wsm[];
   unsigned long long* lm = (unsigned long long*)wsm;  // [kWLab] slots of the A row's arcs by label index
   int32_t* srow = (int32_t*)(lm + kWLab);              // [kWSlots] row at the other end of slot s
-  int32_t* misc = srow + kWSlots;                      // [0] composition, [1] [2] heavy range
+  int32_t* misc = srow + kWSlots;                      // [32]: [0] composition, [1] [2] heavy range, [3] cached,
+                                                       //       [4..4+G] word ranges of the cluster's CTAs
+  uint32_t* lp = (uint32_t*)(misc + 32);               // [8] label indices present in the A row
   const int wprmax = wa.wprmax, rng = (wprmax + G - 1) / G;
-  uint32_t* rowbuf = (uint32_t*)(misc + 16);           // [2][wprmax] current / hot row (whole row)
-  uint32_t* Rrow = rowbuf + 2 * wprmax;                // [wprmax] stage 2: R of the current row
-  uint32_t* pullbuf = Rrow + (kS2 ? wprmax : 0);       // [2][rng] this CTA's pulled words (read by the cluster)
+  uint32_t* rowbuf = lp + kWLab / 32;                  // [2][wprmax] current / hot row (whole row)
+  uint32_t* Rbuf = rowbuf + 2 * wprmax;                // stage 2: [2][wprmax] R of the current / next row
+  uint32_t* pullbuf = Rbuf + (kS2 ? 2 * wprmax : 0);   // [2][rng] this CTA's pulled words (read by the cluster)
+  uint32_t* wo = pullbuf + 2 * rng;                    // [rng] per word of this CTA: ELL row (relative) << 8 | rows
+  uint32_t* cache = wo + rng;                          // this CTA's ELL rows, then its heavy columns' items
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   uint32_t* vis = kS2 ? wa.V : wa.R;
   constexpr int dir = kS2 ? 1 : 0;
@@ -127,35 +146,93 @@ __global__ void __launch_bounds__(kWThreads, 1) k_wave(WaveArgs wa) {
     const int32_t* __restrict__ aother = C.aother[dir];
     const uint8_t* __restrict__ seedA = kS2 ? C.startA : C.accA;
     const uint8_t* __restrict__ seedB = kS2 ? C.startB : C.accB;
-    if (tid == 0) {  // heavy columns inside this CTA's words
+    if (tid == 0) {  // heavy columns inside this CTA's words; cache decision
       int lo = 0, hi = D.nheavy;
       while (lo < hi) { const int m = (lo + hi) >> 1; if (__ldg(&D.heavy[m]).x < w0 * 32) lo = m + 1; else hi = m; }
-      misc[1] = lo;
+      const int hl = lo;
       hi = D.nheavy;
       while (lo < hi) { const int m = (lo + hi) >> 1; if (__ldg(&D.heavy[m]).x < w1 * 32) lo = m + 1; else hi = m; }
+      misc[1] = hl;
       misc[2] = lo;
+      const int64_t nell = (int64_t)(__ldg(&D.woff[w1]) - __ldg(&D.woff[w0])) * 32;
+      const int64_t nh = lo > hl ? (int64_t)__ldg(&D.heavy[lo - 1]).w - __ldg(&D.heavy[hl]).y : 0;
+      misc[3] = nell + nh <= (int64_t)wa.cache_words ? 1 : 0;
     }
+    if (tid <= G) misc[4 + tid] = (int)((int64_t)wpr * tid / G);
     __syncthreads();
     const int h0 = misc[1], h1 = misc[2];
-    int hot = -1, hp = 0;
+    const bool cached = misc[3] != 0;
+    const uint32_t er0 = __ldg(&D.woff[w0]);
+    const uint32_t nell = (__ldg(&D.woff[w1]) - er0) * 32u;
+    const int32_t hb0 = h1 > h0 ? __ldg(&D.heavy[h0]).y : 0;
+    for (int w = w0 + tid; w < w1; w += kWThreads) wo[w - w0] = ((__ldg(&D.woff[w]) - er0) << 8) | __ldg(&D.wmax[w]);
+    if (cached) {
+      for (uint32_t i = tid; i < nell; i += kWThreads) cache[i] = __ldg(&D.ell[(size_t)er0 * 32 + i]);
+      const int32_t nh = h1 > h0 ? __ldg(&D.heavy[h1 - 1]).w - hb0 : 0;
+      for (int32_t i = tid; i < nh; i += kWThreads) cache[nell + i] = __ldg(&D.hitems[hb0 + i]);
+    }
+    // heavy columns' items: shared memory when cached, else global (generic pointer)
+    const uint32_t* hitp = cached ? cache + nell - hb0 : D.hitems;
+    // the first row's A arcs and (stage 2) R row are loaded ahead, like every next row's
+    int r = kS2 ? 0 : VA - 1;
+    int32_t ne0 = 0, nd = 0, nkey = 0, noth = 0;
+    if (VA > 0) {
+      ne0 = __ldg(&aoff[r]);
+      nd = __ldg(&aoff[r + 1]) - ne0;
+      if (tid < nd) {
+        nkey = __ldg(&akey[ne0 + tid]);
+        noth = __ldg(&aother[ne0 + tid]);
+      }
+      if (kS2) {
+        const int64_t rw = W + (int64_t)r * wpr;
+        for (int i = tid; i < wpr; i += kWThreads) __pipeline_memcpy_async(&Rbuf[i], &wa.R[rw + i], 4);
+        __pipeline_commit();
+      }
+    }
+    int hot = -1, hp = 0, rb = 0;
     for (int step = 0; step < VA; ++step) {
-      const int r = kS2 ? step : VA - 1 - step;
+      r = kS2 ? step : VA - 1 - step;
       const int cp = hp ^ 1;
       uint32_t* cur = rowbuf + cp * wprmax;
       const uint32_t* hrow = rowbuf + hp * wprmax;
       uint32_t* pb = pullbuf + cp * rng;
+      const uint32_t* Rrow = Rbuf + rb * wprmax;
       const int64_t rowW = W + (int64_t)r * wpr;
-      const int32_t e0 = __ldg(&aoff[r]), d = __ldg(&aoff[r + 1]) - e0;
+      const int32_t d = nd;
+      const int32_t mykey = nkey, myoth = noth;
+      if (kS2) __pipeline_wait_prior(0);
       for (int i = tid; i < kWLab; i += kWThreads) lm[i] = 0ull;
-      if (kS2)
-        for (int i = tid; i < wpr; i += kWThreads) Rrow[i] = __ldcg(&wa.R[rowW + i]);
+      if (tid < kWLab / 32) lp[tid] = 0u;
       __syncthreads();
-      if (tid < d) {
-        const int li = __ldg(&akey[e0 + tid]) + 2;
-        srow[tid] = __ldg(&aother[e0 + tid]);
-        if (li <= 254) atomicOr(&lm[li], 1ull << tid);
+      // loads for the next row (used next step): its A arcs and, stage 2, its R row
+      if (step + 1 < VA) {
+        const int rn = kS2 ? r + 1 : r - 1;
+        ne0 = __ldg(&aoff[rn]);
+        nd = __ldg(&aoff[rn + 1]) - ne0;
+        if (tid < nd) {
+          nkey = __ldg(&akey[ne0 + tid]);
+          noth = __ldg(&aother[ne0 + tid]);
+        }
+        if (kS2) {
+          const int64_t rw = W + (int64_t)rn * wpr;
+          uint32_t* dstR = Rbuf + (rb ^ 1) * wprmax;
+          for (int i = tid; i < wpr; i += kWThreads) __pipeline_memcpy_async(&dstR[i], &wa.R[rw + i], 4);
+          __pipeline_commit();
+        }
       }
-      __syncthreads();
+      bool slot_hot = true;
+      if (tid < d) {
+        const int li = mykey + 2;
+        srow[tid] = myoth;
+        slot_hot = myoth == hot;
+        if (li <= 254) {
+          atomicOr(&lm[li], 1ull << tid);
+          atomicOr(&lp[li >> 5], 1u << (li & 31));
+        }
+      }
+      // uniform row: every A arc of the row leads to the hot row (a trellis) -- a move exists iff the
+      // item's label occurs in the row and the target column is set in the hot row
+      const bool uni = __syncthreads_and(slot_hot) != 0;
       const unsigned long long meps = lm[1];  // A arcs with olabel eps: M2 (B stays) and M1 eps:eps
       const bool rowseed = __ldg(&seedA[r]) != 0;
       auto test = [&](int32_t row, int32_t col) -> bool {
@@ -163,28 +240,82 @@ __global__ void __launch_bounds__(kWThreads, 1) k_wave(WaveArgs wa) {
         return (__ldcg(&vis[W + (int64_t)row * wpr + (col >> 5)]) >> (col & 31)) & 1u;
       };
       // ---- pull: one warp per word, one lane per column (light columns: items from the ELL)
-      for (int w = w0 + warp; w < w1; w += kWWarps) {
-        const int32_t col = w * 32 + lane;
-        bool in = false;
-        if (col < VB) {
-          const bool allowed = kS2 ? ((Rrow[w] >> lane) & 1u) != 0u : true;
-          if (allowed) {
-            in = rowseed && __ldg(&seedB[col]) != 0;
-            if (!in && d > 0) {
-              for (unsigned long long m = meps; m && !in; m &= m - 1ull) in = test(srow[__ffsll((long long)m) - 1], col);
-              const int jn = __ldg(&D.wmax[w]);
-              const uint32_t* __restrict__ pe = D.ell + (size_t)__ldg(&D.woff[w]) * 32 + lane;
-              for (int j = 0; j < jn && !in; ++j) {
-                const uint32_t it = __ldg(pe + j * 32);
-                const int32_t o = (int32_t)(it & 0xFFFFFFu);
-                for (unsigned long long m = lm[it >> 24]; m && !in; m &= m - 1ull)
-                  in = test(srow[__ffsll((long long)m) - 1], o);
+      auto pull = [&](const uint32_t* __restrict__ ellb) {
+        if (uni && !rowseed) {  // trellis rows: label present in the row AND target set in the hot row
+          bool full = true;     // the row has every label of the light items: no label test
+#pragma unroll
+          for (int k = 0; k < kWLab / 32; ++k) full &= (lp[k] & D.blab[k]) == D.blab[k];
+          for (int w = w0 + warp; w < w1; w += kWWarps) {
+            const uint32_t x = wo[w - w0];
+            const uint32_t* pe = ellb + (size_t)(x >> 8) * 32 + lane;
+            uint32_t in = 0u;
+            if (meps != 0ull) {  // M2 (B stays) and M1 eps:eps, all into the hot row
+              in = hrow[w] >> lane;
+              const uint32_t* ep = D.eell + (size_t)__ldg(&D.ewoff[w]) * 32 + lane;
+              for (int j = __ldg(&D.ewmax[w]); j > 0; --j, ep += 32) {
+                const uint32_t it = __ldg(ep);  // padding (label index 255) never matches
+                in |= (it < 0xFF000000u ? hrow[(it & 0xFFFFFFu) >> 5] : 0u) >> (it & 31u);
+              }
+            }
+            if (full) {
+#pragma unroll 1
+              for (int j = (int)(x & 255u); j > 0; --j, pe += 32) {
+                const uint32_t it = *pe;  // padding (label index 255) never matches
+                in |= (it < 0xFF000000u ? hrow[(it & 0xFFFFFFu) >> 5] : 0u) >> (it & 31u);
+              }
+            } else {
+#pragma unroll 1
+              for (int j = (int)(x & 255u); j > 0; --j, pe += 32) {
+                const uint32_t it = *pe;
+                const uint32_t li = it >> 24;
+                in |= (lp[li >> 5] >> (li & 31u)) & (hrow[(it & 0xFFFFFFu) >> 5] >> (it & 31u));
+              }
+            }
+            uint32_t word = __ballot_sync(0xffffffffu, (in & 1u) != 0u);
+            if (kS2) word &= Rrow[w];
+            if (lane == 0) pb[w - w0] = word;
+          }
+          return;
+        }
+        for (int w = w0 + warp; w < w1; w += kWWarps) {
+          const int32_t col = w * 32 + lane;
+          bool in = false;
+          if (col < VB) {
+            const bool allowed = kS2 ? ((Rrow[w] >> lane) & 1u) != 0u : true;
+            if (allowed) {
+              in = rowseed && __ldg(&seedB[col]) != 0;
+              if (!in && d > 0) {
+                const uint32_t x = wo[w - w0];
+                const int jn = (int)(x & 255u);
+                const uint32_t* pe = ellb + (size_t)(x >> 8) * 32 + lane;
+                for (unsigned long long m = meps; m && !in; m &= m - 1ull) in = test(srow[__ffsll((long long)m) - 1], col);
+                if (meps != 0ull) {  // M1 eps:eps
+                  const uint32_t* ep = D.eell + (size_t)__ldg(&D.ewoff[w]) * 32 + lane;
+                  for (int j = __ldg(&D.ewmax[w]); j > 0 && !in; --j, ep += 32) {
+                    const uint32_t it = __ldg(ep);
+                    if ((it >> 24) != 1u) continue;
+                    for (unsigned long long m = meps; m && !in; m &= m - 1ull)
+                      in = test(srow[__ffsll((long long)m) - 1], (int32_t)(it & 0xFFFFFFu));
+                  }
+                }
+                for (int j = 0; j < jn && !in; ++j) {
+                  const uint32_t it = pe[j * 32];
+                  const int32_t o = (int32_t)(it & 0xFFFFFFu);
+                  for (unsigned long long m = lm[it >> 24]; m && !in; m &= m - 1ull)
+                    in = test(srow[__ffsll((long long)m) - 1], o);
+                }
               }
             }
           }
+          const uint32_t word = __ballot_sync(0xffffffffu, in);
+          if (lane == 0) pb[w - w0] = word;
         }
-        const uint32_t word = __ballot_sync(0xffffffffu, in);
-        if (lane == 0) pb[w - w0] = word;
+      };
+      if (d > 0 || rowseed) {
+        if (cached) pull(cache);
+        else pull(D.ell + (size_t)er0 * 32);
+      } else {  // no A arcs and no seeds: the row is empty before the M3 pass
+        for (int w = w0 + tid; w < w1; w += kWThreads) pb[w - w0] = 0u;
       }
       // ---- heavy columns of this CTA: the whole CTA walks the column's items
       if (h1 > h0 && d > 0) {
@@ -194,16 +325,19 @@ __global__ void __launch_bounds__(kWThreads, 1) k_wave(WaveArgs wa) {
           const int32_t col = hv.x;
           const bool seeded = rowseed && __ldg(&seedB[col]) != 0;
           const bool allowed = kS2 ? bit_of(Rrow, col) != 0u : true;
-          if (seeded || !allowed) continue;  // uniform over the CTA
+          const int eb = meps ? hv.y : hv.z;
+          if (seeded || !allowed || (eb >= hv.w && !meps)) continue;  // uniform over the CTA
           bool found = false;
           if (tid < kWSlots && ((meps >> tid) & 1ull)) found = test(srow[tid], col);
-          for (int e = (meps ? hv.y : hv.z) + tid; e < hv.w && !found; e += kWThreads) {
-            const int li = __ldg(&D.key[e]) + 2;
-            if (li > 254) continue;
-            unsigned long long m = lm[li];
-            if (!m) continue;
-            const int32_t o = __ldg(&D.other[e]);
-            for (; m && !found; m &= m - 1ull) found = test(srow[__ffsll((long long)m) - 1], o);
+          for (int e = eb + tid; e < hv.w && !found; e += kWThreads) {
+            const uint32_t it = hitp[e];
+            const uint32_t li = it >> 24;
+            const int32_t o = (int32_t)(it & 0xFFFFFFu);
+            if (uni) {
+              found = ((lp[li >> 5] >> (li & 31)) & 1u) && bit_of(hrow, o);
+            } else {
+              for (unsigned long long m = lm[li]; m && !found; m &= m - 1ull) found = test(srow[__ffsll((long long)m) - 1], o);
+            }
           }
           if (__syncthreads_or(found) && tid == 0) pb[(col >> 5) - w0] |= 1u << (col & 31);
         }
@@ -211,28 +345,68 @@ __global__ void __launch_bounds__(kWThreads, 1) k_wave(WaveArgs wa) {
       // ---- publish the slices, gather the whole row
       cl.sync();
       for (int k = 0; k < G; ++k) {
-        const int kw0 = (int)((int64_t)wpr * k / G), kw1 = (int)((int64_t)wpr * (k + 1) / G);
+        const int kw0 = misc[4 + k], n = misc[5 + k] - kw0;
         const uint32_t* src = k == crank ? pb : cl.map_shared_rank(pb, k);
-        for (int i = tid; i < kw1 - kw0; i += kWThreads) cur[kw0 + i] = src[i];
+        for (int i = tid; i < n; i += kWThreads) cur[kw0 + i] = src[i];
       }
       __syncthreads();
-      // ---- M3 fixed point of the row (B's eps-input arcs; A stays)
-      if (C.neps > 0) {
+      // ---- M3 fixed point of the row (B's eps-input arcs; A stays).  Hub targets (many eps sources,
+      // kept as a bitmap) are word-parallel, the other eps arcs one thread each.  Pass order: stage 2
+      // hubs then arcs, stage 1 arcs then hubs; another pass runs only when a new bit could feed a unit
+      // already processed in this pass (the relevance masks of DESIGN.md §6c), so lexicon closures take
+      // one pass.
+      if (C.neps > 0 || C.nhub > 0) {
         for (;;) {
           int changed = 0;
-          for (int i = tid; i < C.neps; i += kWThreads) {
-            const int2 a = __ldg(&C.eps[i]);  // B arc a.x -> a.y with ilabel eps
-            if (kS2) {  // (r, a.x) in V  =>  (r, a.y) in V  if in R
-              if (bit_of(cur, a.x) && !bit_of(cur, a.y) && bit_of(Rrow, a.y)) {
-                atomicOr(&cur[a.y >> 5], 1u << (a.y & 31));
-                changed = 1;
-              }
-            } else {    // (r, a.y) in R  =>  (r, a.x) in R
-              if (bit_of(cur, a.y) && !bit_of(cur, a.x)) {
-                atomicOr(&cur[a.x >> 5], 1u << (a.x & 31));
-                changed = 1;
+          auto arcs = [&]() {
+            for (int i = tid; i < C.neps; i += kWThreads) {
+              const int2 a = __ldg(&C.eps[i]);  // B arc a.x -> a.y with ilabel eps
+              if (kS2) {  // (r, a.x) in V  =>  (r, a.y) in V  if in R
+                if (bit_of(cur, a.x) && !bit_of(cur, a.y) && bit_of(Rrow, a.y)) {
+                  atomicOr(&cur[a.y >> 5], 1u << (a.y & 31));
+                  if (bit_of(C.rel[3], a.y)) changed = 1;
+                }
+              } else {    // (r, a.y) in R  =>  (r, a.x) in R
+                if (bit_of(cur, a.y) && !bit_of(cur, a.x)) {
+                  atomicOr(&cur[a.x >> 5], 1u << (a.x & 31));
+                  if (bit_of(C.rel[0], a.x)) changed = 1;
+                }
               }
             }
+          };
+          auto hubs = [&]() {
+            for (int h = 0; h < C.nhub; ++h) {
+              __syncthreads();
+              const int32_t t = __ldg(&C.hub_col[h]);
+              const uint32_t* __restrict__ S = C.hub_src + (size_t)h * wpr;
+              if (kS2) {  // V(r, t) if some eps source of t is in V (and (r, t) in R)
+                if (bit_of(cur, t) || !bit_of(Rrow, t)) continue;  // uniform
+                int any = 0;
+                for (int i = tid; i < wpr; i += kWThreads) any |= (cur[i] & __ldg(&S[i])) != 0u;
+                if (__syncthreads_or(any) && tid == 0) {
+                  cur[t >> 5] |= 1u << (t & 31);
+                  if (bit_of(C.rel[2], t)) changed = 1;
+                }
+              } else {    // R(r, t)  =>  every eps source of t is in R
+                if (!bit_of(cur, t)) continue;  // uniform
+                const uint32_t* __restrict__ M = C.rel[1];
+                for (int i = tid; i < wpr; i += kWThreads) {
+                  const uint32_t x = cur[i], y = x | __ldg(&S[i]);
+                  if (y != x) {
+                    cur[i] = y;
+                    if ((y & ~x) & __ldg(&M[i])) changed = 1;
+                  }
+                }
+              }
+            }
+          };
+          if (kS2) {
+            hubs();
+            __syncthreads();
+            arcs();
+          } else {
+            arcs();
+            hubs();
           }
           if (!__syncthreads_or(changed)) break;
         }
@@ -240,6 +414,7 @@ __global__ void __launch_bounds__(kWThreads, 1) k_wave(WaveArgs wa) {
       for (int i = w0 + tid; i < w1; i += kWThreads) vis[rowW + i] = cur[i];
       hot = r;
       hp = cp;
+      rb ^= 1;
     }
   }
 }
@@ -250,10 +425,15 @@ __global__ void __launch_bounds__(kWThreads, 1) k_wave(WaveArgs wa) {
 // (saturated at 255: the emit recounts those) and kept[block] (exact).  One CTA per row.
 __global__ void __launch_bounds__(kCThreads) k_wave_count(WaveArgs wa) {
   __shared__ unsigned long long lm[kWLab];
+  __shared__ uint32_t lc[kWLab];  // uniform rows: popc(lm[li]) (moves per matching item)
   __shared__ int32_t srow[kWSlots];
+  __shared__ unsigned long long hsum;
+  extern __shared__ uint32_t csm[];  // [wprmax] V of the row's single destination row, [wprmax] V of the row
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr int nwarp = kCThreads / 32;
   const uint32_t* __restrict__ Vg = wa.V;
+  uint32_t* Vd = csm;
+  uint32_t* Vr = csm + wa.wprmax;
   for (int64_t t = blockIdx.x; t < wa.nrows; t += gridDim.x) {
     int lo = 0, hi = wa.ncomp - 1;
     while (lo < hi) {
@@ -266,15 +446,28 @@ __global__ void __launch_bounds__(kCThreads) k_wave_count(WaveArgs wa) {
     const int64_t W = C.W, rowW = W + (int64_t)r * wpr;
     const WaveDir D = C.bd[0];
     const int32_t e0 = __ldg(&C.aoff[0][r]), d = __ldg(&C.aoff[0][r + 1]) - e0;
-    __syncthreads();  // previous task's readers of lm / srow
+    __syncthreads();  // previous task's readers of the shared tables
     for (int i = tid; i < kWLab; i += kCThreads) lm[i] = 0ull;
+    const int32_t dr0 = d > 0 ? __ldg(&C.aother[0][e0]) : r;
     __syncthreads();
+    bool same = true;
     if (tid < d) {
       const int li = __ldg(&C.akey[0][e0 + tid]) + 2;
-      srow[tid] = __ldg(&C.aother[0][e0 + tid]);
+      const int32_t o = __ldg(&C.aother[0][e0 + tid]);
+      srow[tid] = o;
+      same = o == dr0;
       if (li <= 254) atomicOr(&lm[li], 1ull << tid);
     }
-    __syncthreads();
+    // uniform row: every A arc leads to the same row dr0; its V row and this row's are staged
+    const bool uni = __syncthreads_and(same) != 0;
+    if (uni) {
+      for (int i = tid; i < kWLab; i += kCThreads) lc[i] = (uint32_t)__popcll(lm[i]);
+      for (int i = tid; i < wpr; i += kCThreads) {
+        Vd[i] = __ldg(&Vg[W + (int64_t)dr0 * wpr + i]);
+        Vr[i] = __ldg(&Vg[rowW + i]);
+      }
+      __syncthreads();
+    }
     const unsigned long long meps = lm[1];
     auto inV = [&](int32_t row, int32_t col) -> int {
       return (int)((__ldg(&Vg[W + (int64_t)row * wpr + (col >> 5)]) >> (col & 31)) & 1u);
@@ -291,15 +484,36 @@ __global__ void __launch_bounds__(kCThreads) k_wave_count(WaveArgs wa) {
         const int32_t col = w * 32 + lane;
         if ((vw >> lane) & 1u) {
           int cnt = 0;
-          for (unsigned long long m = meps; m; m &= m - 1ull) cnt += inV(srow[__ffsll((long long)m) - 1], col);
-          const int jn = __ldg(&D.wmax[w]);
+          const int jn = __ldg(&D.wmax[w]), ejn = __ldg(&D.ewmax[w]);
           const uint32_t* __restrict__ pe = D.ell + (size_t)__ldg(&D.woff[w]) * 32 + lane;
-          for (int j = 0; j < jn; ++j) {
-            const uint32_t it = __ldg(pe + j * 32);
-            const uint32_t li = it >> 24;
-            const int32_t o = (int32_t)(it & 0xFFFFFFu);
-            for (unsigned long long m = lm[li]; m; m &= m - 1ull) cnt += inV(srow[__ffsll((long long)m) - 1], o);
-            if (li == 1u) cnt += inV(r, o);  // M3
+          const uint32_t* __restrict__ ep = D.eell + (size_t)__ldg(&D.ewoff[w]) * 32 + lane;
+          if (uni) {
+            const int ne = (int)__popcll(meps);
+            cnt = ne * (int)bit_of(Vd, col);  // M2
+            for (int j = 0; j < ejn; ++j) {   // eps items: M1 eps:eps into the destination row, M3 into this row
+              const uint32_t it = __ldg(ep + j * 32);
+              if ((it >> 24) != 1u) continue;
+              const int32_t o = (int32_t)(it & 0xFFFFFFu);
+              cnt += ne * (int)bit_of(Vd, o) + (int)bit_of(Vr, o);
+            }
+            for (int j = 0; j < jn; ++j) {
+              const uint32_t it = __ldg(pe + j * 32);
+              cnt += (int)(lc[it >> 24] * bit_of(Vd, (int32_t)(it & 0xFFFFFFu)));
+            }
+          } else {
+            for (unsigned long long m = meps; m; m &= m - 1ull) cnt += inV(srow[__ffsll((long long)m) - 1], col);
+            for (int j = 0; j < ejn; ++j) {
+              const uint32_t it = __ldg(ep + j * 32);
+              if ((it >> 24) != 1u) continue;
+              const int32_t o = (int32_t)(it & 0xFFFFFFu);
+              for (unsigned long long m = meps; m; m &= m - 1ull) cnt += inV(srow[__ffsll((long long)m) - 1], o);
+              cnt += inV(r, o);  // M3
+            }
+            for (int j = 0; j < jn; ++j) {
+              const uint32_t it = __ldg(pe + j * 32);
+              const int32_t o = (int32_t)(it & 0xFFFFFFu);
+              for (unsigned long long m = lm[it >> 24]; m; m &= m - 1ull) cnt += inV(srow[__ffsll((long long)m) - 1], o);
+            }
           }
           wa.cnt8[(rowW + w) * 32 + lane] = (uint8_t)min(cnt, 255);
           tot += (unsigned long long)cnt;
@@ -317,14 +531,13 @@ __global__ void __launch_bounds__(kCThreads) k_wave_count(WaveArgs wa) {
         unsigned long long cnt = 0;
         if (tid < kWSlots && ((meps >> tid) & 1ull)) cnt += inV(srow[tid], col);
         for (int e = hv.y + tid; e < hv.w; e += kCThreads) {
-          const int li = __ldg(&D.key[e]) + 2;
-          if (li > 254) continue;
-          const int32_t o = __ldg(&D.other[e]);
+          const uint32_t it = __ldg(&D.hitems[e]);
+          const int li = (int)(it >> 24);
+          const int32_t o = (int32_t)(it & 0xFFFFFFu);
           for (unsigned long long m = lm[li]; m; m &= m - 1ull) cnt += inV(srow[__ffsll((long long)m) - 1], o);
           if (li == 1) cnt += inV(r, o);
         }
         cnt = warp_sum(cnt);
-        __shared__ unsigned long long hsum;
         if (tid == 0) hsum = 0ull;
         __syncthreads();
         if (lane == 0 && cnt) atomicAdd(&hsum, cnt);
@@ -402,62 +615,133 @@ fst_status ensure_wave_ell(fst* B, cudaStream_t s) {
       FSTC_CUDA_TRY(cudaMemcpyAsync(other.data(), v.other, sizeof(int32_t) * E, cudaMemcpyDeviceToHost, s));
     }
     FSTC_CUDA_TRY(cudaStreamSynchronize(s));
-    std::vector<uint32_t> woff(wpr + 1, 0), hmask(wpr, 0);
-    std::vector<uint8_t> wmax(std::max(wpr, 1), 0);
+    // light columns: non-eps items (label index >= 2) in `ell`, eps items in `eell` (needed only when an A
+    // row has eps-output arcs: M1 eps:eps; M3 goes through the eps arc list / hubs)
+    std::vector<uint32_t> woff(wpr + 1, 0), ewoff(wpr + 1, 0), hmask(wpr, 0), blab(8, 0u);
+    std::vector<uint8_t> wmax(std::max(wpr, 1), 0), ewmax(std::max(wpr, 1), 0);
     std::vector<int4> heavy;
+    std::vector<uint32_t> hitems;
     std::vector<int2> eps;
+    std::vector<uint32_t> rel;
     for (int w = 0; w < wpr; ++w) {
-      int m = 0;
+      int m = 0, me = 0;
       for (int l = 0; l < 32; ++l) {
         const int32_t b = w * 32 + l;
         if (b >= V) break;
         const int deg = off[b + 1] - off[b];
         if (deg > kWHeavy) {
-          int32_t ne = off[b];
-          while (ne < off[b + 1] && key[ne] < 0) ++ne;
-          heavy.push_back(make_int4(b, off[b], ne, off[b + 1]));
+          const int32_t h0 = (int32_t)hitems.size();
+          int32_t ne = h0;
+          for (int32_t e = off[b]; e < off[b + 1]; ++e) {
+            hitems.push_back(((uint32_t)(key[e] + 2) << 24) | (uint32_t)other[e]);
+            if (key[e] < 0) ++ne;
+          }
+          heavy.push_back(make_int4(b, h0, ne, (int32_t)hitems.size()));
           hmask[w] |= 1u << l;
         } else {
-          m = std::max(m, deg);
+          int ne = 0;
+          for (int32_t e = off[b]; e < off[b + 1]; ++e) ne += key[e] < 0;
+          m = std::max(m, deg - ne);
+          me = std::max(me, ne);
         }
       }
       wmax[w] = (uint8_t)m;
+      ewmax[w] = (uint8_t)me;
       woff[w + 1] = woff[w] + (uint32_t)m;
+      ewoff[w + 1] = ewoff[w] + (uint32_t)me;
     }
-    std::vector<uint32_t> ell((size_t)woff[wpr] * 32 + 32, 0xFF000000u);
+    std::vector<uint32_t> ell((size_t)woff[wpr] * 32 + 32, 0xFF000000u), eell((size_t)ewoff[wpr] * 32 + 32, 0xFF000000u);
     for (int w = 0; w < wpr; ++w)
       for (int l = 0; l < 32; ++l) {
         const int32_t b = w * 32 + l;
         if (b >= V || ((hmask[w] >> l) & 1u)) continue;
-        for (int32_t e = off[b]; e < off[b + 1]; ++e)
-          ell[((size_t)woff[w] + (e - off[b])) * 32 + l] = ((uint32_t)(key[e] + 2) << 24) | (uint32_t)other[e];
+        int j = 0, je = 0;
+        for (int32_t e = off[b]; e < off[b + 1]; ++e) {
+          const uint32_t li = (uint32_t)(key[e] + 2);
+          const uint32_t it = (li << 24) | (uint32_t)other[e];
+          if (key[e] < 0) {
+            eell[((size_t)ewoff[w] + je++) * 32 + l] = it;
+          } else {
+            ell[((size_t)woff[w] + j++) * 32 + l] = it;
+            blab[li >> 5] |= 1u << (li & 31);
+          }
+        }
       }
-    if (dir == 0)
+    for (int k = 0; k < 8; ++k) T.blab[k] = blab[k];
+    std::vector<int32_t> hub_col;
+    std::vector<uint32_t> hub_src;
+    if (dir == 0) {
+      std::vector<int32_t> nin(V, 0), hub_of(V, -1);
       for (int32_t b = 0; b < V; ++b)
-        for (int32_t e = off[b]; e < off[b + 1] && key[e] < 0; ++e) eps.push_back(make_int2(b, other[e]));
+        for (int32_t e = off[b]; e < off[b + 1] && key[e] < 0; ++e) ++nin[other[e]];
+      for (int32_t t = 0; t < V && (int)hub_col.size() < kEpsHubMax; ++t)
+        if (nin[t] >= kEpsHub) {
+          hub_of[t] = (int32_t)hub_col.size();
+          hub_col.push_back(t);
+        }
+      hub_src.assign(hub_col.size() * (size_t)wpr, 0u);
+      for (int32_t b = 0; b < V; ++b)
+        for (int32_t e = off[b]; e < off[b + 1] && key[e] < 0; ++e) {
+          const int32_t t = other[e];
+          if (hub_of[t] >= 0) hub_src[(size_t)hub_of[t] * wpr + (b >> 5)] |= 1u << (b & 31);
+          else eps.push_back(make_int2(b, t));
+        }
+      rel.assign(4 * (size_t)wpr, 0u);
+      auto setb = [&](int k, int32_t c) { rel[(size_t)k * wpr + (c >> 5)] |= 1u << (c & 31); };
+      for (const int2& a : eps) {
+        setb(0, a.y);
+        setb(1, a.y);
+        setb(3, a.x);
+      }
+      for (int32_t t : hub_col) setb(1, t);
+      for (size_t i = 0; i < hub_src.size(); ++i) {
+        rel[2 * (size_t)wpr + i % wpr] |= hub_src[i];
+        rel[3 * (size_t)wpr + i % wpr] |= hub_src[i];
+      }
+    }
     size_t o = 0;
     auto take = [&](size_t bytes) { size_t r = o; o += (bytes + 255) & ~size_t(255); return r; };
+    const size_t o_eell = take(4 * eell.size()), o_ewoff = take(4 * ewoff.size()), o_ewmax = take(ewmax.size());
     const size_t o_ell = take(4 * ell.size()), o_woff = take(4 * woff.size()), o_wmax = take(wmax.size()),
                  o_hm = take(4 * std::max<size_t>(hmask.size(), 1)), o_h = take(16 * std::max<size_t>(heavy.size(), 1)),
-                 o_e = take(8 * std::max<size_t>(eps.size(), 1));
+                 o_e = take(8 * std::max<size_t>(eps.size(), 1)), o_hc = take(4 * std::max<size_t>(hub_col.size(), 1)),
+                 o_hs = take(4 * std::max<size_t>(hub_src.size(), 1)), o_hi = take(4 * std::max<size_t>(hitems.size(), 1)),
+                 o_rel = take(4 * std::max<size_t>(rel.size(), 1));
     BufferPtr buf;
     fst_status st = alloc_buffer(o, s, &buf);
     if (st) return st;
     char* base = (char*)buf->ptr;
+    T.eell = (uint32_t*)(base + o_eell);
+    T.ewoff = (uint32_t*)(base + o_ewoff);
+    T.ewmax = (uint8_t*)(base + o_ewmax);
     T.ell = (uint32_t*)(base + o_ell);
     T.woff = (uint32_t*)(base + o_woff);
     T.wmax = (uint8_t*)(base + o_wmax);
     T.hmask = (uint32_t*)(base + o_hm);
     T.heavy = (int4*)(base + o_h);
     T.eps = (int2*)(base + o_e);
+    T.hub_col = (int32_t*)(base + o_hc);
+    T.hub_src = (uint32_t*)(base + o_hs);
+    T.nhub = (int32_t)hub_col.size();
+    T.hitems = (uint32_t*)(base + o_hi);
+    T.rel = (uint32_t*)(base + o_rel);
     T.nheavy = (int32_t)heavy.size();
     T.neps = (int32_t)eps.size();
     FSTC_CUDA_TRY(cudaMemcpyAsync(T.ell, ell.data(), 4 * ell.size(), cudaMemcpyHostToDevice, s));
+    FSTC_CUDA_TRY(cudaMemcpyAsync(T.eell, eell.data(), 4 * eell.size(), cudaMemcpyHostToDevice, s));
+    FSTC_CUDA_TRY(cudaMemcpyAsync(T.ewoff, ewoff.data(), 4 * ewoff.size(), cudaMemcpyHostToDevice, s));
+    FSTC_CUDA_TRY(cudaMemcpyAsync(T.ewmax, ewmax.data(), ewmax.size(), cudaMemcpyHostToDevice, s));
     FSTC_CUDA_TRY(cudaMemcpyAsync(T.woff, woff.data(), 4 * woff.size(), cudaMemcpyHostToDevice, s));
     FSTC_CUDA_TRY(cudaMemcpyAsync(T.wmax, wmax.data(), wmax.size(), cudaMemcpyHostToDevice, s));
     if (!hmask.empty()) FSTC_CUDA_TRY(cudaMemcpyAsync(T.hmask, hmask.data(), 4 * hmask.size(), cudaMemcpyHostToDevice, s));
     if (!heavy.empty()) FSTC_CUDA_TRY(cudaMemcpyAsync(T.heavy, heavy.data(), 16 * heavy.size(), cudaMemcpyHostToDevice, s));
     if (!eps.empty()) FSTC_CUDA_TRY(cudaMemcpyAsync(T.eps, eps.data(), 8 * eps.size(), cudaMemcpyHostToDevice, s));
+    if (!hitems.empty()) FSTC_CUDA_TRY(cudaMemcpyAsync(T.hitems, hitems.data(), 4 * hitems.size(), cudaMemcpyHostToDevice, s));
+    if (!rel.empty()) FSTC_CUDA_TRY(cudaMemcpyAsync(T.rel, rel.data(), 4 * rel.size(), cudaMemcpyHostToDevice, s));
+    if (!hub_col.empty()) {
+      FSTC_CUDA_TRY(cudaMemcpyAsync(T.hub_col, hub_col.data(), 4 * hub_col.size(), cudaMemcpyHostToDevice, s));
+      FSTC_CUDA_TRY(cudaMemcpyAsync(T.hub_src, hub_src.data(), 4 * hub_src.size(), cudaMemcpyHostToDevice, s));
+    }
     FSTC_CUDA_TRY(cudaStreamSynchronize(s));
     T.buf = buf;
     T.ok = true;
@@ -465,9 +749,12 @@ fst_status ensure_wave_ell(fst* B, cudaStream_t s) {
   return FST_OK;
 }
 
+constexpr size_t kWSmem = 227 * 1024;  // dynamic shared memory of a stage CTA (one CTA per SM)
+
+// shared memory of a stage CTA without the ELL cache (the cache takes the rest of kWSmem)
 size_t wave_smem(int wprmax, int G, bool s2) {
   const int rng = (wprmax + G - 1) / G;
-  return 8 * kWLab + 4 * kWSlots + 4 * 16 + 4 * (size_t)(2 * wprmax + (s2 ? wprmax : 0) + 2 * rng);
+  return 8 * kWLab + 4 * kWSlots + 4 * 32 + 4 * (kWLab / 32) + 4 * (size_t)(2 * wprmax + (s2 ? 2 * wprmax : 0) + 3 * rng);
 }
 
 template <bool kS2>
@@ -519,6 +806,7 @@ struct WavePlan::Impl {
   WaveArgs wa{};
   int G1 = 1, G2 = 1, nc1 = 0, nc2 = 0;
   size_t smem1 = 0, smem2 = 0;
+  uint32_t cw1 = 0, cw2 = 0;
 };
 
 WavePlan::WavePlan() : impl(new Impl) {}
@@ -552,25 +840,41 @@ fst_status wave_plan(int32_t n, const fst_handle* a, const fst_handle* b, const 
   // cluster size: the largest G in {8, 4, 2, 1} that keeps every composition on its own cluster
   // (all run concurrently) with >= 64 words per CTA; else G = 1
   static bool attr_done = false;
-  size_t smem_max = wave_smem(wprmax, 1, true);
-  if (smem_max > (size_t)227 * 1024) return FST_OK;  // rows too wide for the staged row copies
+  if (wave_smem(wprmax, 1, true) + 1024 > kWSmem) return FST_OK;  // rows too wide for the staged row copies
   if (!attr_done) {
-    FSTC_CUDA_TRY(cudaFuncSetAttribute(k_wave<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-    FSTC_CUDA_TRY(cudaFuncSetAttribute(k_wave<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    FSTC_CUDA_TRY(cudaFuncSetAttribute(k_wave<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kWSmem));
+    FSTC_CUDA_TRY(cudaFuncSetAttribute(k_wave<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kWSmem));
     attr_done = true;
   }
   WavePlan::Impl& P = *plan->impl;
+  // cluster size: LPT makespan (in rows, compositions taken longest first by the next free cluster)
+  // times the per-row cost of a G-CTA cluster (its words per CTA + a fixed per-row overhead)
+  std::vector<int32_t> rows_desc(n);
+  for (int i = 0; i < n; ++i) rows_desc[i] = a[i]->V;
+  std::sort(rows_desc.begin(), rows_desc.end(), std::greater<int32_t>());
   P.G1 = P.G2 = 1;
-  for (int G : {8, 4, 2}) {
-    if (wprmax < 64 * G) continue;
-    const int c = max_clusters<true>(G, wave_smem(wprmax, G, true));
-    if (c >= n) {
+  double best = -1.0;
+  for (int G : {8, 4, 2, 1}) {
+    if (G > 1 && wprmax < 32 * G) continue;
+    const int c = max_clusters<true>(G, kWSmem);
+    if (c <= 0) continue;
+    std::vector<int64_t> load(std::min(c, n), 0);
+    for (int32_t rws : rows_desc) *std::min_element(load.begin(), load.end()) += rws;
+    // per-row cost: words per CTA + a cluster overhead growing with G (barrier, DSMEM gather); fitted to
+    // configs[4] (G = 1 / 2 / 4 / 8: 30 / 14 / 10 / 11 us per row step)
+    const double cost = (double)*std::max_element(load.begin(), load.end()) * ((double)wprmax / G + 128.0 * G);
+    if (best < 0 || cost < best) {
+      best = cost;
       P.G1 = P.G2 = G;
-      break;
     }
   }
-  P.smem1 = wave_smem(wprmax, P.G1, false);
-  P.smem2 = wave_smem(wprmax, P.G2, true);
+  if (const char* e = getenv("FSTC_WAVE_G")) {  // A/B: a fixed cluster size
+    const int g = atoi(e);
+    if (g == 1 || g == 2 || g == 4 || g == 8) P.G1 = P.G2 = g;
+  }
+  P.smem1 = P.smem2 = kWSmem;
+  P.cw1 = (uint32_t)((kWSmem - wave_smem(wprmax, P.G1, false)) / 4);
+  P.cw2 = (uint32_t)((kWSmem - wave_smem(wprmax, P.G2, true)) / 4);
   P.nc1 = max_clusters<false>(P.G1, P.smem1);
   P.nc2 = max_clusters<true>(P.G2, P.smem2);
   if (P.nc1 <= 0 || P.nc2 <= 0) return FST_OK;
@@ -600,7 +904,9 @@ fst_status wave_plan(int32_t n, const fst_handle* a, const fst_handle* b, const 
       C.aother[d] = av.other;
       const View& bv = B->views[d == 0 ? kOutByIlabel : kInByIlabel];
       const fst::WaveEll& T = B->wave_ell[d];
-      C.bd[d] = WaveDir{T.ell, T.woff, T.wmax, T.hmask, T.heavy, T.nheavy, bv.key, bv.other};
+      C.bd[d] = WaveDir{T.ell, T.woff, T.wmax, T.eell, T.ewoff, T.ewmax, T.hmask, T.heavy, T.nheavy, T.hitems, {}};
+      for (int k = 0; k < 8; ++k) C.bd[d].blab[k] = T.blab[k];
+      (void)bv;
     }
     C.startA = A->is_start;
     C.accA = A->is_accept;
@@ -608,6 +914,10 @@ fst_status wave_plan(int32_t n, const fst_handle* a, const fst_handle* b, const 
     C.accB = B->is_accept;
     C.eps = B->wave_ell[0].eps;
     C.neps = B->wave_ell[0].neps;
+    C.nhub = B->wave_ell[0].nhub;
+    C.hub_col = B->wave_ell[0].hub_col;
+    C.hub_src = B->wave_ell[0].hub_src;
+    for (int k = 0; k < 4; ++k) C.rel[k] = B->wave_ell[0].rel + (size_t)k * C.wpr;
     order[i] = i;
   }
   std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return comps[x].VA > comps[y].VA; });
@@ -637,6 +947,11 @@ fst_status wave_stage(const WavePlan& plan, int stage, uint32_t* R, uint32_t* V,
   P.wa.R = R;
   P.wa.V = V;
   FSTC_CUDA_TRY(cudaMemsetAsync(P.wa.next, 0, 4, s));
+  static const bool nocache = [] {  // FSTC_WAVE_CACHE=0: items from global memory (tests / A-B)
+    const char* e = getenv("FSTC_WAVE_CACHE");
+    return e && e[0] == '0';
+  }();
+  P.wa.cache_words = nocache ? 0u : (stage == 1 ? P.cw1 : P.cw2);
   return stage == 1 ? launch_wave<false>(P.wa, P.G1, P.nc1, P.smem1, s) : launch_wave<true>(P.wa, P.G2, P.nc2, P.smem2, s);
 }
 
@@ -646,7 +961,13 @@ fst_status wave_count(const WavePlan& plan, uint32_t* V, uint8_t* cnt8, unsigned
   P.wa.cnt8 = cnt8;
   P.wa.kept = kept;
   const int64_t grid = std::min<int64_t>(std::max<int64_t>(P.wa.nrows, 1), (int64_t)sm_count() * 4);
-  k_wave_count<<<(unsigned)grid, kCThreads, 0, s>>>(P.wa);
+  const size_t smem = 8ull * P.wa.wprmax;
+  static size_t smem_set = 0;
+  if (smem > 48 * 1024 && smem > smem_set) {
+    FSTC_CUDA_TRY(cudaFuncSetAttribute(k_wave_count, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    smem_set = smem;
+  }
+  k_wave_count<<<(unsigned)grid, kCThreads, smem, s>>>(P.wa);
   FSTC_LAUNCH_CHECK();
   return FST_OK;
 }
