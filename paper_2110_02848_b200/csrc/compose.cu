@@ -2779,9 +2779,19 @@ fst_status compose_impl(int32_t n, const fst_handle* a, const fst_handle* b, cud
   // ---- emit
   {
     EventTimer te(prof, s);
-    if (tp.ok) launch_tile_emit(tp.emit, tp.grid_emit, tp.smem_emit, s, cx, comps[0], d_tot, tp.vr_rows);
-    else k_emit<<<g_grid, kThreads, kDynSmem, s>>>(cx, d_tot);
-    FSTC_LAUNCH_CHECK();
+    if (tp.ok) {
+      launch_tile_emit(tp.emit, tp.grid_emit, tp.smem_emit, s, cx, comps[0], d_tot, tp.vr_rows);
+      FSTC_LAUNCH_CHECK();
+    } else if (wp.ok && !want_prov) {
+      st = wave_emit(wp, d_comps, d_tot, cx.idbase, cx.arcbase, cx.wpre, cx.V, (int32_t*)(cx.misc + 2), s);
+      if (st) {
+        cleanup();
+        return st;
+      }
+    } else {
+      k_emit<<<g_grid, kThreads, kDynSmem, s>>>(cx, d_tot);
+      FSTC_LAUNCH_CHECK();
+    }
     stats.ms_emit = te.stop();
     k_finish_rowptr<<<nblk(n, 128), 128, 0, s>>>(cx, d_tot);
     FSTC_LAUNCH_CHECK();

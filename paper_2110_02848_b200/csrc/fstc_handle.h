@@ -119,6 +119,10 @@ struct fst {
     uint32_t* ewoff = nullptr;
     uint8_t* ewmax = nullptr;
     uint32_t blab[8] = {};     // label indices (label + 2) of the light non-eps items
+    int2* ellcw = nullptr;     // [0] only: (olabel, weight bits) parallel to ell / eell / hitems (the emit)
+    int2* eellcw = nullptr;
+    int2* hcw = nullptr;
+    uint32_t* hbefore = nullptr;  // [wpr + 1] heavy columns before each word
     uint32_t* hmask = nullptr; // [wpr] lanes of heavy columns
     int4* heavy = nullptr;     // (col, first item, first non-eps item, end) of heavy columns, by col
     int32_t nheavy = 0;

@@ -69,11 +69,18 @@ struct WaveDir {  // B role, one direction (view by ilabel)
   int32_t nheavy;
   const uint32_t* hitems; // items of the heavy columns, packed like the ELL (heavy[h].y/.z/.w index them)
   uint32_t blab[8];       // label indices of the light non-eps items
+  // [0] (out-view) only, for the emit: (B olabel, weight bits) parallel to ell / eell / hitems, and the
+  // heavy columns before each word (heavy index of a column = hbefore[w] + popc(hmask[w] below it))
+  const int2* ellcw;
+  const int2* eellcw;
+  const int2* hcw;
+  const uint32_t* hbefore;
 };
 
 struct WaveComp {
   int64_t W, K;      // first word / block of the composition's pair space
   int64_t rowbase;   // first global row (count tasks)
+  int64_t hcnt_base; // first entry of the composition's exact heavy-state counts ([row][heavy])
   int32_t VA, VB, wpr, bpr;
   const int32_t* aoff[2];   // A role: [0] out-by-olabel (key = olabel, other = dst), [1] in-by-olabel (other = src)
   const int32_t* akey[2];
@@ -106,6 +113,12 @@ struct WaveArgs {
   int32_t* next;         // composition counter of the stage kernels
   uint32_t cache_words;  // shared-memory words for the ELL cache of a stage CTA
   int64_t nrows;         // rows of all compositions (count tasks)
+  int32_t* hcnt;         // exact kept-move counts of heavy states (the emit's arc offsets)
+  // emit inputs (numbering of compose.cu: per-block id / arc bases, per-word popcount prefixes)
+  const int64_t* idbase;
+  const int64_t* arcbase;
+  const uint16_t* wpre;
+  int32_t* err;          // emit: heavy-state queue overflow (reported as an internal error)
 };
 
 __device__ __forceinline__ uint32_t bit_of(const uint32_t* row, int32_t col) { return (row[col >> 5] >> (col & 31)) & 1u; }
@@ -544,11 +557,242 @@ __global__ void __launch_bounds__(kCThreads) k_wave_count(WaveArgs wa) {
         __syncthreads();
         if (tid == 0) {
           wa.cnt8[(rowW + (col >> 5)) * 32 + (col & 31)] = (uint8_t)min(hsum, 255ull);
+          wa.hcnt[C.hcnt_base + (int64_t)r * D.nheavy + h] = (int32_t)hsum;
           atomicAdd(&wa.kept[C.K + (int64_t)r * bpr + (col >> 10)], hsum);
         }
         __syncthreads();
       }
     }
+  }
+}
+
+// ------------------------------------------------------------------------------ pass 2: emit
+// Writes the composed CSR of every state of C: one CTA per row, one warp per 1024-pair
+// block at a time, one lane per column.  A state's arcs are its moves in the general emit's order (M2 in
+// A-slot order, then per B item in view order: M1 in slot order, M3 for an eps item), at consecutive
+// slots from the block's arc base (exclusive scans: deterministic, no cursor atomics), so the arrays
+// equal the level path's.  Rank of a pair = the block's id base + the word's popcount prefix + the
+// popcount below it; the row itself and (uniform rows) its single destination row are staged as (V word,
+// rank) pairs.  Heavy states (> kWHeavy B arcs) take their exact count from k_wave_count and are written
+// by the whole CTA.
+constexpr int kEmThreads = 512;
+constexpr int kEmHeavyQ = 256;
+__global__ void __launch_bounds__(kEmThreads) k_wave_emit(WaveArgs wa, const CompDev* __restrict__ cd,
+                                                          const int64_t* __restrict__ tot) {
+  __shared__ unsigned long long lm[kWLab];
+  __shared__ uint32_t lc[kWLab];
+  __shared__ int32_t srow[kWSlots], scar[kWSlots];
+  __shared__ float sw[kWSlots];
+  __shared__ int32_t hq_n, red[kEmThreads / 32 + 1];
+  __shared__ int32_t hq_col[kEmHeavyQ], hq_h[kEmHeavyQ];
+  __shared__ long long hq_pos[kEmHeavyQ], hq_id[kEmHeavyQ];
+  extern __shared__ int2 esm[];  // [wprmax] own row, [wprmax] destination row: (V word, rank of its first pair)
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int nwarp = kEmThreads / 32;
+  const uint32_t* __restrict__ Vg = wa.V;
+  int2* Vr = esm;
+  int2* Vd = esm + wa.wprmax;
+  for (int64_t t = blockIdx.x; t < wa.nrows; t += gridDim.x) {
+    int ci = 0, hi = wa.ncomp - 1;
+    while (ci < hi) {
+      const int mid = (ci + hi + 1) >> 1;
+      if (wa.comps[mid].rowbase <= t) ci = mid; else hi = mid - 1;
+    }
+    const WaveComp& C = wa.comps[ci];
+    const CompDev& O = cd[ci];
+    const int32_t r = (int32_t)(t - C.rowbase);
+    const int wpr = C.wpr, bpr = C.bpr;
+    const int64_t W = C.W, K = C.K, rowW = W + (int64_t)r * wpr;
+    const int64_t id_comp = tot[2 * ci], arc_comp = tot[2 * ci + 1];
+    if (__ldg(&wa.idbase[K + (int64_t)r * bpr + bpr]) == __ldg(&wa.idbase[K + (int64_t)r * bpr])) continue;  // no states
+    const WaveDir& D = C.bd[0];
+    const int32_t e0 = __ldg(&C.aoff[0][r]), d = __ldg(&C.aoff[0][r + 1]) - e0;
+    const int32_t dr0 = d > 0 ? __ldg(&C.aother[0][e0]) : r;
+    __syncthreads();  // previous task's readers of the shared tables
+    for (int i = tid; i < kWLab; i += kEmThreads) lm[i] = 0ull;
+    if (tid == 0) hq_n = 0;
+    __syncthreads();
+    bool same = true;
+    if (tid < d) {
+      const int li = __ldg(&C.akey[0][e0 + tid]) + 2;
+      const int32_t o = __ldg(&C.aother[0][e0 + tid]);
+      srow[tid] = o;
+      scar[tid] = __ldg(&O.Af.carry[e0 + tid]);
+      sw[tid] = __ldg(&O.Af.w[e0 + tid]);
+      same = o == dr0;
+      if (li <= 254) atomicOr(&lm[li], 1ull << tid);
+    }
+    const bool uni = __syncthreads_and(same) != 0 && dr0 != r;
+    for (int i = tid; i < kWLab; i += kEmThreads) lc[i] = (uint32_t)__popcll(lm[i]);
+    for (int i = tid; i < wpr; i += kEmThreads) {
+      const int64_t bk = K + (int64_t)r * bpr + (i >> 5);
+      Vr[i] = make_int2((int32_t)__ldg(&Vg[rowW + i]), (int32_t)(__ldg(&wa.idbase[bk]) - id_comp + __ldg(&wa.wpre[rowW + i])));
+      if (uni) {
+        const int64_t dW = W + (int64_t)dr0 * wpr;
+        const int64_t dk = K + (int64_t)dr0 * bpr + (i >> 5);
+        Vd[i] = make_int2((int32_t)__ldg(&Vg[dW + i]), (int32_t)(__ldg(&wa.idbase[dk]) - id_comp + __ldg(&wa.wpre[dW + i])));
+      }
+    }
+    __syncthreads();
+    const unsigned long long meps = lm[1];
+    const uint8_t stA = __ldg(&C.startA[r]), acA = __ldg(&C.accA[r]);
+    // (present, rank) of pair (row, col)
+    auto look = [&](int32_t row, int32_t col, int32_t& rank) -> bool {
+      const uint32_t lowm = (1u << (col & 31)) - 1u;
+      if (row == r || (uni && row == dr0)) {
+        const int2 v = (row == r ? Vr : Vd)[col >> 5];
+        rank = v.y + __popc((uint32_t)v.x & lowm);
+        return ((uint32_t)v.x >> (col & 31)) & 1u;
+      }
+      const int64_t gw = W + (int64_t)row * wpr + (col >> 5);
+      const uint32_t v = __ldg(&Vg[gw]);
+      if (!((v >> (col & 31)) & 1u)) return false;
+      rank = (int32_t)(__ldg(&wa.idbase[K + (int64_t)row * bpr + (col >> 10)]) - id_comp + __ldg(&wa.wpre[gw]) + __popc(v & lowm));
+      return true;
+    };
+    auto put = [&](int64_t pos, int32_t dst, int32_t il, int32_t ol, float w) {
+      __stcs(&O.dst[pos], dst);
+      __stcs(&O.ilabel[pos], il);
+      __stcs(&O.olabel[pos], ol);
+      __stcs(&O.weight[pos], w);
+    };
+    for (int blk = warp; blk < bpr; blk += nwarp) {
+      int64_t arc = __ldg(&wa.arcbase[K + (int64_t)r * bpr + blk]) - arc_comp;
+      const int wb = blk * 32, nw = min(32, wpr - wb);
+      for (int i = 0; i < nw; ++i) {
+        const int w = wb + i;
+        const int2 vv = Vr[w];
+        const uint32_t vw = (uint32_t)vv.x;
+        if (!vw) continue;
+        const int32_t col = w * 32 + lane;
+        const bool has = (vw >> lane) & 1u;
+        const uint32_t hm = __ldg(&D.hmask[w]);
+        const bool heavy = (hm >> lane) & 1u;
+        const uint32_t* __restrict__ pe = D.ell + (size_t)__ldg(&D.woff[w]) * 32 + lane;
+        const uint32_t* __restrict__ ep = D.eell + (size_t)__ldg(&D.ewoff[w]) * 32 + lane;
+        const int jn = __ldg(&D.wmax[w]), ejn = __ldg(&D.ewmax[w]);
+        int cnt = 0, hidx = 0, rk;
+        if (has) {
+          if (heavy) {
+            hidx = (int)__ldg(&D.hbefore[w]) + __popc(hm & ((1u << lane) - 1u));
+            cnt = __ldg(&wa.hcnt[C.hcnt_base + (int64_t)r * D.nheavy + hidx]);
+          } else {
+            for (unsigned long long m = meps; m; m &= m - 1ull) cnt += look(srow[__ffsll((long long)m) - 1], col, rk);
+            for (int j = 0; j < ejn; ++j) {
+              const uint32_t it = __ldg(ep + j * 32);
+              if ((it >> 24) != 1u) continue;
+              const int32_t o = (int32_t)(it & 0xFFFFFFu);
+              for (unsigned long long m = meps; m; m &= m - 1ull) cnt += look(srow[__ffsll((long long)m) - 1], o, rk);
+              cnt += look(r, o, rk);
+            }
+            for (int j = 0; j < jn; ++j) {
+              const uint32_t it = __ldg(pe + j * 32);
+              const int32_t o = (int32_t)(it & 0xFFFFFFu);
+              if (uni) {
+                cnt += (int)lc[it >> 24] * (int)look(dr0, o, rk);
+              } else {
+                for (unsigned long long m = lm[it >> 24]; m; m &= m - 1ull) cnt += look(srow[__ffsll((long long)m) - 1], o, rk);
+              }
+            }
+          }
+        }
+        const int inc = warp_incl_scan(cnt);
+        const int wtot = __shfl_sync(0xffffffffu, inc, 31);
+        if (has) {
+          int64_t pos = arc + inc - cnt;
+          const int64_t id = vv.y + __popc(vw & ((1u << lane) - 1u));
+          __stcs((long long*)&O.row_ptr[id], (long long)pos);
+          __stcs(&O.pair_a[id], r);
+          __stcs(&O.pair_b[id], col);
+          O.is_start[id] = (uint8_t)(stA & __ldg(&C.startB[col]));
+          O.is_accept[id] = (uint8_t)(acA & __ldg(&C.accB[col]));
+          if (heavy) {
+            const int q = atomicAdd(&hq_n, 1);
+            if (q < kEmHeavyQ) {
+              hq_col[q] = col;
+              hq_h[q] = hidx;
+              hq_pos[q] = pos;
+            }
+          } else {
+            for (unsigned long long m = meps; m; m &= m - 1ull) {  // M2: B stays
+              const int a = __ffsll((long long)m) - 1;
+              if (look(srow[a], col, rk)) put(pos++, rk, scar[a], FST_EPS, sw[a]);
+            }
+            for (int j = 0; j < ejn; ++j) {  // eps items: M1 eps:eps, then M3
+              const uint32_t it = __ldg(ep + j * 32);
+              if ((it >> 24) != 1u) continue;
+              const int32_t o = (int32_t)(it & 0xFFFFFFu);
+              const int2 bw = __ldg(&D.eellcw[(ep - D.eell) + j * 32]);
+              for (unsigned long long m = meps; m; m &= m - 1ull) {
+                const int a = __ffsll((long long)m) - 1;
+                if (look(srow[a], o, rk)) put(pos++, rk, scar[a], bw.x, __fadd_rn(sw[a], __int_as_float(bw.y)));
+              }
+              if (look(r, o, rk)) put(pos++, rk, FST_EPS, bw.x, __int_as_float(bw.y));
+            }
+            for (int j = 0; j < jn; ++j) {
+              const uint32_t it = __ldg(pe + j * 32);
+              const uint32_t li = it >> 24;
+              const int32_t o = (int32_t)(it & 0xFFFFFFu);
+              unsigned long long m = lm[li];
+              if (!m) continue;
+              if (uni && !look(dr0, o, rk)) continue;
+              const int2 bw = __ldg(&D.ellcw[(pe - D.ell) + j * 32]);
+              for (; m; m &= m - 1ull) {
+                const int a = __ffsll((long long)m) - 1;
+                if (uni || look(srow[a], o, rk)) put(pos++, rk, scar[a], bw.x, __fadd_rn(sw[a], __int_as_float(bw.y)));
+              }
+            }
+          }
+        }
+        arc += wtot;
+      }
+    }
+    __syncthreads();
+    // heavy states: M2 (thread 0), then the items in rounds of kEmThreads with a block scan of their moves
+    const int nq = min(hq_n, kEmHeavyQ);
+    for (int q = 0; q < nq; ++q) {
+      const int32_t col = hq_col[q];
+      const int4 hv = __ldg(&D.heavy[hq_h[q]]);
+      int64_t pos = hq_pos[q];
+      if (tid == 0) {
+        int rk;
+        for (unsigned long long m = meps; m; m &= m - 1ull) {
+          const int a = __ffsll((long long)m) - 1;
+          if (look(srow[a], col, rk)) put(pos++, rk, scar[a], FST_EPS, sw[a]);
+        }
+        hq_id[q] = pos;
+      }
+      __syncthreads();
+      pos = hq_id[q];
+      for (int e0i = hv.y; e0i < hv.w; e0i += kEmThreads) {
+        const int e = e0i + tid;
+        int c = 0, rk;
+        uint32_t it = 0xFF000000u;
+        if (e < hv.w) {
+          it = __ldg(&D.hitems[e]);
+          const uint32_t li = it >> 24;
+          const int32_t o = (int32_t)(it & 0xFFFFFFu);
+          for (unsigned long long m = lm[li]; m; m &= m - 1ull) c += look(srow[__ffsll((long long)m) - 1], o, rk);
+          if (li == 1u) c += look(r, o, rk);
+        }
+        int btot;
+        const int ex = block_excl_scan(c, red, &btot);
+        if (c) {
+          int64_t p = pos + ex;
+          const uint32_t li = it >> 24;
+          const int32_t o = (int32_t)(it & 0xFFFFFFu);
+          const int2 bw = __ldg(&D.hcw[e]);
+          for (unsigned long long m = lm[li]; m; m &= m - 1ull) {
+            const int a = __ffsll((long long)m) - 1;
+            if (look(srow[a], o, rk)) put(p++, rk, scar[a], bw.x, __fadd_rn(sw[a], __int_as_float(bw.y)));
+          }
+          if (li == 1u && look(r, o, rk)) put(p++, rk, FST_EPS, bw.x, __int_as_float(bw.y));
+        }
+        pos += btot;
+      }
+      __syncthreads();
+    }
+    if (hq_n > kEmHeavyQ && tid == 0) atomicAdd(wa.err, 1);
   }
 }
 
@@ -609,10 +853,12 @@ fst_status ensure_wave_ell(fst* B, cudaStream_t s) {
     const View& v = B->views[dir == 0 ? kOutByIlabel : kInByIlabel];
     const int64_t E = B->E;
     std::vector<int32_t> off(V + 1), key(E), other(E);
+    std::vector<int2> cw(dir == 0 ? E : 0);
     FSTC_CUDA_TRY(cudaMemcpyAsync(off.data(), v.off, sizeof(int32_t) * (V + 1), cudaMemcpyDeviceToHost, s));
     if (E) {
       FSTC_CUDA_TRY(cudaMemcpyAsync(key.data(), v.key, sizeof(int32_t) * E, cudaMemcpyDeviceToHost, s));
       FSTC_CUDA_TRY(cudaMemcpyAsync(other.data(), v.other, sizeof(int32_t) * E, cudaMemcpyDeviceToHost, s));
+      if (dir == 0) FSTC_CUDA_TRY(cudaMemcpyAsync(cw.data(), v.cw, sizeof(int2) * E, cudaMemcpyDeviceToHost, s));
     }
     FSTC_CUDA_TRY(cudaStreamSynchronize(s));
     // light columns: non-eps items (label index >= 2) in `ell`, eps items in `eell` (needed only when an A
@@ -620,10 +866,12 @@ fst_status ensure_wave_ell(fst* B, cudaStream_t s) {
     std::vector<uint32_t> woff(wpr + 1, 0), ewoff(wpr + 1, 0), hmask(wpr, 0), blab(8, 0u);
     std::vector<uint8_t> wmax(std::max(wpr, 1), 0), ewmax(std::max(wpr, 1), 0);
     std::vector<int4> heavy;
-    std::vector<uint32_t> hitems;
+    std::vector<uint32_t> hitems, hbefore(wpr + 1, 0);
+    std::vector<int2> hcw;
     std::vector<int2> eps;
     std::vector<uint32_t> rel;
     for (int w = 0; w < wpr; ++w) {
+      hbefore[w] = (uint32_t)heavy.size();
       int m = 0, me = 0;
       for (int l = 0; l < 32; ++l) {
         const int32_t b = w * 32 + l;
@@ -634,6 +882,7 @@ fst_status ensure_wave_ell(fst* B, cudaStream_t s) {
           int32_t ne = h0;
           for (int32_t e = off[b]; e < off[b + 1]; ++e) {
             hitems.push_back(((uint32_t)(key[e] + 2) << 24) | (uint32_t)other[e]);
+            if (dir == 0) hcw.push_back(cw[e]);
             if (key[e] < 0) ++ne;
           }
           heavy.push_back(make_int4(b, h0, ne, (int32_t)hitems.size()));
@@ -651,6 +900,7 @@ fst_status ensure_wave_ell(fst* B, cudaStream_t s) {
       ewoff[w + 1] = ewoff[w] + (uint32_t)me;
     }
     std::vector<uint32_t> ell((size_t)woff[wpr] * 32 + 32, 0xFF000000u), eell((size_t)ewoff[wpr] * 32 + 32, 0xFF000000u);
+    std::vector<int2> ellcw(dir == 0 ? ell.size() : 0), eellcw(dir == 0 ? eell.size() : 0);
     for (int w = 0; w < wpr; ++w)
       for (int l = 0; l < 32; ++l) {
         const int32_t b = w * 32 + l;
@@ -660,9 +910,13 @@ fst_status ensure_wave_ell(fst* B, cudaStream_t s) {
           const uint32_t li = (uint32_t)(key[e] + 2);
           const uint32_t it = (li << 24) | (uint32_t)other[e];
           if (key[e] < 0) {
-            eell[((size_t)ewoff[w] + je++) * 32 + l] = it;
+            const size_t q = ((size_t)ewoff[w] + je++) * 32 + l;
+            eell[q] = it;
+            if (dir == 0) eellcw[q] = cw[e];
           } else {
-            ell[((size_t)woff[w] + j++) * 32 + l] = it;
+            const size_t q = ((size_t)woff[w] + j++) * 32 + l;
+            ell[q] = it;
+            if (dir == 0) ellcw[q] = cw[e];
             blab[li >> 5] |= 1u << (li & 31);
           }
         }
@@ -702,6 +956,8 @@ fst_status ensure_wave_ell(fst* B, cudaStream_t s) {
     size_t o = 0;
     auto take = [&](size_t bytes) { size_t r = o; o += (bytes + 255) & ~size_t(255); return r; };
     const size_t o_eell = take(4 * eell.size()), o_ewoff = take(4 * ewoff.size()), o_ewmax = take(ewmax.size());
+    const size_t o_ellcw = take(8 * std::max<size_t>(ellcw.size(), 1)), o_eellcw = take(8 * std::max<size_t>(eellcw.size(), 1)),
+                 o_hcw = take(8 * std::max<size_t>(hcw.size(), 1)), o_hb = take(4 * hbefore.size());
     const size_t o_ell = take(4 * ell.size()), o_woff = take(4 * woff.size()), o_wmax = take(wmax.size()),
                  o_hm = take(4 * std::max<size_t>(hmask.size(), 1)), o_h = take(16 * std::max<size_t>(heavy.size(), 1)),
                  o_e = take(8 * std::max<size_t>(eps.size(), 1)), o_hc = take(4 * std::max<size_t>(hub_col.size(), 1)),
@@ -711,6 +967,14 @@ fst_status ensure_wave_ell(fst* B, cudaStream_t s) {
     fst_status st = alloc_buffer(o, s, &buf);
     if (st) return st;
     char* base = (char*)buf->ptr;
+    T.ellcw = (int2*)(base + o_ellcw);
+    T.eellcw = (int2*)(base + o_eellcw);
+    T.hcw = (int2*)(base + o_hcw);
+    T.hbefore = (uint32_t*)(base + o_hb);
+    if (!ellcw.empty()) FSTC_CUDA_TRY(cudaMemcpyAsync(T.ellcw, ellcw.data(), 8 * ellcw.size(), cudaMemcpyHostToDevice, s));
+    if (!eellcw.empty()) FSTC_CUDA_TRY(cudaMemcpyAsync(T.eellcw, eellcw.data(), 8 * eellcw.size(), cudaMemcpyHostToDevice, s));
+    if (!hcw.empty()) FSTC_CUDA_TRY(cudaMemcpyAsync(T.hcw, hcw.data(), 8 * hcw.size(), cudaMemcpyHostToDevice, s));
+    FSTC_CUDA_TRY(cudaMemcpyAsync(T.hbefore, hbefore.data(), 4 * hbefore.size(), cudaMemcpyHostToDevice, s));
     T.eell = (uint32_t*)(base + o_eell);
     T.ewoff = (uint32_t*)(base + o_ewoff);
     T.ewmax = (uint8_t*)(base + o_ewmax);
@@ -883,7 +1147,7 @@ fst_status wave_plan(int32_t n, const fst_handle* a, const fst_handle* b, const 
   // per-composition descriptors
   std::vector<WaveComp> comps(n);
   std::vector<int32_t> order(n);
-  int64_t rows = 0;
+  int64_t rows = 0, hrows = 0;
   for (int i = 0; i < n; ++i) {
     fst* A = a[i];
     fst* B = b[i];
@@ -892,6 +1156,8 @@ fst_status wave_plan(int32_t n, const fst_handle* a, const fst_handle* b, const 
     C.W = W[i];
     C.K = K[i];
     C.rowbase = rows;
+    C.hcnt_base = hrows;
+    hrows += (int64_t)A->V * B->wave_ell[0].nheavy;
     rows += A->V;
     C.VA = A->V;
     C.VB = B->V;
@@ -904,7 +1170,8 @@ fst_status wave_plan(int32_t n, const fst_handle* a, const fst_handle* b, const 
       C.aother[d] = av.other;
       const View& bv = B->views[d == 0 ? kOutByIlabel : kInByIlabel];
       const fst::WaveEll& T = B->wave_ell[d];
-      C.bd[d] = WaveDir{T.ell, T.woff, T.wmax, T.eell, T.ewoff, T.ewmax, T.hmask, T.heavy, T.nheavy, T.hitems, {}};
+      C.bd[d] = WaveDir{T.ell, T.woff, T.wmax, T.eell, T.ewoff, T.ewmax, T.hmask, T.heavy, T.nheavy, T.hitems, {},
+                        T.ellcw, T.eellcw, T.hcw, T.hbefore};
       for (int k = 0; k < 8; ++k) C.bd[d].blab[k] = T.blab[k];
       (void)bv;
     }
@@ -923,7 +1190,7 @@ fst_status wave_plan(int32_t n, const fst_handle* a, const fst_handle* b, const 
   std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return comps[x].VA > comps[y].VA; });
   size_t o = 0;
   auto take = [&](size_t bytes) { size_t r = o; o += (bytes + 255) & ~size_t(255); return r; };
-  const size_t o_c = take(sizeof(WaveComp) * n), o_o = take(4 * n), o_n = take(8);
+  const size_t o_c = take(sizeof(WaveComp) * n), o_o = take(4 * n), o_n = take(8), o_h = take(4 * std::max<int64_t>(hrows, 1));
   fst_status st = alloc_buffer(o, s, &P.buf);
   if (st) return st;
   char* base = (char*)P.buf->ptr;
@@ -935,6 +1202,7 @@ fst_status wave_plan(int32_t n, const fst_handle* a, const fst_handle* b, const 
   P.wa.ncomp = n;
   P.wa.wprmax = wprmax;
   P.wa.next = (int32_t*)(base + o_n);
+  P.wa.hcnt = (int32_t*)(base + o_h);
   P.wa.nrows = rows;
   plan->ok = true;
   plan->depth = maxrows;
@@ -968,6 +1236,26 @@ fst_status wave_count(const WavePlan& plan, uint32_t* V, uint8_t* cnt8, unsigned
     smem_set = smem;
   }
   k_wave_count<<<(unsigned)grid, kCThreads, smem, s>>>(P.wa);
+  FSTC_LAUNCH_CHECK();
+  return FST_OK;
+}
+
+fst_status wave_emit(const WavePlan& plan, const CompDev* d_comps, const int64_t* d_tot, const int64_t* idbase,
+                     const int64_t* arcbase, const uint16_t* wpre, uint32_t* V, int32_t* err, cudaStream_t s) {
+  WavePlan::Impl& P = *plan.impl;
+  P.wa.V = V;
+  P.wa.idbase = idbase;
+  P.wa.arcbase = arcbase;
+  P.wa.wpre = wpre;
+  P.wa.err = err;
+  const size_t smem = 16ull * P.wa.wprmax;
+  static size_t smem_set = 0;
+  if (smem > 40 * 1024 && smem > smem_set) {
+    FSTC_CUDA_TRY(cudaFuncSetAttribute(k_wave_emit, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    smem_set = smem;
+  }
+  const int64_t grid = std::min<int64_t>(std::max<int64_t>(P.wa.nrows, 1), (int64_t)sm_count() * 4);
+  k_wave_emit<<<(unsigned)grid, kEmThreads, smem, s>>>(P.wa, d_comps, d_tot);
   FSTC_LAUNCH_CHECK();
   return FST_OK;
 }

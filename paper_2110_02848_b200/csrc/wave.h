@@ -29,6 +29,10 @@ fst_status wave_plan(int32_t n, const fst_handle* a, const fst_handle* b, const 
 fst_status wave_stage(const WavePlan& plan, int stage, uint32_t* R, uint32_t* V, cudaStream_t s);
 // pass-1 counts: cnt8 of every state of C and kept[] of every block (overwritten).
 fst_status wave_count(const WavePlan& plan, uint32_t* V, uint8_t* cnt8, unsigned long long* kept, cudaStream_t s);
+// pass 2 (general emit replacement; no provenance): writes every composition's CSR from the numbering
+// (idbase / arcbase per block, wpre per word).  `err` counts internal inconsistencies (must stay 0).
+fst_status wave_emit(const WavePlan& plan, const struct CompDev* d_comps, const int64_t* d_tot, const int64_t* idbase,
+                     const int64_t* arcbase, const uint16_t* wpre, uint32_t* V, int32_t* err, cudaStream_t s);
 void wave_mode_set(int mode);
 
 }  // namespace fstc

@@ -139,3 +139,24 @@ def test_wave_auto_selects_trellis_batch(fst):
         assert fst.fst_compose(fst.fst_create(A), fst.fst_create(B2)).stats()["tile_path"] == 0
     finally:
         fst.fst_set_wave_mode(2)
+
+
+def test_wave_provenance_uses_general_emit(fst):
+    """FST_COMPOSE_PROVENANCE on the wave path (stages + counts on the wave kernels, the general emit
+    with arc_a / arc_b): the arrays equal the level path's, provenance included."""
+    A, B = fstgen.config_c3(num_words=300, T=30)
+    a, b = fst.fst_create(A), fst.fst_create(B)
+    fst.fst_set_wave_mode(2)
+    cw = fst.fst_compose(a, b, provenance=True)
+    assert cw.stats()["tile_path"] == 2
+    fst.fst_set_wave_mode(0)
+    try:
+        cl = fst.fst_compose(a, b, provenance=True)
+    finally:
+        fst.fst_set_wave_mode(2)
+    hw, hl = cw.to_host(), cl.to_host()
+    for k in hw:
+        assert np.array_equal(np.asarray(hw[k]), np.asarray(hl[k])), k
+    pw, pl = cw.provenance(), cl.provenance()
+    for x, y in zip(pw, pl):
+        assert np.array_equal(np.asarray(x), np.asarray(y))
