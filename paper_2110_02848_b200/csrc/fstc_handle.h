@@ -123,6 +123,8 @@ struct fst {
     int2* eellcw = nullptr;
     int2* hcw = nullptr;
     uint32_t* hbefore = nullptr;  // [wpr + 1] heavy columns before each word
+    uint32_t* wo = nullptr;       // [wpr + 1] woff << 8 | wmax
+    uint32_t* ewo = nullptr;      // [wpr + 1] ewoff << 8 | ewmax
     uint32_t* hmask = nullptr; // [wpr] lanes of heavy columns
     int4* heavy = nullptr;     // (col, first item, first non-eps item, end) of heavy columns, by col
     int32_t nheavy = 0;

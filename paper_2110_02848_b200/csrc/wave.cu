@@ -75,6 +75,8 @@ struct WaveDir {  // B role, one direction (view by ilabel)
   const int2* eellcw;
   const int2* hcw;
   const uint32_t* hbefore;
+  const uint32_t* wo;   // [wpr] woff << 8 | wmax  (the emit: one load per word)
+  const uint32_t* ewo;  // [wpr] ewoff << 8 | ewmax
 };
 
 struct WaveComp {
@@ -586,6 +588,18 @@ __global__ void __launch_bounds__(kEmThreads) k_wave_emit(WaveArgs wa, const Com
   __shared__ int32_t hq_n, red[kEmThreads / 32 + 1];
   __shared__ int32_t hq_col[kEmHeavyQ], hq_h[kEmHeavyQ];
   __shared__ long long hq_pos[kEmHeavyQ], hq_id[kEmHeavyQ];
+  // the task's pointers, in shared memory: held there (global stores cannot alias them) instead of being
+  // re-read from the composition descriptors after every store
+  struct EmitPtrs {
+    int64_t* row_ptr;
+    int32_t *dst, *ilabel, *olabel, *pair_a, *pair_b;
+    float* weight;
+    uint8_t *is_start, *is_accept;
+    const uint32_t *ell, *eell, *wo, *ewo, *hmask, *hbefore;
+    const int2 *ellcw, *eellcw;
+    const int32_t* hcnt;
+  };
+  __shared__ EmitPtrs P;
   extern __shared__ int2 esm[];  // [wprmax] own row, [wprmax] destination row: (V word, rank of its first pair)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr int nwarp = kEmThreads / 32;
@@ -610,7 +624,27 @@ __global__ void __launch_bounds__(kEmThreads) k_wave_emit(WaveArgs wa, const Com
     const int32_t dr0 = d > 0 ? __ldg(&C.aother[0][e0]) : r;
     __syncthreads();  // previous task's readers of the shared tables
     for (int i = tid; i < kWLab; i += kEmThreads) lm[i] = 0ull;
-    if (tid == 0) hq_n = 0;
+    if (tid == 0) {
+      hq_n = 0;
+      P.row_ptr = O.row_ptr;
+      P.dst = O.dst;
+      P.ilabel = O.ilabel;
+      P.olabel = O.olabel;
+      P.pair_a = O.pair_a;
+      P.pair_b = O.pair_b;
+      P.weight = O.weight;
+      P.is_start = O.is_start;
+      P.is_accept = O.is_accept;
+      P.ell = D.ell;
+      P.eell = D.eell;
+      P.wo = D.wo;
+      P.ewo = D.ewo;
+      P.hmask = D.hmask;
+      P.hbefore = D.hbefore;
+      P.ellcw = D.ellcw;
+      P.eellcw = D.eellcw;
+      P.hcnt = wa.hcnt + C.hcnt_base + (int64_t)r * D.nheavy;
+    }
     __syncthreads();
     bool same = true;
     if (tid < d) {
@@ -651,12 +685,107 @@ __global__ void __launch_bounds__(kEmThreads) k_wave_emit(WaveArgs wa, const Com
       return true;
     };
     auto put = [&](int64_t pos, int32_t dst, int32_t il, int32_t ol, float w) {
-      __stcs(&O.dst[pos], dst);
-      __stcs(&O.ilabel[pos], il);
-      __stcs(&O.olabel[pos], ol);
-      __stcs(&O.weight[pos], w);
+      __stcs(&P.dst[pos], dst);
+      __stcs(&P.ilabel[pos], il);
+      __stcs(&P.olabel[pos], ol);
+      __stcs(&P.weight[pos], w);
     };
-    for (int blk = warp; blk < bpr; blk += nwarp) {
+    const uint8_t* __restrict__ startB = C.startB;
+    const uint8_t* __restrict__ accB = C.accB;
+    auto state_out = [&](int64_t id, int32_t col, int64_t pos) {
+      __stcs((long long*)&P.row_ptr[id], (long long)pos);
+      __stcs(&P.pair_a[id], r);
+      __stcs(&P.pair_b[id], col);
+      P.is_start[id] = stA ? __ldg(&startB[col]) : (uint8_t)0;
+      P.is_accept[id] = acA ? __ldg(&accB[col]) : (uint8_t)0;
+    };
+    auto heavy_push = [&](int32_t col, int hidx, int64_t pos) {
+      const int q = atomicAdd(&hq_n, 1);
+      if (q < kEmHeavyQ) {
+        hq_col[q] = col;
+        hq_h[q] = hidx;
+        hq_pos[q] = pos;
+      }
+    };
+    // trellis rows (every A arc to one row dr0, no eps-output A arcs): M1 = label in the row and target in
+    // V(dr0); M3 = eps item with target in V(r)
+    const bool fast = uni && meps == 0ull;
+    for (int blk = fast ? warp : bpr; blk < bpr; blk += nwarp) {
+      int64_t arc = __ldg(&wa.arcbase[K + (int64_t)r * bpr + blk]) - arc_comp;
+      const int wb = blk * 32, nw = min(32, wpr - wb);
+      for (int i = 0; i < nw; ++i) {
+        const int w = wb + i;
+        const int2 vv = Vr[w];
+        const uint32_t vw = (uint32_t)vv.x;
+        if (!vw) continue;
+        const int32_t col = w * 32 + lane;
+        const uint32_t hm = __ldg(&P.hmask[w]);
+        const bool has = (vw >> lane) & 1u, heavy = (hm >> lane) & 1u;
+        const uint32_t xn = __ldg(&P.wo[w]), xe = __ldg(&P.ewo[w]);
+        const uint32_t* __restrict__ pe = P.ell + (size_t)(xn >> 8) * 32 + lane;
+        const uint32_t* __restrict__ ep = P.eell + (size_t)(xe >> 8) * 32 + lane;
+        const int jn = (int)(xn & 255u), ejn = (int)(xe & 255u);
+        int cnt = 0;
+        uint32_t e0it = 0xFF000000u, n0it = 0xFF000000u;  // first items, kept for the write walk
+        if (has) {
+          if (heavy) {
+            cnt = __ldg(&P.hcnt[(int)__ldg(&P.hbefore[w]) + __popc(hm & ((1u << lane) - 1u))]);
+          } else {
+#pragma unroll 1
+            for (int j = 0; j < ejn; ++j) {
+              const uint32_t it = __ldg(ep + j * 32);
+              if (j == 0) e0it = it;
+              const int32_t o = (int32_t)(it & 0xFFFFFFu);
+              if (it < 0xFF000000u) cnt += (int)((((uint32_t)Vr[o >> 5].x) >> (o & 31)) & 1u);
+            }
+#pragma unroll 1
+            for (int j = 0; j < jn; ++j) {
+              const uint32_t it = __ldg(pe + j * 32);
+              if (j == 0) n0it = it;
+              const int32_t o = (int32_t)(it & 0xFFFFFFu);
+              cnt += (int)(lc[it >> 24] * ((((uint32_t)Vd[o >> 5].x) >> (o & 31)) & 1u));
+            }
+          }
+        }
+        const int inc = warp_incl_scan(cnt);
+        const int wtot = __shfl_sync(0xffffffffu, inc, 31);
+        if (has) {
+          int64_t pos = arc + inc - cnt;
+          state_out(vv.y + __popc(vw & ((1u << lane) - 1u)), col, pos);
+          if (heavy) {
+            heavy_push(col, (int)__ldg(&P.hbefore[w]) + __popc(hm & ((1u << lane) - 1u)), pos);
+          } else if (cnt) {
+#pragma unroll 1
+            for (int j = 0; j < ejn; ++j) {  // M3
+              const uint32_t it = j == 0 ? e0it : __ldg(ep + j * 32);
+              if (it >= 0xFF000000u) continue;
+              const int32_t o = (int32_t)(it & 0xFFFFFFu);
+              const int2 v = Vr[o >> 5];
+              if (!(((uint32_t)v.x >> (o & 31)) & 1u)) continue;
+              const int2 bw = __ldg(&P.eellcw[(size_t)(xe >> 8) * 32 + lane + j * 32]);
+              put(pos++, v.y + __popc((uint32_t)v.x & ((1u << (o & 31)) - 1u)), FST_EPS, bw.x, __int_as_float(bw.y));
+            }
+#pragma unroll 1
+            for (int j = 0; j < jn; ++j) {  // M1
+              const uint32_t it = j == 0 ? n0it : __ldg(pe + j * 32);
+              unsigned long long m = lm[it >> 24];
+              if (!m) continue;
+              const int32_t o = (int32_t)(it & 0xFFFFFFu);
+              const int2 v = Vd[o >> 5];
+              if (!(((uint32_t)v.x >> (o & 31)) & 1u)) continue;
+              const int32_t rk = v.y + __popc((uint32_t)v.x & ((1u << (o & 31)) - 1u));
+              const int2 bw = __ldg(&P.ellcw[(size_t)(xn >> 8) * 32 + lane + j * 32]);
+              for (; m; m &= m - 1ull) {
+                const int a = __ffsll((long long)m) - 1;
+                put(pos++, rk, scar[a], bw.x, __fadd_rn(sw[a], __int_as_float(bw.y)));
+              }
+            }
+          }
+        }
+        arc += wtot;
+      }
+    }
+    for (int blk = fast ? bpr : warp; blk < bpr; blk += nwarp) {
       int64_t arc = __ldg(&wa.arcbase[K + (int64_t)r * bpr + blk]) - arc_comp;
       const int wb = blk * 32, nw = min(32, wpr - wb);
       for (int i = 0; i < nw; ++i) {
@@ -700,19 +829,9 @@ __global__ void __launch_bounds__(kEmThreads) k_wave_emit(WaveArgs wa, const Com
         const int wtot = __shfl_sync(0xffffffffu, inc, 31);
         if (has) {
           int64_t pos = arc + inc - cnt;
-          const int64_t id = vv.y + __popc(vw & ((1u << lane) - 1u));
-          __stcs((long long*)&O.row_ptr[id], (long long)pos);
-          __stcs(&O.pair_a[id], r);
-          __stcs(&O.pair_b[id], col);
-          O.is_start[id] = (uint8_t)(stA & __ldg(&C.startB[col]));
-          O.is_accept[id] = (uint8_t)(acA & __ldg(&C.accB[col]));
+          state_out(vv.y + __popc(vw & ((1u << lane) - 1u)), col, pos);
           if (heavy) {
-            const int q = atomicAdd(&hq_n, 1);
-            if (q < kEmHeavyQ) {
-              hq_col[q] = col;
-              hq_h[q] = hidx;
-              hq_pos[q] = pos;
-            }
+            heavy_push(col, hidx, pos);
           } else {
             for (unsigned long long m = meps; m; m &= m - 1ull) {  // M2: B stays
               const int a = __ffsll((long long)m) - 1;
@@ -748,13 +867,32 @@ __global__ void __launch_bounds__(kEmThreads) k_wave_emit(WaveArgs wa, const Com
       }
     }
     __syncthreads();
-    // heavy states: M2 (thread 0), then the items in rounds of kEmThreads with a block scan of their moves
+    // heavy states: M2 (thread 0); the items split into one contiguous run per warp: each warp counts
+    // its run's moves, a scan over the warps gives every run its first slot, then each warp writes its run
+    // in rounds of 32 items (warp scans) -- item order = view order
     const int nq = min(hq_n, kEmHeavyQ);
     for (int q = 0; q < nq; ++q) {
       const int32_t col = hq_col[q];
       const int4 hv = __ldg(&D.heavy[hq_h[q]]);
-      int64_t pos = hq_pos[q];
+      const int per = (hv.w - hv.y + nwarp - 1) / nwarp;
+      const int c0 = hv.y + warp * per, c1 = min(hv.w, c0 + per);
+      auto moves = [&](uint32_t it) -> int {
+        const uint32_t li = it >> 24;
+        const int32_t o = (int32_t)(it & 0xFFFFFFu);
+        int c = 0, rk;
+        if (it >= 0xFF000000u) return 0;
+        if (fast) return (int)(lc[li] * ((((uint32_t)Vd[o >> 5].x) >> (o & 31)) & 1u)) +
+                         (li == 1u ? (int)((((uint32_t)Vr[o >> 5].x) >> (o & 31)) & 1u) : 0);
+        for (unsigned long long m = lm[li]; m; m &= m - 1ull) c += look(srow[__ffsll((long long)m) - 1], o, rk);
+        if (li == 1u) c += look(r, o, rk);
+        return c;
+      };
+      int wc = 0;
+      for (int e = c0 + lane; e < c1; e += 32) wc += moves(__ldg(&D.hitems[e]));
+      wc = warp_sum(wc);
+      if (lane == 0) red[warp] = wc;
       if (tid == 0) {
+        int64_t pos = hq_pos[q];
         int rk;
         for (unsigned long long m = meps; m; m &= m - 1ull) {
           const int a = __ffsll((long long)m) - 1;
@@ -763,22 +901,16 @@ __global__ void __launch_bounds__(kEmThreads) k_wave_emit(WaveArgs wa, const Com
         hq_id[q] = pos;
       }
       __syncthreads();
-      pos = hq_id[q];
-      for (int e0i = hv.y; e0i < hv.w; e0i += kEmThreads) {
-        const int e = e0i + tid;
-        int c = 0, rk;
-        uint32_t it = 0xFF000000u;
-        if (e < hv.w) {
-          it = __ldg(&D.hitems[e]);
-          const uint32_t li = it >> 24;
-          const int32_t o = (int32_t)(it & 0xFFFFFFu);
-          for (unsigned long long m = lm[li]; m; m &= m - 1ull) c += look(srow[__ffsll((long long)m) - 1], o, rk);
-          if (li == 1u) c += look(r, o, rk);
-        }
-        int btot;
-        const int ex = block_excl_scan(c, red, &btot);
+      int64_t pos = hq_id[q];
+      for (int k = 0; k < warp; ++k) pos += red[k];
+      for (int e0i = c0; e0i < c1; e0i += 32) {
+        const int e = e0i + lane;
+        const uint32_t it = e < c1 ? __ldg(&D.hitems[e]) : 0xFF000000u;
+        const int c = moves(it);
+        const int inc = warp_incl_scan(c);
         if (c) {
-          int64_t p = pos + ex;
+          int64_t p = pos + inc - c;
+          int rk;
           const uint32_t li = it >> 24;
           const int32_t o = (int32_t)(it & 0xFFFFFFu);
           const int2 bw = __ldg(&D.hcw[e]);
@@ -788,7 +920,7 @@ __global__ void __launch_bounds__(kEmThreads) k_wave_emit(WaveArgs wa, const Com
           }
           if (li == 1u && look(r, o, rk)) put(p++, rk, FST_EPS, bw.x, __int_as_float(bw.y));
         }
-        pos += btot;
+        pos += __shfl_sync(0xffffffffu, inc, 31);
       }
       __syncthreads();
     }
@@ -956,6 +1088,16 @@ fst_status ensure_wave_ell(fst* B, cudaStream_t s) {
     size_t o = 0;
     auto take = [&](size_t bytes) { size_t r = o; o += (bytes + 255) & ~size_t(255); return r; };
     const size_t o_eell = take(4 * eell.size()), o_ewoff = take(4 * ewoff.size()), o_ewmax = take(ewmax.size());
+    std::vector<uint32_t> wo(wpr + 1, 0), ewo(wpr + 1, 0);
+    for (int w = 0; w < wpr; ++w) {
+      wo[w] = (woff[w] << 8) | wmax[w];
+      ewo[w] = (ewoff[w] << 8) | ewmax[w];
+    }
+    if (woff[wpr] >= (1u << 24) || ewoff[wpr] >= (1u << 24)) {
+      set_error(FST_E_CAPACITY, "wave ELL too large");
+      return FST_E_CAPACITY;
+    }
+    const size_t o_wo = take(4 * wo.size()), o_ewo = take(4 * ewo.size());
     const size_t o_ellcw = take(8 * std::max<size_t>(ellcw.size(), 1)), o_eellcw = take(8 * std::max<size_t>(eellcw.size(), 1)),
                  o_hcw = take(8 * std::max<size_t>(hcw.size(), 1)), o_hb = take(4 * hbefore.size());
     const size_t o_ell = take(4 * ell.size()), o_woff = take(4 * woff.size()), o_wmax = take(wmax.size()),
@@ -967,6 +1109,10 @@ fst_status ensure_wave_ell(fst* B, cudaStream_t s) {
     fst_status st = alloc_buffer(o, s, &buf);
     if (st) return st;
     char* base = (char*)buf->ptr;
+    T.wo = (uint32_t*)(base + o_wo);
+    T.ewo = (uint32_t*)(base + o_ewo);
+    FSTC_CUDA_TRY(cudaMemcpyAsync(T.wo, wo.data(), 4 * wo.size(), cudaMemcpyHostToDevice, s));
+    FSTC_CUDA_TRY(cudaMemcpyAsync(T.ewo, ewo.data(), 4 * ewo.size(), cudaMemcpyHostToDevice, s));
     T.ellcw = (int2*)(base + o_ellcw);
     T.eellcw = (int2*)(base + o_eellcw);
     T.hcw = (int2*)(base + o_hcw);
@@ -1171,7 +1317,7 @@ fst_status wave_plan(int32_t n, const fst_handle* a, const fst_handle* b, const 
       const View& bv = B->views[d == 0 ? kOutByIlabel : kInByIlabel];
       const fst::WaveEll& T = B->wave_ell[d];
       C.bd[d] = WaveDir{T.ell, T.woff, T.wmax, T.eell, T.ewoff, T.ewmax, T.hmask, T.heavy, T.nheavy, T.hitems, {},
-                        T.ellcw, T.eellcw, T.hcw, T.hbefore};
+                        T.ellcw, T.eellcw, T.hcw, T.hbefore, T.wo, T.ewo};
       for (int k = 0; k < 8; ++k) C.bd[d].blab[k] = T.blab[k];
       (void)bv;
     }
