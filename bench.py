@@ -393,11 +393,12 @@ def run_ours(args):
     s2 = statistics.mean(s["ms_stage2"] for s in pstats)
     cnt_ms = statistics.mean(s["ms_count"] for s in pstats)
     num = statistics.mean(s["ms_number"] for s in pstats)
-    tile = bool(pstats[-1]["tile_path"])
+    path = {0: "level", 1: "tile", 2: "wave"}.get(int(pstats[-1]["tile_path"]), "level")
+    tile = path == "tile"
     ab = 24 if args.provenance else 16  # + arc_a / arc_b per arc with provenance
     emit_bytes = ab * E_C + 18 * V_C + P / 8
     step_bytes = ab * E_C + 18 * V_C + 2 * k * (R + V_C) + P / 4
-    emit_name = "k_tile_emit" if tile else "k_emit"
+    emit_name = {"tile": "k_tile_emit", "wave": "k_wave_emit" if not args.provenance else "k_emit"}.get(path, "k_emit")
     traffic = None
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tp):
@@ -419,11 +420,14 @@ def run_ours(args):
     # bound by instruction issue and shared-memory bandwidth, far from HBM-bound (profiles/r02_summary.md)
     bfs_bytes = 2 * k * (R + V_C) + P / 4
     bfs_ms = s1 + s2 - cnt_ms
-    bfs_roof = {"kernel": "k_tile_pull+k_sparse_push" if tile else "k_level", "bound": "hbm", "traffic": None,
+    bfs_name = {"tile": "k_tile_pull+k_sparse_push", "wave": "k_wave<0>+k_wave<1>"}.get(path, "k_level")
+    bfs_roof = {"kernel": bfs_name, "bound": "hbm", "traffic": None,
                 "achieved": bfs_bytes / (bfs_ms / 1e3) / 1e9, "peak": hbm, "unit": "GB/s",
                 "frac": bfs_bytes / (bfs_ms / 1e3) / 1e9 / hbm, "share_of_step": bfs_ms / ms_step,
                 "algorithmic_bytes_per_step": bfs_bytes, "bytes_formula": "2k(|R|+V_C) + P/4 over both BFS stages",
-                "note": "issue / shared-memory bound (profiles/r02_summary.md), not HBM-bound"}
+                "note": "issue / shared-memory bound (profiles/r02_summary.md), not HBM-bound" +
+                        ("; wave path: sequential row steps per composition (DESIGN.md 6c), the count pass is "
+                         "reported in phases_ms.count" if path == "wave" else "")}
     step_roof = {"algorithmic_bytes": step_bytes, "frac_of_hbm": step_bytes / (ms_step / 1e3) / 1e9 / hbm,
                  "formula": f"{ab}*E_C + 18*V_C + 2k(|R|+V_C) + P/4 (SURVEY 8(d) d.4)"}
     # `roofline` names the DOMINANT kernel group of the step (largest device-time share): the BFS level
@@ -443,7 +447,9 @@ def run_ours(args):
         "config": workload_config(args.workload, As, B),
         "result": {"V_C": V_C, "E_C": E_C, "coaccessible": R,
                    "levels": [pstats[-1]["levels_stage1"], pstats[-1]["levels_stage2"]],
-                   "bottom_up_rounds": pstats[-1]["pull_levels"], "tile_path": tile},
+                   "bottom_up_rounds": pstats[-1]["pull_levels"], "tile_path": tile, "path": path,
+                   **({"row_steps": pstats[-1]["levels_stage1"], "cluster_ctas": pstats[-1]["staged_tasks"]}
+                      if path == "wave" else {})},
         "setup": {"parallelism": parallelism, "provenance": bool(args.provenance),
                   **({"seeds": list(input_seeds(args.workload, rank, bump))} if args.workload != "c5" else
                      {"utterances": [int(i) for i in mine]}),
