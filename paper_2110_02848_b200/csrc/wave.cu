@@ -579,7 +579,7 @@ __global__ void __launch_bounds__(kCThreads) k_wave_count(WaveArgs wa) {
 // by the whole CTA.
 constexpr int kEmThreads = 512;
 constexpr int kEmHeavyQ = 256;
-__global__ void __launch_bounds__(kEmThreads) k_wave_emit(WaveArgs wa, const CompDev* __restrict__ cd,
+__global__ void __launch_bounds__(kEmThreads, 2) k_wave_emit(WaveArgs wa, const CompDev* __restrict__ cd,
                                                           const int64_t* __restrict__ tot) {
   __shared__ unsigned long long lm[kWLab];
   __shared__ uint32_t lc[kWLab];
@@ -600,12 +600,15 @@ __global__ void __launch_bounds__(kEmThreads) k_wave_emit(WaveArgs wa, const Com
     const int32_t* hcnt;
   };
   __shared__ EmitPtrs P;
-  extern __shared__ int2 esm[];  // [wprmax] own row, [wprmax] destination row: (V word, rank of its first pair)
+  extern __shared__ int2 esm[];  // [wprmax] own row, [wprmax] destination row: (V word, rank of its first pair),
+                                 // [wprmax] per-word item metadata (wo, ewo, hmask, hbefore) of B
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr int nwarp = kEmThreads / 32;
   const uint32_t* __restrict__ Vg = wa.V;
   int2* Vr = esm;
   int2* Vd = esm + wa.wprmax;
+  uint4* wmeta = (uint4*)(esm + 2 * wa.wprmax);
+  const uint32_t* wtag = nullptr;  // B whose metadata wmeta holds
   for (int64_t t = blockIdx.x; t < wa.nrows; t += gridDim.x) {
     int ci = 0, hi = wa.ncomp - 1;
     while (ci < hi) {
@@ -710,38 +713,80 @@ __global__ void __launch_bounds__(kEmThreads) k_wave_emit(WaveArgs wa, const Com
     // trellis rows (every A arc to one row dr0, no eps-output A arcs): M1 = label in the row and target in
     // V(dr0); M3 = eps item with target in V(r)
     const bool fast = uni && meps == 0ull;
+    if (fast && wtag != P.wo) {  // per-word item metadata of B (same for every row of a composition)
+      __syncthreads();
+      for (int w = tid; w < wpr; w += kEmThreads)
+        wmeta[w] = make_uint4(__ldg(&P.wo[w]), __ldg(&P.ewo[w]), __ldg(&P.hmask[w]), __ldg(&P.hbefore[w]));
+      __syncthreads();
+      wtag = P.wo;
+    }
     for (int blk = fast ? warp : bpr; blk < bpr; blk += nwarp) {
       int64_t arc = __ldg(&wa.arcbase[K + (int64_t)r * bpr + blk]) - arc_comp;
       const int wb = blk * 32, nw = min(32, wpr - wb);
+      // software pipeline: the first items (and their (olabel, weight)) of word w + 1 are loaded while word w
+      // is processed
+      uint32_t pn = 0xFF000000u, pe0 = 0xFF000000u;
+      int2 pbn = make_int2(0, 0), pbe = make_int2(0, 0);
+      auto prefetch = [&](int w) {
+        const uint4 m = wmeta[w];
+        pn = (m.x & 255u) ? __ldg(P.ell + (size_t)(m.x >> 8) * 32 + lane) : 0xFF000000u;
+        pe0 = (m.y & 255u) ? __ldg(P.eell + (size_t)(m.y >> 8) * 32 + lane) : 0xFF000000u;
+        pbn = (m.x & 255u) ? __ldg(P.ellcw + (size_t)(m.x >> 8) * 32 + lane) : make_int2(0, 0);
+        pbe = (m.y & 255u) ? __ldg(P.eellcw + (size_t)(m.y >> 8) * 32 + lane) : make_int2(0, 0);
+      };
+      prefetch(wb);
       for (int i = 0; i < nw; ++i) {
         const int w = wb + i;
+        const uint32_t n0it = pn, e0it = pe0;
+        const int2 n0bw = pbn, e0bw = pbe;
+        if (i + 1 < nw) prefetch(w + 1);
         const int2 vv = Vr[w];
         const uint32_t vw = (uint32_t)vv.x;
         if (!vw) continue;
         const int32_t col = w * 32 + lane;
-        const uint32_t hm = __ldg(&P.hmask[w]);
+        const uint4 mt = wmeta[w];
+        const uint32_t xn = mt.x, xe = mt.y, hm = mt.z;
         const bool has = (vw >> lane) & 1u, heavy = (hm >> lane) & 1u;
-        const uint32_t xn = __ldg(&P.wo[w]), xe = __ldg(&P.ewo[w]);
         const uint32_t* __restrict__ pe = P.ell + (size_t)(xn >> 8) * 32 + lane;
         const uint32_t* __restrict__ ep = P.eell + (size_t)(xe >> 8) * 32 + lane;
         const int jn = (int)(xn & 255u), ejn = (int)(xe & 255u);
+        if (jn <= 1 && ejn <= 1 && !hm) {  // straight-line: at most one eps item (M3) and one item (M1)
+          const int32_t oe = (int32_t)(e0it & 0xFFFFFFu), on = (int32_t)(n0it & 0xFFFFFFu);
+          const int2 ve = Vr[oe >> 5], vn = Vd[on >> 5];
+          const bool he = has && e0it < 0xFF000000u && (((uint32_t)ve.x >> (oe & 31)) & 1u);
+          const unsigned long long mn = lm[n0it >> 24];
+          const bool hn = has && mn != 0ull && (((uint32_t)vn.x >> (on & 31)) & 1u);
+          const int cnt = (int)he + (hn ? (int)lc[n0it >> 24] : 0);
+          const int inc = warp_incl_scan(cnt);
+          if (has) {
+            int64_t pos = arc + inc - cnt;
+            state_out(vv.y + __popc(vw & ((1u << lane) - 1u)), col, pos);
+            if (he) put(pos++, ve.y + __popc((uint32_t)ve.x & ((1u << (oe & 31)) - 1u)), FST_EPS, e0bw.x, __int_as_float(e0bw.y));
+            if (hn) {
+              const int32_t rk = vn.y + __popc((uint32_t)vn.x & ((1u << (on & 31)) - 1u));
+              for (unsigned long long m = mn; m; m &= m - 1ull) {
+                const int a = __ffsll((long long)m) - 1;
+                put(pos++, rk, scar[a], n0bw.x, __fadd_rn(sw[a], __int_as_float(n0bw.y)));
+              }
+            }
+          }
+          arc += __shfl_sync(0xffffffffu, inc, 31);
+          continue;
+        }
         int cnt = 0;
-        uint32_t e0it = 0xFF000000u, n0it = 0xFF000000u;  // first items, kept for the write walk
         if (has) {
           if (heavy) {
-            cnt = __ldg(&P.hcnt[(int)__ldg(&P.hbefore[w]) + __popc(hm & ((1u << lane) - 1u))]);
+            cnt = __ldg(&P.hcnt[(int)mt.w + __popc(hm & ((1u << lane) - 1u))]);
           } else {
 #pragma unroll 1
             for (int j = 0; j < ejn; ++j) {
-              const uint32_t it = __ldg(ep + j * 32);
-              if (j == 0) e0it = it;
+              const uint32_t it = j == 0 ? e0it : __ldg(ep + j * 32);
               const int32_t o = (int32_t)(it & 0xFFFFFFu);
               if (it < 0xFF000000u) cnt += (int)((((uint32_t)Vr[o >> 5].x) >> (o & 31)) & 1u);
             }
 #pragma unroll 1
             for (int j = 0; j < jn; ++j) {
-              const uint32_t it = __ldg(pe + j * 32);
-              if (j == 0) n0it = it;
+              const uint32_t it = j == 0 ? n0it : __ldg(pe + j * 32);
               const int32_t o = (int32_t)(it & 0xFFFFFFu);
               cnt += (int)(lc[it >> 24] * ((((uint32_t)Vd[o >> 5].x) >> (o & 31)) & 1u));
             }
@@ -753,7 +798,7 @@ __global__ void __launch_bounds__(kEmThreads) k_wave_emit(WaveArgs wa, const Com
           int64_t pos = arc + inc - cnt;
           state_out(vv.y + __popc(vw & ((1u << lane) - 1u)), col, pos);
           if (heavy) {
-            heavy_push(col, (int)__ldg(&P.hbefore[w]) + __popc(hm & ((1u << lane) - 1u)), pos);
+            heavy_push(col, (int)mt.w + __popc(hm & ((1u << lane) - 1u)), pos);
           } else if (cnt) {
 #pragma unroll 1
             for (int j = 0; j < ejn; ++j) {  // M3
@@ -762,7 +807,7 @@ __global__ void __launch_bounds__(kEmThreads) k_wave_emit(WaveArgs wa, const Com
               const int32_t o = (int32_t)(it & 0xFFFFFFu);
               const int2 v = Vr[o >> 5];
               if (!(((uint32_t)v.x >> (o & 31)) & 1u)) continue;
-              const int2 bw = __ldg(&P.eellcw[(size_t)(xe >> 8) * 32 + lane + j * 32]);
+              const int2 bw = j == 0 ? e0bw : __ldg(&P.eellcw[(size_t)(xe >> 8) * 32 + lane + j * 32]);
               put(pos++, v.y + __popc((uint32_t)v.x & ((1u << (o & 31)) - 1u)), FST_EPS, bw.x, __int_as_float(bw.y));
             }
 #pragma unroll 1
@@ -774,7 +819,7 @@ __global__ void __launch_bounds__(kEmThreads) k_wave_emit(WaveArgs wa, const Com
               const int2 v = Vd[o >> 5];
               if (!(((uint32_t)v.x >> (o & 31)) & 1u)) continue;
               const int32_t rk = v.y + __popc((uint32_t)v.x & ((1u << (o & 31)) - 1u));
-              const int2 bw = __ldg(&P.ellcw[(size_t)(xn >> 8) * 32 + lane + j * 32]);
+              const int2 bw = j == 0 ? n0bw : __ldg(&P.ellcw[(size_t)(xn >> 8) * 32 + lane + j * 32]);
               for (; m; m &= m - 1ull) {
                 const int a = __ffsll((long long)m) - 1;
                 put(pos++, rk, scar[a], bw.x, __fadd_rn(sw[a], __int_as_float(bw.y)));
@@ -1394,7 +1439,7 @@ fst_status wave_emit(const WavePlan& plan, const CompDev* d_comps, const int64_t
   P.wa.arcbase = arcbase;
   P.wa.wpre = wpre;
   P.wa.err = err;
-  const size_t smem = 16ull * P.wa.wprmax;
+  const size_t smem = 32ull * P.wa.wprmax;
   static size_t smem_set = 0;
   if (smem > 40 * 1024 && smem > smem_set) {
     FSTC_CUDA_TRY(cudaFuncSetAttribute(k_wave_emit, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
