@@ -1989,6 +1989,12 @@ int32_t* level_scratch() {
   return p;
 }
 
+cudaStream_t side_stream() {
+  static thread_local cudaStream_t ss = nullptr;
+  if (!ss && cudaStreamCreateWithFlags(&ss, cudaStreamNonBlocking) != cudaSuccess) ss = nullptr;
+  return ss;
+}
+
 cudaStream_t capture_stream() {
   static thread_local cudaStream_t cs = nullptr;
   if (!cs && cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking) != cudaSuccess) cs = nullptr;
@@ -2655,12 +2661,32 @@ fst_status compose_impl(int32_t n, const fst_handle* a, const fst_handle* b, cud
     cx.seedbase = d_seed2;
     if (wp.ok) {
       if (seed2[n] > 0 && seed1[n] > 0) {
-        st = wave_stage(wp, 2, cx.R, cx.V, s);
+        // the pass-1 counts need only R: they run on a side stream concurrently with stage 2 (on the SMs
+        // its clusters leave idle); the block sums over V join after stage 2
+        cudaStream_t s2 = side_stream();
+        if (!s2) {
+          set_error(FST_E_CUDA, "side stream creation failed");
+          return FST_E_CUDA;
+        }
+        cudaEvent_t e1 = nullptr, e2 = nullptr;
+        FSTC_CUDA_TRY(cudaEventCreateWithFlags(&e1, cudaEventDisableTiming));
+        FSTC_CUDA_TRY(cudaEventCreateWithFlags(&e2, cudaEventDisableTiming));
+        FSTC_CUDA_TRY(cudaEventRecord(e1, s));
+        st = wave_stage(wp, 2, cx.R, cx.V, s);  // first: its clusters take their SMs before the counts
         if (st) return st;
-        EventTimer tc(prof, s);
-        st = wave_count(wp, cx.V, cx.cnt8, cx.kept, s);
+        FSTC_CUDA_TRY(cudaStreamWaitEvent(s2, e1, 0));
+        {
+          EventTimer tc(prof, s2);
+          st = wave_count(wp, cx.R, cx.cnt8, s2);
+          if (st) return st;
+          FSTC_CUDA_TRY(cudaEventRecord(e2, s2));
+          stats.ms_count = tc.stop();
+        }
+        FSTC_CUDA_TRY(cudaStreamWaitEvent(s, e2, 0));
+        cudaEventDestroy(e1);
+        cudaEventDestroy(e2);
+        st = wave_kept(wp, cx.V, cx.kept, s);
         if (st) return st;
-        stats.ms_count = tc.stop();
       }
     } else if (seed2[n] > 0 && seed1[n] > 0) {
       k_seed<true><<<nblk(seed2[n], 256), 256, 0, s>>>(cx);

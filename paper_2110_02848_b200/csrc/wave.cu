@@ -435,9 +435,12 @@ __global__ void __launch_bounds__(kWThreads, 1) k_wave(WaveArgs wa) {
 }
 
 // ------------------------------------------------------------------------------ pass-1 counts
-// Per state (a, b) of C: the number of moves into V (= into R for a state of V) -- M1 over A's
-// out-arcs x B's out-items, M2 (A eps olabel, B stays), M3 (B eps ilabel, A stays) -- as cnt8
-// (saturated at 255: the emit recounts those) and kept[block] (exact).  One CTA per row.
+// Per pair (a, b) of R: the number of moves into R -- M1 over A's out-arcs x B's out-items, M2 (A eps
+// olabel, B stays), M3 (B eps ilabel, A stays) -- as cnt8 (saturated at 255: the general emit recounts
+// those) and, for heavy states, exactly (hcnt).  For a state of V the moves into R are its moves into V
+// (the target is accessible), i.e. its out-degree in C; the kernel needs only R, so it runs on a second
+// stream CONCURRENTLY with stage 2 (on the SMs the stage-2 clusters leave idle), and k_wave_kept sums
+// the counts over V.  One CTA per row.
 __global__ void __launch_bounds__(kCThreads) k_wave_count(WaveArgs wa) {
   __shared__ unsigned long long lm[kWLab];
   __shared__ uint32_t lc[kWLab];  // uniform rows: popc(lm[li]) (moves per matching item)
@@ -446,7 +449,7 @@ __global__ void __launch_bounds__(kCThreads) k_wave_count(WaveArgs wa) {
   extern __shared__ uint32_t csm[];  // [wprmax] V of the row's single destination row, [wprmax] V of the row
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr int nwarp = kCThreads / 32;
-  const uint32_t* __restrict__ Vg = wa.V;
+  const uint32_t* __restrict__ Vg = wa.R;  // counts against R (see above)
   uint32_t* Vd = csm;
   uint32_t* Vr = csm + wa.wprmax;
   for (int64_t t = blockIdx.x; t < wa.nrows; t += gridDim.x) {
@@ -534,11 +537,9 @@ __global__ void __launch_bounds__(kCThreads) k_wave_count(WaveArgs wa) {
           tot += (unsigned long long)cnt;
         }
       }
-      tot = warp_sum(tot);
-      if (lane == 0) wa.kept[C.K + (int64_t)r * bpr + blk] = tot;
+      (void)tot;
     }
     if (D.nheavy > 0) {
-      __syncthreads();  // kept[] stores of the warps before the heavy credits
       for (int h = 0; h < D.nheavy; ++h) {
         const int4 hv = __ldg(&D.heavy[h]);
         const int32_t col = hv.x;
@@ -560,11 +561,47 @@ __global__ void __launch_bounds__(kCThreads) k_wave_count(WaveArgs wa) {
         if (tid == 0) {
           wa.cnt8[(rowW + (col >> 5)) * 32 + (col & 31)] = (uint8_t)min(hsum, 255ull);
           wa.hcnt[C.hcnt_base + (int64_t)r * D.nheavy + h] = (int32_t)hsum;
-          atomicAdd(&wa.kept[C.K + (int64_t)r * bpr + (col >> 10)], hsum);
         }
         __syncthreads();
       }
     }
+  }
+}
+
+// ------------------------------------------------------------------------------ pass-1 block sums
+// kept[block] = sum of the out-degrees in C of the block's states (cnt8 of k_wave_count, exact counts of
+// heavy states from hcnt), OVERWRITTEN for every block.  One warp per block.
+__global__ void __launch_bounds__(256) k_wave_kept(WaveArgs wa, int64_t nblocks) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nw_all = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t g = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); g < nblocks; g += nw_all) {
+    int lo = 0, hi = wa.ncomp - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (wa.comps[mid].K <= g) lo = mid; else hi = mid - 1;
+    }
+    const WaveComp& C = wa.comps[lo];
+    const int64_t local = g - C.K;
+    const int32_t r = (int32_t)(local / C.bpr), j = (int32_t)(local - (int64_t)r * C.bpr);
+    const int wb = j * 32, nw = min(32, C.wpr - wb);
+    const int64_t rowW = C.W + (int64_t)r * C.wpr;
+    const WaveDir& D = C.bd[0];
+    const uint32_t myv = lane < nw ? __ldg(&wa.V[rowW + wb + lane]) : 0u;
+    const uint32_t myh = lane < nw ? __ldg(&D.hmask[wb + lane]) : 0u;
+    unsigned long long tot = 0;
+    for (int i = 0; i < nw; ++i) {
+      const uint32_t vw = __shfl_sync(0xffffffffu, myv, i);
+      if (!vw) continue;
+      const uint32_t hm = __shfl_sync(0xffffffffu, myh, i);
+      if (!((vw >> lane) & 1u)) continue;
+      if ((hm >> lane) & 1u)
+        tot += (unsigned long long)__ldg(&wa.hcnt[C.hcnt_base + (int64_t)r * D.nheavy + __ldg(&D.hbefore[wb + i]) +
+                                                 __popc(hm & ((1u << lane) - 1u))]);
+      else
+        tot += __ldg(&wa.cnt8[(rowW + wb + i) * 32 + lane]);
+    }
+    tot = warp_sum(tot);
+    if (lane == 0) wa.kept[g] = tot;
   }
 }
 
@@ -1262,6 +1299,7 @@ struct WavePlan::Impl {
   int G1 = 1, G2 = 1, nc1 = 0, nc2 = 0;
   size_t smem1 = 0, smem2 = 0;
   uint32_t cw1 = 0, cw2 = 0;
+  int64_t nblocks = 0;
 };
 
 WavePlan::WavePlan() : impl(new Impl) {}
@@ -1354,6 +1392,7 @@ fst_status wave_plan(int32_t n, const fst_handle* a, const fst_handle* b, const 
     C.VB = B->V;
     C.wpr = (B->V + 31) / 32;
     C.bpr = (C.wpr + kWordsPerBlock - 1) / kWordsPerBlock;
+    P.nblocks = std::max<int64_t>(P.nblocks, C.K + (int64_t)C.VA * C.bpr);
     for (int d = 0; d < 2; ++d) {
       const View& av = A->views[d == 0 ? kOutByOlabel : kInByOlabel];
       C.aoff[d] = av.off;
@@ -1414,19 +1453,29 @@ fst_status wave_stage(const WavePlan& plan, int stage, uint32_t* R, uint32_t* V,
   return stage == 1 ? launch_wave<false>(P.wa, P.G1, P.nc1, P.smem1, s) : launch_wave<true>(P.wa, P.G2, P.nc2, P.smem2, s);
 }
 
-fst_status wave_count(const WavePlan& plan, uint32_t* V, uint8_t* cnt8, unsigned long long* kept, cudaStream_t s) {
+fst_status wave_count(const WavePlan& plan, uint32_t* R, uint8_t* cnt8, cudaStream_t s) {
   WavePlan::Impl& P = *plan.impl;
-  P.wa.V = V;
+  P.wa.R = R;
   P.wa.cnt8 = cnt8;
-  P.wa.kept = kept;
-  const int64_t grid = std::min<int64_t>(std::max<int64_t>(P.wa.nrows, 1), (int64_t)sm_count() * 4);
   const size_t smem = 8ull * P.wa.wprmax;
   static size_t smem_set = 0;
   if (smem > 48 * 1024 && smem > smem_set) {
     FSTC_CUDA_TRY(cudaFuncSetAttribute(k_wave_count, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     smem_set = smem;
   }
+  const int64_t grid = std::min<int64_t>(std::max<int64_t>(P.wa.nrows, 1), (int64_t)sm_count() * 4);
   k_wave_count<<<(unsigned)grid, kCThreads, smem, s>>>(P.wa);
+  FSTC_LAUNCH_CHECK();
+  return FST_OK;
+}
+
+fst_status wave_kept(const WavePlan& plan, uint32_t* V, unsigned long long* kept, cudaStream_t s) {
+  WavePlan::Impl& P = *plan.impl;
+  P.wa.V = V;
+  P.wa.kept = kept;
+  const int64_t warps = std::max<int64_t>(P.nblocks, 1);
+  const int64_t grid = std::min<int64_t>((warps + 7) / 8, (int64_t)sm_count() * 16);
+  k_wave_kept<<<(unsigned)grid, 256, 0, s>>>(P.wa, P.nblocks);
   FSTC_LAUNCH_CHECK();
   return FST_OK;
 }

@@ -27,8 +27,11 @@ fst_status wave_plan(int32_t n, const fst_handle* a, const fst_handle* b, const 
                      cudaStream_t s, WavePlan* plan);
 // stage 1 writes every word of R, stage 2 every word of V (reads R).
 fst_status wave_stage(const WavePlan& plan, int stage, uint32_t* R, uint32_t* V, cudaStream_t s);
-// pass-1 counts: cnt8 of every state of C and kept[] of every block (overwritten).
-fst_status wave_count(const WavePlan& plan, uint32_t* V, uint8_t* cnt8, unsigned long long* kept, cudaStream_t s);
+// pass-1 counts of every pair of R (cnt8, saturated; exact for heavy states): needs only R, so it may run
+// on another stream concurrently with stage 2.
+fst_status wave_count(const WavePlan& plan, uint32_t* R, uint8_t* cnt8, cudaStream_t s);
+// pass-1 block sums over V: kept[] of every block (overwritten); after wave_count and stage 2.
+fst_status wave_kept(const WavePlan& plan, uint32_t* V, unsigned long long* kept, cudaStream_t s);
 // pass 2 (general emit replacement; no provenance): writes every composition's CSR from the numbering
 // (idbase / arcbase per block, wpre per word).  `err` counts internal inconsistencies (must stay 0).
 fst_status wave_emit(const WavePlan& plan, const struct CompDev* d_comps, const int64_t* d_tot, const int64_t* idbase,
