@@ -2808,7 +2808,11 @@ fst_status compose_impl(int32_t n, const fst_handle* a, const fst_handle* b, cud
     if (tp.ok) {
       launch_tile_emit(tp.emit, tp.grid_emit, tp.smem_emit, s, cx, comps[0], d_tot, tp.vr_rows);
       FSTC_LAUNCH_CHECK();
-    } else if (wp.ok && !want_prov) {
+    } else if (wp.ok && !want_prov && [&] {  // the wave emit indexes a composition's arcs with 32 bits
+                 for (int i = 0; i < n; ++i)
+                   if (tot[2 * i + 3] - tot[2 * i + 1] >= INT32_MAX) return false;
+                 return true;
+               }()) {
       st = wave_emit(wp, d_comps, d_tot, cx.idbase, cx.arcbase, cx.wpre, cx.V, (int32_t*)(cx.misc + 2), s);
       if (st) {
         cleanup();

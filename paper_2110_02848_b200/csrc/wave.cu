@@ -759,6 +759,7 @@ __global__ void __launch_bounds__(kEmThreads, 2) k_wave_emit(WaveArgs wa, const 
     }
     for (int blk = fast ? warp : bpr; blk < bpr; blk += nwarp) {
       int64_t arc = __ldg(&wa.arcbase[K + (int64_t)r * bpr + blk]) - arc_comp;
+      uint32_t arc32 = (uint32_t)arc;  // the straight-line words: 32-bit slots (composition arcs < 2^31)
       const int wb = blk * 32, nw = min(32, wpr - wb);
       // software pipeline: the first items (and their (olabel, weight)) of word w + 1 are loaded while word w
       // is processed
@@ -796,18 +797,34 @@ __global__ void __launch_bounds__(kEmThreads, 2) k_wave_emit(WaveArgs wa, const 
           const int cnt = (int)he + (hn ? (int)lc[n0it >> 24] : 0);
           const int inc = warp_incl_scan(cnt);
           if (has) {
-            int64_t pos = arc + inc - cnt;
-            state_out(vv.y + __popc(vw & ((1u << lane) - 1u)), col, pos);
-            if (he) put(pos++, ve.y + __popc((uint32_t)ve.x & ((1u << (oe & 31)) - 1u)), FST_EPS, e0bw.x, __int_as_float(e0bw.y));
+            uint32_t pos = arc32 + (uint32_t)(inc - cnt);
+            const uint32_t id = (uint32_t)vv.y + __popc(vw & ((1u << lane) - 1u));
+            __stcs((long long*)(P.row_ptr + id), (long long)pos);
+            __stcs(P.pair_a + id, r);
+            __stcs(P.pair_b + id, col);
+            P.is_start[id] = stA ? __ldg(&startB[col]) : (uint8_t)0;
+            P.is_accept[id] = acA ? __ldg(&accB[col]) : (uint8_t)0;
+            if (he) {
+              __stcs(P.dst + pos, ve.y + __popc((uint32_t)ve.x & ((1u << (oe & 31)) - 1u)));
+              __stcs(P.ilabel + pos, FST_EPS);
+              __stcs(P.olabel + pos, e0bw.x);
+              __stcs(P.weight + pos, __int_as_float(e0bw.y));
+              ++pos;
+            }
             if (hn) {
               const int32_t rk = vn.y + __popc((uint32_t)vn.x & ((1u << (on & 31)) - 1u));
-              for (unsigned long long m = mn; m; m &= m - 1ull) {
+              for (unsigned long long m = mn; m; m &= m - 1ull, ++pos) {
                 const int a = __ffsll((long long)m) - 1;
-                put(pos++, rk, scar[a], n0bw.x, __fadd_rn(sw[a], __int_as_float(n0bw.y)));
+                __stcs(P.dst + pos, rk);
+                __stcs(P.ilabel + pos, scar[a]);
+                __stcs(P.olabel + pos, n0bw.x);
+                __stcs(P.weight + pos, __fadd_rn(sw[a], __int_as_float(n0bw.y)));
               }
             }
           }
-          arc += __shfl_sync(0xffffffffu, inc, 31);
+          const uint32_t t = (uint32_t)__shfl_sync(0xffffffffu, inc, 31);
+          arc32 += t;
+          arc += t;
           continue;
         }
         int cnt = 0;
@@ -865,6 +882,7 @@ __global__ void __launch_bounds__(kEmThreads, 2) k_wave_emit(WaveArgs wa, const 
           }
         }
         arc += wtot;
+        arc32 += (uint32_t)wtot;
       }
     }
     for (int blk = fast ? bpr : warp; blk < bpr; blk += nwarp) {
