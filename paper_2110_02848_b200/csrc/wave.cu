@@ -204,6 +204,9 @@ __global__ void __launch_bounds__(kWThreads, 1) k_wave(WaveArgs wa) {
         __pipeline_commit();
       }
     }
+    for (int i = tid; i < kWLab; i += kWThreads) lm[i] = 0ull;
+    if (tid < kWLab / 32) lp[tid] = 0u;
+    __syncthreads();
     int hot = -1, hp = 0, rb = 0;
     for (int step = 0; step < VA; ++step) {
       r = kS2 ? step : VA - 1 - step;
@@ -215,10 +218,7 @@ __global__ void __launch_bounds__(kWThreads, 1) k_wave(WaveArgs wa) {
       const int64_t rowW = W + (int64_t)r * wpr;
       const int32_t d = nd;
       const int32_t mykey = nkey, myoth = noth;
-      if (kS2) __pipeline_wait_prior(0);
-      for (int i = tid; i < kWLab; i += kWThreads) lm[i] = 0ull;
-      if (tid < kWLab / 32) lp[tid] = 0u;
-      __syncthreads();
+      if (kS2) __pipeline_wait_prior(0);  // (lm / lp were cleared after the previous step's pull)
       // loads for the next row (used next step): its A arcs and, stage 2, its R row
       if (step + 1 < VA) {
         const int rn = kS2 ? r + 1 : r - 1;
@@ -359,6 +359,8 @@ __global__ void __launch_bounds__(kWThreads, 1) k_wave(WaveArgs wa) {
       }
       // ---- publish the slices, gather the whole row
       cl.sync();
+      for (int i = tid; i < kWLab; i += kWThreads) lm[i] = 0ull;  // for the next row (the pulls are done)
+      if (tid < kWLab / 32) lp[tid] = 0u;
       for (int k = 0; k < G; ++k) {
         const int kw0 = misc[4 + k], n = misc[5 + k] - kw0;
         const uint32_t* src = k == crank ? pb : cl.map_shared_rank(pb, k);
@@ -391,7 +393,7 @@ __global__ void __launch_bounds__(kWThreads, 1) k_wave(WaveArgs wa) {
           };
           auto hubs = [&]() {
             for (int h = 0; h < C.nhub; ++h) {
-              __syncthreads();
+              if (h > 0 || !kS2) __syncthreads();  // (stage 2 starts with the hubs, right after a barrier)
               const int32_t t = __ldg(&C.hub_col[h]);
               const uint32_t* __restrict__ S = C.hub_src + (size_t)h * wpr;
               if (kS2) {  // V(r, t) if some eps source of t is in V (and (r, t) in R)
