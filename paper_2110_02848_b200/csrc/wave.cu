@@ -492,16 +492,28 @@ __global__ void __launch_bounds__(kCThreads) k_wave_count(WaveArgs wa) {
     auto inV = [&](int32_t row, int32_t col) -> int {
       return (int)((__ldg(&Vg[W + (int64_t)row * wpr + (col >> 5)]) >> (col & 31)) & 1u);
     };
+    const bool line = uni && meps == 0ull;  // trellis rows: straight-line words (<= 1 item of each kind)
     for (int blk = warp; blk < bpr; blk += nwarp) {
       const int wb = blk * 32, nw = min(32, wpr - wb);
       const uint32_t myw = lane < nw ? __ldg(&Vg[rowW + wb + lane]) : 0u;
       const uint32_t myh = lane < nw ? __ldg(&D.hmask[wb + lane]) : 0u;
+      const uint32_t myx = lane < nw ? __ldg(&D.wo[wb + lane]) : 0u;
+      const uint32_t mye = lane < nw ? __ldg(&D.ewo[wb + lane]) : 0u;
       unsigned long long tot = 0;
       for (int i = 0; i < nw; ++i) {
         const uint32_t vw = __shfl_sync(0xffffffffu, myw, i) & ~__shfl_sync(0xffffffffu, myh, i);
         if (!vw) continue;
         const int w = wb + i;
         const int32_t col = w * 32 + lane;
+        const uint32_t xn = __shfl_sync(0xffffffffu, myx, i), xe = __shfl_sync(0xffffffffu, mye, i);
+        if (line && (xn & 255u) <= 1u && (xe & 255u) <= 1u) {
+          const uint32_t itn = (xn & 255u) ? __ldg(D.ell + (size_t)(xn >> 8) * 32 + lane) : 0xFF000000u;
+          const uint32_t ite = (xe & 255u) ? __ldg(D.eell + (size_t)(xe >> 8) * 32 + lane) : 0xFF000000u;
+          const int32_t on = (int32_t)(itn & 0xFFFFFFu), oe = (int32_t)(ite & 0xFFFFFFu);
+          const int cnt = (int)(lc[itn >> 24] * bit_of(Vd, on)) + ((ite >> 24) == 1u ? (int)bit_of(Vr, oe) : 0);
+          wa.cnt8[(rowW + w) * 32 + lane] = ((vw >> lane) & 1u) ? (uint8_t)cnt : (uint8_t)0;
+          continue;
+        }
         if ((vw >> lane) & 1u) {
           int cnt = 0;
           const int jn = __ldg(&D.wmax[w]), ejn = __ldg(&D.ewmax[w]);
@@ -585,22 +597,32 @@ __global__ void __launch_bounds__(256) k_wave_kept(WaveArgs wa, int64_t nblocks)
     const WaveComp& C = wa.comps[lo];
     const int64_t local = g - C.K;
     const int32_t r = (int32_t)(local / C.bpr), j = (int32_t)(local - (int64_t)r * C.bpr);
-    const int wb = j * 32, nw = min(32, C.wpr - wb);
+    const int w = j * 32 + lane;  // one lane per word
     const int64_t rowW = C.W + (int64_t)r * C.wpr;
     const WaveDir& D = C.bd[0];
-    const uint32_t myv = lane < nw ? __ldg(&wa.V[rowW + wb + lane]) : 0u;
-    const uint32_t myh = lane < nw ? __ldg(&D.hmask[wb + lane]) : 0u;
     unsigned long long tot = 0;
-    for (int i = 0; i < nw; ++i) {
-      const uint32_t vw = __shfl_sync(0xffffffffu, myv, i);
-      if (!vw) continue;
-      const uint32_t hm = __shfl_sync(0xffffffffu, myh, i);
-      if (!((vw >> lane) & 1u)) continue;
-      if ((hm >> lane) & 1u)
-        tot += (unsigned long long)__ldg(&wa.hcnt[C.hcnt_base + (int64_t)r * D.nheavy + __ldg(&D.hbefore[wb + i]) +
-                                                 __popc(hm & ((1u << lane) - 1u))]);
-      else
-        tot += __ldg(&wa.cnt8[(rowW + wb + i) * 32 + lane]);
+    if (w < C.wpr) {
+      const uint32_t hm = __ldg(&D.hmask[w]);
+      uint32_t vw = __ldg(&wa.V[rowW + w]);
+      if (vw & hm) {  // heavy states of V: exact counts
+        const int64_t hb = C.hcnt_base + (int64_t)r * D.nheavy + __ldg(&D.hbefore[w]);
+        for (uint32_t m = vw & hm; m; m &= m - 1u)
+          tot += (unsigned long long)__ldg(&wa.hcnt[hb + __popc(hm & ((1u << (__ffs(m) - 1)) - 1u))]);
+        vw &= ~hm;
+      }
+      if (vw) {
+        const uint4* q = (const uint4*)(wa.cnt8 + (rowW + w) * 32);
+        const uint4 c0 = __ldg(q), c1 = __ldg(q + 1);
+        const uint32_t cw[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const uint32_t sel = (vw >> (4 * k)) & 15u;
+          if (!sel) continue;
+          const uint32_t x = cw[k];
+          tot += ((sel & 1u) ? (x & 255u) : 0u) + ((sel & 2u) ? ((x >> 8) & 255u) : 0u) +
+                 ((sel & 4u) ? ((x >> 16) & 255u) : 0u) + ((sel & 8u) ? (x >> 24) : 0u);
+        }
+      }
     }
     tot = warp_sum(tot);
     if (lane == 0) wa.kept[g] = tot;
