@@ -1,6 +1,7 @@
 """Small workload for compute-sanitizer (memcheck / racecheck / synccheck): configs[0] and configs[1]
 compositions, configs[3] shape at V=2000/D=8 on both paths (push levels only, the tile path, and the
-tile path with every level bottom-up), a batch, the eps-filtered variant, provenance + gradient scatter.
+tile path with every level bottom-up), a batch, the wave path (trellises, a trellis batch, eps DAGs), the
+eps-filtered variant, provenance + gradient scatter.
 Checks each result against the oracle so a sanitizer run also proves the instrumented run is correct."""
 import os
 import sys
@@ -37,6 +38,21 @@ cs = p.fst_compose_batch([p.fst_create(a) for a in As], [p.fst_create(b) for b i
 for s, c in enumerate(cs):
     pins.assert_canonical_equal(pins.canonicalize_rows(c.to_host(), Bs[s].num_states),
                                 oracle.canonical(As[s], Bs[s]), f"batch {s}")
+# the wave path (topological A): a lexicon o emissions trellis (heavy root / closure state, M3 hubs), a
+# batch of trellises over one lexicon (one cluster each), random DAGs with eps (non-uniform rows), with and
+# without the shared-memory ELL cache
+p.fst_set_wave_mode(2)
+A3, B3 = fstgen.config_c3(num_words=200, T=12)
+chk(A3, B3, "wave c3 200/12")
+for s in range(3):
+    chk(fstgen.random_dag(40, 5, 4, 0.2, 50 + s), fstgen.random_graph(50, 3, 4, 60 + s, acceptor=False, eps_prob=0.2),
+        f"wave dag {s}")
+As5 = [fstgen.emissions_graph(5 + 3 * i, 10000 + i) for i in range(5)]
+cs = p.fst_compose_batch([p.fst_create(a) for a in As5], [p.fst_create(B3)] * len(As5))
+for i, c in enumerate(cs):
+    pins.assert_canonical_equal(pins.canonicalize_rows(c.to_host(), B3.num_states), oracle.canonical(As5[i], B3),
+                                f"wave batch {i}")
+p.fst_set_wave_mode(1)
 A, B = fstgen.config_c2(0, V=300)
 p.compose(A, B, eps_filter=True)
 c = p.fst_compose(p.fst_create(A), p.fst_create(B), provenance=True)

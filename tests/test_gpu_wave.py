@@ -160,3 +160,17 @@ def test_wave_provenance_uses_general_emit(fst):
     pw, pl = cw.provenance(), cl.provenance()
     for x, y in zip(pw, pl):
         assert np.array_equal(np.asarray(x), np.asarray(y))
+
+
+def test_wave_deterministic_batch(fst):
+    """Repeated calls give identical arrays (clusters take compositions from a counter in any order, the
+    counts run on a side stream: the result must not depend on the schedule)."""
+    As, B = fstgen.config_c5(num_utts=9, num_words=1500)
+    As = [fstgen.emissions_graph(20 + 7 * i, 10000 + i) for i in range(9)]
+    hb = fst.fst_create(B)
+    ha = [fst.fst_create(A) for A in As]
+    runs = [[c.to_host() for c in fst.fst_compose_batch(ha, [hb] * len(ha))] for _ in range(3)]
+    for r in runs[1:]:
+        for x, y in zip(runs[0], r):
+            for k in x:
+                assert np.array_equal(np.asarray(x[k]), np.asarray(y[k])), k
