@@ -114,6 +114,7 @@ struct WaveArgs {
   unsigned long long* kept;
   int32_t* next;         // composition counter of the stage kernels
   uint32_t cache_words;  // shared-memory words for the ELL cache of a stage CTA
+  long long* probe;      // FSTC_WAVE_PROBE=1: per-cluster cycle counts of the row-step phases (else null)
   int64_t nrows;         // rows of all compositions (count tasks)
   int32_t* hcnt;         // exact kept-move counts of heavy states (the emit's arc offsets)
   // emit inputs (numbering of compose.cu: per-block id / arc bases, per-word popcount prefixes)
@@ -142,6 +143,12 @@ __global__ void __launch_bounds__(kWThreads, 1) k_wave(WaveArgs wa) {
   uint32_t* pullbuf = Rbuf + (kS2 ? 2 * wprmax : 0);   // [2][rng] this CTA's pulled words (read by the cluster)
   uint32_t* wo = pullbuf + 2 * rng;                    // [rng] per word of this CTA: ELL row (relative) << 8 | rows
   uint32_t* cache = wo + rng;                          // this CTA's ELL rows, then its heavy columns' items
+  struct ClosurePtrs {
+    const uint32_t *S, *Ma, *Mh;
+    const int2* E;
+    const int32_t* H;
+  };
+  __shared__ ClosurePtrs cp_;  // the M3 pass's tables (shared or global memory)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   uint32_t* vis = kS2 ? wa.V : wa.R;
   constexpr int dir = kS2 ? 1 : 0;
@@ -186,6 +193,45 @@ __global__ void __launch_bounds__(kWThreads, 1) k_wave(WaveArgs wa) {
       const int32_t nh = h1 > h0 ? __ldg(&D.heavy[h1 - 1]).w - hb0 : 0;
       for (int32_t i = tid; i < nh; i += kWThreads) cache[nell + i] = __ldg(&D.hitems[hb0 + i]);
     }
+    // the M3 pass's tables (hub source bitmaps, this stage's two relevance masks, hub columns, the other
+    // eps arcs) in shared memory after the ELL cache when they fit (they are read every row step)
+    const int neps = C.neps, nhub = C.nhub;
+    // (the table pointers live in shared memory: registers are the stage kernels' scarce resource)
+    if (tid == 0) {
+      cp_.S = C.hub_src;
+      cp_.Ma = C.rel[kS2 ? 3 : 0];
+      cp_.Mh = C.rel[kS2 ? 2 : 1];
+      cp_.E = C.eps;
+      cp_.H = C.hub_col;
+    }
+    {
+      const uint32_t used = cached ? nell + (uint32_t)(h1 > h0 ? __ldg(&D.heavy[h1 - 1]).w - hb0 : 0) : 0u;
+      const uint64_t need = (uint64_t)nhub * wpr + 2ull * wpr + 2ull * neps + (uint64_t)nhub + 1;  // (+1: alignment)
+      if ((neps > 0 || nhub > 0) && used + need <= wa.cache_words) {
+        uint32_t* q = cache + used;
+        const uint32_t* gMa = C.rel[kS2 ? 3 : 0];
+        const uint32_t* gMh = C.rel[kS2 ? 2 : 1];
+        for (int i = tid; i < nhub * wpr; i += kWThreads) q[i] = __ldg(&C.hub_src[i]);
+        for (int i = tid; i < wpr; i += kWThreads) {
+          q[nhub * wpr + i] = __ldg(&gMa[i]);
+          q[nhub * wpr + wpr + i] = __ldg(&gMh[i]);
+        }
+        uint32_t* qa = q + nhub * wpr + 2 * wpr;
+        if ((uintptr_t)qa & 7u) ++qa;  // int2 alignment
+        int2* qe = (int2*)qa;
+        for (int i = tid; i < neps; i += kWThreads) qe[i] = __ldg(&C.eps[i]);
+        int32_t* qh = (int32_t*)(qe + neps);
+        for (int i = tid; i < nhub; i += kWThreads) qh[i] = __ldg(&C.hub_col[i]);
+        __syncthreads();  // (thread 0's global pointers written above are replaced)
+        if (tid == 0) {
+          cp_.S = q;
+          cp_.Ma = q + nhub * wpr;
+          cp_.Mh = q + nhub * wpr + wpr;
+          cp_.E = qe;
+          cp_.H = qh;
+        }
+      }
+    }
     // heavy columns' items: shared memory when cached, else global (generic pointer)
     const uint32_t* hitp = cached ? cache + nell - hb0 : D.hitems;
     // the first row's A arcs and (stage 2) R row are loaded ahead, like every next row's
@@ -207,6 +253,19 @@ __global__ void __launch_bounds__(kWThreads, 1) k_wave(WaveArgs wa) {
     for (int i = tid; i < kWLab; i += kWThreads) lm[i] = 0ull;
     if (tid < kWLab / 32) lp[tid] = 0u;
     __syncthreads();
+#ifdef FSTC_WAVE_PROBE_BUILD  // per-phase cycle counts (a build with -DFSTC_WAVE_PROBE_BUILD + FSTC_WAVE_PROBE=1)
+    long long pc[8] = {0, 0, 0, 0, 0, 0, 0, 0}, pt = clock64();
+    const bool probing = wa.probe != nullptr && tid == 0 && crank == 0;
+    auto probe = [&](int k) {
+      if (probing) {
+        const long long x = clock64();
+        pc[k] += x - pt;
+        pt = x;
+      }
+    };
+#else
+    auto probe = [](int) {};
+#endif
     int hot = -1, hp = 0, rb = 0;
     for (int step = 0; step < VA; ++step) {
       r = kS2 ? step : VA - 1 - step;
@@ -219,22 +278,6 @@ __global__ void __launch_bounds__(kWThreads, 1) k_wave(WaveArgs wa) {
       const int32_t d = nd;
       const int32_t mykey = nkey, myoth = noth;
       if (kS2) __pipeline_wait_prior(0);  // (lm / lp were cleared after the previous step's pull)
-      // loads for the next row (used next step): its A arcs and, stage 2, its R row
-      if (step + 1 < VA) {
-        const int rn = kS2 ? r + 1 : r - 1;
-        ne0 = __ldg(&aoff[rn]);
-        nd = __ldg(&aoff[rn + 1]) - ne0;
-        if (tid < nd) {
-          nkey = __ldg(&akey[ne0 + tid]);
-          noth = __ldg(&aother[ne0 + tid]);
-        }
-        if (kS2) {
-          const int64_t rw = W + (int64_t)rn * wpr;
-          uint32_t* dstR = Rbuf + (rb ^ 1) * wprmax;
-          for (int i = tid; i < wpr; i += kWThreads) __pipeline_memcpy_async(&dstR[i], &wa.R[rw + i], 4);
-          __pipeline_commit();
-        }
-      }
       bool slot_hot = true;
       if (tid < d) {
         const int li = mykey + 2;
@@ -248,6 +291,7 @@ __global__ void __launch_bounds__(kWThreads, 1) k_wave(WaveArgs wa) {
       // uniform row: every A arc of the row leads to the hot row (a trellis) -- a move exists iff the
       // item's label occurs in the row and the target column is set in the hot row
       const bool uni = __syncthreads_and(slot_hot) != 0;
+      probe(0);
       const unsigned long long meps = lm[1];  // A arcs with olabel eps: M2 (B stays) and M1 eps:eps
       const bool rowseed = __ldg(&seedA[r]) != 0;
       auto test = [&](int32_t row, int32_t col) -> bool {
@@ -333,6 +377,7 @@ __global__ void __launch_bounds__(kWThreads, 1) k_wave(WaveArgs wa) {
         for (int w = w0 + tid; w < w1; w += kWThreads) pb[w - w0] = 0u;
       }
       // ---- heavy columns of this CTA: the whole CTA walks the column's items
+      probe(1);
       if (h1 > h0 && d > 0) {
         __syncthreads();
         for (int h = h0; h < h1; ++h) {
@@ -358,60 +403,91 @@ __global__ void __launch_bounds__(kWThreads, 1) k_wave(WaveArgs wa) {
         }
       }
       // ---- publish the slices, gather the whole row
+      // loads for the next row (used next step): its A arcs and, stage 2, its R row -- issued here so that
+      // their latency overlaps the cluster barrier and the gather
+      if (step + 1 < VA) {
+        const int rn = kS2 ? r + 1 : r - 1;
+        ne0 = __ldg(&aoff[rn]);
+        nd = __ldg(&aoff[rn + 1]) - ne0;
+        if (tid < nd) {
+          nkey = __ldg(&akey[ne0 + tid]);
+          noth = __ldg(&aother[ne0 + tid]);
+        }
+        if (kS2) {
+          const int64_t rw = W + (int64_t)rn * wpr;
+          uint32_t* dstR = Rbuf + (rb ^ 1) * wprmax;
+          for (int i = tid; i < wpr; i += kWThreads) __pipeline_memcpy_async(&dstR[i], &wa.R[rw + i], 4);
+          __pipeline_commit();
+        }
+      }
+      probe(2);
       cl.sync();
+      probe(3);
       for (int i = tid; i < kWLab; i += kWThreads) lm[i] = 0ull;  // for the next row (the pulls are done)
       if (tid < kWLab / 32) lp[tid] = 0u;
-      for (int k = 0; k < G; ++k) {
-        const int kw0 = misc[4 + k], n = misc[5 + k] - kw0;
-        const uint32_t* src = k == crank ? pb : cl.map_shared_rank(pb, k);
-        for (int i = tid; i < n; i += kWThreads) cur[kw0 + i] = src[i];
+      if (rng <= kWThreads) {  // every slice has <= one word per thread: all remote loads in flight at once
+        uint32_t v[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          v[k] = 0u;
+          if (k < G && tid < misc[5 + k] - misc[4 + k]) v[k] = (k == crank ? pb : cl.map_shared_rank(pb, k))[tid];
+        }
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          if (k < G && tid < misc[5 + k] - misc[4 + k]) cur[misc[4 + k] + tid] = v[k];
+      } else {
+        for (int k = 0; k < G; ++k) {
+          const int kw0 = misc[4 + k], n = misc[5 + k] - kw0;
+          const uint32_t* src = k == crank ? pb : cl.map_shared_rank(pb, k);
+          for (int i = tid; i < n; i += kWThreads) cur[kw0 + i] = src[i];
+        }
       }
       __syncthreads();
+      probe(4);
       // ---- M3 fixed point of the row (B's eps-input arcs; A stays).  Hub targets (many eps sources,
       // kept as a bitmap) are word-parallel, the other eps arcs one thread each.  Pass order: stage 2
       // hubs then arcs, stage 1 arcs then hubs; another pass runs only when a new bit could feed a unit
       // already processed in this pass (the relevance masks of DESIGN.md §6c), so lexicon closures take
       // one pass.
-      if (C.neps > 0 || C.nhub > 0) {
+      if (neps > 0 || nhub > 0) {
         for (;;) {
           int changed = 0;
           auto arcs = [&]() {
-            for (int i = tid; i < C.neps; i += kWThreads) {
-              const int2 a = __ldg(&C.eps[i]);  // B arc a.x -> a.y with ilabel eps
+            for (int i = tid; i < neps; i += kWThreads) {
+              const int2 a = cp_.E[i];  // B arc a.x -> a.y with ilabel eps
               if (kS2) {  // (r, a.x) in V  =>  (r, a.y) in V  if in R
                 if (bit_of(cur, a.x) && !bit_of(cur, a.y) && bit_of(Rrow, a.y)) {
                   atomicOr(&cur[a.y >> 5], 1u << (a.y & 31));
-                  if (bit_of(C.rel[3], a.y)) changed = 1;
+                  if (bit_of(cp_.Ma, a.y)) changed = 1;
                 }
               } else {    // (r, a.y) in R  =>  (r, a.x) in R
                 if (bit_of(cur, a.y) && !bit_of(cur, a.x)) {
                   atomicOr(&cur[a.x >> 5], 1u << (a.x & 31));
-                  if (bit_of(C.rel[0], a.x)) changed = 1;
+                  if (bit_of(cp_.Ma, a.x)) changed = 1;
                 }
               }
             }
           };
           auto hubs = [&]() {
-            for (int h = 0; h < C.nhub; ++h) {
+            for (int h = 0; h < nhub; ++h) {
               if (h > 0 || !kS2) __syncthreads();  // (stage 2 starts with the hubs, right after a barrier)
-              const int32_t t = __ldg(&C.hub_col[h]);
-              const uint32_t* __restrict__ S = C.hub_src + (size_t)h * wpr;
+              const int32_t t = cp_.H[h];
+              const uint32_t* S = cp_.S + (size_t)h * wpr;
               if (kS2) {  // V(r, t) if some eps source of t is in V (and (r, t) in R)
                 if (bit_of(cur, t) || !bit_of(Rrow, t)) continue;  // uniform
                 int any = 0;
-                for (int i = tid; i < wpr; i += kWThreads) any |= (cur[i] & __ldg(&S[i])) != 0u;
+                for (int i = tid; i < wpr; i += kWThreads) any |= (cur[i] & S[i]) != 0u;
                 if (__syncthreads_or(any) && tid == 0) {
                   cur[t >> 5] |= 1u << (t & 31);
-                  if (bit_of(C.rel[2], t)) changed = 1;
+                  if (bit_of(cp_.Mh, t)) changed = 1;
                 }
               } else {    // R(r, t)  =>  every eps source of t is in R
                 if (!bit_of(cur, t)) continue;  // uniform
-                const uint32_t* __restrict__ M = C.rel[1];
                 for (int i = tid; i < wpr; i += kWThreads) {
-                  const uint32_t x = cur[i], y = x | __ldg(&S[i]);
+                  const uint32_t x = cur[i], y = x | S[i];
                   if (y != x) {
                     cur[i] = y;
-                    if ((y & ~x) & __ldg(&M[i])) changed = 1;
+                    if ((y & ~x) & cp_.Mh[i]) changed = 1;
                   }
                 }
               }
@@ -428,11 +504,20 @@ __global__ void __launch_bounds__(kWThreads, 1) k_wave(WaveArgs wa) {
           if (!__syncthreads_or(changed)) break;
         }
       }
+      probe(5);
       for (int i = w0 + tid; i < w1; i += kWThreads) vis[rowW + i] = cur[i];
+      probe(6);
       hot = r;
       hp = cp;
       rb ^= 1;
     }
+#ifdef FSTC_WAVE_PROBE_BUILD
+    if (probing) {
+      const int cid = blockIdx.x / G;
+      for (int k = 0; k < 7; ++k) wa.probe[cid * 8 + k] += pc[k];
+      wa.probe[cid * 8 + 7] += VA;
+    }
+#endif
   }
 }
 
@@ -1283,7 +1368,7 @@ fst_status ensure_wave_ell(fst* B, cudaStream_t s) {
   return FST_OK;
 }
 
-constexpr size_t kWSmem = 227 * 1024;  // dynamic shared memory of a stage CTA (one CTA per SM)
+constexpr size_t kWSmem = 225 * 1024;  // dynamic shared memory of a stage CTA (one CTA per SM; + static)
 
 // shared memory of a stage CTA without the ELL cache (the cache takes the rest of kWSmem)
 size_t wave_smem(int wprmax, int G, bool s2) {
@@ -1492,6 +1577,31 @@ fst_status wave_stage(const WavePlan& plan, int stage, uint32_t* R, uint32_t* V,
     return e && e[0] == '0';
   }();
   P.wa.cache_words = nocache ? 0u : (stage == 1 ? P.cw1 : P.cw2);
+  static const bool probe_on = [] {
+    const char* e = getenv("FSTC_WAVE_PROBE");
+    return e && e[0] == '1';
+  }();
+  static long long* d_probe = nullptr;
+  const int ncl = stage == 1 ? P.nc1 : P.nc2;
+  if (probe_on && !d_probe) FSTC_CUDA_TRY(cudaMalloc(&d_probe, 8 * 8 * 1024));
+  if (probe_on) FSTC_CUDA_TRY(cudaMemsetAsync(d_probe, 0, 8 * 8 * 1024, s));
+  P.wa.probe = probe_on ? d_probe : nullptr;
+  if (probe_on) {
+    fst_status st = stage == 1 ? launch_wave<false>(P.wa, P.G1, P.nc1, P.smem1, s) : launch_wave<true>(P.wa, P.G2, P.nc2, P.smem2, s);
+    if (st) return st;
+    std::vector<long long> h(8 * 1024);
+    FSTC_CUDA_TRY(cudaMemcpyAsync(h.data(), d_probe, 8 * 8 * ncl, cudaMemcpyDeviceToHost, s));
+    FSTC_CUDA_TRY(cudaStreamSynchronize(s));
+    int best = 0;
+    for (int c = 0; c < ncl; ++c)
+      if (h[c * 8 + 7] > h[best * 8 + 7]) best = c;
+    const double rows = (double)std::max(1ll, h[best * 8 + 7]);
+    fprintf(stderr, "wave probe stage %d cluster %d rows %.0f cycles/row: setup %.0f pull %.0f heavy %.0f csync %.0f gather %.0f closure %.0f store %.0f\n",
+            stage, best, rows, h[best * 8 + 0] / rows, h[best * 8 + 1] / rows, h[best * 8 + 2] / rows, h[best * 8 + 3] / rows,
+            h[best * 8 + 4] / rows, h[best * 8 + 5] / rows, h[best * 8 + 6] / rows);
+    P.wa.probe = nullptr;
+    return FST_OK;
+  }
   return stage == 1 ? launch_wave<false>(P.wa, P.G1, P.nc1, P.smem1, s) : launch_wave<true>(P.wa, P.G2, P.nc2, P.smem2, s);
 }
 
