@@ -125,6 +125,13 @@ struct WaveArgs {
 };
 
 __device__ __forceinline__ uint32_t bit_of(const uint32_t* row, int32_t col) { return (row[col >> 5] >> (col & 31)) & 1u; }
+// shared-memory load at a 32-bit shared-window address, for data that does not change while it is read
+// (not volatile: the compiler may schedule it freely)
+__device__ __forceinline__ uint32_t lds32(uint32_t a) {
+  uint32_t v;
+  asm("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
+}
 
 // ------------------------------------------------------------------------------ stage kernels
 template <bool kS2>
@@ -299,11 +306,32 @@ __global__ void __launch_bounds__(kWThreads, 1) k_wave(WaveArgs wa) {
         return (__ldcg(&vis[W + (int64_t)row * wpr + (col >> 5)]) >> (col & 31)) & 1u;
       };
       // ---- pull: one warp per word, one lane per column (light columns: items from the ELL)
-      auto pull = [&](const uint32_t* __restrict__ ellb) {
+      auto pull = [&](const uint32_t* __restrict__ ellb, bool smem_items) {
         if (uni && !rowseed) {  // trellis rows: label present in the row AND target set in the hot row
           bool full = true;     // the row has every label of the light items: no label test
 #pragma unroll
           for (int k = 0; k < kWLab / 32; ++k) full &= (lp[k] & D.blab[k]) == D.blab[k];
+          if (full && meps == 0ull && smem_items) {
+            // the common trellis case on 32-bit shared-window addresses computed once (the generic
+            // pointers cost a window-base recomputation per access under this kernel's register limit);
+            // wo, the item cache and the hot row are not written during the pull
+            const uint32_t wo_s = (uint32_t)__cvta_generic_to_shared(wo) - 4u * (uint32_t)w0;
+            const uint32_t it_s = (uint32_t)__cvta_generic_to_shared(ellb) + 4u * (uint32_t)lane;
+            const uint32_t hr_s = (uint32_t)__cvta_generic_to_shared(hrow);
+            for (int w = w0 + warp; w < w1; w += kWWarps) {
+              const uint32_t x = lds32(wo_s + 4u * (uint32_t)w);
+              uint32_t a = it_s + ((x >> 8) << 7), in = 0u;
+#pragma unroll 1
+              for (int j = (int)(x & 255u); j > 0; --j, a += 128u) {
+                const uint32_t it = lds32(a);  // padding (label index 255) never matches
+                in |= (it < 0xFF000000u ? lds32(hr_s + (((it & 0xFFFFFFu) >> 5) << 2)) : 0u) >> (it & 31u);
+              }
+              uint32_t word = __ballot_sync(0xffffffffu, (in & 1u) != 0u);
+              if (kS2) word &= Rrow[w];
+              if (lane == 0) pb[w - w0] = word;
+            }
+            return;
+          }
           for (int w = w0 + warp; w < w1; w += kWWarps) {
             const uint32_t x = wo[w - w0];
             const uint32_t* pe = ellb + (size_t)(x >> 8) * 32 + lane;
@@ -371,8 +399,8 @@ __global__ void __launch_bounds__(kWThreads, 1) k_wave(WaveArgs wa) {
         }
       };
       if (d > 0 || rowseed) {
-        if (cached) pull(cache);
-        else pull(D.ell + (size_t)er0 * 32);
+        if (cached) pull(cache, true);
+        else pull(D.ell + (size_t)er0 * 32, false);
       } else {  // no A arcs and no seeds: the row is empty before the M3 pass
         for (int w = w0 + tid; w < w1; w += kWThreads) pb[w - w0] = 0u;
       }
