@@ -111,9 +111,11 @@ typedef struct {
   int64_t emit_launches;  /* of which emit kernels */
   int64_t expand_launches;/* of which BFS level kernels */
   int64_t staged_tasks;   /* chunk tasks of the BFS levels that used shared-memory staging (wave path: CTAs per cluster) */
-  int32_t tile_path;      /* 1: the call ran the tile kernels (bottom-up levels, count, emit) */
+  int32_t tile_path;      /* 1: the call ran the tile kernels (bottom-up levels, count, emit);
+                             2: the wave kernels (row-by-row stages for a topologically numbered A, §6c) */
   int32_t pull_levels;    /* BFS rounds (both stages) that ran bottom-up on the tile kernels */
-  float ms_count;         /* tile path: pass-1 count kernel (profiling only; included in ms_stage2) */
+  float ms_count;         /* tile path: pass-1 count kernel (profiling only; included in ms_stage2); wave path:
+                             the counts on the side stream, concurrent with stage 2 (not additive) */
 } fst_compose_stats;
 
 /* Upload + validate + build label-sorted adjacency views.  On success *out is a
