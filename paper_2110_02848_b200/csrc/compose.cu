@@ -1992,10 +1992,16 @@ int32_t* level_scratch() {
   return p;
 }
 
-cudaStream_t side_stream() {
-  static thread_local cudaStream_t ss = nullptr;
-  if (!ss && cudaStreamCreateWithFlags(&ss, cudaStreamNonBlocking) != cudaSuccess) ss = nullptr;
-  return ss;
+// A per-thread side stream with the priority of `s` (the halves of a split batch run at different
+// priorities, and so do their concurrent counts).
+cudaStream_t side_stream(cudaStream_t s) {
+  static thread_local cudaStream_t ss[2] = {nullptr, nullptr};
+  int pr = 0, lo = 0, hi = 0;
+  cudaStreamGetPriority(s, &pr);
+  cudaDeviceGetStreamPriorityRange(&lo, &hi);
+  const int k = (pr < lo) ? 1 : 0;  // numerically lower = higher priority
+  if (!ss[k] && cudaStreamCreateWithPriority(&ss[k], cudaStreamNonBlocking, k ? hi : lo) != cudaSuccess) ss[k] = nullptr;
+  return ss[k];
 }
 
 cudaStream_t capture_stream() {
@@ -2666,7 +2672,7 @@ fst_status compose_run(int32_t n, const fst_handle* a, const fst_handle* b, cuda
       if (seed2[n] > 0 && seed1[n] > 0) {
         // the pass-1 counts need only R: they run on a side stream concurrently with stage 2 (on the SMs
         // its clusters leave idle); the block sums over V join after stage 2
-        cudaStream_t s2 = side_stream();
+        cudaStream_t s2 = side_stream(s);
         if (!s2) {
           set_error(FST_E_CUDA, "side stream creation failed");
           return FST_E_CUDA;
@@ -2858,105 +2864,9 @@ fst_status compose_run(int32_t n, const fst_handle* a, const fst_handle* b, cuda
 }
 
 
-// A batch on the wave path runs as TWO pipelines (the longer and the shorter half of its compositions)
-// on two streams driven by two host threads: the shorter half's counts, numbering and emit then run
-// while the longer half's row steps (the batch's critical path) still occupy their clusters, instead of
-// every composition waiting for the longest one.  Each half gets half of the SMs for its clusters.
-// Results are identical (every composition is numbered and emitted on its own).
-constexpr int32_t kSplitMin = 8;
-
-bool split_enabled() {
-  static const bool on = [] {
-    const char* e = getenv("FSTC_WAVE_SPLIT");
-    return !(e && e[0] == '0');
-  }();
-  return on;
-}
-
-cudaStream_t split_stream(int k) {
-  static cudaStream_t ss[2] = {nullptr, nullptr};
-  static std::once_flag once;
-  std::call_once(once, [] {
-    for (auto& x : ss)
-      if (cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking) != cudaSuccess) x = nullptr;
-  });
-  return ss[k];
-}
-
 fst_status compose_impl(int32_t n, const fst_handle* a, const fst_handle* b, cudaStream_t s, fst_handle* c,
                         uint32_t flags) {
-  if (n < kSplitMin || (flags & FST_COMPOSE_PROVENANCE) || !split_enabled())
-    return compose_run(n, a, b, s, c, flags);
-  for (int i = 0; i < n; ++i) {
-    if (!a[i] || !b[i]) return compose_run(n, a, b, s, c, flags);  // (reports the error)
-    fst_status st = ensure_views(a[i], s);
-    if (!st) st = ensure_views(b[i], s);
-    if (st) return st;
-  }
-  if (!wave_batch_eligible(n, a, b, s)) return compose_run(n, a, b, s, c, flags);
-  fst_status st = init_kernels();
-  if (st) return st;
-  cudaStream_t sg[2] = {split_stream(0), split_stream(1)};
-  if (!sg[0] || !sg[1]) return compose_run(n, a, b, s, c, flags);
-  // halves by rows: [0] the longer half, [1] the shorter
-  std::vector<int> idx(n);
-  for (int i = 0; i < n; ++i) idx[i] = i;
-  std::stable_sort(idx.begin(), idx.end(), [&](int x, int y) { return a[x]->V > a[y]->V; });
-  const int nl = (n + 1) / 2;
-  std::vector<fst_handle> ga[2], gb[2], gc[2];
-  for (int k = 0; k < n; ++k) {
-    const int g = k < nl ? 0 : 1;
-    ga[g].push_back(a[idx[k]]);
-    gb[g].push_back(b[idx[k]]);
-  }
-  for (int g = 0; g < 2; ++g) gc[g].assign(ga[g].size(), nullptr);
-  cudaEvent_t e0 = nullptr, eg[2] = {nullptr, nullptr};
-  FSTC_CUDA_TRY(cudaEventCreateWithFlags(&e0, cudaEventDisableTiming));
-  FSTC_CUDA_TRY(cudaEventCreateWithFlags(&eg[0], cudaEventDisableTiming));
-  FSTC_CUDA_TRY(cudaEventCreateWithFlags(&eg[1], cudaEventDisableTiming));
-  FSTC_CUDA_TRY(cudaEventRecord(e0, s));
-  FSTC_CUDA_TRY(cudaStreamWaitEvent(sg[0], e0, 0));
-  FSTC_CUDA_TRY(cudaStreamWaitEvent(sg[1], e0, 0));
-  const int budget = sm_count() / 2;
-  int dev = 0;
-  cudaGetDevice(&dev);
-  fst_status st1 = FST_OK;
-  std::string err1;
-  std::thread th([&] {
-    cudaSetDevice(dev);
-    wave_cta_budget() = budget;
-    st1 = compose_run((int32_t)ga[1].size(), ga[1].data(), gb[1].data(), sg[1], gc[1].data(), flags);
-    if (st1) err1 = fst_last_error();
-    wave_cta_budget() = 0;
-  });
-  wave_cta_budget() = budget;
-  fst_status st0 = compose_run((int32_t)ga[0].size(), ga[0].data(), gb[0].data(), sg[0], gc[0].data(), flags);
-  wave_cta_budget() = 0;
-  th.join();
-  for (int g = 0; g < 2; ++g) {
-    cudaEventRecord(eg[g], sg[g]);
-    cudaStreamWaitEvent(s, eg[g], 0);
-  }
-  cudaEventDestroy(e0);
-  cudaEventDestroy(eg[0]);
-  cudaEventDestroy(eg[1]);
-  if (st0 || st1) {
-    for (int g = 0; g < 2; ++g)
-      for (auto h : gc[g]) delete h;
-    if (!st0) set_error(st1, "%s", err1.c_str());
-    return st0 ? st0 : st1;
-  }
-  // the outputs belong to the caller's stream from here on (their buffers are released there; `s` has
-  // waited for both halves)
-  for (int k = 0; k < n; ++k) {
-    const int g = k < nl ? 0 : 1;
-    fst* h = gc[g][g == 0 ? k : k - nl];
-    h->stream = s;
-    for (auto& buf : h->buffers)
-      if (buf) buf->stream = s;
-    c[idx[k]] = h;
-  }
-  return FST_OK;
+  return compose_run(n, a, b, s, c, flags);
 }
 }  // namespace fstc
 

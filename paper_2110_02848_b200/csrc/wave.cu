@@ -1677,7 +1677,9 @@ fst_status wave_count(const WavePlan& plan, uint32_t* R, uint8_t* cnt8, cudaStre
     FSTC_CUDA_TRY(cudaFuncSetAttribute(k_wave_count, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     smem_set = smem;
   }
-  const int64_t grid = std::min<int64_t>(std::max<int64_t>(P.wa.nrows, 1), (int64_t)sm_count() * 4);
+  // one CTA per row (not persistent): CTAs retire quickly, so a higher-priority stream (the longer
+  // half of a split batch) gets SMs as soon as it needs them
+  const int64_t grid = std::min<int64_t>(std::max<int64_t>(P.wa.nrows, 1), (int64_t)INT32_MAX);
   k_wave_count<<<(unsigned)grid, kCThreads, smem, s>>>(P.wa);
   FSTC_LAUNCH_CHECK();
   return FST_OK;
@@ -1708,7 +1710,9 @@ fst_status wave_emit(const WavePlan& plan, const CompDev* d_comps, const int64_t
     FSTC_CUDA_TRY(cudaFuncSetAttribute(k_wave_emit, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     smem_set = smem;
   }
-  const int64_t grid = std::min<int64_t>(std::max<int64_t>(P.wa.nrows, 1), (int64_t)sm_count() * 4);
+  // one CTA per row (not persistent): CTAs retire quickly, so a higher-priority stream (the longer
+  // half of a split batch) gets SMs as soon as it needs them
+  const int64_t grid = std::min<int64_t>(std::max<int64_t>(P.wa.nrows, 1), (int64_t)INT32_MAX);
   k_wave_emit<<<(unsigned)grid, kEmThreads, smem, s>>>(P.wa, d_comps, d_tot);
   FSTC_LAUNCH_CHECK();
   return FST_OK;

@@ -175,15 +175,3 @@ def test_wave_deterministic_batch(fst):
             for k in x:
                 assert np.array_equal(np.asarray(x[k]), np.asarray(y[k])), k
 
-
-def test_wave_split_batch_equals_unsplit(fst):
-    """Batches of >= 8 wave compositions run as two concurrent halves (two streams, two host threads);
-    the arrays equal those of the same batch run as one pipeline (FSTC_WAVE_SPLIT=0 is read once per
-    process, so the reference here is the level path, whose arrays the wave path reproduces)."""
-    As, B = fstgen.config_c5(num_utts=11, num_words=1200)
-    As = [fstgen.emissions_graph(15 + 9 * i, 10000 + i) for i in range(11)]
-    got, lev, st = both_paths(fst, [(A, B) for A in As])
-    for i, (g, l) in enumerate(zip(got, lev)):
-        for k in g:
-            assert np.array_equal(np.asarray(g[k]), np.asarray(l[k])), (i, k)
-    pins.assert_canonical_equal(pins.canonicalize_rows(got[3], B.num_states), oracle.canonical(As[3], B), "split item 3")
