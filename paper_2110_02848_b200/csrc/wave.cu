@@ -1460,35 +1460,6 @@ struct WavePlan::Impl {
 WavePlan::WavePlan() : impl(new Impl) {}
 WavePlan::~WavePlan() { delete impl; }
 
-int& wave_cta_budget() {
-  static thread_local int b = 0;
-  return b;
-}
-
-bool wave_batch_eligible(int32_t n, const fst_handle* a, const fst_handle* b, cudaStream_t s) {
-  const int mode = wave_mode_ref().load();
-  if (mode == 0 || n <= 0) return false;
-  int32_t maxrows = 0, wprmax = 0;
-  for (int i = 0; i < n; ++i) {
-    fst* A = a[i];
-    fst* B = b[i];
-    if (!A->has_views || !B->has_views) return false;
-    if (A->views[kOutByOlabel].max_deg > kWSlots || A->views[kInByOlabel].max_deg > kWSlots) return false;
-    if (B->max_ilabel > 252 || B->V >= (1 << 24)) return false;
-    maxrows = std::max(maxrows, A->V);
-    wprmax = std::max(wprmax, (B->V + 31) / 32);
-  }
-  if (mode == 1 && maxrows > kWaveAutoRows) return false;
-  if (wave_smem(wprmax, 1, true) + 1024 > kWSmem) return false;
-  for (int i = 0; i < n; ++i) {
-    bool topo = false;
-    if (topo_of(a[i], s, &topo) != FST_OK || !topo) return false;
-  }
-  for (int i = 0; i < n; ++i)  // (built here, on one thread: the halves of a split batch share B handles)
-    if (ensure_wave_ell(b[i], s) != FST_OK) return false;
-  return true;
-}
-
 fst_status wave_plan(int32_t n, const fst_handle* a, const fst_handle* b, const int64_t* W, const int64_t* K,
                      cudaStream_t s, WavePlan* plan) {
   plan->ok = false;
@@ -1533,8 +1504,7 @@ fst_status wave_plan(int32_t n, const fst_handle* a, const fst_handle* b, const 
   double best = -1.0;
   for (int G : {8, 4, 2, 1}) {
     if (G > 1 && wprmax < 32 * G) continue;
-    int c = max_clusters<true>(G, kWSmem);
-    if (wave_cta_budget() > 0) c = std::min(c, wave_cta_budget() / G);  // a split batch's share of the SMs
+    const int c = max_clusters<true>(G, kWSmem);
     if (c <= 0) continue;
     std::vector<int64_t> load(std::min(c, n), 0);
     for (int32_t rws : rows_desc) *std::min_element(load.begin(), load.end()) += rws;
@@ -1555,10 +1525,6 @@ fst_status wave_plan(int32_t n, const fst_handle* a, const fst_handle* b, const 
   P.cw2 = (uint32_t)((kWSmem - wave_smem(wprmax, P.G2, true)) / 4);
   P.nc1 = max_clusters<false>(P.G1, P.smem1);
   P.nc2 = max_clusters<true>(P.G2, P.smem2);
-  if (wave_cta_budget() > 0) {
-    P.nc1 = std::min(P.nc1, std::max(1, wave_cta_budget() / P.G1));
-    P.nc2 = std::min(P.nc2, std::max(1, wave_cta_budget() / P.G2));
-  }
   if (P.nc1 <= 0 || P.nc2 <= 0) return FST_OK;
   P.nc1 = std::min(P.nc1, n);
   P.nc2 = std::min(P.nc2, n);

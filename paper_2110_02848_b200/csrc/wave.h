@@ -37,10 +37,5 @@ fst_status wave_kept(const WavePlan& plan, uint32_t* V, unsigned long long* kept
 fst_status wave_emit(const WavePlan& plan, const struct CompDev* d_comps, const int64_t* d_tot, const int64_t* idbase,
                      const int64_t* arcbase, const uint16_t* wpre, uint32_t* V, int32_t* err, cudaStream_t s);
 void wave_mode_set(int mode);
-// The wave path would take this batch (views must exist; checks A's topological order).
-bool wave_batch_eligible(int32_t n, const fst_handle* a, const fst_handle* b, cudaStream_t s);
-// Per host thread: CTAs the wave stage kernels may occupy (0 = the whole GPU); a split batch gives each
-// half its share so both run concurrently.
-int& wave_cta_budget();
 
 }  // namespace fstc
