@@ -28,9 +28,6 @@
 
 #include <algorithm>
 #include <atomic>
-#include <mutex>
-#include <string>
-#include <thread>
 #include <vector>
 
 #include "fstc_handle.h"
@@ -1992,8 +1989,7 @@ int32_t* level_scratch() {
   return p;
 }
 
-// A per-thread side stream with the priority of `s` (the halves of a split batch run at different
-// priorities, and so do their concurrent counts).
+// A per-thread side stream with the priority of `s`.
 cudaStream_t side_stream(cudaStream_t s) {
   static thread_local cudaStream_t ss[2] = {nullptr, nullptr};
   int pr = 0, lo = 0, hi = 0;
