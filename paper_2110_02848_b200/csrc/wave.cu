@@ -1639,7 +1639,7 @@ fst_status wave_count(const WavePlan& plan, uint32_t* R, uint8_t* cnt8, cudaStre
   P.wa.cnt8 = cnt8;
   const size_t smem = 8ull * P.wa.wprmax;
   static std::atomic<size_t> smem_set{0};
-  if (smem > 48 * 1024 && smem > smem_set) {
+  if (smem > smem_set) {  // (dynamic + static may pass the 48 KB default below that size)
     FSTC_CUDA_TRY(cudaFuncSetAttribute(k_wave_count, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     smem_set = smem;
   }
@@ -1672,7 +1672,7 @@ fst_status wave_emit(const WavePlan& plan, const CompDev* d_comps, const int64_t
   P.wa.err = err;
   const size_t smem = 32ull * P.wa.wprmax;
   static std::atomic<size_t> smem_set{0};
-  if (smem > 40 * 1024 && smem > smem_set) {
+  if (smem > smem_set) {  // (dynamic + static may pass the 48 KB default below that size)
     FSTC_CUDA_TRY(cudaFuncSetAttribute(k_wave_emit, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     smem_set = smem;
   }

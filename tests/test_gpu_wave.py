@@ -175,3 +175,12 @@ def test_wave_deterministic_batch(fst):
             for k in x:
                 assert np.array_equal(np.asarray(x[k]), np.asarray(y[k])), k
 
+
+
+@pytest.mark.parametrize("words", [5000, 5600, 6200])
+def test_wave_lexicon_sizes(fst, words):
+    """Lexicon sizes around the shared-memory thresholds of the count / emit kernels (their staged rows
+    grow with V_B): the dynamic + static shared memory passes the 48 KB launch default in this range."""
+    As, B = fstgen.config_c5(num_utts=2, num_words=words)
+    As = [fstgen.emissions_graph(12, 10000), fstgen.emissions_graph(9, 10001)]
+    check_pairs(fst, [(A, B) for A in As], f"lexicon {words}")
