@@ -156,6 +156,7 @@ __global__ void __launch_bounds__(kWThreads, 1) k_wave(WaveArgs wa) {
     const int32_t* H;
   };
   __shared__ ClosurePtrs cp_;  // the M3 pass's tables (shared or global memory)
+  __shared__ uint32_t* peer_row[2][8];  // [buffer][rank]: the cluster CTAs' row buffers (DSMEM)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   uint32_t* vis = kS2 ? wa.V : wa.R;
   constexpr int dir = kS2 ? 1 : 0;
@@ -188,6 +189,7 @@ __global__ void __launch_bounds__(kWThreads, 1) k_wave(WaveArgs wa) {
       misc[3] = nell + nh <= (int64_t)wa.cache_words ? 1 : 0;
     }
     if (tid <= G) misc[4 + tid] = (int)((int64_t)wpr * tid / G);
+    if (tid < 2 * G) peer_row[tid / G][tid % G] = cl.map_shared_rank(rowbuf + (tid / G) * wprmax, tid % G);
     __syncthreads();
     const int h0 = misc[1], h1 = misc[2];
     const bool cached = misc[3] != 0;
@@ -279,7 +281,6 @@ __global__ void __launch_bounds__(kWThreads, 1) k_wave(WaveArgs wa) {
       const int cp = hp ^ 1;
       uint32_t* cur = rowbuf + cp * wprmax;
       const uint32_t* hrow = rowbuf + hp * wprmax;
-      uint32_t* pb = pullbuf + cp * rng;
       const uint32_t* Rrow = Rbuf + rb * wprmax;
       const int64_t rowW = W + (int64_t)r * wpr;
       const int32_t d = nd;
@@ -328,7 +329,7 @@ __global__ void __launch_bounds__(kWThreads, 1) k_wave(WaveArgs wa) {
               }
               uint32_t word = __ballot_sync(0xffffffffu, (in & 1u) != 0u);
               if (kS2) word &= Rrow[w];
-              if (lane == 0) pb[w - w0] = word;
+              if (lane < G) peer_row[cp][lane][w] = word;  // into every cluster CTA's copy of the row
             }
             return;
           }
@@ -360,7 +361,7 @@ __global__ void __launch_bounds__(kWThreads, 1) k_wave(WaveArgs wa) {
             }
             uint32_t word = __ballot_sync(0xffffffffu, (in & 1u) != 0u);
             if (kS2) word &= Rrow[w];
-            if (lane == 0) pb[w - w0] = word;
+            if (lane < G) peer_row[cp][lane][w] = word;
           }
           return;
         }
@@ -395,14 +396,14 @@ __global__ void __launch_bounds__(kWThreads, 1) k_wave(WaveArgs wa) {
             }
           }
           const uint32_t word = __ballot_sync(0xffffffffu, in);
-          if (lane == 0) pb[w - w0] = word;
+          if (lane < G) peer_row[cp][lane][w] = word;
         }
       };
       if (d > 0 || rowseed) {
         if (cached) pull(cache, true);
         else pull(D.ell + (size_t)er0 * 32, false);
       } else {  // no A arcs and no seeds: the row is empty before the M3 pass
-        for (int w = w0 + tid; w < w1; w += kWThreads) pb[w - w0] = 0u;
+        for (int i = tid; i < (w1 - w0) * G; i += kWThreads) peer_row[cp][i % G][w0 + i / G] = 0u;
       }
       // ---- heavy columns of this CTA: the whole CTA walks the column's items
       probe(1);
@@ -427,10 +428,10 @@ __global__ void __launch_bounds__(kWThreads, 1) k_wave(WaveArgs wa) {
               for (unsigned long long m = lm[li]; m && !found; m &= m - 1ull) found = test(srow[__ffsll((long long)m) - 1], o);
             }
           }
-          if (__syncthreads_or(found) && tid == 0) pb[(col >> 5) - w0] |= 1u << (col & 31);
+          if (__syncthreads_or(found) && tid < G) atomicOr(&peer_row[cp][tid][col >> 5], 1u << (col & 31));
         }
       }
-      // ---- publish the slices, gather the whole row
+      // ---- the cluster barrier publishes the row (pushed into every CTA's copy during the pull)
       // loads for the next row (used next step): its A arcs and, stage 2, its R row -- issued here so that
       // their latency overlaps the cluster barrier and the gather
       if (step + 1 < VA) {
@@ -453,23 +454,7 @@ __global__ void __launch_bounds__(kWThreads, 1) k_wave(WaveArgs wa) {
       probe(3);
       for (int i = tid; i < kWLab; i += kWThreads) lm[i] = 0ull;  // for the next row (the pulls are done)
       if (tid < kWLab / 32) lp[tid] = 0u;
-      if (rng <= kWThreads) {  // every slice has <= one word per thread: all remote loads in flight at once
-        uint32_t v[8];
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          v[k] = 0u;
-          if (k < G && tid < misc[5 + k] - misc[4 + k]) v[k] = (k == crank ? pb : cl.map_shared_rank(pb, k))[tid];
-        }
-#pragma unroll
-        for (int k = 0; k < 8; ++k)
-          if (k < G && tid < misc[5 + k] - misc[4 + k]) cur[misc[4 + k] + tid] = v[k];
-      } else {
-        for (int k = 0; k < G; ++k) {
-          const int kw0 = misc[4 + k], n = misc[5 + k] - kw0;
-          const uint32_t* src = k == crank ? pb : cl.map_shared_rank(pb, k);
-          for (int i = tid; i < n; i += kWThreads) cur[kw0 + i] = src[i];
-        }
-      }
+      // (every CTA pushed its words into all the cluster's copies of the row: the barrier completes them)
       __syncthreads();
       probe(4);
       // ---- M3 fixed point of the row (B's eps-input arcs; A stays).  Hub targets (many eps sources,
