@@ -48,7 +48,7 @@ namespace cg = cooperative_groups;
 namespace fstc {
 namespace {
 
-constexpr int kWThreads = 1024;
+constexpr int kWThreads = 512;
 constexpr int kWWarps = kWThreads / 32;
 constexpr int kWHeavy = 32;    // B columns with more items (in a direction) are walked by the whole CTA
 constexpr int kWSlots = 64;    // A arcs per row (label -> slot masks are 64-bit)
@@ -322,9 +322,16 @@ __global__ void __launch_bounds__(kWThreads, 1) k_wave(WaveArgs wa) {
             for (int w = w0 + warp; w < w1; w += kWWarps) {
               const uint32_t x = lds32(wo_s + 4u * (uint32_t)w);
               uint32_t a = it_s + ((x >> 8) << 7), in = 0u;
+              int j = (int)(x & 255u);
 #pragma unroll 1
-              for (int j = (int)(x & 255u); j > 0; --j, a += 128u) {
-                const uint32_t it = lds32(a);  // padding (label index 255) never matches
+              for (; j >= 2; j -= 2, a += 256u) {  // two independent item -> hot-row load chains in flight
+                const uint32_t i0 = lds32(a), i1 = lds32(a + 128u);  // padding (label index 255) never matches
+                const uint32_t h0 = i0 < 0xFF000000u ? lds32(hr_s + (((i0 & 0xFFFFFFu) >> 5) << 2)) : 0u;
+                const uint32_t h1 = i1 < 0xFF000000u ? lds32(hr_s + (((i1 & 0xFFFFFFu) >> 5) << 2)) : 0u;
+                in |= (h0 >> (i0 & 31u)) | (h1 >> (i1 & 31u));
+              }
+              if (j) {
+                const uint32_t it = lds32(a);
                 in |= (it < 0xFF000000u ? lds32(hr_s + (((it & 0xFFFFFFu) >> 5) << 2)) : 0u) >> (it & 31u);
               }
               uint32_t word = __ballot_sync(0xffffffffu, (in & 1u) != 0u);
