@@ -14,7 +14,8 @@ SOURCES = ["api.cu", "create.cu", "compose.cu", "scan.cu", "memory.cu", "forward
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xcompiler", "-O2", "--expt-relaxed-constexpr", "--extended-lambda",
-         "-I", os.path.join(ROOT, "include")] + (["-DFSTC_WAVE_PROBE_BUILD"] if os.environ.get("FSTC_WAVE_PROBE_BUILD") == "1" else [])
+         "-I", os.path.join(ROOT, "include")] + (["-DFSTC_WAVE_PROBE_BUILD"] if os.environ.get("FSTC_WAVE_PROBE_BUILD") == "1" else []) + \
+        ["-D" + d for d in os.environ.get("FSTC_BUILD_DEFS", "").split()]  # build experiments: "FSTC_WAVE_THREADS=256 ..."
 # no --use_fast_math: the emit add must be IEEE binary32 round-to-nearest-even (reading 12)
 
 

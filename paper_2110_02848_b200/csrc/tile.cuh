@@ -27,7 +27,10 @@
 //   k_tile_count        pass-1 arc counts: kept moves per 1024-pair block / word.
 //   k_tile_emit         pass 2: writes the composed CSR at scan-derived slots.
 
-constexpr int kTThreads = 1024;          // pull / count CTAs (1 per SM: the 64-bit RT takes the smem)
+#ifndef FSTC_T_THREADS
+#define FSTC_T_THREADS 1024
+#endif
+constexpr int kTThreads = FSTC_T_THREADS;  // pull / count CTAs (1 per SM: the 64-bit RT takes the smem)
 constexpr int kTWarps = kTThreads / 32;
 #ifndef FSTC_E_THREADS
 #define FSTC_E_THREADS 1024

@@ -48,12 +48,21 @@ namespace cg = cooperative_groups;
 namespace fstc {
 namespace {
 
-constexpr int kWThreads = 512;
+#ifndef FSTC_WAVE_THREADS  // (build experiments: FSTC_BUILD_DEFS="FSTC_WAVE_THREADS=n" python build.py)
+#define FSTC_WAVE_THREADS 512
+#endif
+constexpr int kWThreads = FSTC_WAVE_THREADS;
 constexpr int kWWarps = kWThreads / 32;
 constexpr int kWHeavy = 32;    // B columns with more items (in a direction) are walked by the whole CTA
 constexpr int kWSlots = 64;    // A arcs per row (label -> slot masks are 64-bit)
 constexpr int kWLab = 256;     // label index = label + 2 (eps = 1); 255 = ELL padding (never set)
-constexpr int kCThreads = 512; // count CTAs
+#ifndef FSTC_WC_THREADS
+#define FSTC_WC_THREADS 256
+#endif
+#ifndef FSTC_WC_MINB
+#define FSTC_WC_MINB 4
+#endif
+constexpr int kCThreads = FSTC_WC_THREADS; // count CTAs
 constexpr int kEpsHub = 64;    // eps in-arcs that make a column an M3 hub (source set kept as a bitmap)
 constexpr int kEpsHubMax = 16;
 
@@ -548,7 +557,7 @@ __global__ void __launch_bounds__(kWThreads, 1) k_wave(WaveArgs wa) {
 // (the target is accessible), i.e. its out-degree in C; the kernel needs only R, so it runs on a second
 // stream CONCURRENTLY with stage 2 (on the SMs the stage-2 clusters leave idle), and k_wave_kept sums
 // the counts over V.  One CTA per row.
-__global__ void __launch_bounds__(kCThreads) k_wave_count(WaveArgs wa) {
+__global__ void __launch_bounds__(kCThreads, FSTC_WC_MINB) k_wave_count(WaveArgs wa) {
   __shared__ unsigned long long lm[kWLab];
   __shared__ uint32_t lc[kWLab];  // uniform rows: popc(lm[li]) (moves per matching item)
   __shared__ int32_t srow[kWSlots];
@@ -743,9 +752,15 @@ __global__ void __launch_bounds__(256) k_wave_kept(WaveArgs wa, int64_t nblocks)
 // popcount below it; the row itself and (uniform rows) its single destination row are staged as (V word,
 // rank) pairs.  Heavy states (> kWHeavy B arcs) take their exact count from k_wave_count and are written
 // by the whole CTA.
-constexpr int kEmThreads = 512;
+#ifndef FSTC_WEM_THREADS
+#define FSTC_WEM_THREADS 384
+#endif
+#ifndef FSTC_WEM_MINB
+#define FSTC_WEM_MINB 2
+#endif
+constexpr int kEmThreads = FSTC_WEM_THREADS;
 constexpr int kEmHeavyQ = 256;
-__global__ void __launch_bounds__(kEmThreads, 2) k_wave_emit(WaveArgs wa, const CompDev* __restrict__ cd,
+__global__ void __launch_bounds__(kEmThreads, FSTC_WEM_MINB) k_wave_emit(WaveArgs wa, const CompDev* __restrict__ cd,
                                                           const int64_t* __restrict__ tot) {
   __shared__ unsigned long long lm[kWLab];
   __shared__ uint32_t lc[kWLab];
