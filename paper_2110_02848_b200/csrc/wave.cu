@@ -53,6 +53,10 @@ namespace {
 #endif
 constexpr int kWThreads = FSTC_WAVE_THREADS;
 constexpr int kWWarps = kWThreads / 32;
+#ifndef FSTC_WAVE_WPI
+#define FSTC_WAVE_WPI 4
+#endif
+constexpr int kWpi = FSTC_WAVE_WPI;  // words per warp iteration of the trellis pull
 constexpr int kWHeavy = 32;    // B columns with more items (in a direction) are walked by the whole CTA
 constexpr int kWSlots = 64;    // A arcs per row (label -> slot masks are 64-bit)
 constexpr int kWLab = 256;     // label index = label + 2 (eps = 1); 255 = ELL padding (never set)
@@ -322,30 +326,41 @@ __global__ void __launch_bounds__(kWThreads, 1) k_wave(WaveArgs wa) {
 #pragma unroll
           for (int k = 0; k < kWLab / 32; ++k) full &= (lp[k] & D.blab[k]) == D.blab[k];
           if (full && meps == 0ull && smem_items) {
-            // the common trellis case on 32-bit shared-window addresses computed once (the generic
-            // pointers cost a window-base recomputation per access under this kernel's register limit);
-            // wo, the item cache and the hot row are not written during the pull
+            // the common trellis case on 32-bit shared-window addresses computed once (generic pointers
+            // cost a window-base computation per access); wo, the item cache and the hot row are not
+            // written during the pull
             const uint32_t wo_s = (uint32_t)__cvta_generic_to_shared(wo) - 4u * (uint32_t)w0;
             const uint32_t it_s = (uint32_t)__cvta_generic_to_shared(ellb) + 4u * (uint32_t)lane;
             const uint32_t hr_s = (uint32_t)__cvta_generic_to_shared(hrow);
-            for (int w = w0 + warp; w < w1; w += kWWarps) {
-              const uint32_t x = lds32(wo_s + 4u * (uint32_t)w);
-              uint32_t a = it_s + ((x >> 8) << 7), in = 0u;
-              int j = (int)(x & 255u);
+            // kWpi words per warp iteration: their item -> hot-row load chains are in flight together
+            for (int wb = w0 + warp; wb < w1; wb += kWpi * kWWarps) {
+              uint32_t x[kWpi], in[kWpi];
+              int jm = 0;
+#pragma unroll
+              for (int u = 0; u < kWpi; ++u) {
+                const int w = wb + u * kWWarps;
+                x[u] = w < w1 ? lds32(wo_s + 4u * (uint32_t)w) : 0u;
+                in[u] = 0u;
+                jm = max(jm, (int)(x[u] & 255u));
+              }
 #pragma unroll 1
-              for (; j >= 2; j -= 2, a += 256u) {  // two independent item -> hot-row load chains in flight
-                const uint32_t i0 = lds32(a), i1 = lds32(a + 128u);  // padding (label index 255) never matches
-                const uint32_t h0 = i0 < 0xFF000000u ? lds32(hr_s + (((i0 & 0xFFFFFFu) >> 5) << 2)) : 0u;
-                const uint32_t h1 = i1 < 0xFF000000u ? lds32(hr_s + (((i1 & 0xFFFFFFu) >> 5) << 2)) : 0u;
-                in |= (h0 >> (i0 & 31u)) | (h1 >> (i1 & 31u));
+              for (int j = 0; j < jm; ++j) {
+                uint32_t it[kWpi];
+#pragma unroll
+                for (int u = 0; u < kWpi; ++u)  // padding (label index 255) never matches
+                  it[u] = j < (int)(x[u] & 255u) ? lds32(it_s + ((x[u] >> 8) << 7) + 128u * (uint32_t)j) : 0xFF000000u;
+#pragma unroll
+                for (int u = 0; u < kWpi; ++u)
+                  in[u] |= (it[u] < 0xFF000000u ? lds32(hr_s + (((it[u] & 0xFFFFFFu) >> 5) << 2)) : 0u) >> (it[u] & 31u);
               }
-              if (j) {
-                const uint32_t it = lds32(a);
-                in |= (it < 0xFF000000u ? lds32(hr_s + (((it & 0xFFFFFFu) >> 5) << 2)) : 0u) >> (it & 31u);
+#pragma unroll
+              for (int u = 0; u < kWpi; ++u) {
+                const int w = wb + u * kWWarps;
+                if (w >= w1) break;  // (warp-uniform)
+                uint32_t word = __ballot_sync(0xffffffffu, (in[u] & 1u) != 0u);
+                if (kS2) word &= Rrow[w];
+                if (lane < G) peer_row[cp][lane][w] = word;  // into every cluster CTA's copy of the row
               }
-              uint32_t word = __ballot_sync(0xffffffffu, (in & 1u) != 0u);
-              if (kS2) word &= Rrow[w];
-              if (lane < G) peer_row[cp][lane][w] = word;  // into every cluster CTA's copy of the row
             }
             return;
           }
