@@ -920,26 +920,25 @@ __global__ void __launch_bounds__(kEmThreads, FSTC_WEM_MINB) k_wave_emit(WaveArg
       int64_t arc = __ldg(&wa.arcbase[K + (int64_t)r * bpr + blk]) - arc_comp;
       uint32_t arc32 = (uint32_t)arc;  // the straight-line words: 32-bit slots (composition arcs < 2^31)
       const int wb = blk * 32, nw = min(32, wpr - wb);
-      // software pipeline: the first items (and their (olabel, weight)) of word w + 1 are loaded while word w
-      // is processed
-      uint32_t pn = 0xFF000000u, pe0 = 0xFF000000u;
-      int2 pbn = make_int2(0, 0), pbe = make_int2(0, 0);
-      auto prefetch = [&](int w) {
-        const uint4 m = wmeta[w];
-        pn = (m.x & 255u) ? __ldg(P.ell + (size_t)(m.x >> 8) * 32 + lane) : 0xFF000000u;
-        pe0 = (m.y & 255u) ? __ldg(P.eell + (size_t)(m.y >> 8) * 32 + lane) : 0xFF000000u;
-        pbn = (m.x & 255u) ? __ldg(P.ellcw + (size_t)(m.x >> 8) * 32 + lane) : make_int2(0, 0);
-        pbe = (m.y & 255u) ? __ldg(P.eellcw + (size_t)(m.y >> 8) * 32 + lane) : make_int2(0, 0);
+      // software pipeline: the first items (and their (olabel, weight)) of words w + 2, w + 3 are loaded
+      // while words w, w + 1 are processed
+      uint32_t pn[2], pe0[2];
+      int2 pbn[2], pbe[2];
+      auto prefetch = [&](int i) {
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const uint4 m = i + u < nw ? wmeta[wb + i + u] : make_uint4(0u, 0u, 0u, 0u);
+          pn[u] = (m.x & 255u) ? __ldg(P.ell + (size_t)(m.x >> 8) * 32 + lane) : 0xFF000000u;
+          pe0[u] = (m.y & 255u) ? __ldg(P.eell + (size_t)(m.y >> 8) * 32 + lane) : 0xFF000000u;
+          pbn[u] = (m.x & 255u) ? __ldg(P.ellcw + (size_t)(m.x >> 8) * 32 + lane) : make_int2(0, 0);
+          pbe[u] = (m.y & 255u) ? __ldg(P.eellcw + (size_t)(m.y >> 8) * 32 + lane) : make_int2(0, 0);
+        }
       };
-      prefetch(wb);
-      for (int i = 0; i < nw; ++i) {
-        const int w = wb + i;
-        const uint32_t n0it = pn, e0it = pe0;
-        const int2 n0bw = pbn, e0bw = pbe;
-        if (i + 1 < nw) prefetch(w + 1);
+      // one word, any shape (straight-line or general); advances arc / arc32
+      auto one_word = [&](int w, uint32_t n0it, uint32_t e0it, int2 n0bw, int2 e0bw) {
         const int2 vv = Vr[w];
         const uint32_t vw = (uint32_t)vv.x;
-        if (!vw) continue;
+        if (!vw) return;
         const int32_t col = w * 32 + lane;
         const uint4 mt = wmeta[w];
         const uint32_t xn = mt.x, xe = mt.y, hm = mt.z;
@@ -984,7 +983,7 @@ __global__ void __launch_bounds__(kEmThreads, FSTC_WEM_MINB) k_wave_emit(WaveArg
           const uint32_t t = (uint32_t)__shfl_sync(0xffffffffu, inc, 31);
           arc32 += t;
           arc += t;
-          continue;
+          return;
         }
         int cnt = 0;
         if (has) {
@@ -1042,6 +1041,81 @@ __global__ void __launch_bounds__(kEmThreads, FSTC_WEM_MINB) k_wave_emit(WaveArg
         }
         arc += wtot;
         arc32 += (uint32_t)wtot;
+      };
+      // straight-line word (at most one eps item (M3) and one item (M1) per column): its moves
+      struct SL {
+        bool he, hn;
+        int2 ve, vn;
+        unsigned long long mn;
+        int cnt;
+      };
+      auto sl_count = [&](int2 vv, uint32_t n0it, uint32_t e0it) -> SL {
+        SL q;
+        const bool has = ((uint32_t)vv.x >> lane) & 1u;
+        const int32_t oe = (int32_t)(e0it & 0xFFFFFFu), on = (int32_t)(n0it & 0xFFFFFFu);
+        q.ve = Vr[oe >> 5];
+        q.vn = Vd[on >> 5];
+        q.he = has && e0it < 0xFF000000u && (((uint32_t)q.ve.x >> (oe & 31)) & 1u);
+        q.mn = lm[n0it >> 24];
+        q.hn = has && q.mn != 0ull && (((uint32_t)q.vn.x >> (on & 31)) & 1u);
+        q.cnt = (int)q.he + (q.hn ? (int)lc[n0it >> 24] : 0);
+        return q;
+      };
+      auto sl_store = [&](int w, int2 vv, const SL& q, uint32_t pos, uint32_t n0it, uint32_t e0it, int2 n0bw, int2 e0bw) {
+        const uint32_t vw = (uint32_t)vv.x;
+        const int32_t col = w * 32 + lane;
+        const uint32_t id = (uint32_t)vv.y + __popc(vw & ((1u << lane) - 1u));
+        __stcs((long long*)(P.row_ptr + id), (long long)pos);
+        __stcs(P.pair_a + id, r);
+        __stcs(P.pair_b + id, col);
+        P.is_start[id] = stA ? __ldg(&startB[col]) : (uint8_t)0;
+        P.is_accept[id] = acA ? __ldg(&accB[col]) : (uint8_t)0;
+        if (q.he) {
+          const int32_t oe = (int32_t)(e0it & 0xFFFFFFu);
+          __stcs(P.dst + pos, q.ve.y + __popc((uint32_t)q.ve.x & ((1u << (oe & 31)) - 1u)));
+          __stcs(P.ilabel + pos, FST_EPS);
+          __stcs(P.olabel + pos, e0bw.x);
+          __stcs(P.weight + pos, __int_as_float(e0bw.y));
+          ++pos;
+        }
+        if (q.hn) {
+          const int32_t on = (int32_t)(n0it & 0xFFFFFFu);
+          const int32_t rk = q.vn.y + __popc((uint32_t)q.vn.x & ((1u << (on & 31)) - 1u));
+          for (unsigned long long m = q.mn; m; m &= m - 1ull, ++pos) {
+            const int a = __ffsll((long long)m) - 1;
+            __stcs(P.dst + pos, rk);
+            __stcs(P.ilabel + pos, scar[a]);
+            __stcs(P.olabel + pos, n0bw.x);
+            __stcs(P.weight + pos, __fadd_rn(sw[a], __int_as_float(n0bw.y)));
+          }
+        }
+      };
+      prefetch(0);
+      for (int i = 0; i < nw; i += 2) {
+        const int w = wb + i;
+        const bool twoB = i + 1 < nw;
+        const uint32_t nA = pn[0], nB = pn[1], eA = pe0[0], eB = pe0[1];
+        const int2 bnA = pbn[0], bnB = pbn[1], beA = pbe[0], beB = pbe[1];
+        if (i + 2 < nw) prefetch(i + 2);
+        const uint4 mA = wmeta[w], mB = twoB ? wmeta[w + 1] : make_uint4(0u, 0u, 0u, 0u);
+        const bool sA = (mA.x & 255u) <= 1u && (mA.y & 255u) <= 1u && !mA.z;
+        const bool sB = (mB.x & 255u) <= 1u && (mB.y & 255u) <= 1u && !mB.z;
+        if (sA && sB) {  // two straight-line words: one warp scan of both counts (16-bit halves)
+          const int2 vA = Vr[w], vB = twoB ? Vr[w + 1] : make_int2(0, 0);
+          if (!(vA.x | vB.x)) continue;
+          const SL qA = sl_count(vA, nA, eA), qB = sl_count(vB, nB, eB);
+          const uint32_t pk = (uint32_t)qA.cnt | ((uint32_t)qB.cnt << 16);  // (sums < 32 * 65: no carry)
+          const uint32_t inc = warp_incl_scan(pk);
+          const uint32_t tt = __shfl_sync(0xffffffffu, inc, 31);
+          const uint32_t tA = tt & 0xFFFFu, tB = tt >> 16;
+          if (((uint32_t)vA.x >> lane) & 1u) sl_store(w, vA, qA, arc32 + (inc & 0xFFFFu) - (uint32_t)qA.cnt, nA, eA, bnA, beA);
+          if (((uint32_t)vB.x >> lane) & 1u) sl_store(w + 1, vB, qB, arc32 + tA + (inc >> 16) - (uint32_t)qB.cnt, nB, eB, bnB, beB);
+          arc32 += tA + tB;
+          arc += tA + tB;
+          continue;
+        }
+        one_word(w, nA, eA, bnA, beA);
+        if (twoB) one_word(w + 1, nB, eB, bnB, beB);
       }
     }
     for (int blk = fast ? bpr : warp; blk < bpr; blk += nwarp) {
