@@ -2815,7 +2815,7 @@ fst_status compose_run(int32_t n, const fst_handle* a, const fst_handle* b, cuda
     if (tp.ok) {
       launch_tile_emit(tp.emit, tp.grid_emit, tp.smem_emit, s, cx, comps[0], d_tot, tp.vr_rows);
       FSTC_LAUNCH_CHECK();
-    } else if (wp.ok && !want_prov && [&] {  // the wave emit indexes a composition's arcs with 32 bits
+    } else if (wp.ok && wp.emit_ok && !want_prov && [&] {  // the wave emit indexes a composition's arcs with 32 bits
                  for (int i = 0; i < n; ++i)
                    if (tot[2 * i + 3] - tot[2 * i + 1] >= INT32_MAX) return false;
                  return true;

@@ -1686,6 +1686,18 @@ fst_status wave_plan(int32_t n, const fst_handle* a, const fst_handle* b, const 
   P.wa.hcnt = (int32_t*)(base + o_h);
   P.wa.nrows = rows;
   plan->ok = true;
+  {  // the wave emit stages 32 bytes per word of the widest row: wider rows take the general emit
+    static const size_t emit_limit = [] {
+      int dev = 0, optin = 0;
+      cudaFuncAttributes fa{};
+      if (cudaGetDevice(&dev) != cudaSuccess ||
+          cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess ||
+          cudaFuncGetAttributes(&fa, k_wave_emit) != cudaSuccess)
+        return (size_t)0;
+      return (size_t)optin > fa.sharedSizeBytes ? (size_t)optin - fa.sharedSizeBytes : (size_t)0;
+    }();
+    plan->emit_ok = 32ull * (size_t)wprmax <= emit_limit;
+  }
   plan->depth = maxrows;
   plan->cluster = P.G2;
   return FST_OK;

@@ -12,6 +12,7 @@ struct WavePlan {
   bool ok = false;
   int32_t depth = 0;    // row steps of the longest composition (sequential per cluster)
   int32_t cluster = 1;  // CTAs per cluster (one composition per cluster)
+  bool emit_ok = false;  // the wave emit's staged rows fit in shared memory (else the general emit runs)
   struct Impl;
   Impl* impl;
   WavePlan();
@@ -32,7 +33,7 @@ fst_status wave_stage(const WavePlan& plan, int stage, uint32_t* R, uint32_t* V,
 fst_status wave_count(const WavePlan& plan, uint32_t* R, uint8_t* cnt8, cudaStream_t s);
 // pass-1 block sums over V: kept[] of every block (overwritten); after wave_count and stage 2.
 fst_status wave_kept(const WavePlan& plan, uint32_t* V, unsigned long long* kept, cudaStream_t s);
-// pass 2 (general emit replacement; no provenance): writes every composition's CSR from the numbering
+// pass 2 (general emit replacement; no provenance; needs plan.emit_ok): writes every composition's CSR from the numbering
 // (idbase / arcbase per block, wpre per word).  `err` counts internal inconsistencies (must stay 0).
 fst_status wave_emit(const WavePlan& plan, const struct CompDev* d_comps, const int64_t* d_tot, const int64_t* idbase,
                      const int64_t* arcbase, const uint16_t* wpre, uint32_t* V, int32_t* err, cudaStream_t s);

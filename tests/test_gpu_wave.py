@@ -184,3 +184,14 @@ def test_wave_lexicon_sizes(fst, words):
     As, B = fstgen.config_c5(num_utts=2, num_words=words)
     As = [fstgen.emissions_graph(12, 10000), fstgen.emissions_graph(9, 10001)]
     check_pairs(fst, [(A, B) for A in As], f"lexicon {words}")
+
+
+@pytest.mark.parametrize("words", [28000, 33000])
+def test_wave_wide_rows(fst, words):
+    """Rows near the wave emit's shared-memory limit (32 bytes per word of the widest row: ~6,900 words):
+    a 28k-word lexicon (~6,300 words per row) takes the wave emit, a 33k-word one (~7,500) the general
+    emit after the wave stages; both equal the level path and the oracle."""
+    As, B = fstgen.config_c5(num_utts=2, num_words=words)
+    As = [fstgen.emissions_graph(4, 10000), fstgen.emissions_graph(3, 10001)]
+    check_pairs(fst, [(A, B) for A in As], f"lexicon {words}")
+
