@@ -768,7 +768,7 @@ __global__ void __launch_bounds__(256) k_wave_kept(WaveArgs wa, int64_t nblocks)
 // rank) pairs.  Heavy states (> kWHeavy B arcs) take their exact count from k_wave_count and are written
 // by the whole CTA.
 #ifndef FSTC_WEM_THREADS
-#define FSTC_WEM_THREADS 384
+#define FSTC_WEM_THREADS 256
 #endif
 #ifndef FSTC_WEM_MINB
 #define FSTC_WEM_MINB 2
