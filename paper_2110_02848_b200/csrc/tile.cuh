@@ -33,7 +33,7 @@
 constexpr int kTThreads = FSTC_T_THREADS;  // pull / count CTAs (1 per SM: the 64-bit RT takes the smem)
 constexpr int kTWarps = kTThreads / 32;
 #ifndef FSTC_E_THREADS
-#define FSTC_E_THREADS 1024
+#define FSTC_E_THREADS 896
 #endif
 constexpr int kEThreads = FSTC_E_THREADS; // emit CTAs (1 per SM: the rank tables take the shared memory)
 constexpr int kEWarps = kEThreads / 32;
