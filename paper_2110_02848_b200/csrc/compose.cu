@@ -2368,8 +2368,8 @@ fst_status tile_plan(fst* A, fst* B, int64_t pairs, bool want_prov, cudaStream_t
   if (!attrs) {
     const void* fs[] = {(const void*)k_tile_push<false, 8>, (const void*)k_tile_push<false, 16>,
                         (const void*)k_tile_push<true, 8>,  (const void*)k_tile_push<true, 16>,
-                        (const void*)k_tile_pull<false, 8>, (const void*)k_tile_pull<false, 16>,
-                        (const void*)k_tile_pull<true, 8>,  (const void*)k_tile_pull<true, 16>,
+                        (const void*)k_tile_pull<false, 8, kTP1Threads>, (const void*)k_tile_pull<false, 16, kTP1Threads>,
+                        (const void*)k_tile_pull<true, 8, kTP2Threads>,  (const void*)k_tile_pull<true, 16, kTP2Threads>,
                         (const void*)k_tile_count<false, 8>, (const void*)k_tile_count<false, 16>,
                         (const void*)k_tile_count<true, 8>,  (const void*)k_tile_count<true, 16>,
                         (const void*)k_tile_emit<8>,        (const void*)k_tile_emit<16>};
@@ -2393,8 +2393,9 @@ fst_status tile_plan(fst* A, fst* B, int64_t pairs, bool want_prov, cudaStream_t
 
 template <bool kStage2>
 void launch_tile_pull(const TileArgs& ta, int grid, size_t smem, cudaStream_t s, const Ctx& cx, int level) {
-  if (ta.kj == 8) k_tile_pull<kStage2, 8><<<grid, kTThreads, smem, s>>>(cx, ta, level);
-  else k_tile_pull<kStage2, 16><<<grid, kTThreads, smem, s>>>(cx, ta, level);
+  constexpr int nt = kStage2 ? kTP2Threads : kTP1Threads;
+  if (ta.kj == 8) k_tile_pull<kStage2, 8, nt><<<grid, nt, smem, s>>>(cx, ta, level);
+  else k_tile_pull<kStage2, 16, nt><<<grid, nt, smem, s>>>(cx, ta, level);
 }
 // push level in tile form: stage 1 walks the reversed moves (in-view tiles: TilePlan::s2), stage 2 the
 // forward moves (out-view tiles: TilePlan::s1)

@@ -30,7 +30,15 @@
 #ifndef FSTC_T_THREADS
 #define FSTC_T_THREADS 1024
 #endif
-constexpr int kTThreads = FSTC_T_THREADS;  // pull / count CTAs (1 per SM: the 64-bit RT takes the smem)
+constexpr int kTThreads = FSTC_T_THREADS;  // count / tile-push CTAs (1 per SM: the 64-bit RT takes the smem)
+#ifndef FSTC_TP1_THREADS
+#define FSTC_TP1_THREADS 1024
+#endif
+#ifndef FSTC_TP2_THREADS
+#define FSTC_TP2_THREADS 896
+#endif
+constexpr int kTP1Threads = FSTC_TP1_THREADS;  // stage-1 bottom-up rounds
+constexpr int kTP2Threads = FSTC_TP2_THREADS;  // stage-2 rounds (fewer threads, more registers: no spills at kJ = 16)
 constexpr int kTWarps = kTThreads / 32;
 #ifndef FSTC_E_THREADS
 #define FSTC_E_THREADS 896
@@ -271,8 +279,8 @@ __device__ __forceinline__ void for_items(const uint32_t* __restrict__ ell, int 
 // per-round sizes differ from per-BFS-distance counts.  Each tile also consumes the current frontier
 // words and chunk flags of its rows and lists the chunks that gained next-frontier bits (for a
 // following push level), so no separate merge pass is needed.
-template <bool kStage2, int kJ>
-__global__ void __launch_bounds__(kTThreads, 1) k_tile_pull(Ctx cx, TileArgs ta, int level) {
+template <bool kStage2, int kJ, int NT>
+__global__ void __launch_bounds__(NT, 1) k_tile_pull(Ctx cx, TileArgs ta, int level) {
   using M = unsigned long long;
   __shared__ TileSmem<M> t;
   __shared__ uint32_t chit[kTRows][2];  // per tile row: chunks (<= 64) that gained next-frontier bits
@@ -312,7 +320,7 @@ __global__ void __launch_bounds__(kTThreads, 1) k_tile_pull(Ctx cx, TileArgs ta,
     __syncthreads();
     // consume the rows' frontier words; any unvisited pair left?
     bool any = false;
-    for (int i = threadIdx.x; i < nr * wpr; i += kTThreads) {
+    for (int i = threadIdx.x; i < nr * wpr; i += NT) {
       const int x = i / wpr, w = i - x * wpr;
       const int64_t gw = c.W + (int64_t)(r0 + x) * wpr + w;
       if (Fc[gw]) Fc[gw] = 0u;
@@ -321,7 +329,7 @@ __global__ void __launch_bounds__(kTThreads, 1) k_tile_pull(Ctx cx, TileArgs ta,
     if (any) s_any = 1;
     __syncthreads();
     if (s_any) {
-      tile_rt(RT, t, vis, c.W, wpr, kTWarps);
+      tile_rt(RT, t, vis, c.W, wpr, (NT / 32));
       __syncthreads();
       const int j0 = t.lm[kLiSent] ? 0 : 1;  // the sentinel column only matters with A eps arcs
       M rm[kTRows];
@@ -348,8 +356,8 @@ __global__ void __launch_bounds__(kTThreads, 1) k_tile_pull(Ctx cx, TileArgs ta,
         }
       };
       const int wd = ta.sd.wd;
-      for (int w = warp; w < wpr; w += 2 * kTWarps) {
-        const int w2 = w + kTWarps;
+      for (int w = warp; w < wpr; w += 2 * (NT / 32)) {
+        const int w2 = w + (NT / 32);
         const uint32_t u1 = lane < nr ? unvisited(r0 + lane, w) : 0u;
         const uint32_t u2 = (w2 < wpr && lane < nr) ? unvisited(r0 + lane, w2) : 0u;
         const bool a1 = __any_sync(0xffffffffu, u1 != 0u), a2 = __any_sync(0xffffffffu, u2 != 0u);
@@ -383,7 +391,7 @@ __global__ void __launch_bounds__(kTThreads, 1) k_tile_pull(Ctx cx, TileArgs ta,
     }
     __syncthreads();
     // chunk flags of the tile's rows: consumed ones cleared, chunks with new bits listed
-    for (int i = threadIdx.x; i < nr * c.cpr; i += kTThreads) {
+    for (int i = threadIdx.x; i < nr * c.cpr; i += NT) {
       const int x = i / c.cpr, j = i - x * c.cpr;
       if (!c.own(r0 + x)) continue;
       const int64_t q = c.Q + (int64_t)(r0 + x) * c.cpr + j;
