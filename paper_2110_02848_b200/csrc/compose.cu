@@ -2455,7 +2455,7 @@ fst_status run_stage_tile(const Ctx& cx, const TilePlan& tp, int64_t total, cuda
       k_push_finish<<<sm_count() * 8, 256, 0, s>>>(cx, level);
       FSTC_LAUNCH_CHECK();
     } else if (sparse_push_ok) {
-      k_sparse_push<kStage2><<<sm_count() * 8, 256, 0, s>>>(cx, tb, level);
+      k_sparse_push<kStage2><<<sm_count() * kSPGrid, 256, 0, s>>>(cx, tb, level);
       FSTC_LAUNCH_CHECK();
       k_push_finish<<<sm_count() * 8, 256, 0, s>>>(cx, level);
       FSTC_LAUNCH_CHECK();

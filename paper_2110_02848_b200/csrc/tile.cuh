@@ -543,8 +543,15 @@ __global__ void __launch_bounds__(kTThreads, 1) k_tile_push(Ctx cx, TileArgs ta,
 // has its bit set, so the next frontier gets exactly this level's new pairs; duplicates are ORs).
 // k_push_finish then counts the next frontier and lists its chunks.
 constexpr int kSPLab = 64;  // label-mask entries staged per warp (label index < 64; else the tile rounds' k_level)
+#ifndef FSTC_SP_MINB
+#define FSTC_SP_MINB 0
+#endif
+#ifndef FSTC_SP_GRID
+#define FSTC_SP_GRID 16
+#endif
+constexpr int kSPGrid = FSTC_SP_GRID;  // CTAs per SM of the push levels
 template <bool kStage2>
-__global__ void __launch_bounds__(256) k_sparse_push(Ctx cx, TileArgs ta, int level) {
+__global__ void __launch_bounds__(256, FSTC_SP_MINB) k_sparse_push(Ctx cx, TileArgs ta, int level) {
   __shared__ unsigned long long lmw[8][kSPLab];
   __shared__ int32_t sroww[8][64];
   tile_level_prologue(cx, level);
